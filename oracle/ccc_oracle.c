@@ -1,0 +1,180 @@
+/*
+ * oracle/ccc_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, obviously-correct CPU brute force of the CCC method of
+ * PAPER.md (arXiv 1705.08213, Joubert et al.), used by tests/, by
+ * __graft_entry__.smoke() and by bench.py's cpu_baseline / --impl reference leg.
+ * Nothing in the product path (paper_1705_08213_b200/) may link, load or call
+ * this file; it shares no code, header, table or constant with the CUDA path.
+ *
+ * Every function is a literal transcription of a definition of the paper:
+ *
+ *   element   v_{i,q} = (r1, r2) in S_2, S = {0,1}            (§2.1)
+ *             stored as one byte code = 2*r1 + r2              (R-1)
+ *   rho_{i,q}(a) = sum_r chi_a((v_{i,q})_r)
+ *   S_i(a)  = sum_q rho_{i,q}(a),   f_i(a) = S_i(a) / (2 n_f)   (Eq.1)
+ *   T_ij(a,b) = sum_q sum_{r in v_iq} sum_{r' in v_jq} [r=a][r'=b]
+ *             -- the enumeration of all pairings of Fig.1,
+ *                equal to sum_q rho_{i,q}(a) rho_{j,q}(b)       (Eq.2)
+ *   f_ij = T_ij / (4 n_f)
+ *   CCC_ij(a,b) = f_ij(a,b) (1 - g f_i(a)) (1 - g f_j(b))       (Eq.3)
+ *   T_ijk(a,b,c): the 8 combinations of Fig.2      (Eq.5)
+ *   f_ijk = T_ijk / (8 n_f)
+ *   CCC_ijk(a,b,c) = f_ijk(a,b,c) prod (1 - g f(.))            (Eq.4)
+ *
+ * Unique results: pairs i<j, triples i<j<k, emitted in
+ * lexicographic order, cells a-major (index 2a+b, 4a+2b+c).
+ *
+ * Tallies are accumulated in int64; CCC is evaluated in fp64 in the order the
+ * equations are written.  OpenMP parallelises the outer record loop only.
+ */
+#include <stdint.h>
+#include <stddef.h>
+
+/* (v_{i,q})_1 and (v_{i,q})_2 of the stored code (R-1). */
+static int elem_r1(uint8_t code) { return (code >> 1) & 1; }
+static int elem_r2(uint8_t code) { return code & 1; }
+
+/* Eq.1 numerator: S_i(a) = sum_q rho_{i,q}(a), for a = 0,1.  S[i*2 + a]. */
+void oracle_allele_sums(const uint8_t* codes, int64_t n_v, int64_t n_f, int64_t* S)
+{
+    for (int64_t i = 0; i < n_v; ++i) {
+        int64_t s0 = 0, s1 = 0;
+        for (int64_t q = 0; q < n_f; ++q) {
+            uint8_t c = codes[i * n_f + q];
+            int r[2] = {elem_r1(c), elem_r2(c)};
+            for (int t = 0; t < 2; ++t) {          /* rho_{i,q}(a) = sum_r chi_a(r) */
+                if (r[t] == 0) s0 += 1;
+                if (r[t] == 1) s1 += 1;
+            }
+        }
+        S[i * 2 + 0] = s0;
+        S[i * 2 + 1] = s1;
+    }
+}
+
+/* Fig.1 / Eq.2: the 2x2 tally of one pair, by enumerating the 4 pairings per field. */
+static void tally2_one(const uint8_t* vi, const uint8_t* vj, int64_t n_f, int64_t T[4])
+{
+    T[0] = T[1] = T[2] = T[3] = 0;
+    for (int64_t q = 0; q < n_f; ++q) {
+        int ri[2] = {elem_r1(vi[q]), elem_r2(vi[q])};
+        int rj[2] = {elem_r1(vj[q]), elem_r2(vj[q])};
+        for (int s = 0; s < 2; ++s)
+            for (int t = 0; t < 2; ++t)
+                T[2 * ri[s] + rj[t]] += 1;          /* tuple (a,b) = (ri[s], rj[t]) */
+    }
+}
+
+/* Fig.2 / Eq.5: the 2x2x2 tally of one triple, by enumerating the 8 combinations. */
+static void tally3_one(const uint8_t* vi, const uint8_t* vj, const uint8_t* vk,
+                       int64_t n_f, int64_t T[8])
+{
+    for (int c = 0; c < 8; ++c) T[c] = 0;
+    for (int64_t q = 0; q < n_f; ++q) {
+        int ri[2] = {elem_r1(vi[q]), elem_r2(vi[q])};
+        int rj[2] = {elem_r1(vj[q]), elem_r2(vj[q])};
+        int rk[2] = {elem_r1(vk[q]), elem_r2(vk[q])};
+        for (int s = 0; s < 2; ++s)
+            for (int t = 0; t < 2; ++t)
+                for (int u = 0; u < 2; ++u)
+                    T[4 * ri[s] + 2 * rj[t] + rk[u]] += 1;
+    }
+}
+
+/* Eq.3 for one pair. */
+static void ccc2_one(const int64_t T[4], const int64_t* Si, const int64_t* Sj,
+                     int64_t n_f, double gamma, double out[4])
+{
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) {
+            double f_ij = (double)T[2 * a + b] / (4.0 * (double)n_f);
+            double f_ia = (double)Si[a] / (2.0 * (double)n_f);
+            double f_jb = (double)Sj[b] / (2.0 * (double)n_f);
+            out[2 * a + b] = f_ij * (1.0 - gamma * f_ia) * (1.0 - gamma * f_jb);
+        }
+}
+
+/* Eq.4 for one triple. */
+static void ccc3_one(const int64_t T[8], const int64_t* Si, const int64_t* Sj,
+                     const int64_t* Sk, int64_t n_f, double gamma, double out[8])
+{
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b)
+            for (int c = 0; c < 2; ++c) {
+                double f_ijk = (double)T[4 * a + 2 * b + c] / (8.0 * (double)n_f);
+                double f_ia = (double)Si[a] / (2.0 * (double)n_f);
+                double f_jb = (double)Sj[b] / (2.0 * (double)n_f);
+                double f_kc = (double)Sk[c] / (2.0 * (double)n_f);
+                out[4 * a + 2 * b + c] =
+                    f_ijk * (1.0 - gamma * f_ia) * (1.0 - gamma * f_jb) * (1.0 - gamma * f_kc);
+            }
+}
+
+/*
+ * Tallies and CCC for an explicit list of pairs (idx[m][2], global vector ids).
+ * S must come from oracle_allele_sums over the same codes.  ccc may be NULL.
+ */
+void oracle_pairs(const uint8_t* codes, int64_t n_v, int64_t n_f, const int64_t* S,
+                  double gamma, const int64_t* idx, int64_t m, int64_t* T, double* ccc)
+{
+    (void)n_v;
+    #pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t r = 0; r < m; ++r) {
+        int64_t i = idx[2 * r], j = idx[2 * r + 1];
+        tally2_one(codes + i * n_f, codes + j * n_f, n_f, T + 4 * r);
+        if (ccc) ccc2_one(T + 4 * r, S + 2 * i, S + 2 * j, n_f, gamma, ccc + 4 * r);
+    }
+}
+
+/* Same for an explicit list of triples (idx[m][3]). */
+void oracle_triples(const uint8_t* codes, int64_t n_v, int64_t n_f, const int64_t* S,
+                    double gamma, const int64_t* idx, int64_t m, int64_t* T, double* ccc)
+{
+    (void)n_v;
+    #pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t r = 0; r < m; ++r) {
+        int64_t i = idx[3 * r], j = idx[3 * r + 1], k = idx[3 * r + 2];
+        tally3_one(codes + i * n_f, codes + j * n_f, codes + k * n_f, n_f, T + 8 * r);
+        if (ccc)
+            ccc3_one(T + 8 * r, S + 2 * i, S + 2 * j, S + 2 * k, n_f, gamma, ccc + 8 * r);
+    }
+}
+
+/*
+ * All unique pairs i<j in lexicographic order.  Record r of the
+ * output is the r-th pair of the double loop below; T[C(n_v,2)][4], ccc likewise.
+ */
+void oracle_all_pairs(const uint8_t* codes, int64_t n_v, int64_t n_f, const int64_t* S,
+                      double gamma, int64_t* T, double* ccc)
+{
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t i = 0; i < n_v; ++i) {
+        /* records before row i: sum_{i' < i} (n_v - 1 - i') */
+        int64_t r = 0;
+        for (int64_t ii = 0; ii < i; ++ii) r += n_v - 1 - ii;
+        for (int64_t j = i + 1; j < n_v; ++j, ++r) {
+            tally2_one(codes + i * n_f, codes + j * n_f, n_f, T + 4 * r);
+            if (ccc) ccc2_one(T + 4 * r, S + 2 * i, S + 2 * j, n_f, gamma, ccc + 4 * r);
+        }
+    }
+}
+
+/* All unique triples i<j<k in lexicographic order. */
+void oracle_all_triples(const uint8_t* codes, int64_t n_v, int64_t n_f, const int64_t* S,
+                        double gamma, int64_t* T, double* ccc)
+{
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t i = 0; i < n_v; ++i) {
+        int64_t r = 0;                       /* records before pivot row i, counted */
+        for (int64_t ii = 0; ii < i; ++ii)
+            for (int64_t jj = ii + 1; jj < n_v; ++jj) r += n_v - 1 - jj;
+        for (int64_t j = i + 1; j < n_v; ++j)
+            for (int64_t k = j + 1; k < n_v; ++k, ++r) {
+                tally3_one(codes + i * n_f, codes + j * n_f, codes + k * n_f, n_f, T + 8 * r);
+                if (ccc)
+                    ccc3_one(T + 8 * r, S + 2 * i, S + 2 * j, S + 2 * k, n_f, gamma,
+                             ccc + 8 * r);
+            }
+    }
+}

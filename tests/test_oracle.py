@@ -1,0 +1,289 @@
+"""Pins of the CPU oracle against things other than itself (CPU only).
+
+Each test names what fixes the expected value: a value printed in SPEC.md / hand
+enumeration of the paper's figure procedure (tests/golden/), a closed form, an
+invariant the paper states, exact rational arithmetic, a textbook routine (numpy
+integer matmul / einsum) or the paper's own Table-1 route.
+"""
+from fractions import Fraction
+from itertools import combinations, permutations
+
+import numpy as np
+import pytest
+
+import oracle
+import synthgen
+from conftest import read_golden
+
+
+def _vec(spec):
+    """'0*65' / '1,3' / '0*3,3*5' -> list of codes."""
+    out = []
+    for part in spec.split(","):
+        if "*" in part:
+            c, n = part.split("*")
+            out += [int(c)] * int(n)
+        else:
+            out.append(int(part))
+    return out
+
+
+def _args(s):
+    d = {}
+    for kv in s.split(";"):
+        k, v = kv.split("=")
+        d[k.strip()] = v.strip()
+    return d
+
+
+# ------------------------------------------------------------------ golden values
+@pytest.mark.parametrize("row", read_golden("spec_hand_values.txt"))
+def test_spec_hand_values(row):
+    name, inputs, expected, _cite = row
+    if name in ("unique_pairs", "unique_triples"):
+        n = int(inputs.split("=")[1])
+        lst = oracle.pair_list(n) if name == "unique_pairs" else oracle.triple_list(n)
+        assert len(lst) == int(expected)
+        if name == "unique_pairs":
+            T, _ = oracle.all_pairs(np.zeros((n, 3), np.uint8))
+            assert T.size == 4 * int(expected)       # "6 tables, 24 values"
+        return
+    a = _args(inputs)
+    exp = _args(expected) if "=" in expected and ";" in expected else None
+    if name == "allele_freq":
+        v = _vec(a["v"])
+        f = oracle.frequencies(np.array([v], np.uint8))[0]
+        assert oracle.freq_exact(v, 1) == Fraction(exp["f1"])
+        assert oracle.freq_exact(v, 0) == Fraction(exp["f0"])
+        assert f[1] == float(Fraction(exp["f1"])) and f[0] == float(Fraction(exp["f0"]))
+        return
+    vs = [_vec(a[k]) for k in ("vi", "vj", "vk") if k in a]
+    codes = np.array(vs, np.uint8)
+    key, val = expected.split("=")
+    want = [Fraction(x) for x in val.split(",")]
+    if name in ("pair_tally",):
+        T, _ = oracle.pairs(codes, [[0, 1]])
+        assert list(T[0]) == [int(x) for x in want]
+        assert oracle.tally2_py(vs[0], vs[1]) == [int(x) for x in want]
+    elif name == "reconstruct3":
+        T, _ = oracle.triples(codes, [[0, 1, 2]])
+        assert list(T[0]) == [int(x) for x in want]
+        assert oracle.tally3_via_table1(*vs) == [int(x) for x in want]
+    elif name == "ccc2":
+        assert oracle.ccc2_exact(vs[0], vs[1]) == want
+        _, C = oracle.pairs(codes, [[0, 1]])
+        np.testing.assert_allclose(C[0], [float(x) for x in want], rtol=1e-15)
+    elif name == "ccc3":
+        assert oracle.ccc3_exact(*vs) == want
+        _, C = oracle.triples(codes, [[0, 1, 2]])
+        np.testing.assert_allclose(C[0], [float(x) for x in want], rtol=1e-15)
+    else:
+        raise AssertionError(name)
+
+
+@pytest.mark.parametrize("row", read_golden("fig_examples_nf1.txt"))
+def test_figure_style_examples_nf1(row):
+    way, codes, expected, _ = row
+    cs = [int(c) for c in codes.split()]
+    want = [int(x) for x in expected.split(",")]
+    arr = np.array([[c] for c in cs], np.uint8)
+    if way == "2":
+        assert oracle.tally2_py([cs[0]], [cs[1]]) == want
+        assert list(oracle.pairs(arr, [[0, 1]])[0][0]) == want
+    else:
+        assert oracle.tally3_py([cs[0]], [cs[1]], [cs[2]]) == want
+        assert list(oracle.triples(arr, [[0, 1, 2]])[0][0]) == want
+        assert oracle.tally3_via_table1([cs[0]], [cs[1]], [cs[2]]) == want
+
+
+def test_table1_reading_A3():
+    """Table 1 as printed agrees with the text rule only with its first two
+    columns swapped (reading A-3); the literal header reading contradicts the text."""
+    rows = read_golden("table1.txt")
+    tup = lambda s: tuple(int(x) for x in s.split(","))
+    swapped_ok = literal_ok = True
+    for c1, c2, x1, x2, x3 in rows:
+        want = [tup(x1), tup(x2), tup(x3)]
+        got_swapped = [oracle.x_entry(tup(c2), tup(c1), xi) for xi in (1, 2, 3)]
+        got_literal = [oracle.x_entry(tup(c1), tup(c2), xi) for xi in (1, 2, 3)]
+        swapped_ok &= got_swapped == want
+        literal_ok &= got_literal == want
+    assert swapped_ok
+    assert not literal_ok
+
+
+# ------------------------------------------------------------- C vs brute force py
+@pytest.mark.parametrize("n_f", [1, 3, 17])
+def test_c_oracle_equals_python_enumeration(n_f):
+    rng = np.random.default_rng(n_f)
+    codes = rng.integers(0, 4, size=(6, n_f), dtype=np.uint8)
+    T2, C2 = oracle.all_pairs(codes)
+    for r, (i, j) in enumerate(combinations(range(6), 2)):
+        assert list(T2[r]) == oracle.tally2_py(codes[i], codes[j])
+        ex = oracle.ccc2_exact(codes[i], codes[j])
+        np.testing.assert_allclose(C2[r], [float(x) for x in ex], rtol=2e-15, atol=0)
+    T3, C3 = oracle.all_triples(codes)
+    for r, (i, j, k) in enumerate(combinations(range(6), 3)):
+        assert list(T3[r]) == oracle.tally3_py(codes[i], codes[j], codes[k])
+        ex = oracle.ccc3_exact(codes[i], codes[j], codes[k])
+        np.testing.assert_allclose(C3[r], [float(x) for x in ex], rtol=2e-15, atol=0)
+        assert list(T3[r]) == oracle.tally3_via_table1(codes[i], codes[j], codes[k])
+
+
+def test_literal_req_order_fails():
+    """Reading A-2: the printed R-eqs with the first slot as the i-allele (Eq.5 order)
+    disagree with the brute force; with the first slot as the pivot allele they agree."""
+    rng = np.random.default_rng(5)
+    c = rng.integers(0, 4, size=(3, 40), dtype=np.uint8)
+    B = [oracle.masked_tally(c[1], c[0], c[2], xi) for xi in (1, 2, 3)]
+    literal = [0] * 8
+    for x in (0, 1):
+        for y in (0, 1):
+            for z in (0, 1):
+                Bx = B[0] if x == 0 else B[2]
+                literal[4 * x + 2 * y + z] = 2 * Bx[2 * y + z] + B[1][2 * y + z]
+    truth = oracle.tally3_py(c[0], c[1], c[2])
+    assert oracle.reconstruct3(*B) == truth
+    assert literal != truth
+
+
+# ------------------------------------------------------- textbook-routine identities
+def _counts(codes):
+    """allele-1 count n_{iq} = rho_{i,q}(1) by direct decode (not via the oracle)."""
+    return ((codes >> 1) & 1).astype(np.int64) + (codes & 1).astype(np.int64)
+
+
+@pytest.mark.parametrize("shape", [(9, 130), (23, 257)])
+def test_pairs_equal_integer_matmul(shape):
+    """T(a,b) = R_a R_b^T with R_1 = N, R_0 = 2 - N (numpy integer matmul)."""
+    codes = synthgen.random_codes(*shape, seed=11).numpy()
+    N = _counts(codes)
+    R = {1: N, 0: 2 - N}
+    T, _ = oracle.all_pairs(codes)
+    iu = np.triu_indices(shape[0], 1)
+    for a in (0, 1):
+        for b in (0, 1):
+            G = R[a] @ R[b].T
+            np.testing.assert_array_equal(T[:, 2 * a + b], G[iu])
+
+
+def test_triples_equal_einsum():
+    codes = synthgen.hwe_codes(8, 77, seed=4).numpy()
+    N = _counts(codes)
+    R = {1: N, 0: 2 - N}
+    T, _ = oracle.all_triples(codes)
+    tl = oracle.triple_list(8)
+    for a in (0, 1):
+        for b in (0, 1):
+            for c in (0, 1):
+                G3 = np.einsum("iq,jq,kq->ijk", R[a], R[b], R[c])
+                np.testing.assert_array_equal(T[:, 4 * a + 2 * b + c],
+                                              G3[tl[:, 0], tl[:, 1], tl[:, 2]])
+
+
+# ---------------------------------------------------------------- invariants
+def test_invariants_random():
+    codes = synthgen.random_codes(10, 101, seed=7).numpy()
+    n_f = codes.shape[1]
+    S = oracle.allele_sums(codes)
+    assert np.all(S.sum(1) == 2 * n_f)                       # f_i(0)+f_i(1) = 1
+    T2, C2 = oracle.all_pairs(codes)
+    assert np.all(T2.sum(1) == 4 * n_f)                      # sum f_ij = 1
+    assert np.all(T2 >= 0) and np.all(C2 >= 0)
+    T3, _ = oracle.all_triples(codes)
+    assert np.all(T3.sum(1) == 8 * n_f)
+    # marginalisation: sum_b T3(a,b,c) = 2 T2_ik(a,c)   (rho_j(0)+rho_j(1) = 2)
+    pidx = {tuple(p): r for r, p in enumerate(oracle.pair_list(10))}
+    for r, (i, j, k) in enumerate(oracle.triple_list(10)):
+        t2 = T2[pidx[(i, k)]]
+        for a in (0, 1):
+            for c in (0, 1):
+                assert T3[r, 4 * a + c] + T3[r, 4 * a + 2 + c] == 2 * t2[2 * a + c]
+
+
+def test_permutation_symmetry():
+    """f_ij symmetric; f_ijk symmetric in i,j,k."""
+    codes = synthgen.random_codes(5, 64, seed=9).numpy()
+    T, C = oracle.pairs(codes, [[1, 3], [3, 1]])
+    assert [T[0][0], T[0][1], T[0][2], T[0][3]] == [T[1][0], T[1][2], T[1][1], T[1][3]]
+    np.testing.assert_allclose(C[0][[0, 1, 2, 3]], C[1][[0, 2, 1, 3]], rtol=1e-15)
+    base = (0, 2, 4)
+    T0, C0 = oracle.triples(codes, [base])
+    for p in permutations(range(3)):
+        idx = [base[p[0]], base[p[1]], base[p[2]]]
+        Tp, Cp = oracle.triples(codes, [idx])
+        for a in (0, 1):
+            for b in (0, 1):
+                for c in (0, 1):
+                    abc = (a, b, c)
+                    q = [abc[p[0]], abc[p[1]], abc[p[2]]]
+                    assert T0[0][4 * a + 2 * b + c] == Tp[0][4 * q[0] + 2 * q[1] + q[2]]
+
+
+def test_closed_forms_ccc():
+    n_f = 9
+    het = np.ones((3, n_f), np.uint8)
+    _, C = oracle.pairs(het, [[0, 1]])
+    np.testing.assert_allclose(C[0], [1 / 9] * 4, rtol=1e-15)
+    _, C = oracle.triples(het, [[0, 1, 2]])
+    np.testing.assert_allclose(C[0], [1 / 27] * 8, rtol=1e-15)
+    codes = synthgen.random_codes(4, 33, seed=3).numpy()
+    _, C = oracle.all_pairs(codes, gamma=0.0)
+    np.testing.assert_allclose(C.sum(1), 1.0, rtol=1e-15)    # gamma=0 -> sum CCC = 1
+    _, C = oracle.all_triples(codes, gamma=0.0)
+    np.testing.assert_allclose(C.sum(1), 1.0, rtol=1e-15)
+    vi, vj = codes[0], codes[1]
+    assert sum(oracle.ccc2_exact(vi, vj, gamma=Fraction(0))) == 1
+
+
+def test_planted_closed_form():
+    codes, L, H, _ = synthgen.planted_codes(12, 97, seed=3)
+    codes = codes.numpy()
+    T2, _ = oracle.all_pairs(codes)
+    for r, (i, j) in enumerate(oracle.pair_list(12)):
+        assert list(T2[r]) == oracle.planted_tally2(L, H, 97, i, j)
+    T3, _ = oracle.all_triples(codes[:7])
+    for r, (i, j, k) in enumerate(oracle.triple_list(7)):
+        assert list(T3[r]) == oracle.planted_tally3(L, H, 97, i, j, k)
+
+
+def test_padding_independence():
+    """Results are over exactly n_f fields (A-9): appending fields changes sums by the
+    appended contribution only; n_f=65 all-(0,0) gives 260 (not 4*128)."""
+    z = np.zeros((2, 65), np.uint8)
+    assert list(oracle.pairs(z, [[0, 1]])[0][0]) == [260, 0, 0, 0]
+
+
+# ----------------------------------------------------------------- checksum
+def test_checksum_properties():
+    codes = synthgen.random_codes(9, 40, seed=2).numpy()
+    T, _ = oracle.all_pairs(codes)
+    idx = oracle.pair_list(9)
+    full = oracle.checksum(2, idx, T)
+    assert oracle.checksum(2, idx[:0], T[:0]) == 0
+    perm = np.random.default_rng(1).permutation(len(idx))
+    assert oracle.checksum(2, idx[perm], T[perm]) == full
+    part = (oracle.checksum(2, idx[:10], T[:10]) + oracle.checksum(2, idx[10:], T[10:])) % (1 << 128)
+    assert part == full
+    # a single flipped tally changes it
+    T2 = T.copy()
+    T2[5, 1] += 1
+    assert oracle.checksum(2, idx, T2) != full
+    # distinct single-record digests on a sample
+    digs = {oracle.record_digest(2, idx[r], T[r]) for r in range(len(idx))}
+    assert len(digs) == len(idx)
+    assert oracle.fmix64(0) == 0 and oracle.fmix64(1) != 1
+
+
+# ----------------------------------------------------------------- synthgen pins
+def test_synthgen_scalar_vs_tensor_and_tiling():
+    t = synthgen.random_codes(5, 70, seed=7)
+    for i in range(5):
+        for q in (0, 1, 57, 69):
+            assert int(t[i, q]) == synthgen.code_scalar(7, i, q)
+    tail = synthgen.random_codes(3, 70, seed=7, row0=2)
+    assert np.array_equal(t[2:].numpy(), tail.numpy())
+    assert not np.array_equal(t.numpy(), synthgen.random_codes(5, 70, seed=8).numpy())
+    big = synthgen.random_codes(64, 4096, seed=1).numpy()
+    freq = np.bincount(big.ravel(), minlength=4) / big.size
+    assert np.all(np.abs(freq - 0.25) < 0.01)
