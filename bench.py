@@ -1,0 +1,405 @@
+"""bench.py -- CCC comparisons/s of the B200 hot path.
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                [--workload c2|c4|c1] [--no-e2e] [--no-cpu]
+
+One step = one pass of the whole hot path over one synthetic batch resident in HBM:
+  2-way (default, BASELINE configs[1] = C2: 20,000 vectors x 50,000 individuals):
+      ccc_pack -> ccc_expand -> ccc_2way_block (fused tally GEMM + CCC epilogue,
+      every unique pair's uint32 tallies + fp64 CCC written to HBM)
+  3-way (--workload c4: 4,096 x 16,384, 16 stages, FULL output, buffer reused)
+At N > 1 (torchrun), the 2-way path runs the block-circulant decomposition with the
+packed vector blocks passed round a ring over NCCL send/recv; per-GPU load is kept at
+C2's (weak scaling: n_v = 20,000 * sqrt(N)).
+value = unique comparisons (pairs x n_f) of all ranks / max-over-ranks device time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CCC elementwise comparisons/sec (2-way, 3-way) at 1/2/4/8 B200; % int8 TC peak"
+UNIT = "comparisons/s"
+WORKLOADS = {
+    "c1": dict(way=2, n_v=64, n_f=1024, label="2-way CCC, 64 x 1,024 (configs[0])"),
+    "c2": dict(way=2, n_v=20000, n_f=50000,
+               label="2-way CCC, 20,000 SNP vectors x 50,000 individuals (configs[1])"),
+    "c4": dict(way=3, n_v=4096, n_f=16384, n_st=16,
+               label="3-way CCC, 4,096 SNP vectors x 16,384 individuals, 16 stages (configs[3])"),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------ helpers
+def comparisons(way, n_v, n_f):
+    if way == 2:
+        return n_f * (n_v * (n_v - 1) // 2)
+    return n_f * (n_v * (n_v - 1) * (n_v - 2) // 6)
+
+
+def ncu_traffic(kernel: str):
+    """dram bytes per launch of `kernel` from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(kernel, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_baseline(way, n_v, n_f, target_s=12.0, kind="random"):  # noqa: C901
+    """The oracle as it stands, on the host cores, on a bounded sample of the workload."""
+    import numpy as np
+
+    import oracle
+    import synthgen
+    cores = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    rng = np.random.default_rng(0)
+    rows = np.sort(rng.choice(n_v, size=min(n_v, 1024 if way == 2 else 128), replace=False))
+    sub = np.concatenate([synthgen.make_codes(kind, 1, n_f, row0=int(r)).numpy() for r in rows])
+    oracle.lib()
+    m_local = len(rows)
+    if way == 2:
+        allidx = np.array([(a, b) for a in range(m_local) for b in range(a + 1, m_local)])
+        f = oracle.pairs
+    else:
+        allidx = np.array([(a, b, c) for a in range(m_local) for b in range(a + 1, m_local)
+                           for c in range(b + 1, m_local)])
+        f = oracle.triples
+    S = oracle.allele_sums(sub)
+    # calibrate, then run a sample sized for ~target_s seconds
+    m = 64
+    while True:
+        t0 = time.perf_counter()
+        f(sub, allidx[:m], S=S)
+        dt = time.perf_counter() - t0
+        if dt > 0.5 or m >= len(allidx):
+            break
+        m = min(len(allidx), m * 4)
+    m_run = int(min(len(allidx), max(m, m * target_s / max(dt, 1e-6))))
+    t0 = time.perf_counter()
+    f(sub, allidx[:m_run], S=S)
+    dt = time.perf_counter() - t0
+    what = "pairs" if way == 2 else "triples"
+    return {"value": m_run * n_f / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{m_run} {what} (n_f={n_f}) among {m_local} sampled vectors of the "
+                      f"workload, brute-force Fig.1/Fig.2 enumeration, {dt:.1f} s"}
+
+
+# ------------------------------------------------------------------------ ours, 1 GPU
+def run_2way_single(args, wl):
+    import torch
+
+    import synthgen
+    from paper_1705_08213_b200 import ccc
+    n_v, n_f = wl["n_v"], wl["n_f"]
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    flags = ccc.OUT_TALLY | ccc.OUT_CCC_F64
+    codes = synthgen.random_codes(n_v, n_f, seed=1, device=dev)        # resident in HBM
+    packed = torch.empty((n_v, ccc.ccc_packed_stride(n_f)), dtype=torch.uint8, device=dev)
+    N = torch.empty((n_v, ccc.ccc_k_pad(n_f)), dtype=torch.int8, device=dev)
+    s = torch.empty(n_v, dtype=torch.int32, device=dev)
+    w = torch.empty((n_v, 2), dtype=torch.float64, device=dev)
+    m = ccc.ccc_num_unique(2, n_v)
+    T = torch.empty((m, 4), dtype=torch.int32, device=dev)
+    C = torch.empty((m, 4), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+    launches = [0]
+
+    def step(ev=None):
+        ccc.ccc_pack(codes, packed)
+        launches[0] += ccc.ccc_last_launch_count()
+        ccc.ccc_expand(packed, n_f, ccc.GAMMA, N, s, w)
+        launches[0] += ccc.ccc_last_launch_count()
+        if ev:
+            ev[0].record(stream)
+        ccc.ccc_2way_block(N, s, w, 0, 0, n_v, N, s, w, 0, True, n_f, flags, T, C)
+        launches[0] += ccc.ccc_last_launch_count()
+        if ev:
+            ev[1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches[0] = 0
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for k in range(args.steps):
+            step(kev[k])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    k_ms = sum(a.elapsed_time(b) for a, b in kev) / args.steps
+    comps = comparisons(2, n_v, n_f)
+    res = {
+        "ms": ms, "kernel_ms": k_ms, "comparisons": comps, "launches": launches[0],
+        "clocks": clk.summary(), "kernel": "tally2_kernel",
+        "out_bytes": m * 48,
+    }
+    del T, C
+    torch.cuda.empty_cache()
+    if args.e2e:
+        res["e2e"] = run_2way_e2e(args, wl, codes)
+    return res
+
+
+def run_2way_e2e(args, wl, codes_dev):
+    """Same metric through the public host-buffer call (ccc_2way_host): every step copies
+    the step's genotype codes H2D from pinned memory and all tallies + CCC D2H."""
+    import torch
+
+    from paper_1705_08213_b200 import ccc
+    n_v, n_f = wl["n_v"], wl["n_f"]
+    flags = ccc.OUT_TALLY | ccc.OUT_CCC_F64
+    m = ccc.ccc_num_unique(2, n_v)
+    codes_h = codes_dev.cpu().pin_memory()
+    T_h = torch.empty((m, 4), dtype=torch.int32, pin_memory=True)
+    C_h = torch.empty((m, 4), dtype=torch.float64, pin_memory=True)
+    ws = torch.empty(ccc.ccc_e2e_workspace_bytes(n_v, n_f, flags), dtype=torch.uint8,
+                     device="cuda")
+    steps = max(1, min(args.steps, 3))
+    ccc.ccc_2way_host(codes_h, ccc.GAMMA, flags, T_h, C_h, None, ws)   # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        ccc.ccc_2way_host(codes_h, ccc.GAMMA, flags, T_h, C_h, None, ws)
+    dt = (time.perf_counter() - t0) / steps
+    return {"value": comparisons(2, n_v, n_f) / dt, "unit": UNIT,
+            "h2d_bytes_per_step": n_v * n_f, "d2h_bytes_per_step": m * 48,
+            "steps": steps, "ms_per_step": dt * 1e3,
+            "api": "ccc_2way_host (pinned host codes in, pinned host tallies+fp64 CCC out)"}
+
+
+def run_3way_single(args, wl):
+    import torch
+
+    import synthgen
+    from paper_1705_08213_b200 import ccc
+    n_v, n_f, n_st = wl["n_v"], wl["n_f"], wl["n_st"]
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    flags = ccc.OUT_TALLY | ccc.OUT_CCC_F64
+    codes = synthgen.random_codes(n_v, n_f, seed=1, device=dev)
+    packed = torch.empty((n_v, ccc.ccc_packed_stride(n_f)), dtype=torch.uint8, device=dev)
+    ws = ccc.workspace(3, n_v, n_f, dev)
+    rmax = max(ccc.ccc_stage_range(n_v, n_st, s)[3] for s in range(n_st))
+    T = torch.empty((rmax, 8), dtype=torch.int32, device=dev)
+    C = torch.empty((rmax, 8), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+    launches = [0]
+
+    def step(ev=None):
+        ccc.ccc_pack(codes, packed)
+        launches[0] += ccc.ccc_last_launch_count()
+        ccc.ccc_3way_prepare(packed, n_f, ccc.GAMMA, ws)
+        launches[0] += ccc.ccc_last_launch_count()
+        for st in range(n_st):
+            if ev:
+                ev[st][0].record(stream)
+            ccc.ccc_3way_stage(n_v, n_f, n_st, st, ws, flags, T, C)
+            launches[0] += ccc.ccc_last_launch_count()
+            if ev:
+                ev[st][1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches[0] = 0
+    kev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in range(n_st)] for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for k in range(args.steps):
+            step(kev[k])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    k_ms = sum(a.elapsed_time(b) for st in kev for a, b in st) / (args.steps * n_st)
+    return {"ms": ms, "kernel_ms": k_ms, "comparisons": comparisons(3, n_v, n_f),
+            "launches": launches[0], "clocks": clk.summary(), "kernel": "tally3_kernel",
+            "out_bytes": comparisons(3, n_v, n_f) // n_f * 96, "stages": n_st}
+
+
+# ------------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--no-cpu", dest="cpu", action="store_false")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    wl = dict(WORKLOADS[args.workload])
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        # The reference arm is the CPU oracle (no runnable reference implementation
+        # exists for this paper): a bounded sample of the same workload per step.
+        vals = []
+        for _ in range(args.warmup + args.steps):
+            vals.append(cpu_baseline(wl["way"], wl["n_v"], wl["n_f"], target_s=4.0))
+        vals = vals[args.warmup:]
+        v = sorted(x["value"] for x in vals)[len(vals) // 2]
+        cb = dict(vals[0])
+        cb["value"] = v
+        out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
+               "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+               "dtype": "int64", "data": "synthetic",
+               "config": {"workload": wl["label"], "n_v": wl["n_v"], "n_f": wl["n_f"]},
+               "cpu_baseline": cb,
+               "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
+                       "d2h_bytes_per_step": 0}}
+        print(json.dumps(out))
+        return
+
+    if world > 1 or args.gpus > 1:
+        from paper_1705_08213_b200 import dist
+        return dist.bench_main(args, wl, METRIC, UNIT)
+
+    pk, pk_kind = peaks()
+    if wl["way"] == 2:
+        r = run_2way_single(args, wl)
+    else:
+        r = run_3way_single(args, wl)
+    ms_step = r["ms"] / args.steps
+    value = r["comparisons"] / (ms_step / 1e3)
+    # roofline of the dominant kernel (the fused tally GEMM): 2 int8 ops per comparison
+    k_s = r["kernel_ms"] / 1e3
+    if wl["way"] == 2:
+        ops = 2.0 * r["comparisons"]
+    else:
+        ops = 2.0 * r["comparisons"] / wl["n_st"]
+    int8_peak = 2.0 * pk["bf16_tflops_sustained"]   # int8 dense = 2 x bf16 dense (nominal ratio)
+    achieved = ops / k_s / 1e12
+    roof = {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s",
+            "frac": achieved / int8_peak, "traffic": ncu_traffic(r["kernel"]),
+            "kernel": r["kernel"], "kernel_ms": r["kernel_ms"],
+            "peak_source": f"2 x bf16_tflops_sustained of MEASURED_PEAKS.json ({pk_kind}); "
+                           "int8 ops = 2 per MAC = 2 per comparison",
+            "nominal_int8_frac": achieved / 4500.0}
+    hbm_write = r["out_bytes"] / (ms_step / 1e3) / 1e9
+    roof["out_write_GBps"] = hbm_write
+    roof["out_write_frac_of_hbm"] = hbm_write / pk["hbm_gbs"]
+    if wl["way"] == 3:
+        roof["bound"] = "hbm"
+        roof["achieved"] = r["out_bytes"] / wl["n_st"] / k_s / 1e9
+        roof["peak"] = pk["hbm_gbs"]
+        roof["unit"] = "GB/s"
+        roof["frac"] = roof["achieved"] / pk["hbm_gbs"]
+        roof["peak_source"] = f"hbm_gbs of MEASURED_PEAKS.json ({pk_kind}); FULL output 96 B/triple"
+        roof["tensor_TOPS"] = achieved
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int8",
+        "data": "synthetic",
+        "config": {"workload": wl["label"], "n_v": wl["n_v"], "n_f": wl["n_f"],
+                   "input": "type-1 uniform random 2-bit codes, seed 1 (P:657)",
+                   "output": "FULL: uint32 tallies + fp64 CCC for every unique record",
+                   "l2": "inputs larger than L2 (codes %.2f GB, N %.2f GB)" % (
+                       wl["n_v"] * wl["n_f"] / 1e9, wl["n_v"] * wl["n_f"] / 1e9),
+                   "parallelism": "single GPU"},
+        "roofline": roof,
+        "gpu_launches": r["launches"],
+        "clocks": r["clocks"],
+    }
+    if "e2e" in r:
+        out["e2e"] = r["e2e"]
+    if args.cpu:
+        out["cpu_baseline"] = cpu_baseline(wl["way"], wl["n_v"], wl["n_f"])
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

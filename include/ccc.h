@@ -1,0 +1,212 @@
+/*
+ * ccc.h -- C ABI of libccc, the B200 (sm_100a) CCC tally engine.
+ *
+ * Implements the hot path of PAPER.md (arXiv 1705.08213, "Parallel Accelerated
+ * Custom Correlation Coefficient Calculations for Genomics Applications"): for n_v
+ * vectors of n_f 2-bit genotype entries, the 2x2 (2-way) / 2x2x2 (3-way) allele
+ * co-occurrence tallies of every unique pair i<j / triple i<j<k and the CCC values
+ * formed from them and the per-vector allele frequencies.
+ *
+ *   v_{i,q} = (r1, r2) in S_2                                  P:259-264 (§2.1)
+ *   rho_{i,q}(a) = #{r in v_{i,q} : r = a}
+ *   f_i(a)   = (1/2n_f) sum_q rho_{i,q}(a)                       Eq.1
+ *   f_ij(a,b) = (1/4n_f) sum_q rho_{i,q}(a) rho_{j,q}(b)         Eq.2
+ *   CCC_ij(a,b) = f_ij(a,b)(1 - g f_i(a))(1 - g f_j(b)), g=2/3   Eq.3
+ *   f_ijk(a,b,c) = (1/8n_f) sum_q rho_i(a) rho_j(b) rho_k(c)     Eq.5
+ *   CCC_ijk = f_ijk (1-g f_i(a))(1-g f_j(b))(1-g f_k(c))          Eq.4
+ *   unique results: distinct i<j, i<j<k
+ *
+ * CONVENTIONS (all functions)
+ *  - Element code: one byte code = 2*r1 + r2 in {0,1,2,3}; (1,0) and (0,1) are the
+ *    same heterozygote in dense mode.  Indices are 0-based.
+ *  - Tally cell order is a-major: [T00,T01,T10,T11] and [T000 ... T111] with slot
+ *    order (i,j,k) as in Eq.5.  Tallies are integer counts (sum = 4n_f / 8n_f);
+ *    f = T/(4n_f) or T/(8n_f).  CCC is computed in fp64 (or emitted as fp32).
+ *  - Records are emitted in lexicographic order of (i,j) / (i,j,k); see
+ *    ccc_pair_index / ccc_triple_index.
+ *  - Pointers named *_d are DEVICE pointers (CUDA global memory of the current
+ *    device), *_h HOST pointers.  The caller owns every buffer; the library never
+ *    allocates, frees or retains caller memory.  Scratch comes from a caller
+ *    workspace sized by ccc_workspace_bytes.  No hidden global state besides a
+ *    thread-local error string and a per-process device-property cache.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Device functions only enqueue work: they are asynchronous on `stream`;
+ *    execution faults surface at the caller's next synchronisation.
+ *  - Arguments are validated synchronously before any launch.  Invalid sizes or
+ *    NULL / misaligned (16 B) required pointers -> CCC_ERR_INVALID_ARGUMENT; a
+ *    device that is not sm_100 -> CCC_ERR_UNSUPPORTED; n_f > CCC_MAX_NF (int32
+ *    accumulator bound 8 n_f < 2^31) -> CCC_ERR_UNSUPPORTED; a launch failure ->
+ *    CCC_ERR_CUDA with detail in ccc_last_error().  n_v < num_way is not an error:
+ *    the result is empty and nothing is launched.
+ *  - Re-entrant; calls on different streams / devices may run concurrently.
+ */
+#ifndef CCC_H_
+#define CCC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CCC_OK = 0,
+    CCC_ERR_INVALID_ARGUMENT = 1,
+    CCC_ERR_UNSUPPORTED = 2,
+    CCC_ERR_CUDA = 3,
+    CCC_ERR_WORKSPACE = 4
+} ccc_status;
+
+/* Output selection bits (out_flags). */
+enum {
+    CCC_OUT_TALLY = 1,     /* uint32 tallies [records][4 or 8]                         */
+    CCC_OUT_CCC_F64 = 2,   /* double CCC     [records][4 or 8]                         */
+    CCC_OUT_CCC_F32 = 4,   /* float  CCC     [records][4 or 8] (exclusive with F64)    */
+    CCC_OUT_CHECKSUM = 8   /* add every record's 128-bit digest into checksum_d[2]      */
+};
+
+#define CCC_MAX_NF 268435455LL   /* 8 * n_f must fit an int32 TMEM accumulator      */
+#define CCC_MAX_NV 1048575LL     /* 20-bit index fields of the checksum digest       */
+
+/* ---------------------------------------------------------------- host helpers */
+
+/* Library / ABI version (major*10000 + minor*100 + patch). */
+int ccc_version(void);
+
+/* Human-readable name of a status code (static storage). */
+const char* ccc_status_string(int status);
+
+/* Detail of the last error raised on the calling thread ("" if none). */
+const char* ccc_last_error(void);
+
+/* Number of unique results: C(n_v,2) for num_way=2, C(n_v,3) for num_way=3
+ * (P:293-295); 0 when n_v < num_way; -1 for an invalid num_way. */
+int64_t ccc_num_unique(int num_way, int64_t n_v);
+
+/* Lexicographic record index of pair i<j: i(2n_v-i-1)/2 + (j-i-1); -1 if not
+ * 0 <= i < j < n_v. */
+int64_t ccc_pair_index(int64_t n_v, int64_t i, int64_t j);
+
+/* Lexicographic record index of triple i<j<k:
+ * C(n_v,3) - C(n_v-i,3) + C(n_v-i-1,2) - C(n_v-j,2) + (k-j-1); -1 if invalid. */
+int64_t ccc_triple_index(int64_t n_v, int64_t i, int64_t j, int64_t k);
+
+/* Byte stride of one packed vector: ceil(n_f/64)*16 (64 entries per 16 bytes, the
+ * density of the paper's double-complex packing unit). */
+int64_t ccc_packed_stride(int64_t n_f);
+
+/* Byte stride of one row of the expanded allele-count matrix N: ceil(n_f/128)*128. */
+int64_t ccc_k_pad(int64_t n_f);
+
+/* 3-way stages: stage s of n_stages covers pivots i in [i_begin,i_end)
+ * (first index of the triple), i.e. the contiguous record range
+ * [rec_begin, rec_begin+rec_count) of the lexicographic triple array.  Boundaries
+ * balance the record count.  out[4] = {i_begin, i_end, rec_begin, rec_count}. */
+ccc_status ccc_stage_range(int64_t n_v, int64_t n_stages, int64_t stage, int64_t* out);
+
+/* Device workspace bytes needed by ccc_2way (num_way=2) or ccc_3way_prepare /
+ * ccc_3way_stage / ccc_3way (num_way=3) for this problem size. */
+size_t ccc_workspace_bytes(int num_way, int64_t n_v, int64_t n_f);
+
+/* ---------------------------------------------------------------- device path */
+
+/* KB-pack (§8(a) a1; P:403-410 packing): codes_d uint8 [n_v][n_f] (row-major, one
+ * code per byte, values 0..3; higher bits are ignored) -> packed_d uint8
+ * [n_v][ccc_packed_stride(n_f)], element q of vector i in bits 2(q%4)..2(q%4)+1 of
+ * byte q/4 of its row (LSB first); the tail of each row is zero. */
+ccc_status ccc_pack(const uint8_t* codes_d, int64_t n_v, int64_t n_f, uint8_t* packed_d,
+                    void* stream);
+
+/* KB-expand (§8(a) a2; Eq.1): packed_d -> N_d int8 [n_v][ccc_k_pad(n_f)] with
+ * N[i][q] = rho_{i,q}(1) in {0,1,2} (0 for q >= n_f), s_d int32 [n_v] with
+ * s_i = sum_q rho_{i,q}(1) = S_i(1), and w_d double [n_v][2] with
+ * w_i(a) = 1 - gamma * f_i(a), f_i(1) = s_i/(2n_f), f_i(0) = (2n_f - s_i)/(2n_f).
+ * N_d must be 128-B aligned. */
+ccc_status ccc_expand(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
+                      int8_t* N_d, int32_t* s_d, double* w_d, void* stream);
+
+/* Whole 2-way problem on one GPU (§8(a) a2-a4): expand packed_d into the workspace,
+ * then the persistent tcgen05 kind::i8 tally GEMM G = N N^T over the upper
+ * triangle with the fused epilogue
+ *   T11 = G, T10 = 2s_i - G, T01 = 2s_j - G, T00 = 4n_f - 2s_i - 2s_j + G,
+ *   CCC(a,b) = T(a,b) / (4n_f) * w_i(a) * w_j(b)                   (Eq.2-3)
+ * writing record p = ccc_pair_index(n_v,i,j) for every i<j:
+ *   tallies_d uint32 [C(n_v,2)][4]   (if out_flags & CCC_OUT_TALLY)
+ *   ccc_d     double/float [C(n_v,2)][4] (CCC_OUT_CCC_F64 / _F32)
+ *   checksum_d uint64 [2] (lo, hi) += sum of record digests (CCC_OUT_CHECKSUM; the
+ *              caller zeroes it first).
+ * Outputs not selected may be NULL.  ws_d: >= ccc_workspace_bytes(2,...) bytes,
+ * 256-B aligned. */
+ccc_status ccc_2way(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
+                    uint32_t out_flags, uint32_t* tallies_d, void* ccc_d, uint64_t* checksum_d,
+                    void* ws_d, size_t ws_bytes, void* stream);
+
+/* One block of the block-circulant 2-way decomposition (§4; §8(e)):
+ * rows [a_lo, a_hi) of block A (expanded N_a / s_a / w_a, n_a rows, global index of
+ * its row 0 = a_row0) against all n_b rows of block B (global row0 b_row0).
+ *  diag != 0: A and B are the same block (pass the same pointers); only local pairs
+ *             i<j are produced, record index = ccc_pair_index(n_b, i, j) - offset
+ *             where offset = ccc_pair_index-origin of row a_lo (records of rows
+ *             < a_lo are skipped, so row a_lo starts at record 0);
+ *  diag == 0: every (i,j), record index (i - a_lo) * n_b + j; the caller passes
+ *             the block with the lower global indices as A so that records are
+ *             canonical (i < j globally).
+ * Output buffers / flags as in ccc_2way.  N_a, N_b: [rows][ccc_k_pad(n_f)], 128-B
+ * aligned.  If g_d != NULL the raw int32 G_ij = sum_q n_iq n_jq of every computed
+ * tile is also stored at g_d[i*ldg + j] (local indices; used by the 3-way path). */
+ccc_status ccc_2way_block(const int8_t* N_a, const int32_t* s_a, const double* w_a,
+                          int64_t n_a, int64_t a_row0, int64_t a_lo, int64_t a_hi,
+                          const int8_t* N_b, const int32_t* s_b, const double* w_b,
+                          int64_t n_b, int64_t b_row0, int diag, int64_t n_f,
+                          uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
+                          uint64_t* checksum_d, int32_t* g_d, int64_t ldg, void* stream);
+
+/* 3-way preparation (§8(a) a2, a5 prerequisites): expand packed_d into the workspace
+ * and compute the pairwise G = N N^T (upper triangle) that the 3-way epilogue needs. */
+ccc_status ccc_3way_prepare(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
+                            void* ws_d, size_t ws_bytes, void* stream);
+
+/* One 3-way stage (§8(a) a5-a6, a8; stages P:621-626) on a workspace prepared by
+ * ccc_3way_prepare: for every pivot i of the stage (ccc_stage_range) the
+ * Hadamard-weighted GEMM G3 = (N_{>i} o n_i) N_{>i}^T on tcgen05, then the fused
+ * epilogue
+ *   T111 = G3, T110 = 2G_ij - G3, T101 = 2G_ik - G3, T011 = 2G_jk - G3,
+ *   T100 = 4s_i - 2G_ij - 2G_ik + G3, T010 = 4s_j - 2G_ij - 2G_jk + G3,
+ *   T001 = 4s_k - 2G_ik - 2G_jk + G3,
+ *   T000 = 8n_f - 4(s_i+s_j+s_k) + 2(G_ij+G_ik+G_jk) - G3,
+ *   CCC(a,b,c) = T/(8n_f) * w_i(a) w_j(b) w_k(c)                 (Eq.4-5)
+ * writing record t = ccc_triple_index(n_v,i,j,k) - rec_begin of every triple of the
+ * stage: tallies_d uint32 [rec_count][8], ccc_d double/float [rec_count][8],
+ * checksum_d as in ccc_2way. */
+ccc_status ccc_3way_stage(int64_t n_v, int64_t n_f, int64_t n_stages, int64_t stage,
+                          uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
+                          uint64_t* checksum_d, void* ws_d, size_t ws_bytes, void* stream);
+
+/* ccc_3way_prepare followed by ccc_3way_stage(n_stages, stage). */
+ccc_status ccc_3way(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
+                    uint32_t out_flags, int64_t n_stages, int64_t stage, uint32_t* tallies_d,
+                    void* ccc_d, uint64_t* checksum_d, void* ws_d, size_t ws_bytes,
+                    void* stream);
+
+/* End-to-end 2-way with HOST buffers (the e2e measurement of bench.py): copies
+ * codes_h (uint8 [n_v][n_f], pinned for full speed) to the device, packs, runs
+ * ccc_2way, and copies the selected outputs back to tallies_h / ccc_h / checksum_h
+ * (host, [C(n_v,2)][4] each, pinned for full speed).  Row bands of the output are
+ * copied back while the next band computes.  Device scratch: dev_ws_d of at least
+ * ccc_e2e_workspace_bytes(n_v, n_f, out_flags) bytes.  Synchronises `stream`
+ * before returning. */
+size_t ccc_e2e_workspace_bytes(int64_t n_v, int64_t n_f, uint32_t out_flags);
+ccc_status ccc_2way_host(const uint8_t* codes_h, int64_t n_v, int64_t n_f, double gamma,
+                         uint32_t out_flags, uint32_t* tallies_h, void* ccc_h,
+                         uint64_t* checksum_h, void* dev_ws_d, size_t dev_ws_bytes,
+                         void* stream);
+
+/* Number of kernels the last successful call on this thread enqueued (for the
+ * bench's gpu_launches count). */
+int64_t ccc_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CCC_H_ */

@@ -364,9 +364,40 @@ def record_digest(way: int, idx, tallies) -> int:
     return (fmix64(h ^ CK_HI) << 64) | h
 
 
-def checksum(way: int, idx, T) -> int:
-    """Sum of record digests mod 2^128: independent of record order and partition."""
+def checksum_scalar(way: int, idx, T) -> int:
+    """Sum of record digests mod 2^128 (record by record, Python integers)."""
     acc = 0
     for r in range(len(idx)):
         acc = (acc + record_digest(way, idx[r], T[r])) & ((1 << 128) - 1)
     return acc
+
+
+def _fmix64_np(k):
+    k = k ^ (k >> np.uint64(33))
+    k = k * np.uint64(0xFF51AFD7ED558CCD)
+    k = k ^ (k >> np.uint64(33))
+    k = k * np.uint64(0xC4CEB9FE1A85EC53)
+    return k ^ (k >> np.uint64(33))
+
+
+def checksum(way: int, idx, T) -> int:
+    """Same value as checksum_scalar, evaluated with numpy uint64 (wrap-around) arrays."""
+    if len(T) == 0:
+        return 0
+    idx = np.asarray(idx, dtype=np.int64).reshape(len(T), -1).astype(np.uint64)
+    T = np.asarray(T, dtype=np.int64).astype(np.uint64) & np.uint64(0xFFFFFFFF)
+    k = idx[:, 2] if way == 3 else np.zeros(len(T), np.uint64)
+    lane0 = ((np.uint64(way) << np.uint64(60)) | (idx[:, 0] << np.uint64(40))
+             | (idx[:, 1] << np.uint64(20)) | k)
+    with np.errstate(over="ignore"):
+        h = _fmix64_np(np.uint64(CK_SEED) ^ lane0)
+        for p in range(0, T.shape[1], 2):
+            h = _fmix64_np(h ^ (T[:, p] | (T[:, p + 1] << np.uint64(32))))
+        hi = _fmix64_np(h ^ np.uint64(CK_HI))
+    m32 = np.uint64(0xFFFFFFFF)
+    total = 0
+    for part, shift in ((h, 0), (hi, 64)):
+        lo32 = int((part & m32).sum(dtype=np.uint64))
+        hi32 = int((part >> np.uint64(32)).sum(dtype=np.uint64))
+        total += (lo32 + (hi32 << 32)) << shift
+    return total & ((1 << 128) - 1)

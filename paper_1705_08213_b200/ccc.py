@@ -1,0 +1,311 @@
+"""ctypes binding of libccc (include/ccc.h): the same names as the C ABI, argument
+marshalling only.  Every step of the hot path runs in the CUDA kernels of libccc.so;
+there is no CPU fallback -- if the library is missing or the device is not sm_100a,
+calls raise.
+
+Tensors are torch tensors used purely as device memory; launches go on torch's
+current CUDA stream unless `stream` is given.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import torch
+
+from . import build as _build
+
+OK, ERR_INVALID_ARGUMENT, ERR_UNSUPPORTED, ERR_CUDA, ERR_WORKSPACE = 0, 1, 2, 3, 4
+OUT_TALLY, OUT_CCC_F64, OUT_CCC_F32, OUT_CHECKSUM = 1, 2, 4, 8
+GAMMA = 2.0 / 3.0
+HEADER = os.path.join(_build.ROOT, "include", "ccc.h")
+
+
+class CCCError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(msg)
+        self.status = status
+
+
+_lib = None
+_vp, _i64, _u32, _dbl, _int, _sz = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32,
+                                    ctypes.c_double, ctypes.c_int, ctypes.c_size_t)
+_SIGS = {
+    "ccc_version": (_int, []),
+    "ccc_status_string": (ctypes.c_char_p, [_int]),
+    "ccc_last_error": (ctypes.c_char_p, []),
+    "ccc_last_launch_count": (_i64, []),
+    "ccc_num_unique": (_i64, [_int, _i64]),
+    "ccc_pair_index": (_i64, [_i64, _i64, _i64]),
+    "ccc_triple_index": (_i64, [_i64, _i64, _i64, _i64]),
+    "ccc_packed_stride": (_i64, [_i64]),
+    "ccc_k_pad": (_i64, [_i64]),
+    "ccc_stage_range": (_int, [_i64, _i64, _i64, _vp]),
+    "ccc_workspace_bytes": (_sz, [_int, _i64, _i64]),
+    "ccc_pack": (_int, [_vp, _i64, _i64, _vp, _vp]),
+    "ccc_expand": (_int, [_vp, _i64, _i64, _dbl, _vp, _vp, _vp, _vp]),
+    "ccc_2way": (_int, [_vp, _i64, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "ccc_2way_block": (_int, [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _i64, _i64,
+                              _int, _i64, _u32, _vp, _vp, _vp, _vp, _i64, _vp]),
+    "ccc_3way_prepare": (_int, [_vp, _i64, _i64, _dbl, _vp, _sz, _vp]),
+    "ccc_3way_stage": (_int, [_i64, _i64, _i64, _i64, _u32, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "ccc_3way": (_int, [_vp, _i64, _i64, _dbl, _u32, _i64, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "ccc_e2e_workspace_bytes": (_sz, [_i64, _i64, _u32]),
+    "ccc_2way_host": (_int, [_vp, _i64, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _sz, _vp]),
+}
+
+
+def header_symbols() -> list[str]:
+    """Every function the public header declares."""
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(ccc_[a-z0-9_]+)\s*\(", txt)))
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def lib():
+    """Load libccc.so (built in-tree by __graft_entry__.build()); raise if absent."""
+    global _lib
+    if _lib is None:
+        path = _build.LIB
+        if not os.path.exists(path):
+            raise ImportError(f"libccc.so not built at {path}: run __graft_entry__.build() "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(path)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != OK:
+        msg = lib().ccc_last_error().decode()
+        name = lib().ccc_status_string(status).decode()
+        if status == ERR_INVALID_ARGUMENT:
+            raise ValueError(f"{name}: {msg}")
+        raise CCCError(status, f"{name}: {msg}")
+
+
+def _p(t):
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, torch.cuda.Stream):
+        return ctypes.c_void_p(stream.cuda_stream)
+    return ctypes.c_void_p(stream)
+
+
+def _dev(t, dtype, name):
+    if t is None:
+        return
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+# ----------------------------------------------------------------------- host helpers
+def ccc_version() -> int:
+    return lib().ccc_version()
+
+
+def ccc_last_launch_count() -> int:
+    return lib().ccc_last_launch_count()
+
+
+def ccc_num_unique(num_way: int, n_v: int) -> int:
+    return lib().ccc_num_unique(num_way, n_v)
+
+
+def ccc_pair_index(n_v: int, i: int, j: int) -> int:
+    return lib().ccc_pair_index(n_v, i, j)
+
+
+def ccc_triple_index(n_v: int, i: int, j: int, k: int) -> int:
+    return lib().ccc_triple_index(n_v, i, j, k)
+
+
+def ccc_packed_stride(n_f: int) -> int:
+    return lib().ccc_packed_stride(n_f)
+
+
+def ccc_k_pad(n_f: int) -> int:
+    return lib().ccc_k_pad(n_f)
+
+
+def ccc_stage_range(n_v: int, n_stages: int, stage: int):
+    out = (ctypes.c_int64 * 4)()
+    _check(lib().ccc_stage_range(n_v, n_stages, stage, ctypes.cast(out, ctypes.c_void_p)))
+    return tuple(int(x) for x in out)
+
+
+def ccc_workspace_bytes(num_way: int, n_v: int, n_f: int) -> int:
+    return lib().ccc_workspace_bytes(num_way, n_v, n_f)
+
+
+def ccc_e2e_workspace_bytes(n_v: int, n_f: int, out_flags: int) -> int:
+    return lib().ccc_e2e_workspace_bytes(n_v, n_f, out_flags)
+
+
+def workspace(num_way: int, n_v: int, n_f: int, device=None) -> torch.Tensor:
+    n = max(ccc_workspace_bytes(num_way, n_v, n_f), 256)
+    return torch.empty(n, dtype=torch.uint8, device=device or "cuda")
+
+
+# ----------------------------------------------------------------------- device path
+def ccc_pack(codes: torch.Tensor, packed: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    _dev(codes, torch.uint8, "codes")
+    n_v, n_f = codes.shape
+    if packed is None:
+        packed = torch.empty((n_v, ccc_packed_stride(n_f)), dtype=torch.uint8, device=codes.device)
+    _dev(packed, torch.uint8, "packed")
+    _check(lib().ccc_pack(_p(codes), n_v, n_f, _p(packed), _stream(stream)))
+    return packed
+
+
+def ccc_expand(packed: torch.Tensor, n_f: int, gamma: float = GAMMA, N=None, s=None, w=None,
+               stream=None):
+    _dev(packed, torch.uint8, "packed")
+    n_v = packed.shape[0]
+    dev = packed.device
+    if N is None:
+        N = torch.empty((n_v, ccc_k_pad(n_f)), dtype=torch.int8, device=dev)
+    if s is None:
+        s = torch.empty(n_v, dtype=torch.int32, device=dev)
+    if w is None:
+        w = torch.empty((n_v, 2), dtype=torch.float64, device=dev)
+    _dev(N, torch.int8, "N"), _dev(s, torch.int32, "s"), _dev(w, torch.float64, "w")
+    _check(lib().ccc_expand(_p(packed), n_v, n_f, gamma, _p(N), _p(s), _p(w), _stream(stream)))
+    return N, s, w
+
+
+def _outputs(n_rec: int, width: int, out_flags: int, device, tallies=None, ccc=None,
+             checksum=None):
+    if out_flags & OUT_TALLY and tallies is None:
+        tallies = torch.empty((n_rec, width), dtype=torch.int32, device=device)
+    if out_flags & OUT_CCC_F64 and ccc is None:
+        ccc = torch.empty((n_rec, width), dtype=torch.float64, device=device)
+    if out_flags & OUT_CCC_F32 and ccc is None:
+        ccc = torch.empty((n_rec, width), dtype=torch.float32, device=device)
+    if out_flags & OUT_CHECKSUM and checksum is None:
+        checksum = torch.zeros(2, dtype=torch.int64, device=device)
+    return tallies, ccc, checksum
+
+
+def ccc_2way(packed: torch.Tensor, n_f: int, gamma: float = GAMMA,
+             out_flags: int = OUT_TALLY | OUT_CCC_F64, tallies=None, ccc=None, checksum=None,
+             ws=None, stream=None):
+    """Tallies (uint32 bit patterns in an int32 tensor) [C(n_v,2)][4], CCC, checksum[2]."""
+    _dev(packed, torch.uint8, "packed")
+    n_v = packed.shape[0]
+    tallies, ccc, checksum = _outputs(ccc_num_unique(2, n_v), 4, out_flags, packed.device,
+                                      tallies, ccc, checksum)
+    if ws is None:
+        ws = workspace(2, n_v, n_f, packed.device)
+    _check(lib().ccc_2way(_p(packed), n_v, n_f, gamma, out_flags, _p(tallies), _p(ccc),
+                          _p(checksum), _p(ws), ws.numel(), _stream(stream)))
+    return tallies, ccc, checksum
+
+
+def ccc_2way_block(N_a, s_a, w_a, a_row0, a_lo, a_hi, N_b, s_b, w_b, b_row0, diag: bool, n_f,
+                   out_flags, tallies=None, ccc=None, checksum=None, g=None, ldg=0,
+                   stream=None):
+    n_a, n_b = N_a.shape[0], N_b.shape[0]
+    for t, n in ((N_a, "N_a"), (N_b, "N_b")):
+        _dev(t, torch.int8, n)
+    _check(lib().ccc_2way_block(_p(N_a), _p(s_a), _p(w_a), n_a, a_row0, a_lo, a_hi, _p(N_b),
+                                _p(s_b), _p(w_b), n_b, b_row0, int(bool(diag)), n_f, out_flags,
+                                _p(tallies), _p(ccc), _p(checksum), _p(g), ldg, _stream(stream)))
+    return tallies, ccc, checksum
+
+
+def ccc_3way_prepare(packed, n_f, gamma=GAMMA, ws=None, stream=None):
+    _dev(packed, torch.uint8, "packed")
+    n_v = packed.shape[0]
+    if ws is None:
+        ws = workspace(3, n_v, n_f, packed.device)
+    _check(lib().ccc_3way_prepare(_p(packed), n_v, n_f, gamma, _p(ws), ws.numel(),
+                                  _stream(stream)))
+    return ws
+
+
+def ccc_3way_stage(n_v, n_f, n_stages, stage, ws, out_flags=OUT_TALLY | OUT_CCC_F64,
+                   tallies=None, ccc=None, checksum=None, stream=None):
+    _, _, _, rec_count = ccc_stage_range(n_v, n_stages, stage)
+    tallies, ccc, checksum = _outputs(rec_count, 8, out_flags, ws.device, tallies, ccc, checksum)
+    _check(lib().ccc_3way_stage(n_v, n_f, n_stages, stage, out_flags, _p(tallies), _p(ccc),
+                                _p(checksum), _p(ws), ws.numel(), _stream(stream)))
+    return tallies, ccc, checksum
+
+
+def ccc_3way(packed, n_f, gamma=GAMMA, out_flags=OUT_TALLY | OUT_CCC_F64, n_stages=1, stage=0,
+             tallies=None, ccc=None, checksum=None, ws=None, stream=None):
+    _dev(packed, torch.uint8, "packed")
+    n_v = packed.shape[0]
+    _, _, _, rec_count = ccc_stage_range(n_v, n_stages, stage)
+    tallies, ccc, checksum = _outputs(rec_count, 8, out_flags, packed.device, tallies, ccc,
+                                      checksum)
+    if ws is None:
+        ws = workspace(3, n_v, n_f, packed.device)
+    _check(lib().ccc_3way(_p(packed), n_v, n_f, gamma, out_flags, n_stages, stage, _p(tallies),
+                          _p(ccc), _p(checksum), _p(ws), ws.numel(), _stream(stream)))
+    return tallies, ccc, checksum
+
+
+def ccc_2way_host(codes_h: torch.Tensor, gamma: float = GAMMA,
+                  out_flags: int = OUT_TALLY | OUT_CCC_F64, tallies_h=None, ccc_h=None,
+                  checksum_h=None, dev_ws=None, stream=None):
+    """End-to-end 2-way with host (pinned) buffers in and out."""
+    if codes_h.is_cuda or codes_h.dtype != torch.uint8 or not codes_h.is_contiguous():
+        raise ValueError("codes_h must be a contiguous host uint8 tensor")
+    n_v, n_f = codes_h.shape
+    m = ccc_num_unique(2, n_v)
+    pin = codes_h.is_pinned()
+    if out_flags & OUT_TALLY and tallies_h is None:
+        tallies_h = torch.empty((m, 4), dtype=torch.int32, pin_memory=pin)
+    if out_flags & OUT_CCC_F64 and ccc_h is None:
+        ccc_h = torch.empty((m, 4), dtype=torch.float64, pin_memory=pin)
+    if out_flags & OUT_CCC_F32 and ccc_h is None:
+        ccc_h = torch.empty((m, 4), dtype=torch.float32, pin_memory=pin)
+    if out_flags & OUT_CHECKSUM and checksum_h is None:
+        checksum_h = torch.zeros(2, dtype=torch.int64, pin_memory=pin)
+    if dev_ws is None:
+        dev_ws = torch.empty(ccc_e2e_workspace_bytes(n_v, n_f, out_flags), dtype=torch.uint8,
+                             device="cuda")
+    _check(lib().ccc_2way_host(_p(codes_h), n_v, n_f, gamma, out_flags, _p(tallies_h), _p(ccc_h),
+                               _p(checksum_h), _p(dev_ws), dev_ws.numel(), _stream(stream)))
+    return tallies_h, ccc_h, checksum_h
+
+
+# ----------------------------------------------------------------------- conveniences
+def checksum_int(ck: torch.Tensor) -> int:
+    """checksum tensor [2] (lo, hi as int64 bit patterns) -> Python int mod 2^128."""
+    lo, hi = (int(x) & ((1 << 64) - 1) for x in ck.cpu().tolist())
+    return (hi << 64) | lo
+
+
+def two_way(codes: torch.Tensor, gamma: float = GAMMA, out_flags: int = OUT_TALLY | OUT_CCC_F64,
+            stream=None):
+    """codes uint8 [n_v][n_f] on the GPU -> (tallies, ccc, checksum) for all i<j."""
+    packed = ccc_pack(codes, stream=stream)
+    return ccc_2way(packed, codes.shape[1], gamma, out_flags, stream=stream)
+
+
+def three_way(codes: torch.Tensor, gamma: float = GAMMA, out_flags: int = OUT_TALLY | OUT_CCC_F64,
+              n_stages: int = 1, stage: int = 0, stream=None):
+    packed = ccc_pack(codes, stream=stream)
+    return ccc_3way(packed, codes.shape[1], gamma, out_flags, n_stages, stage, stream=stream)

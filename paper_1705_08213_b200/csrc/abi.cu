@@ -1,0 +1,584 @@
+// abi.cu -- the extern "C" boundary of libccc (include/ccc.h): argument validation,
+// workspace layout, TMA descriptor construction and kernel launches.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "ccc.h"
+#include "internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+
+ccc_status fail(ccc_status st, const std::string& msg) {
+    g_err = msg;
+    return st;
+}
+
+ccc_status cuda_fail(cudaError_t e, const char* what) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return CCC_ERR_CUDA;
+}
+
+#define CCC_CUDA(call, what)                              \
+    do {                                                  \
+        cudaError_t e_ = (call);                          \
+        if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+    } while (0)
+
+#define CCC_CHECK(call)                      \
+    do {                                     \
+        ccc_status st_ = (call);             \
+        if (st_ != CCC_OK) return st_;       \
+    } while (0)
+
+bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+int64_t c2(int64_t n) { return n < 2 ? 0 : n * (n - 1) / 2; }
+int64_t c3(int64_t n) { return n < 3 ? 0 : n * (n - 1) * (n - 2) / 6; }
+int64_t kpad_of(int64_t n_f) { return (n_f + 127) / 128 * 128; }
+int64_t pstride_of(int64_t n_f) { return (n_f + 63) / 64 * 16; }
+
+struct DevInfo {
+    int sms = 0, major = 0, minor = 0;
+    bool valid = false;
+};
+std::mutex g_dev_mu;
+DevInfo g_dev[64];
+
+ccc_status check_device(int* num_sms) {
+    int dev = 0;
+    CCC_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+    if (dev < 0 || dev >= 64) return fail(CCC_ERR_UNSUPPORTED, "device ordinal out of range");
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    DevInfo& d = g_dev[dev];
+    if (!d.valid) {
+        CCC_CUDA(cudaDeviceGetAttribute(&d.major, cudaDevAttrComputeCapabilityMajor, dev),
+                 "cudaDeviceGetAttribute");
+        CCC_CUDA(cudaDeviceGetAttribute(&d.minor, cudaDevAttrComputeCapabilityMinor, dev),
+                 "cudaDeviceGetAttribute");
+        CCC_CUDA(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev),
+                 "cudaDeviceGetAttribute");
+        d.valid = true;
+    }
+    if (d.major != 10 || d.minor != 0) {
+        char buf[128];
+        snprintf(buf, sizeof buf, "device is sm_%d%d; libccc is built for sm_100a only", d.major,
+                 d.minor);
+        return fail(CCC_ERR_UNSUPPORTED, buf);
+    }
+    *num_sms = d.sms;
+    return CCC_OK;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+ccc_status get_encode(EncodeTiledFn* out) {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    static cudaError_t err = cudaSuccess;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        err = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+        if (err == cudaSuccess && q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    if (!fn) return fail(CCC_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    *out = fn;
+    return CCC_OK;
+}
+
+// 2-D uint8 tensor map over an expanded N block [rows][k_pad], box = 128 B x box_rows,
+// 128-byte swizzle (matches the UMMA SWIZZLE_128B K-major smem descriptor).
+ccc_status make_tmap(CUtensorMap* tm, const void* base, int64_t rows, int64_t k_pad,
+                     uint32_t box_rows) {
+    EncodeTiledFn enc;
+    CCC_CHECK(get_encode(&enc));
+    cuuint64_t dims[2] = {(cuuint64_t)k_pad, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)k_pad};
+    cuuint32_t box[2] = {(cuuint32_t)ccc::kBK, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        char buf[96];
+        snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
+        return fail(CCC_ERR_CUDA, buf);
+    }
+    return CCC_OK;
+}
+
+ccc_status check_sizes(int64_t n_v, int64_t n_f) {
+    if (n_v < 0) return fail(CCC_ERR_INVALID_ARGUMENT, "n_v must be >= 0");
+    if (n_f < 1) return fail(CCC_ERR_INVALID_ARGUMENT, "n_f must be >= 1");
+    if (n_f > CCC_MAX_NF) return fail(CCC_ERR_UNSUPPORTED, "n_f exceeds CCC_MAX_NF (8 n_f must fit int32)");
+    if (n_v > CCC_MAX_NV) return fail(CCC_ERR_UNSUPPORTED, "n_v exceeds CCC_MAX_NV");
+    return CCC_OK;
+}
+
+ccc_status check_outputs(uint32_t flags, const uint32_t* tallies, const void* ccc,
+                         const uint64_t* ck) {
+    if (flags & ~15u) return fail(CCC_ERR_INVALID_ARGUMENT, "unknown out_flags bits");
+    if ((flags & CCC_OUT_CCC_F64) && (flags & CCC_OUT_CCC_F32))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "CCC_OUT_CCC_F64 and CCC_OUT_CCC_F32 are exclusive");
+    if ((flags & CCC_OUT_TALLY) && (!tallies || !aligned(tallies, 16)))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "tallies must be a non-NULL 16-B aligned pointer");
+    if ((flags & (CCC_OUT_CCC_F64 | CCC_OUT_CCC_F32)) && (!ccc || !aligned(ccc, 16)))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "ccc must be a non-NULL 16-B aligned pointer");
+    if ((flags & CCC_OUT_CHECKSUM) && (!ck || !aligned(ck, 8)))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "checksum must be a non-NULL 8-B aligned pointer");
+    return CCC_OK;
+}
+
+struct WsLayout {
+    size_t N = 0, s = 0, w = 0, G = 0, total = 0;
+};
+
+WsLayout ws_layout(int way, int64_t n_v, int64_t n_f) {
+    WsLayout L;
+    size_t off = 0;
+    L.N = off;
+    off += al256((size_t)n_v * (size_t)kpad_of(n_f));
+    L.s = off;
+    off += al256((size_t)n_v * 4);
+    L.w = off;
+    off += al256((size_t)n_v * 16);
+    if (way == 3) {
+        L.G = off;
+        off += al256((size_t)n_v * (size_t)n_v * 4);
+    }
+    L.total = off + 256;  // slack so a caller base need only be 256-B aligned
+    return L;
+}
+
+ccc_status block_impl(const int8_t* N_a, const int32_t* s_a, const double* w_a, int64_t n_a,
+                      int64_t a_row0, int64_t a_lo, int64_t a_hi, const int8_t* N_b,
+                      const int32_t* s_b, const double* w_b, int64_t n_b, int64_t b_row0,
+                      int diag, int64_t n_f, uint32_t flags, uint32_t* tallies, void* ccc,
+                      uint64_t* ck, int32_t* g, int64_t ldg, cudaStream_t stream, int num_sms) {
+    const int64_t k_pad = kpad_of(n_f);
+    CUtensorMap tmA, tmB;
+    CCC_CHECK(make_tmap(&tmA, N_a, n_a, k_pad, ccc::kBM));
+    CCC_CHECK(make_tmap(&tmB, N_b, n_b, k_pad, ccc::kBN));
+    ccc::Tally2Args a{};
+    a.a_lo = a_lo;
+    a.nA = a_hi - a_lo;
+    a.nB = n_b;
+    a.a_row0 = a_row0;
+    a.b_row0 = b_row0;
+    a.diag = diag ? 1 : 0;
+    a.n_f = (int32_t)n_f;
+    a.k_blocks = (int32_t)(k_pad / ccc::kBK);
+    a.out_flags = (int32_t)flags;
+    a.s_a = s_a;
+    a.s_b = s_b;
+    a.w_a = w_a;
+    a.w_b = w_b;
+    a.tallies = tallies;
+    a.ccc = ccc;
+    a.checksum = reinterpret_cast<unsigned long long*>(ck);
+    a.g_out = g;
+    a.ldg = ldg;
+    a.rec_row_base = diag ? (a_lo * (2 * n_b - a_lo - 1)) / 2 : 0;
+    int64_t tiles = 0;
+    CCC_CUDA(ccc::launch_tally2(tmA, tmB, a, num_sms, stream, &tiles), "tally2 launch");
+    if (tiles) ++g_launches;
+    return CCC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ccc_version(void) { return 100; }
+
+const char* ccc_status_string(int st) {
+    switch (st) {
+        case CCC_OK: return "CCC_OK";
+        case CCC_ERR_INVALID_ARGUMENT: return "CCC_ERR_INVALID_ARGUMENT";
+        case CCC_ERR_UNSUPPORTED: return "CCC_ERR_UNSUPPORTED";
+        case CCC_ERR_CUDA: return "CCC_ERR_CUDA";
+        case CCC_ERR_WORKSPACE: return "CCC_ERR_WORKSPACE";
+        default: return "CCC_ERR_UNKNOWN";
+    }
+}
+
+const char* ccc_last_error(void) { return g_err.c_str(); }
+
+int64_t ccc_last_launch_count(void) { return g_launches; }
+
+int64_t ccc_num_unique(int num_way, int64_t n_v) {
+    if (num_way == 2) return c2(n_v);
+    if (num_way == 3) return c3(n_v);
+    return -1;
+}
+
+int64_t ccc_pair_index(int64_t n_v, int64_t i, int64_t j) {
+    if (!(0 <= i && i < j && j < n_v)) return -1;
+    return i * (2 * n_v - i - 1) / 2 + (j - i - 1);
+}
+
+int64_t ccc_triple_index(int64_t n_v, int64_t i, int64_t j, int64_t k) {
+    if (!(0 <= i && i < j && j < k && k < n_v)) return -1;
+    return c3(n_v) - c3(n_v - i) + c2(n_v - i - 1) - c2(n_v - j) + (k - j - 1);
+}
+
+int64_t ccc_packed_stride(int64_t n_f) { return n_f < 1 ? -1 : pstride_of(n_f); }
+
+int64_t ccc_k_pad(int64_t n_f) { return n_f < 1 ? -1 : kpad_of(n_f); }
+
+ccc_status ccc_stage_range(int64_t n_v, int64_t n_stages, int64_t stage, int64_t* out) {
+    if (!out) return fail(CCC_ERR_INVALID_ARGUMENT, "out must not be NULL");
+    if (n_v < 0 || n_stages < 1 || stage < 0 || stage >= n_stages)
+        return fail(CCC_ERR_INVALID_ARGUMENT, "need n_v >= 0, n_stages >= 1, 0 <= stage < n_stages");
+    const int64_t tot = c3(n_v);
+    // cum(i) = records of pivots < i = C(n_v,3) - C(n_v-i,3); stage boundary b(s) is the
+    // smallest i with cum(i) >= ceil(s * tot / n_stages).
+    auto cum = [&](int64_t i) { return tot - c3(n_v - i); };
+    auto bound = [&](int64_t s) -> int64_t {
+        if (s <= 0) return 0;
+        if (s >= n_stages) return n_v;
+        const __int128 t = (__int128)s * tot;
+        const int64_t target = (int64_t)((t + n_stages - 1) / n_stages);
+        int64_t lo = 0, hi = n_v;  // cum(n_v) = tot >= target
+        while (lo < hi) {
+            int64_t mid = (lo + hi) / 2;
+            if (cum(mid) >= target) hi = mid;
+            else lo = mid + 1;
+        }
+        return lo;
+    };
+    const int64_t ib = bound(stage), ie = bound(stage + 1);
+    out[0] = ib;
+    out[1] = ie;
+    out[2] = cum(ib);
+    out[3] = cum(ie) - cum(ib);
+    return CCC_OK;
+}
+
+size_t ccc_workspace_bytes(int num_way, int64_t n_v, int64_t n_f) {
+    if ((num_way != 2 && num_way != 3) || n_v < 0 || n_f < 1) return 0;
+    return ws_layout(num_way, n_v, n_f).total;
+}
+
+ccc_status ccc_pack(const uint8_t* codes_d, int64_t n_v, int64_t n_f, uint8_t* packed_d,
+                    void* stream) {
+    g_launches = 0;
+    CCC_CHECK(check_sizes(n_v, n_f));
+    if (n_v == 0) return CCC_OK;
+    if (!codes_d || !packed_d || !aligned(packed_d, 16))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "codes_d / packed_d must be non-NULL, packed_d 16-B aligned");
+    int sms;
+    CCC_CHECK(check_device(&sms));
+    CCC_CUDA(ccc::launch_pack(codes_d, n_v, n_f, packed_d, sms, (cudaStream_t)stream), "pack launch");
+    g_launches = 1;
+    return CCC_OK;
+}
+
+ccc_status ccc_expand(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
+                      int8_t* N_d, int32_t* s_d, double* w_d, void* stream) {
+    g_launches = 0;
+    CCC_CHECK(check_sizes(n_v, n_f));
+    if (n_v == 0) return CCC_OK;
+    if (!packed_d || !N_d || !s_d || !w_d || !aligned(packed_d, 16) || !aligned(N_d, 128) ||
+        !aligned(s_d, 4) || !aligned(w_d, 8))
+        return fail(CCC_ERR_INVALID_ARGUMENT,
+                    "packed_d (16-B), N_d (128-B), s_d, w_d must be non-NULL and aligned");
+    int sms;
+    CCC_CHECK(check_device(&sms));
+    CCC_CUDA(ccc::launch_expand(packed_d, n_v, n_f, gamma, N_d, s_d, w_d, sms, (cudaStream_t)stream),
+             "expand launch");
+    g_launches = 1;
+    return CCC_OK;
+}
+
+ccc_status ccc_2way_block(const int8_t* N_a, const int32_t* s_a, const double* w_a, int64_t n_a,
+                          int64_t a_row0, int64_t a_lo, int64_t a_hi, const int8_t* N_b,
+                          const int32_t* s_b, const double* w_b, int64_t n_b, int64_t b_row0,
+                          int diag, int64_t n_f, uint32_t out_flags, uint32_t* tallies_d,
+                          void* ccc_d, uint64_t* checksum_d, int32_t* g_d, int64_t ldg,
+                          void* stream) {
+    g_launches = 0;
+    CCC_CHECK(check_sizes(n_a, n_f));
+    CCC_CHECK(check_sizes(n_b, n_f));
+    if (out_flags & ~15u) return fail(CCC_ERR_INVALID_ARGUMENT, "unknown out_flags bits");
+    if (!(0 <= a_lo && a_lo <= a_hi && a_hi <= n_a))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "need 0 <= a_lo <= a_hi <= n_a");
+    if (diag && (N_a != N_b || n_a != n_b || a_row0 != b_row0))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "diag block needs A == B");
+    if (a_row0 < 0 || b_row0 < 0 || a_row0 + n_a > CCC_MAX_NV || b_row0 + n_b > CCC_MAX_NV)
+        return fail(CCC_ERR_INVALID_ARGUMENT, "global row indices out of range");
+    if (g_d && ldg < n_b) return fail(CCC_ERR_INVALID_ARGUMENT, "ldg must be >= n_b");
+    if (a_hi == a_lo || n_b == 0) return CCC_OK;
+    CCC_CHECK(check_outputs(out_flags, tallies_d, ccc_d, checksum_d));
+    if (!N_a || !N_b || !s_a || !s_b || !w_a || !w_b || !aligned(N_a, 128) || !aligned(N_b, 128))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "N_a/N_b (128-B aligned), s, w must be non-NULL");
+    int sms;
+    CCC_CHECK(check_device(&sms));
+    return block_impl(N_a, s_a, w_a, n_a, a_row0, a_lo, a_hi, N_b, s_b, w_b, n_b, b_row0, diag,
+                      n_f, out_flags, tallies_d, ccc_d, checksum_d, g_d, ldg,
+                      (cudaStream_t)stream, sms);
+}
+
+ccc_status ccc_2way(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
+                    uint32_t out_flags, uint32_t* tallies_d, void* ccc_d, uint64_t* checksum_d,
+                    void* ws_d, size_t ws_bytes, void* stream) {
+    g_launches = 0;
+    CCC_CHECK(check_sizes(n_v, n_f));
+    if (out_flags & ~15u) return fail(CCC_ERR_INVALID_ARGUMENT, "unknown out_flags bits");
+    if (n_v < 2) return CCC_OK;  // empty result: nothing to write
+    CCC_CHECK(check_outputs(out_flags, tallies_d, ccc_d, checksum_d));
+    if (!packed_d || !aligned(packed_d, 16))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "packed_d must be non-NULL and 16-B aligned");
+    const WsLayout L = ws_layout(2, n_v, n_f);
+    if (!ws_d || !aligned(ws_d, 256)) return fail(CCC_ERR_INVALID_ARGUMENT, "ws_d must be 256-B aligned");
+    if (ws_bytes < L.total) return fail(CCC_ERR_WORKSPACE, "workspace too small (see ccc_workspace_bytes)");
+    int sms;
+    CCC_CHECK(check_device(&sms));
+    uint8_t* ws = static_cast<uint8_t*>(ws_d);
+    int8_t* N = reinterpret_cast<int8_t*>(ws + L.N);
+    int32_t* s = reinterpret_cast<int32_t*>(ws + L.s);
+    double* w = reinterpret_cast<double*>(ws + L.w);
+    cudaStream_t st = (cudaStream_t)stream;
+    CCC_CUDA(ccc::launch_expand(packed_d, n_v, n_f, gamma, N, s, w, sms, st), "expand launch");
+    CCC_CHECK(block_impl(N, s, w, n_v, 0, 0, n_v, N, s, w, n_v, 0, 1, n_f, out_flags, tallies_d,
+                         ccc_d, checksum_d, nullptr, 0, st, sms));
+    g_launches += 1;
+    return CCC_OK;
+}
+
+ccc_status ccc_3way_prepare(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
+                            void* ws_d, size_t ws_bytes, void* stream) {
+    g_launches = 0;
+    CCC_CHECK(check_sizes(n_v, n_f));
+    if (n_v < 3) return CCC_OK;
+    if (!packed_d || !aligned(packed_d, 16))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "packed_d must be non-NULL and 16-B aligned");
+    const WsLayout L = ws_layout(3, n_v, n_f);
+    if (!ws_d || !aligned(ws_d, 256)) return fail(CCC_ERR_INVALID_ARGUMENT, "ws_d must be 256-B aligned");
+    if (ws_bytes < L.total) return fail(CCC_ERR_WORKSPACE, "workspace too small (see ccc_workspace_bytes)");
+    int sms;
+    CCC_CHECK(check_device(&sms));
+    uint8_t* ws = static_cast<uint8_t*>(ws_d);
+    int8_t* N = reinterpret_cast<int8_t*>(ws + L.N);
+    int32_t* s = reinterpret_cast<int32_t*>(ws + L.s);
+    double* w = reinterpret_cast<double*>(ws + L.w);
+    int32_t* G = reinterpret_cast<int32_t*>(ws + L.G);
+    cudaStream_t st = (cudaStream_t)stream;
+    CCC_CUDA(ccc::launch_expand(packed_d, n_v, n_f, gamma, N, s, w, sms, st), "expand launch");
+    CCC_CHECK(block_impl(N, s, w, n_v, 0, 0, n_v, N, s, w, n_v, 0, 1, n_f, 0, nullptr, nullptr,
+                         nullptr, G, n_v, st, sms));
+    g_launches += 1;
+    return CCC_OK;
+}
+
+ccc_status ccc_3way_stage(int64_t n_v, int64_t n_f, int64_t n_stages, int64_t stage,
+                          uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
+                          uint64_t* checksum_d, void* ws_d, size_t ws_bytes, void* stream) {
+    g_launches = 0;
+    CCC_CHECK(check_sizes(n_v, n_f));
+    if (out_flags & ~15u) return fail(CCC_ERR_INVALID_ARGUMENT, "unknown out_flags bits");
+    int64_t rng[4];
+    CCC_CHECK(ccc_stage_range(n_v, n_stages, stage, rng));
+    if (n_v < 3 || rng[3] == 0) return CCC_OK;  // empty stage: nothing to write
+    CCC_CHECK(check_outputs(out_flags, tallies_d, ccc_d, checksum_d));
+    const WsLayout L = ws_layout(3, n_v, n_f);
+    if (!ws_d || !aligned(ws_d, 256)) return fail(CCC_ERR_INVALID_ARGUMENT, "ws_d must be 256-B aligned");
+    if (ws_bytes < L.total) return fail(CCC_ERR_WORKSPACE, "workspace too small (see ccc_workspace_bytes)");
+    int sms;
+    CCC_CHECK(check_device(&sms));
+    uint8_t* ws = static_cast<uint8_t*>(ws_d);
+    const int64_t k_pad = kpad_of(n_f);
+    ccc::Tally3Args a{};
+    a.n_v = n_v;
+    a.i_begin = rng[0];
+    a.i_end = rng[1];
+    a.rec_begin = rng[2];
+    a.n_f = (int32_t)n_f;
+    a.k_blocks = (int32_t)(k_pad / ccc::kBK);
+    a.out_flags = (int32_t)out_flags;
+    a.N = reinterpret_cast<const int8_t*>(ws + L.N);
+    a.k_pad = k_pad;
+    a.s = reinterpret_cast<const int32_t*>(ws + L.s);
+    a.w = reinterpret_cast<const double*>(ws + L.w);
+    a.G = reinterpret_cast<const int32_t*>(ws + L.G);
+    a.tallies = tallies_d;
+    a.ccc = ccc_d;
+    a.checksum = reinterpret_cast<unsigned long long*>(checksum_d);
+    CUtensorMap tmA, tmB;
+    CCC_CHECK(make_tmap(&tmA, a.N, n_v, k_pad, ccc::kBM));
+    CCC_CHECK(make_tmap(&tmB, a.N, n_v, k_pad, ccc::kBN));
+    int64_t units = 0;
+    CCC_CUDA(ccc::launch_tally3(tmA, tmB, a, sms, (cudaStream_t)stream, &units), "tally3 launch");
+    if (units) g_launches = 1;
+    return CCC_OK;
+}
+
+ccc_status ccc_3way(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
+                    uint32_t out_flags, int64_t n_stages, int64_t stage, uint32_t* tallies_d,
+                    void* ccc_d, uint64_t* checksum_d, void* ws_d, size_t ws_bytes,
+                    void* stream) {
+    if (n_v >= 3) CCC_CHECK(check_outputs(out_flags, tallies_d, ccc_d, checksum_d));
+    CCC_CHECK(ccc_3way_prepare(packed_d, n_v, n_f, gamma, ws_d, ws_bytes, stream));
+    const int64_t n1 = g_launches;
+    CCC_CHECK(ccc_3way_stage(n_v, n_f, n_stages, stage, out_flags, tallies_d, ccc_d, checksum_d,
+                             ws_d, ws_bytes, stream));
+    g_launches += n1;
+    return CCC_OK;
+}
+
+// ----------------------------------------------------------------------------- e2e
+static const int64_t kBandRecords = 32ll << 20;  // records per output band buffer
+
+struct E2eLayout {
+    size_t codes = 0, packed = 0, ws = 0, ck = 0, band_t[2] = {0, 0}, band_c[2] = {0, 0};
+    size_t total = 0;
+    int64_t band_cap = 0;
+};
+
+static E2eLayout e2e_layout(int64_t n_v, int64_t n_f, uint32_t flags) {
+    E2eLayout L;
+    size_t off = 0;
+    L.codes = off;
+    off += al256((size_t)n_v * n_f);
+    L.packed = off;
+    off += al256((size_t)n_v * pstride_of(n_f));
+    L.ws = off;
+    off += al256(ws_layout(2, n_v, n_f).total);
+    L.ck = off;
+    off += 256;
+    const int64_t recs = c2(n_v);
+    L.band_cap = std::min<int64_t>(recs, kBandRecords);
+    const int64_t min_cap = 128 * std::max<int64_t>(n_v - 1, 1);  // one 128-row band
+    if (L.band_cap < std::min<int64_t>(recs, min_cap)) L.band_cap = std::min<int64_t>(recs, min_cap);
+    const size_t cb = (flags & CCC_OUT_CCC_F64) ? 32 : (flags & CCC_OUT_CCC_F32) ? 16 : 0;
+    for (int b = 0; b < 2; ++b) {
+        L.band_t[b] = off;
+        if (flags & CCC_OUT_TALLY) off += al256((size_t)L.band_cap * 16);
+        L.band_c[b] = off;
+        off += al256((size_t)L.band_cap * cb);
+    }
+    L.total = off + 256;
+    return L;
+}
+
+size_t ccc_e2e_workspace_bytes(int64_t n_v, int64_t n_f, uint32_t out_flags) {
+    if (n_v < 0 || n_f < 1) return 0;
+    return e2e_layout(n_v, n_f, out_flags).total;
+}
+
+ccc_status ccc_2way_host(const uint8_t* codes_h, int64_t n_v, int64_t n_f, double gamma,
+                         uint32_t out_flags, uint32_t* tallies_h, void* ccc_h,
+                         uint64_t* checksum_h, void* dev_ws_d, size_t dev_ws_bytes,
+                         void* stream) {
+    g_launches = 0;
+    CCC_CHECK(check_sizes(n_v, n_f));
+    if (out_flags & ~15u) return fail(CCC_ERR_INVALID_ARGUMENT, "unknown out_flags bits");
+    if (n_v < 2) return CCC_OK;
+    CCC_CHECK(check_outputs(out_flags, tallies_h, ccc_h, checksum_h));
+    if (!codes_h) return fail(CCC_ERR_INVALID_ARGUMENT, "codes_h must not be NULL");
+    const E2eLayout L = e2e_layout(n_v, n_f, out_flags);
+    if (!dev_ws_d || !aligned(dev_ws_d, 256))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "dev_ws_d must be 256-B aligned");
+    if (dev_ws_bytes < L.total) return fail(CCC_ERR_WORKSPACE, "device workspace too small");
+    int sms;
+    CCC_CHECK(check_device(&sms));
+    uint8_t* base = static_cast<uint8_t*>(dev_ws_d);
+    uint8_t* codes = base + L.codes;
+    uint8_t* packed = base + L.packed;
+    const WsLayout W = ws_layout(2, n_v, n_f);
+    int8_t* N = reinterpret_cast<int8_t*>(base + L.ws + W.N);
+    int32_t* s = reinterpret_cast<int32_t*>(base + L.ws + W.s);
+    double* w = reinterpret_cast<double*>(base + L.ws + W.w);
+    uint64_t* ck = reinterpret_cast<uint64_t*>(base + L.ck);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t cbytes = (out_flags & CCC_OUT_CCC_F64) ? 8 : 4;
+    const bool want_c = out_flags & (CCC_OUT_CCC_F64 | CCC_OUT_CCC_F32);
+
+    CCC_CUDA(cudaMemcpyAsync(codes, codes_h, (size_t)n_v * n_f, cudaMemcpyHostToDevice, st), "H2D codes");
+    CCC_CUDA(ccc::launch_pack(codes, n_v, n_f, packed, sms, st), "pack launch");
+    CCC_CUDA(ccc::launch_expand(packed, n_v, n_f, gamma, N, s, w, sms, st), "expand launch");
+    int64_t launches = 2;
+    if (out_flags & CCC_OUT_CHECKSUM) CCC_CUDA(cudaMemsetAsync(ck, 0, 16, st), "memset");
+
+    cudaStream_t cs = nullptr;
+    cudaEvent_t done[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
+    ccc_status rc = CCC_OK;
+    auto cleanup = [&]() {
+        for (int b = 0; b < 2; ++b) {
+            if (done[b]) cudaEventDestroy(done[b]);
+            if (copied[b]) cudaEventDestroy(copied[b]);
+        }
+        if (cs) cudaStreamDestroy(cs);
+    };
+    cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+        e = cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) {
+        cleanup();
+        return cuda_fail(e, "stream/event create");
+    }
+    auto rowstart = [&](int64_t i) { return i * (2 * n_v - i - 1) / 2; };
+    int64_t r0 = 0, band = 0;
+    while (r0 < n_v - 1 && rc == CCC_OK) {
+        // grow the band in 128-row steps while its records fit the band buffer
+        int64_t r1 = std::min<int64_t>(n_v, r0 + 128);
+        while (r1 < n_v && rowstart(std::min<int64_t>(n_v, r1 + 128)) - rowstart(r0) <= L.band_cap)
+            r1 = std::min<int64_t>(n_v, r1 + 128);
+        const int64_t rec0 = rowstart(r0), nrec = rowstart(r1) - rec0;
+        const int b = (int)(band & 1);
+        if (band >= 2 && (e = cudaStreamWaitEvent(st, copied[b], 0)) != cudaSuccess) {
+            rc = cuda_fail(e, "wait");
+            break;
+        }
+        uint32_t* bt = reinterpret_cast<uint32_t*>(base + L.band_t[b]);
+        void* bc = base + L.band_c[b];
+        rc = block_impl(N, s, w, n_v, 0, r0, r1, N, s, w, n_v, 0, 1, n_f, out_flags, bt, bc, ck,
+                        nullptr, 0, st, sms);
+        if (rc != CCC_OK) break;
+        ++launches;
+        if ((e = cudaEventRecord(done[b], st)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(cs, done[b], 0)) != cudaSuccess) {
+            rc = cuda_fail(e, "event");
+            break;
+        }
+        if (out_flags & CCC_OUT_TALLY)
+            e = cudaMemcpyAsync(tallies_h + 4 * rec0, bt, (size_t)nrec * 16, cudaMemcpyDeviceToHost, cs);
+        if (e == cudaSuccess && want_c)
+            e = cudaMemcpyAsync(static_cast<uint8_t*>(ccc_h) + (size_t)rec0 * 4 * cbytes, bc,
+                                (size_t)nrec * 4 * cbytes, cudaMemcpyDeviceToHost, cs);
+        if (e == cudaSuccess) e = cudaEventRecord(copied[b], cs);
+        if (e != cudaSuccess) {
+            rc = cuda_fail(e, "D2H band");
+            break;
+        }
+        r0 = r1;
+        ++band;
+    }
+    if (rc == CCC_OK && (out_flags & CCC_OUT_CHECKSUM)) {
+        e = cudaMemcpyAsync(checksum_h, ck, 16, cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) rc = cuda_fail(e, "D2H checksum");
+    }
+    if ((e = cudaStreamSynchronize(cs)) != cudaSuccess && rc == CCC_OK) rc = cuda_fail(e, "sync copy stream");
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess && rc == CCC_OK) rc = cuda_fail(e, "sync stream");
+    cleanup();
+    if (rc == CCC_OK) g_launches = launches;
+    return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,139 @@
+// common.cuh -- structures shared by the CCC kernels and their host launchers.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace ccc {
+
+constexpr int kBM = 128;        // tile rows   (UMMA M, one TMEM lane per row)
+constexpr int kBN = 256;        // tile cols   (UMMA N, TMEM columns per accumulator)
+constexpr int kBK = 128;        // K bytes per pipeline stage (one 128-B swizzle atom)
+constexpr int kUMMA_K = 32;     // K of one kind::i8 tcgen05.mma
+constexpr int kSuperM = 16;     // super-tile: 16 x 8 tiles = 2048 x 2048 elements
+constexpr int kSuperN = 8;
+
+// Record digest for the order-independent checksum (R-9).
+constexpr uint64_t kCkSeed = 0x243F6A8885A308D3ull;
+constexpr uint64_t kCkHi = 0x13198A2E03707344ull;
+
+// 2-way tile space: rows [a_lo, a_lo + nA) of block A against cols [0, nB) of block B.
+// diag: A and B are one block and only local pairs i < j are wanted.
+// Tiles are visited in super-tile order (kSuperM x kSuperN tiles, row-major over
+// super tiles, row-major inside) so that the ~148 concurrently active tiles share
+// few A / B panels in L2.
+struct TriSched {
+    int64_t a_lo, nA, nB;
+    int32_t diag, nbm, nbn, SP, SQ;
+    // cursor
+    int32_t P, Q, cnt;
+    int64_t base;
+
+    __host__ __device__ void init(int64_t a_lo_, int64_t nA_, int64_t nB_, int diag_) {
+        a_lo = a_lo_;
+        nA = nA_;
+        nB = nB_;
+        diag = diag_;
+        nbm = (int32_t)((nA + kBM - 1) / kBM);
+        nbn = (int32_t)((nB + kBN - 1) / kBN);
+        SP = (nbm + kSuperM - 1) / kSuperM;
+        SQ = (nbn + kSuperN - 1) / kSuperN;
+        P = 0;
+        Q = 0;
+        base = 0;
+        cnt = (SP > 0 && SQ > 0) ? super_count(0, 0) : 0;
+    }
+    // first valid column tile for row tile bm (diag), or 0 (rect); nbn if none.
+    __host__ __device__ int32_t bn_first(int32_t bm) const {
+        if (!diag) return 0;
+        int64_t i_min = a_lo + (int64_t)bm * kBM;
+        if (i_min >= nB - 1) return nbn;
+        // need bn*kBN + kBN - 1 > i_min  <=>  bn >= floor((i_min + 1) / kBN)
+        return (int32_t)((i_min + 1) / kBN);
+    }
+    __host__ __device__ int32_t row_count(int32_t bm, int32_t Qs) const {
+        int32_t lo = Qs * kSuperN, hi = lo + kSuperN;
+        if (hi > nbn) hi = nbn;
+        int32_t f = bn_first(bm);
+        if (f > lo) lo = f;
+        return hi > lo ? hi - lo : 0;
+    }
+    __host__ __device__ int32_t super_count(int32_t Ps, int32_t Qs) const {
+        int32_t r0 = Ps * kSuperM, r1 = r0 + kSuperM, c = 0;
+        if (r1 > nbm) r1 = nbm;
+        for (int32_t bm = r0; bm < r1; ++bm) c += row_count(bm, Qs);
+        return c;
+    }
+    // Map the (monotonically increasing) linear tile index t -> (bm, bn).
+    __host__ __device__ bool get(int64_t t, int32_t& bm, int32_t& bn) {
+        while (t >= base + cnt) {
+            base += cnt;
+            if (++Q == SQ) {
+                Q = 0;
+                if (++P == SP) { cnt = 0; return false; }
+            }
+            cnt = super_count(P, Q);
+        }
+        int64_t local = t - base;
+        int32_t r0 = P * kSuperM, r1 = r0 + kSuperM;
+        if (r1 > nbm) r1 = nbm;
+        for (int32_t r = r0; r < r1; ++r) {
+            int32_t c = row_count(r, Q);
+            if (local < c) {
+                int32_t lo = Q * kSuperN, f = bn_first(r);
+                bm = r;
+                bn = (f > lo ? f : lo) + (int32_t)local;
+                return true;
+            }
+            local -= c;
+        }
+        return false;  // unreachable
+    }
+    __host__ int64_t total() {
+        int64_t s = 0;
+        for (int32_t p = 0; p < SP; ++p)
+            for (int32_t q = 0; q < SQ; ++q) s += super_count(p, q);
+        return s;
+    }
+};
+
+// Kernel arguments of the fused 2-way tally GEMM (KB-2W).
+struct Tally2Args {
+    int64_t a_lo, nA, nB;      // A rows [a_lo, a_lo+nA) (local), B rows [0, nB)
+    int64_t a_row0, b_row0;    // global index of local row 0 of A / B (checksum)
+    int32_t diag;
+    int32_t n_f;
+    int32_t k_blocks;          // K_pad / kBK
+    int32_t out_flags;
+    const int32_t* s_a;
+    const int32_t* s_b;
+    const double* w_a;         // [rows][2]
+    const double* w_b;
+    uint32_t* tallies;         // [records][4]
+    void* ccc;                 // [records][4] double or float
+    unsigned long long* checksum;  // [2]
+    int32_t* g_out;            // optional raw G
+    int64_t ldg;
+    int64_t rec_row_base;      // diag: record index of row a_lo's first pair
+};
+
+// Kernel arguments of the fused 3-way pivot GEMM (KB-3W).
+struct Tally3Args {
+    int64_t n_v;
+    int64_t i_begin, i_end;    // pivot range of the stage
+    int64_t rec_begin;         // record index of the stage's first triple
+    int32_t n_f;
+    int32_t k_blocks;
+    int32_t out_flags;
+    int32_t pad_;
+    const int8_t* N;           // [n_v][K_pad]  (pivot rows read directly)
+    int64_t k_pad;
+    const int32_t* s;
+    const double* w;
+    const int32_t* G;          // [n_v][n_v] pairwise G (upper triangle valid)
+    uint32_t* tallies;         // [rec_count][8]
+    void* ccc;
+    unsigned long long* checksum;
+};
+
+}  // namespace ccc

@@ -1,0 +1,118 @@
+// pack_expand.cu -- KB-pack and KB-expand. HBM-bound.
+//
+// pack  : one byte per genotype code -> 2 bits per code, 4 codes per byte, LSB
+//         first, rows padded to 64-entry (16-byte) units -- the storage density of
+//         the paper's packed double-complex word.
+// expand: packed codes -> int8 allele-1 counts n_{iq} = rho_{i,q}(1)
+//         laid out K-major with rows padded to K_pad = 128-byte multiples (zero pad:
+//         padding contributes nothing to N N^T, so no correction term is needed,
+//         cf. P:444-446), plus the per-vector sums s_i = S_i(1) and the frequency
+//         weights w_i(a) = 1 - gamma f_i(a) of Eq.1/Eq.3.
+#include "common.cuh"
+#include "internal.h"
+
+namespace ccc {
+
+// One thread -> one 32-bit packed word (16 codes).
+__global__ void __launch_bounds__(256) pack_kernel(const uint8_t* __restrict__ codes,
+                                                   int64_t n_v, int64_t n_f, int64_t words_per_row,
+                                                   uint32_t* __restrict__ packed) {
+    const int64_t total = n_v * words_per_row;
+    const bool vec_ok = (n_f % 16) == 0 && (reinterpret_cast<uintptr_t>(codes) % 16) == 0;
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
+         w += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = w / words_per_row;
+        const int64_t q0 = (w - i * words_per_row) * 16;
+        const uint8_t* src = codes + i * n_f + q0;
+        uint32_t out = 0;
+        if (vec_ok && q0 + 16 <= n_f) {
+            const uint4 c = __ldcs(reinterpret_cast<const uint4*>(src));
+            const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                uint32_t x = cw[b] & 0x03030303u;  // 4 codes, one per byte
+                // gather bits: byte k (2 bits) -> bits 2k..2k+1
+                x = (x | (x >> 6)) & 0x000F000Fu;
+                x = (x | (x >> 12)) & 0xFFu;
+                out |= x << (8 * b);
+            }
+        } else {
+            for (int u = 0; u < 16; ++u) {
+                const int64_t q = q0 + u;
+                if (q < n_f) out |= (uint32_t)(src[u] & 3u) << (2 * u);
+            }
+        }
+        packed[w] = out;
+    }
+}
+
+// One CTA per vector row.  Each thread expands 16 codes (one packed word) per step.
+__global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict__ packed,
+                                                     int64_t n_v, int64_t n_f,
+                                                     int64_t words_per_row, int64_t k_pad,
+                                                     double gamma, int8_t* __restrict__ N,
+                                                     int32_t* __restrict__ s_out,
+                                                     double* __restrict__ w_out) {
+    __shared__ int32_t red[8];
+    const int64_t groups = k_pad / 16;
+    for (int64_t i = blockIdx.x; i < n_v; i += gridDim.x) {
+        const uint32_t* prow = packed + i * words_per_row;
+        uint4* nrow = reinterpret_cast<uint4*>(N + i * k_pad);
+        int32_t sum = 0;
+        for (int64_t g = threadIdx.x; g < groups; g += blockDim.x) {
+            const uint32_t p = g < words_per_row ? __ldg(prow + g) : 0u;
+            // n = r1 + r2 per 2-bit code: (p & 0x5555...) + ((p >> 1) & 0x5555...)
+            const uint32_t cnt = (p & 0x55555555u) + ((p >> 1) & 0x55555555u);
+            uint32_t o[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                uint32_t x = (cnt >> (8 * b)) & 0xFFu;  // 4 counts, 2 bits each
+                x = (x | (x << 12)) & 0x000F000Fu;
+                x = (x | (x << 6)) & 0x03030303u;
+                o[b] = x;
+            }
+            sum += __popc(p);  // sum of r1 + r2 over the 16 codes
+            __stcs(nrow + g, make_uint4(o[0], o[1], o[2], o[3]));
+        }
+        for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int32_t s = 0;
+            for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += red[k];
+            s_out[i] = s;
+            const double two_nf = 2.0 * (double)n_f;
+            const double f1 = (double)s / two_nf;                       // Eq.1, a = 1
+            const double f0 = (double)(2 * n_f - (int64_t)s) / two_nf;  // Eq.1, a = 0
+            w_out[2 * i + 0] = 1.0 - gamma * f0;
+            w_out[2 * i + 1] = 1.0 - gamma * f1;
+        }
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_pack(const uint8_t* codes, int64_t n_v, int64_t n_f, uint8_t* packed,
+                        int num_sms, cudaStream_t stream) {
+    const int64_t wpr = (n_f + 63) / 64 * 4;
+    const int64_t total = n_v * wpr;
+    int64_t blocks = (total + 255) / 256;
+    const int64_t cap = (int64_t)num_sms * 8;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    pack_kernel<<<(int)blocks, 256, 0, stream>>>(codes, n_v, n_f, wpr,
+                                                 reinterpret_cast<uint32_t*>(packed));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_expand(const uint8_t* packed, int64_t n_v, int64_t n_f, double gamma,
+                          int8_t* N, int32_t* s, double* w, int num_sms, cudaStream_t stream) {
+    const int64_t wpr = (n_f + 63) / 64 * 4;
+    const int64_t k_pad = (n_f + 127) / 128 * 128;
+    int64_t blocks = n_v < (int64_t)num_sms * 8 ? n_v : (int64_t)num_sms * 8;
+    if (blocks < 1) blocks = 1;
+    expand_kernel<<<(int)blocks, 256, 0, stream>>>(reinterpret_cast<const uint32_t*>(packed),
+                                                   n_v, n_f, wpr, k_pad, gamma, N, s, w);
+    return cudaGetLastError();
+}
+
+}  // namespace ccc

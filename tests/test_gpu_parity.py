@@ -1,0 +1,280 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle, on a B200.
+
+Bars: tallies bit-exact; CCC |x - y| <= 1e-12 |y| in fp64 (1e-6 for the
+fp32 variant), x == 0 exactly where the tally is 0; checksums equal.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synthgen
+
+pytestmark = pytest.mark.gpu
+
+ccc = pytest.importorskip("paper_1705_08213_b200.ccc")
+
+F64, F32, TAL, CK = ccc.OUT_CCC_F64, ccc.OUT_CCC_F32, ccc.OUT_TALLY, ccc.OUT_CHECKSUM
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.init()
+
+
+def _t(t):
+    """device int32 tally tensor -> numpy int64 (uint32 bit patterns)."""
+    return t.cpu().numpy().astype(np.int64) & 0xFFFFFFFF
+
+
+def _ccc_close(got, want, rtol=1e-12):
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    assert np.all((want == 0) == (got == 0))
+    nz = want != 0
+    rel = np.abs(got[nz] - want[nz]) / np.abs(want[nz])
+    assert rel.size == 0 or rel.max() <= rtol, rel.max()
+
+
+def _codes(kind, n_v, n_f, seed=None):
+    return synthgen.make_codes(kind, n_v, n_f, seed)
+
+
+# ------------------------------------------------------------------- pack / expand
+@pytest.mark.parametrize("n_v,n_f", [(1, 1), (3, 63), (5, 64), (7, 65), (9, 1000), (33, 4111)])
+def test_pack_expand(n_v, n_f):
+    codes = _codes("random", n_v, n_f, seed=n_f)
+    packed = ccc.ccc_pack(codes.cuda())
+    # expected packing (layout of include/ccc.h, built independently here)
+    c = codes.numpy().astype(np.uint32)
+    stride = ccc.ccc_packed_stride(n_f)
+    exp = np.zeros((n_v, stride), np.uint8)
+    for q in range(n_f):
+        exp[:, q // 4] |= ((c[:, q] & 3) << (2 * (q % 4))).astype(np.uint8)
+    np.testing.assert_array_equal(packed.cpu().numpy(), exp)
+    N, s, w = ccc.ccc_expand(packed, n_f)
+    S = oracle.allele_sums(codes)
+    n1 = ((codes.numpy() >> 1) & 1) + (codes.numpy() & 1)
+    Nn = N.cpu().numpy()
+    np.testing.assert_array_equal(Nn[:, :n_f], n1)
+    assert np.all(Nn[:, n_f:] == 0)
+    np.testing.assert_array_equal(s.cpu().numpy(), S[:, 1])
+    f = oracle.frequencies(codes)
+    np.testing.assert_allclose(w.cpu().numpy(), 1.0 - oracle.GAMMA * f, rtol=1e-15, atol=0)
+
+
+# ------------------------------------------------------------------- 2-way, full
+def _check_2way_full(codes, flags=TAL | F64 | CK, gamma=oracle.GAMMA):
+    n_v, n_f = codes.shape
+    T, C, ck = ccc.two_way(codes.cuda(), gamma=gamma, out_flags=flags)
+    torch.cuda.synchronize()
+    To, Co = oracle.all_pairs(codes, gamma)
+    if flags & TAL:
+        np.testing.assert_array_equal(_t(T), To)
+    if flags & F64:
+        _ccc_close(C.cpu().numpy(), Co)
+    if flags & F32:
+        _ccc_close(C.cpu().numpy(), Co, rtol=1e-6)
+    if flags & CK:
+        assert ccc.checksum_int(ck) == oracle.checksum(2, oracle.pair_list(n_v), To)
+
+
+def test_2way_C1_full():
+    """configs[0]: 64 vectors x 1,024 individuals, bit-exact against the brute force."""
+    _check_2way_full(_codes("random", 64, 1024, seed=1))
+
+
+@pytest.mark.parametrize("n_v", [2, 3, 63, 64, 65, 127, 129, 257, 300])
+@pytest.mark.parametrize("n_f", [1, 63, 65, 127, 1000])
+def test_2way_ragged_shapes(n_v, n_f):
+    if n_v * n_v * n_f > 2e8:
+        pytest.skip("covered by smaller combos")
+    _check_2way_full(_codes("random", n_v, n_f, seed=n_v * 1000 + n_f))
+
+
+@pytest.mark.parametrize("kind", ["hwe", "planted"])
+def test_2way_other_inputs(kind):
+    _check_2way_full(_codes(kind, 200, 777))
+
+
+def test_2way_f32_and_gamma():
+    codes = _codes("random", 150, 300, seed=5)
+    _check_2way_full(codes, flags=TAL | F32)
+    _check_2way_full(codes, flags=F64, gamma=0.0)
+
+
+def test_2way_checksum_only_and_tally_only():
+    codes = _codes("random", 333, 257, seed=6)
+    _check_2way_full(codes, flags=CK)
+    _check_2way_full(codes, flags=TAL)
+
+
+def test_2way_degenerate_inputs():
+    for codes in (torch.zeros(70, 300, dtype=torch.uint8), torch.ones(70, 300, dtype=torch.uint8),
+                  torch.full((70, 300), 3, dtype=torch.uint8)):
+        _check_2way_full(codes)
+    assert ccc.two_way(torch.zeros(1, 5, dtype=torch.uint8).cuda())[0].shape == (0, 4)
+
+
+def test_2way_planted_closed_form_every_record():
+    n_v, n_f = 700, 3001
+    codes, L, H, _ = synthgen.planted_codes(n_v, n_f, seed=3)
+    T, _, _ = ccc.two_way(codes.cuda(), out_flags=TAL)
+    T = _t(T)
+    for r, (i, j) in enumerate(oracle.pair_list(n_v)):
+        if r % 7:           # every 7th record through the closed form (35k records)
+            continue
+        assert list(T[r]) == oracle.planted_tally2(L, H, n_f, i, j)
+
+
+def test_2way_block_rect_and_row_split():
+    """Off-diagonal blocks (block-circulant) and the antipodal row split."""
+    n_v, n_f = 400, 517
+    codes = _codes("random", n_v, n_f, seed=8)
+    packed = ccc.ccc_pack(codes.cuda())
+    N, s, w = ccc.ccc_expand(packed, n_f)
+    To, Co = oracle.all_pairs(codes)
+    a0, a1, b0, b1 = 0, 150, 150, 400         # A = rows [0,150), B = rows [150,400)
+    lo, hi = 40, 131                          # rows [40,131) of A only
+    nA, nB = a1 - a0, b1 - b0
+    m = (hi - lo) * nB
+    T = torch.empty((m, 4), dtype=torch.int32, device="cuda")
+    C = torch.empty((m, 4), dtype=torch.float64, device="cuda")
+    ck = torch.zeros(2, dtype=torch.int64, device="cuda")
+    ccc.ccc_2way_block(N[a0:a1], s[a0:a1], w[a0:a1], a0, lo, hi, N[b0:b1], s[b0:b1], w[b0:b1], b0,
+                       False, n_f, TAL | F64 | CK, T, C, ck)
+    T, C = _t(T), C.cpu().numpy()
+    idx = [(a0 + i, b0 + j) for i in range(lo, hi) for j in range(nB)]
+    rows = [ccc.ccc_pair_index(n_v, i, j) for i, j in idx]
+    np.testing.assert_array_equal(T, To[rows])
+    _ccc_close(C, Co[rows])
+    assert ccc.checksum_int(ck) == oracle.checksum(2, np.array(idx), To[rows])
+    # diag block with a row range: records start at row lo
+    Td = torch.empty((ccc.ccc_pair_index(n_v, 0, 1) + 1, 4), dtype=torch.int32, device="cuda")
+    lo, hi = 100, 230
+    m = sum(n_v - 1 - i for i in range(lo, hi))
+    Td = torch.empty((m, 4), dtype=torch.int32, device="cuda")
+    ccc.ccc_2way_block(N, s, w, 0, lo, hi, N, s, w, 0, True, n_f, TAL, Td)
+    r0 = ccc.ccc_pair_index(n_v, lo, lo + 1)
+    np.testing.assert_array_equal(_t(Td), To[r0:r0 + m])
+
+
+def test_2way_host_e2e_api():
+    codes = _codes("random", 300, 999, seed=12)
+    T, C, ck = ccc.ccc_2way_host(codes.pin_memory(), out_flags=TAL | F64 | CK)
+    To, Co = oracle.all_pairs(codes)
+    np.testing.assert_array_equal(T.numpy().astype(np.int64) & 0xFFFFFFFF, To)
+    _ccc_close(C.numpy(), Co)
+    assert ccc.checksum_int(ck) == oracle.checksum(2, oracle.pair_list(300), To)
+
+
+# ------------------------------------------------------------------- 2-way at C2 size
+def test_2way_C2_full_size_sampled_and_invariants():
+    """configs[1]: 20,000 x 50,000 in the launch configuration bench.py times.
+    Sampled records against the brute force, the whole T(1,1) against an independent
+    cuBLASLt int8 GEMM (torch._int_mm), sum T = 4 n_f for every record."""
+    n_v, n_f = 20000, 50000
+    codes = synthgen.random_codes(n_v, n_f, seed=1, device="cuda")
+    T, C, _ = ccc.two_way(codes, out_flags=TAL | F64)
+    torch.cuda.synchronize()
+    assert bool((T.sum(1, dtype=torch.int64) == 4 * n_f).all())
+    rng = np.random.default_rng(2)
+    edges = [0, 1, 127, 128, 129, 255, 256, 257, 2047, 2048, 4095, 4096, n_v - 2, n_v - 1]
+    ii = list(rng.integers(0, n_v - 1, 6000)) + edges
+    pairs = []
+    for i in ii:
+        i = int(min(i, n_v - 2))
+        j = int(rng.integers(i + 1, n_v))
+        pairs.append((i, j))
+        pairs.append((i, n_v - 1))
+        pairs.append((i, i + 1))
+    pairs = np.array(sorted(set(pairs)), dtype=np.int64)
+    rows = torch.tensor([ccc.ccc_pair_index(n_v, int(i), int(j)) for i, j in pairs], device="cuda")
+    Tg, Cg = _t(T[rows]), C[rows].cpu().numpy()
+    codes_h = codes.cpu()
+    To, Co = oracle.pairs(codes_h, pairs)
+    np.testing.assert_array_equal(Tg, To)
+    _ccc_close(Cg, Co)
+    # independent library GEMM for T(1,1) on every record
+    n1 = ((codes >> 1) & 1) + (codes & 1)
+    n1 = n1.to(torch.int8)
+    K = (n_f + 31) // 32 * 32
+    A = torch.zeros((n_v, K), dtype=torch.int8, device="cuda")
+    A[:, :n_f] = n1
+    del n1
+    G = torch._int_mm(A, A.t().contiguous())
+    iu = torch.triu_indices(n_v, n_v, 1, device="cuda")
+    assert bool((G[iu[0], iu[1]] == T[:, 3]).all())
+
+
+# ------------------------------------------------------------------- 3-way
+def _check_3way_full(codes, n_stages=1, flags=TAL | F64 | CK):
+    n_v, n_f = codes.shape
+    To, Co = oracle.all_triples(codes)
+    packed = ccc.ccc_pack(codes.cuda())
+    ws = ccc.ccc_3way_prepare(packed, n_f)
+    Ts, Cs, cks = [], [], 0
+    for st in range(n_stages):
+        T, C, ck = ccc.ccc_3way_stage(n_v, n_f, n_stages, st, ws, out_flags=flags)
+        if flags & TAL:
+            Ts.append(_t(T))
+        if flags & (F64 | F32):
+            Cs.append(C.cpu().numpy())
+        if flags & CK:
+            cks = (cks + ccc.checksum_int(ck)) % (1 << 128)
+    if flags & TAL:
+        np.testing.assert_array_equal(np.concatenate(Ts), To)
+    if flags & F64:
+        _ccc_close(np.concatenate(Cs), Co)
+    if flags & F32:
+        _ccc_close(np.concatenate(Cs), Co, rtol=1e-6)
+    if flags & CK:
+        assert cks == oracle.checksum(3, oracle.triple_list(n_v), To)
+
+
+@pytest.mark.parametrize("n_v,n_f", [(3, 1), (4, 65), (5, 127), (40, 200), (130, 65),
+                                     (131, 300), (260, 129)])
+def test_3way_full(n_v, n_f):
+    _check_3way_full(_codes("random", n_v, n_f, seed=n_v + n_f))
+
+
+def test_3way_stages_and_variants():
+    codes = _codes("hwe", 150, 333)
+    _check_3way_full(codes, n_stages=7)
+    _check_3way_full(codes, n_stages=3, flags=TAL | F32)
+    _check_3way_full(_codes("planted", 90, 250), n_stages=2)
+    _check_3way_full(torch.full((70, 130), 3, dtype=torch.uint8))
+
+
+def test_3way_C4_full_size_stage_sampled():
+    """configs[3]: 4,096 x 16,384, 16 stages; first and last stage checked on samples."""
+    n_v, n_f, n_st = 4096, 16384, 16
+    codes = synthgen.random_codes(n_v, n_f, seed=1, device="cuda")
+    packed = ccc.ccc_pack(codes)
+    ws = ccc.ccc_3way_prepare(packed, n_f)
+    codes_h = codes.cpu()
+    rng = np.random.default_rng(4)
+    for st in (0, n_st - 1):
+        ib, ie, rb, rc = ccc.ccc_stage_range(n_v, n_st, st)
+        T, C, _ = ccc.ccc_3way_stage(n_v, n_f, n_st, st, ws, out_flags=TAL | F64)
+        assert bool((T.sum(1, dtype=torch.int64) == 8 * n_f).all())
+        trip = set()
+        for _ in range(1500):
+            i = int(rng.integers(ib, ie))
+            if i > n_v - 3:
+                continue
+            j = int(rng.integers(i + 1, n_v - 1))
+            k = int(rng.integers(j + 1, n_v))
+            trip.add((i, j, k))
+            trip.add((i, i + 1, n_v - 1))
+            trip.add((i, j, j + 1))
+        trip = np.array(sorted(trip), dtype=np.int64)
+        rows = torch.tensor([ccc.ccc_triple_index(n_v, *map(int, t)) - rb for t in trip],
+                            device="cuda")
+        To, Co = oracle.triples(codes_h, trip)
+        np.testing.assert_array_equal(_t(T[rows]), To)
+        _ccc_close(C[rows].cpu().numpy(), Co)
+        del T, C
+        torch.cuda.empty_cache()

@@ -260,6 +260,10 @@ def test_checksum_properties():
     T, _ = oracle.all_pairs(codes)
     idx = oracle.pair_list(9)
     full = oracle.checksum(2, idx, T)
+    assert full == oracle.checksum_scalar(2, idx, T)
+    T3, _ = oracle.all_triples(codes[:7])
+    tl = oracle.triple_list(7)
+    assert oracle.checksum(3, tl, T3) == oracle.checksum_scalar(3, tl, T3)
     assert oracle.checksum(2, idx[:0], T[:0]) == 0
     perm = np.random.default_rng(1).permutation(len(idx))
     assert oracle.checksum(2, idx[perm], T[perm]) == full
