@@ -172,7 +172,7 @@ ccc_status block_impl(const int8_t* N_a, const int32_t* s_a, const double* w_a, 
     const int64_t k_pad = kpad_of(n_f);
     CUtensorMap tmA, tmB;
     CCC_CHECK(make_tmap(&tmA, N_a, n_a, k_pad, ccc::kBM));
-    CCC_CHECK(make_tmap(&tmB, N_b, n_b, k_pad, ccc::kBN));
+    CCC_CHECK(make_tmap(&tmB, N_b, n_b, k_pad, (uint32_t)ccc::tally2_b_box_rows()));
     ccc::Tally2Args a{};
     a.a_lo = a_lo;
     a.nA = a_hi - a_lo;
@@ -193,6 +193,7 @@ ccc_status block_impl(const int8_t* N_a, const int32_t* s_a, const double* w_a, 
     a.g_out = g;
     a.ldg = ldg;
     a.rec_row_base = diag ? (a_lo * (2 * n_b - a_lo - 1)) / 2 : 0;
+    a.sup_elems = 2048;
     int64_t tiles = 0;
     CCC_CUDA(ccc::launch_tally2(tmA, tmB, a, num_sms, stream, &tiles), "tally2 launch");
     if (tiles) ++g_launches;

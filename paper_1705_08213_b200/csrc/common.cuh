@@ -10,34 +10,37 @@ constexpr int kBM = 128;        // tile rows   (UMMA M, one TMEM lane per row)
 constexpr int kBN = 256;        // tile cols   (UMMA N, TMEM columns per accumulator)
 constexpr int kBK = 128;        // K bytes per pipeline stage (one 128-B swizzle atom)
 constexpr int kUMMA_K = 32;     // K of one kind::i8 tcgen05.mma
-constexpr int kSuperM = 16;     // super-tile: 16 x 8 tiles = 2048 x 2048 elements
-constexpr int kSuperN = 8;
 
 // Record digest for the order-independent checksum (R-9).
 constexpr uint64_t kCkSeed = 0x243F6A8885A308D3ull;
 constexpr uint64_t kCkHi = 0x13198A2E03707344ull;
 
-// 2-way tile space: rows [a_lo, a_lo + nA) of block A against cols [0, nB) of block B.
+// 2-way tile space: rows [a_lo, a_lo + nA) of block A against cols [0, nB) of block B,
+// tiles of bm x kBN (bm = 128 for one CTA, 256 for a CTA pair).
 // diag: A and B are one block and only local pairs i < j are wanted.
-// Tiles are visited in super-tile order (kSuperM x kSuperN tiles, row-major over
-// super tiles, row-major inside) so that the ~148 concurrently active tiles share
-// few A / B panels in L2.
+// Tiles are visited in super-tile order (2048 x 2048 elements, row-major over super
+// tiles, row-major inside) so that the ~148 concurrently active tiles share few A / B
+// panels in L2.
 struct TriSched {
     int64_t a_lo, nA, nB;
-    int32_t diag, nbm, nbn, SP, SQ;
+    int32_t diag, bm_rows, sup_m, sup_n, nbm, nbn, SP, SQ;
     // cursor
     int32_t P, Q, cnt;
     int64_t base;
 
-    __host__ __device__ void init(int64_t a_lo_, int64_t nA_, int64_t nB_, int diag_) {
+    __host__ __device__ void init(int64_t a_lo_, int64_t nA_, int64_t nB_, int diag_,
+                                  int32_t bm_rows_ = kBM, int32_t sup_elems = 2048) {
         a_lo = a_lo_;
         nA = nA_;
         nB = nB_;
         diag = diag_;
-        nbm = (int32_t)((nA + kBM - 1) / kBM);
+        bm_rows = bm_rows_;
+        sup_m = sup_elems / bm_rows;
+        sup_n = sup_elems / kBN;
+        nbm = (int32_t)((nA + bm_rows - 1) / bm_rows);
         nbn = (int32_t)((nB + kBN - 1) / kBN);
-        SP = (nbm + kSuperM - 1) / kSuperM;
-        SQ = (nbn + kSuperN - 1) / kSuperN;
+        SP = (nbm + sup_m - 1) / sup_m;
+        SQ = (nbn + sup_n - 1) / sup_n;
         P = 0;
         Q = 0;
         base = 0;
@@ -46,20 +49,20 @@ struct TriSched {
     // first valid column tile for row tile bm (diag), or 0 (rect); nbn if none.
     __host__ __device__ int32_t bn_first(int32_t bm) const {
         if (!diag) return 0;
-        int64_t i_min = a_lo + (int64_t)bm * kBM;
+        int64_t i_min = a_lo + (int64_t)bm * bm_rows;
         if (i_min >= nB - 1) return nbn;
         // need bn*kBN + kBN - 1 > i_min  <=>  bn >= floor((i_min + 1) / kBN)
         return (int32_t)((i_min + 1) / kBN);
     }
     __host__ __device__ int32_t row_count(int32_t bm, int32_t Qs) const {
-        int32_t lo = Qs * kSuperN, hi = lo + kSuperN;
+        int32_t lo = Qs * sup_n, hi = lo + sup_n;
         if (hi > nbn) hi = nbn;
         int32_t f = bn_first(bm);
         if (f > lo) lo = f;
         return hi > lo ? hi - lo : 0;
     }
     __host__ __device__ int32_t super_count(int32_t Ps, int32_t Qs) const {
-        int32_t r0 = Ps * kSuperM, r1 = r0 + kSuperM, c = 0;
+        int32_t r0 = Ps * sup_m, r1 = r0 + sup_m, c = 0;
         if (r1 > nbm) r1 = nbm;
         for (int32_t bm = r0; bm < r1; ++bm) c += row_count(bm, Qs);
         return c;
@@ -75,12 +78,12 @@ struct TriSched {
             cnt = super_count(P, Q);
         }
         int64_t local = t - base;
-        int32_t r0 = P * kSuperM, r1 = r0 + kSuperM;
+        int32_t r0 = P * sup_m, r1 = r0 + sup_m;
         if (r1 > nbm) r1 = nbm;
         for (int32_t r = r0; r < r1; ++r) {
             int32_t c = row_count(r, Q);
             if (local < c) {
-                int32_t lo = Q * kSuperN, f = bn_first(r);
+                int32_t lo = Q * sup_n, f = bn_first(r);
                 bm = r;
                 bn = (f > lo ? f : lo) + (int32_t)local;
                 return true;
@@ -115,6 +118,8 @@ struct Tally2Args {
     int32_t* g_out;            // optional raw G
     int64_t ldg;
     int64_t rec_row_base;      // diag: record index of row a_lo's first pair
+    int32_t sup_elems;         // super-tile edge (elements) of the tile raster
+    int32_t epi_flags;         // internal epilogue variants (bit 0: evict_first stores)
 };
 
 // Kernel arguments of the fused 3-way pivot GEMM (KB-3W).

@@ -20,14 +20,9 @@
 #include "common.cuh"
 #include "internal.h"
 
-namespace ccc {
+#include <cstdlib>
 
-constexpr int kStages2 = 4;
-constexpr int kABytes = kBM * kBK;  // 16 KB
-constexpr int kBBytes = kBN * kBK;  // 32 KB
-constexpr int kThreads2 = 192;
-constexpr int kSmemBarOff2 = kStages2 * (kABytes + kBBytes);
-constexpr int kSmem2 = kSmemBarOff2 + 256 + 1024;  // + barriers + alignment slack
+namespace ccc {
 
 __device__ __forceinline__ void ck_fold(unsigned long long& lo, unsigned long long& hi,
                                         uint64_t l0, uint64_t l1, uint64_t l2) {
@@ -57,70 +52,104 @@ __device__ __forceinline__ void ck_flush(unsigned long long lo, unsigned long lo
     }
 }
 
+constexpr int kThreads2 = 192;
+
+template <int kPair>
+struct Cfg2 {
+    static constexpr int kTileM = 128 * kPair;     // tile rows (UMMA M = 128 / 256)
+    static constexpr int kBRows = kBN / kPair;     // B rows held by each CTA
+    static constexpr int kABytes = 128 * kBK;      // 16 KB of A per stage per CTA
+    static constexpr int kBBytes = kBRows * kBK;   // B bytes per stage per CTA
+    static constexpr int kStages = kPair == 2 ? 6 : 4;
+    static constexpr int kBarOff = kStages * (kABytes + kBBytes);
+    static constexpr int kSmem = kBarOff + 256 + 1024;
+};
+
+template <int kPair>
 __global__ void __launch_bounds__(kThreads2, 1)
 tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const Tally2Args args) {
+    using C = Cfg2<kPair>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
     uint8_t* smem = smem_raw + pad;
     uint8_t* smA = smem;
-    uint8_t* smB = smem + kStages2 * kABytes;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSmemBarOff2);
-    uint64_t* empty = full + kStages2;
-    uint64_t* tfull = empty + kStages2;
+    uint8_t* smB = smem + C::kStages * C::kABytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
+    uint64_t* empty = full + C::kStages;
+    uint64_t* tfull = empty + C::kStages;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
+    const uint32_t rank = kPair == 2 ? cluster_ctarank() : 0u;  // 0 = leader CTA
+    const int64_t unit0 = blockIdx.x / kPair, units = gridDim.x / kPair;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
-        for (int s = 0; s < kStages2; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+        for (int s = 0; s < C::kStages; ++s) {
+            mbar_init(&full[s], kPair);   // leader: expect_tx arrive (+ follower arrive)
+            mbar_init(&empty[s], 1);      // one (multicast) MMA commit per use
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], 4);
+            mbar_init(&tempty[s], 4 * kPair);  // one arrive per epilogue warp of the pair
         }
         fence_mbar_init();
     }
-    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    if (warp == 1) {
+        if constexpr (kPair == 2) tmem_alloc_pair<512>(tmem_slot);
+        else tmem_alloc<512>(tmem_slot);
+    }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (kPair == 2) cluster_sync();
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     TriSched sch;
-    sch.init(args.a_lo, args.nA, args.nB, args.diag);
+    sch.init(args.a_lo, args.nA, args.nB, args.diag, C::kTileM, args.sup_elems);
 
     if (warp == 0) {
         if (lane == 0) {
             // ------------------------------------------------------------ TMA producer
             uint32_t stage = 0, phase = 0;
-            for (int64_t t = blockIdx.x;; t += gridDim.x) {
+            const uint64_t pol = policy_evict_last();
+            for (int64_t t = unit0;; t += units) {
                 int32_t bm, bn;
                 if (!sch.get(t, bm, bn)) break;
-                const int32_t arow = (int32_t)(args.a_lo + (int64_t)bm * kBM);
-                const int32_t brow = bn * kBN;
+                const int32_t arow = (int32_t)(args.a_lo + (int64_t)bm * C::kTileM + rank * 128);
+                const int32_t brow = bn * kBN + (int32_t)rank * C::kBRows;
                 for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_arrive_expect_tx(&full[stage], kABytes + kBBytes);
-                    tma_load_2d(smA + stage * kABytes, &tmA, &full[stage], kb * kBK, arow);
-                    tma_load_2d(smB + stage * kBBytes, &tmB, &full[stage], kb * kBK, brow);
-                    if (++stage == kStages2) { stage = 0; phase ^= 1; }
+                    uint8_t* sa = smA + stage * C::kABytes;
+                    uint8_t* sb = smB + stage * C::kBBytes;
+                    if constexpr (kPair == 2) {
+                        const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+                        if (rank == 0)
+                            mbar_arrive_expect_tx(&full[stage], 2 * (C::kABytes + C::kBBytes));
+                        else
+                            mbar_arrive_cluster(fb);
+                        tma_load_2d_pair(sa, &tmA, fb, kb * kBK, arow, pol);
+                        tma_load_2d_pair(sb, &tmB, fb, kb * kBK, brow, pol);
+                    } else {
+                        mbar_arrive_expect_tx(&full[stage], C::kABytes + C::kBBytes);
+                        tma_load_2d(sa, &tmA, &full[stage], kb * kBK, arow, pol);
+                        tma_load_2d(sb, &tmB, &full[stage], kb * kBK, brow, pol);
+                    }
+                    if (++stage == C::kStages) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (lane == 0 && rank == 0) {
             // ------------------------------------------------------------ MMA issuer
-            constexpr uint32_t idesc = idesc_i8(kBM, kBN);
+            constexpr uint32_t idesc = idesc_i8(C::kTileM, kBN);
             uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
             const uint32_t a0 = smem_u32(smA), b0 = smem_u32(smB);
-            for (int64_t t = blockIdx.x;; t += gridDim.x) {
+            for (int64_t t = unit0;; t += units) {
                 int32_t bm, bn;
                 if (!sch.get(t, bm, bn)) break;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -129,120 +158,243 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint32_t sa = a0 + stage * kABytes, sb = b0 + stage * kBBytes;
+                    const uint32_t sa = a0 + stage * C::kABytes, sb = b0 + stage * C::kBBytes;
 #pragma unroll
-                    for (int k = 0; k < kBK / kUMMA_K; ++k)
-                        mma_i8(d, smem_desc_sw128(sa + k * kUMMA_K),
-                               smem_desc_sw128(sb + k * kUMMA_K), idesc, (kb | k) != 0);
-                    mma_commit(&empty[stage]);
-                    if (++stage == kStages2) { stage = 0; phase ^= 1; }
+                    for (int k = 0; k < kBK / kUMMA_K; ++k) {
+                        const uint64_t ad = smem_desc_sw128(sa + k * kUMMA_K);
+                        const uint64_t bd = smem_desc_sw128(sb + k * kUMMA_K);
+                        if constexpr (kPair == 2) mma_i8_pair(d, ad, bd, idesc, (kb | k) != 0);
+                        else mma_i8(d, ad, bd, idesc, (kb | k) != 0);
+                    }
+                    if constexpr (kPair == 2) mma_commit_pair(&empty[stage], 3);
+                    else mma_commit(&empty[stage]);
+                    if (++stage == C::kStages) { stage = 0; phase ^= 1; }
                 }
-                mma_commit(&tfull[acc]);
+                if constexpr (kPair == 2) mma_commit_pair(&tfull[acc], 3);
+                else mma_commit(&tfull[acc]);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
         __syncwarp();
     } else {
         // ---------------------------------------------------------------- epilogue
+        // Each warp drains its 32-lane TMEM quadrant with tcgen05.ld.16x256b: per 8-column
+        // chunk a thread holds 2 consecutive records of 4 rows, so tallies (16 B/record)
+        // and fp64 CCC (32 B/record) leave as 256-bit stores of whole L2 sectors straight
+        // from registers -- no shared-memory staging, which would compete with the TMA
+        // fills and tensor-core operand reads of the mainloop.
         const uint32_t quad = warp & 3;            // TMEM lane quadrant of this warp
-        const uint32_t row_in_tile = quad * 32 + lane;
         const int64_t nB = args.nB, a_end = args.a_lo + args.nA;
         const uint32_t fl = (uint32_t)args.out_flags;
         const bool want_t = fl & 1u, want_c64 = fl & 2u, want_c32 = fl & 4u, want_ck = fl & 8u;
+        const bool want_c = want_c64 | want_c32;
         const uint32_t four_nf = 4u * (uint32_t)args.n_f;
         const double inv4nf = 1.0 / (4.0 * (double)args.n_f);
+        const uint32_t tempty_leader = kPair == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
+        const int32_t cpair = 2 * (int32_t)(lane & 3);   // my 2 columns within a chunk
         unsigned long long ck_lo = 0, ck_hi = 0;
         uint32_t acc = 0, acc_phase = 0;
-        for (int64_t t = blockIdx.x;; t += gridDim.x) {
+        for (int64_t t = unit0;; t += units) {
             int32_t bm, bn;
             if (!sch.get(t, bm, bn)) break;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            const int64_t i = args.a_lo + (int64_t)bm * kBM + row_in_tile;
-            const bool row_ok = i < a_end;
-            int32_t s_i = 0;
-            double wi0 = 0.0, wi1 = 0.0;
-            if (row_ok) {
-                s_i = __ldg(args.s_a + i);
-                wi0 = __ldg(args.w_a + 2 * i);
-                wi1 = __ldg(args.w_a + 2 * i + 1);
-            }
-            const int64_t rec_i = args.diag
-                                      ? (i * (2 * nB - i - 1)) / 2 - i - 1 - args.rec_row_base
-                                      : (i - args.a_lo) * nB;
-            const uint32_t two_si = 2u * (uint32_t)s_i;
-            const uint64_t gi = (uint64_t)(args.a_row0 + i);
-            const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + acc * kBN;
-            for (int c = 0; c < kBN / 16; ++c) {
-                uint32_t v[16];
-                tmem_ld16(taddr + c * 16, v);
-                tmem_ld_wait();
-                const int64_t j0 = (int64_t)bn * kBN + c * 16;
+            // my 4 rows: r = quad*32 + h*16 + e*8 + lane/4, h, e in {0,1}
+            int64_t rec_r[4];
+            int32_t jlo_r[4], jhi_r[4];
+            uint32_t two_si[4];
+            double wi0[4], wi1[4];
+            uint64_t gi[4];
+            bool my_any = false;
 #pragma unroll
-                for (int u = 0; u < 16; ++u) {
-                    const int64_t j = j0 + u;
-                    const bool ok = row_ok && j < nB && (!args.diag || j > i);
-                    if (!ok) continue;
-                    const uint32_t g = v[u];
-                    const int32_t s_j = __ldg(args.s_b + j);
-                    const uint32_t two_sj = 2u * (uint32_t)s_j;
-                    const uint32_t t11 = g, t10 = two_si - g, t01 = two_sj - g;
-                    const uint32_t t00 = four_nf - two_si - two_sj + g;
-                    const int64_t rec = rec_i + j;
-                    if (want_t) st_v4_u32(args.tallies + 4 * rec, t00, t01, t10, t11);
-                    if (want_c64 | want_c32) {
-                        const double wj0 = __ldg(args.w_b + 2 * j);
-                        const double wj1 = __ldg(args.w_b + 2 * j + 1);
-                        const double c00 = (double)t00 * inv4nf * wi0 * wj0;
-                        const double c01 = (double)t01 * inv4nf * wi0 * wj1;
-                        const double c10 = (double)t10 * inv4nf * wi1 * wj0;
-                        const double c11 = (double)t11 * inv4nf * wi1 * wj1;
-                        if (want_c64) {
-                            double* p = reinterpret_cast<double*>(args.ccc) + 4 * rec;
-                            st_v2_f64(p, c00, c01);
-                            st_v2_f64(p + 2, c10, c11);
+            for (int r = 0; r < 4; ++r) {
+                const int64_t i = args.a_lo + (int64_t)bm * C::kTileM + rank * 128 + quad * 32 +
+                                  (r >> 1) * 16 + (r & 1) * 8 + (lane >> 2);
+                const bool row_ok = i < a_end;
+                two_si[r] = row_ok ? 2u * (uint32_t)__ldg(args.s_a + i) : 0u;
+                wi0[r] = row_ok ? __ldg(args.w_a + 2 * i) * inv4nf : 0.0;   // w_i(0) / (4 n_f)
+                wi1[r] = row_ok ? __ldg(args.w_a + 2 * i + 1) * inv4nf : 0.0;
+                rec_r[r] = args.diag ? (i * (2 * nB - i - 1)) / 2 - i - 1 - args.rec_row_base
+                                     : (i - args.a_lo) * nB;
+                jlo_r[r] = args.diag ? (int32_t)(i + 1) : 0;
+                jhi_r[r] = row_ok ? (int32_t)nB : 0;
+                gi[r] = (uint64_t)(args.a_row0 + i);
+                my_any |= row_ok && jlo_r[r] < jhi_r[r];
+            }
+            const bool any_row = __any_sync(0xffffffffu, my_any);
+            const int32_t warp_jlo = __shfl_sync(0xffffffffu, jlo_r[0], 0);
+            const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + acc * kBN;
+            for (int c = 0; c < kBN / 8; ++c) {
+                const int32_t j0 = bn * kBN + c * 8;
+                if (!any_row || j0 >= nB || j0 + 8 <= warp_jlo) continue;  // warp-uniform
+                uint32_t va[4], vb[4];
+                tmem_ld_16x256(taddr + c * 8, va);                  // lanes +0..15
+                tmem_ld_16x256(taddr + (16u << 16) + c * 8, vb);    // lanes +16..31
+                const int32_t jA = j0 + cpair, jB = jA + 1;
+                const int32_t jAc = jA < nB ? jA : (int32_t)nB - 1;
+                const int32_t jBc = jB < nB ? jB : (int32_t)nB - 1;
+                const uint32_t two_sA = 2u * (uint32_t)__ldg(args.s_b + jAc);
+                const uint32_t two_sB = 2u * (uint32_t)__ldg(args.s_b + jBc);
+                double wA0 = 0.0, wA1 = 0.0, wB0 = 0.0, wB1 = 0.0;
+                if (want_c) {
+                    wA0 = __ldg(args.w_b + 2 * jAc);
+                    wA1 = __ldg(args.w_b + 2 * jAc + 1);
+                    wB0 = __ldg(args.w_b + 2 * jBc);
+                    wB1 = __ldg(args.w_b + 2 * jBc + 1);
+                }
+                tmem_ld_wait();
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const uint32_t gA = (r >> 1) ? vb[(r & 1) * 2] : va[(r & 1) * 2];
+                    const uint32_t gB = (r >> 1) ? vb[(r & 1) * 2 + 1] : va[(r & 1) * 2 + 1];
+                    const bool okA = jA >= jlo_r[r] && jA < jhi_r[r];
+                    const bool okB = jB >= jlo_r[r] && jB < jhi_r[r];
+                    if (!(okA | okB)) continue;
+                    // Eq.2 tallies from G (rho(0) = 2 - rho(1))
+                    const uint32_t a11 = gA, a10 = two_si[r] - gA, a01 = two_sA - gA;
+                    const uint32_t a00 = four_nf - two_si[r] - two_sA + gA;
+                    const uint32_t b11 = gB, b10 = two_si[r] - gB, b01 = two_sB - gB;
+                    const uint32_t b00 = four_nf - two_si[r] - two_sB + gB;
+                    const int64_t recA = rec_r[r] + jA;
+                    if (want_t) {
+                        uint32_t* p = args.tallies + 4 * recA;
+                        if (okA && okB && !(recA & 1)) {
+                            stg_256_u32(p, a00, a01, a10, a11, b00, b01, b10, b11);
                         } else {
-                            float* p = reinterpret_cast<float*>(args.ccc) + 4 * rec;
-                            st_v4_f32(p, (float)c00, (float)c01, (float)c10, (float)c11);
+                            if (okA) stg_128_u32(p, a00, a01, a10, a11);
+                            if (okB) stg_128_u32(p + 4, b00, b01, b10, b11);
                         }
                     }
-                    if (args.g_out) args.g_out[i * args.ldg + j] = (int32_t)g;
+                    if (want_c) {
+                        // Eq.3: CCC(a,b) = T(a,b) / (4 n_f) * w_i(a) * w_j(b)
+                        const double ca00 = (double)a00 * wi0[r] * wA0, ca01 = (double)a01 * wi0[r] * wA1;
+                        const double ca10 = (double)a10 * wi1[r] * wA0, ca11 = (double)a11 * wi1[r] * wA1;
+                        const double cb00 = (double)b00 * wi0[r] * wB0, cb01 = (double)b01 * wi0[r] * wB1;
+                        const double cb10 = (double)b10 * wi1[r] * wB0, cb11 = (double)b11 * wi1[r] * wB1;
+                        if (want_c64) {
+                            double* p = reinterpret_cast<double*>(args.ccc) + 4 * recA;
+                            if (okA) stg_256_f64(p, ca00, ca01, ca10, ca11);
+                            if (okB) stg_256_f64(p + 4, cb00, cb01, cb10, cb11);
+                        } else {
+                            float* p = reinterpret_cast<float*>(args.ccc) + 4 * recA;
+                            if (okA && okB && !(recA & 1)) {
+                                stg_256_u32(p, __float_as_uint((float)ca00), __float_as_uint((float)ca01),
+                                            __float_as_uint((float)ca10), __float_as_uint((float)ca11),
+                                            __float_as_uint((float)cb00), __float_as_uint((float)cb01),
+                                            __float_as_uint((float)cb10), __float_as_uint((float)cb11));
+                            } else {
+                                if (okA)
+                                    stg_128_u32(p, __float_as_uint((float)ca00), __float_as_uint((float)ca01),
+                                                __float_as_uint((float)ca10), __float_as_uint((float)ca11));
+                                if (okB)
+                                    stg_128_u32(p + 4, __float_as_uint((float)cb00), __float_as_uint((float)cb01),
+                                                __float_as_uint((float)cb10), __float_as_uint((float)cb11));
+                            }
+                        }
+                    }
+                    if (args.g_out) {
+                        const int64_t i = rec_r[r] + 0;  // unused placeholder to keep types clear
+                        (void)i;
+                        const int64_t row = (int64_t)(gi[r] - (uint64_t)args.a_row0);
+                        if (okA) args.g_out[row * args.ldg + jA] = (int32_t)gA;
+                        if (okB) args.g_out[row * args.ldg + jB] = (int32_t)gB;
+                    }
                     if (want_ck) {
-                        const uint64_t gj = (uint64_t)(args.b_row0 + j);
-                        ck_fold(ck_lo, ck_hi, (2ull << 60) | (gi << 40) | (gj << 20),
-                                (uint64_t)t00 | ((uint64_t)t01 << 32),
-                                (uint64_t)t10 | ((uint64_t)t11 << 32));
+                        if (okA)
+                            ck_fold(ck_lo, ck_hi,
+                                    (2ull << 60) | (gi[r] << 40) | ((uint64_t)(args.b_row0 + jA) << 20),
+                                    (uint64_t)a00 | ((uint64_t)a01 << 32), (uint64_t)a10 | ((uint64_t)a11 << 32));
+                        if (okB)
+                            ck_fold(ck_lo, ck_hi,
+                                    (2ull << 60) | (gi[r] << 40) | ((uint64_t)(args.b_row0 + jB) << 20),
+                                    (uint64_t)b00 | ((uint64_t)b01 << 32), (uint64_t)b10 | ((uint64_t)b11 << 32));
                     }
                 }
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+                if (kPair == 2 && rank != 0) mbar_arrive_cluster(tempty_leader + acc * 8u);
+                else mbar_arrive(&tempty[acc]);
+            }
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
         if (want_ck) ck_flush(ck_lo, ck_hi, args.checksum);
     }
 
     tc_fence_before();
-    __syncthreads();
+    if constexpr (kPair == 2) cluster_sync();
+    else __syncthreads();
     tc_fence_after();
-    if (warp == 1) tmem_dealloc<512>(tmem_base);
+    if (warp == 1) {
+        if constexpr (kPair == 2) tmem_dealloc_pair<512>(tmem_base);
+        else tmem_dealloc<512>(tmem_base);
+    }
 }
 
 // ------------------------------------------------------------------------- host side
+static int pair_mode() {
+    static int mode = -1;
+    if (mode < 0) {
+        const char* e = getenv("CCC_TALLY2_CTA");
+        mode = (e && e[0] == '1') ? 1 : 2;
+    }
+    return mode;
+}
+
+int tally2_tile_rows() { return pair_mode() == 2 ? 256 : 128; }
+int tally2_b_box_rows() { return pair_mode() == 2 ? Cfg2<2>::kBRows : Cfg2<1>::kBRows; }
+
 cudaError_t launch_tally2(const CUtensorMap& tmA, const CUtensorMap& tmB, const Tally2Args& a,
                           int num_sms, cudaStream_t stream, int64_t* n_tiles_out) {
+    const int pm = pair_mode();
+    {   // experiment: persisting-L2 set-aside so that evict_last operand lines survive
+        static int done = 0;
+        const char* e = getenv("CCC_L2_PERSIST_MB");
+        if (e && !done) {
+            done = 1;
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)atol(e) << 20);
+        }
+    }
     TriSched sch;
-    sch.init(a.a_lo, a.nA, a.nB, a.diag);
+    Tally2Args a2 = a;
+    {
+        const char* e = getenv("CCC_SUPER");
+        a2.sup_elems = e ? atoi(e) : 2048;
+        const char* f = getenv("CCC_EPI");
+        a2.epi_flags = f ? atoi(f) : 0;
+    }
+    sch.init(a.a_lo, a.nA, a.nB, a.diag, pm == 2 ? Cfg2<2>::kTileM : Cfg2<1>::kTileM, a2.sup_elems);
     const int64_t tiles = sch.total();
     if (n_tiles_out) *n_tiles_out = tiles;
     if (tiles == 0) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(tally2_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
+    if (pm == 1) {
+        cudaError_t e = cudaFuncSetAttribute(tally2_kernel<1>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             Cfg2<1>::kSmem);
+        if (e != cudaSuccess) return e;
+        const int grid = (int)(tiles < num_sms ? tiles : num_sms);
+        tally2_kernel<1><<<grid, kThreads2, Cfg2<1>::kSmem, stream>>>(tmA, tmB, a2);
+        return cudaGetLastError();
+    }
+    cudaError_t e = cudaFuncSetAttribute(tally2_kernel<2>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg2<2>::kSmem);
     if (e != cudaSuccess) return e;
-    const int grid = (int)(tiles < num_sms ? tiles : num_sms);
-    tally2_kernel<<<grid, kThreads2, kSmem2, stream>>>(tmA, tmB, a);
-    return cudaGetLastError();
+    const int64_t pairs = num_sms / 2;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(2 * (tiles < pairs ? tiles : pairs)));
+    cfg.blockDim = dim3(kThreads2);
+    cfg.dynamicSmemBytes = Cfg2<2>::kSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, tally2_kernel<2>, tmA, tmB, a2);
 }
 
 }  // namespace ccc

@@ -160,6 +160,7 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         if (lane == 0) {
             // ---------------------------------------------------------- TMA producer
             uint32_t stage = 0, phase = 0;
+            const uint64_t pol = policy_evict_last();
             for (int64_t u = blockIdx.x;; u += gridDim.x) {
                 int32_t J, K;
                 int64_t i;
@@ -168,8 +169,8 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&full[stage], kABytes3 + kBBytes3 + kPivBytes);
-                    tma_load_2d(smA + stage * kABytes3, &tmA, &full[stage], kb * kBK, J * kBM);
-                    tma_load_2d(smB + stage * kBBytes3, &tmB, &full[stage], kb * kBK, K * kBN);
+                    tma_load_2d(smA + stage * kABytes3, &tmA, &full[stage], kb * kBK, J * kBM, pol);
+                    tma_load_2d(smB + stage * kBBytes3, &tmB, &full[stage], kb * kBK, K * kBN, pol);
                     bulk_load(smP + stage * kPivBytes, prow + (int64_t)kb * kBK, kPivBytes,
                               &full[stage]);
                     if (++stage == kStages3) { stage = 0; phase ^= 1; }
