@@ -360,12 +360,14 @@ def main():
         ops = 2.0 * r["comparisons"]
     else:
         ops = 2.0 * r["comparisons"] / wl["n_st"]
-    int8_peak = 2.0 * pk["bf16_tflops_sustained"]   # int8 dense = 2 x bf16 dense (nominal ratio)
+    # int8 dense = 2 x bf16 dense (the guide's nominal ratio, 4.5 vs 2.25 PFLOP/s); the
+    # burst figure applies: the timed region is ~0.1 s of back-to-back steps, not seconds.
+    int8_peak = 2.0 * pk["bf16_tflops"]
     achieved = ops / k_s / 1e12
     roof = {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s",
             "frac": achieved / int8_peak, "traffic": ncu_traffic(r["kernel"]),
             "kernel": r["kernel"], "kernel_ms": r["kernel_ms"],
-            "peak_source": f"2 x bf16_tflops_sustained of MEASURED_PEAKS.json ({pk_kind}); "
+            "peak_source": f"2 x bf16_tflops (burst) of MEASURED_PEAKS.json ({pk_kind}); "
                            "int8 ops = 2 per MAC = 2 per comparison",
             "nominal_int8_frac": achieved / 4500.0}
     hbm_write = r["out_bytes"] / (ms_step / 1e3) / 1e9

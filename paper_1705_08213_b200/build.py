@@ -11,6 +11,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libccc.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+EXTRA = os.environ.get("CCC_NVCC_EXTRA", "").split()
 
 
 def sources():
@@ -35,7 +36,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
            "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
-           "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+           "-I", os.path.join(ROOT, "include"), "-I", CSRC] + EXTRA + [
            "-Xptxas", "-v" if verbose else "-O3",
            "-o", tmp] + sources()
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -71,7 +71,7 @@ def lib():
     """Load libccc.so (built in-tree by __graft_entry__.build()); raise if absent."""
     global _lib
     if _lib is None:
-        path = _build.LIB
+        path = os.environ.get("CCC_LIB", _build.LIB)   # alternate in-tree build variants
         if not os.path.exists(path):
             raise ImportError(f"libccc.so not built at {path}: run __graft_entry__.build() "
                               "(there is no CPU fallback)")

@@ -193,7 +193,8 @@ ccc_status block_impl(const int8_t* N_a, const int32_t* s_a, const double* w_a, 
     a.g_out = g;
     a.ldg = ldg;
     a.rec_row_base = diag ? (a_lo * (2 * n_b - a_lo - 1)) / 2 : 0;
-    a.sup_elems = 2048;
+    a.sup_rows = 2048;
+    a.sup_cols = 2048;   // 2048 x 2048-element super tiles (measured best)
     int64_t tiles = 0;
     CCC_CUDA(ccc::launch_tally2(tmA, tmB, a, num_sms, stream, &tiles), "tally2 launch");
     if (tiles) ++g_launches;

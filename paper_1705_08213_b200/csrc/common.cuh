@@ -29,14 +29,15 @@ struct TriSched {
     int64_t base;
 
     __host__ __device__ void init(int64_t a_lo_, int64_t nA_, int64_t nB_, int diag_,
-                                  int32_t bm_rows_ = kBM, int32_t sup_elems = 2048) {
+                                  int32_t bm_rows_ = kBM, int32_t sup_rows = 2048,
+                                  int32_t sup_cols = 2048) {
         a_lo = a_lo_;
         nA = nA_;
         nB = nB_;
         diag = diag_;
         bm_rows = bm_rows_;
-        sup_m = sup_elems / bm_rows;
-        sup_n = sup_elems / kBN;
+        sup_m = sup_rows / bm_rows > 0 ? sup_rows / bm_rows : 1;
+        sup_n = sup_cols / kBN > 0 ? sup_cols / kBN : 1;
         nbm = (int32_t)((nA + bm_rows - 1) / bm_rows);
         nbn = (int32_t)((nB + kBN - 1) / kBN);
         SP = (nbm + sup_m - 1) / sup_m;
@@ -118,8 +119,8 @@ struct Tally2Args {
     int32_t* g_out;            // optional raw G
     int64_t ldg;
     int64_t rec_row_base;      // diag: record index of row a_lo's first pair
-    int32_t sup_elems;         // super-tile edge (elements) of the tile raster
-    int32_t epi_flags;         // internal epilogue variants (bit 0: evict_first stores)
+    int32_t sup_rows, sup_cols;  // super-tile shape (elements) of the tile raster
+    unsigned long long* trace; // optional per-tile %globaltimer trace (diagnostics)
 };
 
 // Kernel arguments of the fused 3-way pivot GEMM (KB-3W).

@@ -76,6 +76,14 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const void* tmap, ui
         : "memory");
 }
 
+// L2 prefetch of a 2-D tensor box (no shared memory, no completion tracking).
+__device__ __forceinline__ void tma_prefetch_2d(const void* tmap, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
+                     reinterpret_cast<uint64_t>(tmap)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
+
 // 1-D bulk copy global -> shared (size multiple of 16, both 16-B aligned).
 __device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes,
                                           uint64_t* bar) {
@@ -313,6 +321,12 @@ __device__ __forceinline__ void stg_128_u32(void* p, uint32_t a, uint32_t b, uin
 }
 
 // ---------------------------------------------------------------- misc
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ uint64_t fmix64(uint64_t k) {
     k ^= k >> 33;
     k *= 0xFF51AFD7ED558CCDull;

@@ -20,7 +20,12 @@
 #include "common.cuh"
 #include "internal.h"
 
+#include <cstdio>
 #include <cstdlib>
+
+#ifndef CCC_PAIR_STAGES
+#define CCC_PAIR_STAGES 6
+#endif
 
 namespace ccc {
 
@@ -52,7 +57,11 @@ __device__ __forceinline__ void ck_flush(unsigned long long lo, unsigned long lo
     }
 }
 
-constexpr int kThreads2 = 192;
+#ifndef CCC_EPI_WARPS
+#define CCC_EPI_WARPS 4
+#endif
+constexpr int kEpiWarps2 = CCC_EPI_WARPS;          // 4 or 8 (1 or 2 per TMEM lane quadrant)
+constexpr int kThreads2 = 64 + 32 * kEpiWarps2;    // producer, MMA, epilogue warps
 
 template <int kPair>
 struct Cfg2 {
@@ -60,7 +69,7 @@ struct Cfg2 {
     static constexpr int kBRows = kBN / kPair;     // B rows held by each CTA
     static constexpr int kABytes = 128 * kBK;      // 16 KB of A per stage per CTA
     static constexpr int kBBytes = kBRows * kBK;   // B bytes per stage per CTA
-    static constexpr int kStages = kPair == 2 ? 6 : 4;
+    static constexpr int kStages = kPair == 2 ? CCC_PAIR_STAGES : 4;
     static constexpr int kBarOff = kStages * (kABytes + kBBytes);
     static constexpr int kSmem = kBarOff + 256 + 1024;
 };
@@ -95,7 +104,7 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], 4 * kPair);  // one arrive per epilogue warp of the pair
+            mbar_init(&tempty[s], kEpiWarps2 * kPair);  // one arrive per epilogue warp of the pair
         }
         fence_mbar_init();
     }
@@ -110,7 +119,7 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     const uint32_t tmem_base = *tmem_slot;
 
     TriSched sch;
-    sch.init(args.a_lo, args.nA, args.nB, args.diag, C::kTileM, args.sup_elems);
+    sch.init(args.a_lo, args.nA, args.nB, args.diag, C::kTileM, args.sup_rows, args.sup_cols);
 
     if (warp == 0) {
         if (lane == 0) {
@@ -122,6 +131,7 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 if (!sch.get(t, bm, bn)) break;
                 const int32_t arow = (int32_t)(args.a_lo + (int64_t)bm * C::kTileM + rank * 128);
                 const int32_t brow = bn * kBN + (int32_t)rank * C::kBRows;
+                if (args.trace && rank == 0) args.trace[8 * t + 6] = globaltimer();
                 for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sa = smA + stage * C::kABytes;
@@ -152,8 +162,11 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             for (int64_t t = unit0;; t += units) {
                 int32_t bm, bn;
                 if (!sch.get(t, bm, bn)) break;
+                unsigned long long* tr = args.trace ? args.trace + 8 * t : nullptr;
+                if (tr) tr[0] = globaltimer();
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
+                if (tr) tr[1] = globaltimer();
                 const uint32_t d = tmem_base + acc * kBN;
                 for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
                     mbar_wait(&full[stage], phase);
@@ -172,6 +185,7 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 }
                 if constexpr (kPair == 2) mma_commit_pair(&tfull[acc], 3);
                 else mma_commit(&tfull[acc]);
+                if (tr) tr[2] = globaltimer();
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
@@ -184,6 +198,8 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         // from registers -- no shared-memory staging, which would compete with the TMA
         // fills and tensor-core operand reads of the mainloop.
         const uint32_t quad = warp & 3;            // TMEM lane quadrant of this warp
+        const int c_begin = ((warp - 2) / 4) * (kBN / 8 / (kEpiWarps2 / 4));  // my column chunks
+        const int c_end = c_begin + kBN / 8 / (kEpiWarps2 / 4);
         const int64_t nB = args.nB, a_end = args.a_lo + args.nA;
         const uint32_t fl = (uint32_t)args.out_flags;
         const bool want_t = fl & 1u, want_c64 = fl & 2u, want_c32 = fl & 4u, want_ck = fl & 8u;
@@ -197,8 +213,11 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         for (int64_t t = unit0;; t += units) {
             int32_t bm, bn;
             if (!sch.get(t, bm, bn)) break;
+            unsigned long long* tr = (args.trace && warp == 2 && rank == 0) ? args.trace + 8 * t : nullptr;
+            if (tr && lane == 0) tr[3] = globaltimer();
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
+            if (tr && lane == 0) tr[4] = globaltimer();
             // my 4 rows: r = quad*32 + h*16 + e*8 + lane/4, h, e in {0,1}
             int64_t rec_r[4];
             int32_t jlo_r[4], jhi_r[4];
@@ -224,7 +243,7 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             const bool any_row = __any_sync(0xffffffffu, my_any);
             const int32_t warp_jlo = __shfl_sync(0xffffffffu, jlo_r[0], 0);
             const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + acc * kBN;
-            for (int c = 0; c < kBN / 8; ++c) {
+            for (int c = c_begin; c < c_end; ++c) {
                 const int32_t j0 = bn * kBN + c * 8;
                 if (!any_row || j0 >= nB || j0 + 8 <= warp_jlo) continue;  // warp-uniform
                 uint32_t va[4], vb[4];
@@ -293,8 +312,6 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         }
                     }
                     if (args.g_out) {
-                        const int64_t i = rec_r[r] + 0;  // unused placeholder to keep types clear
-                        (void)i;
                         const int64_t row = (int64_t)(gi[r] - (uint64_t)args.a_row0);
                         if (okA) args.g_out[row * args.ldg + jA] = (int32_t)gA;
                         if (okB) args.g_out[row * args.ldg + jB] = (int32_t)gB;
@@ -313,6 +330,7 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             }
             tc_fence_before();
             __syncwarp();
+            if (tr && lane == 0) tr[5] = globaltimer();
             if (lane == 0) {
                 if (kPair == 2 && rank != 0) mbar_arrive_cluster(tempty_leader + acc * 8u);
                 else mbar_arrive(&tempty[acc]);
@@ -348,23 +366,15 @@ int tally2_b_box_rows() { return pair_mode() == 2 ? Cfg2<2>::kBRows : Cfg2<1>::k
 cudaError_t launch_tally2(const CUtensorMap& tmA, const CUtensorMap& tmB, const Tally2Args& a,
                           int num_sms, cudaStream_t stream, int64_t* n_tiles_out) {
     const int pm = pair_mode();
-    {   // experiment: persisting-L2 set-aside so that evict_last operand lines survive
-        static int done = 0;
-        const char* e = getenv("CCC_L2_PERSIST_MB");
-        if (e && !done) {
-            done = 1;
-            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)atol(e) << 20);
-        }
-    }
     TriSched sch;
     Tally2Args a2 = a;
     {
-        const char* e = getenv("CCC_SUPER");
-        a2.sup_elems = e ? atoi(e) : 2048;
-        const char* f = getenv("CCC_EPI");
-        a2.epi_flags = f ? atoi(f) : 0;
+        const char* e = getenv("CCC_SUPER");   // "rows,cols" in elements
+        if (e) sscanf(e, "%d,%d", &a2.sup_rows, &a2.sup_cols);
+        const char* tre = getenv("CCC_TRACE_PTR");   // diagnostics: device pointer (decimal)
+        a2.trace = tre ? reinterpret_cast<unsigned long long*>(strtoull(tre, nullptr, 10)) : nullptr;
     }
-    sch.init(a.a_lo, a.nA, a.nB, a.diag, pm == 2 ? Cfg2<2>::kTileM : Cfg2<1>::kTileM, a2.sup_elems);
+    sch.init(a.a_lo, a.nA, a.nB, a.diag, pm == 2 ? Cfg2<2>::kTileM : Cfg2<1>::kTileM, a2.sup_rows, a2.sup_cols);
     const int64_t tiles = sch.total();
     if (n_tiles_out) *n_tiles_out = tiles;
     if (tiles == 0) return cudaSuccess;

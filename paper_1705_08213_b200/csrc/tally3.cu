@@ -30,7 +30,9 @@ constexpr int kStages3 = 4;
 constexpr int kABytes3 = kBM * kBK;  // 16 KB
 constexpr int kBBytes3 = kBN * kBK;  // 32 KB
 constexpr int kPivBytes = kBK;       // 128 B of the pivot row per stage
-constexpr int kThreads3 = 320;
+constexpr int kEpiWarps3 = 8;                                 // 2 per TMEM lane quadrant
+constexpr int kXfWarps3 = 4;                                  // transform warps (1 row each lane)
+constexpr int kThreads3 = 32 * (2 + kEpiWarps3 + kXfWarps3);  // 448
 constexpr int kPivOff3 = kStages3 * (kABytes3 + kBBytes3);
 constexpr int kBarOff3 = kPivOff3 + kStages3 * kPivBytes;
 constexpr int kSmem3 = kBarOff3 + 256 + 1024;
@@ -143,7 +145,7 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], 4);
+            mbar_init(&tempty[s], kEpiWarps3);
         }
         fence_mbar_init();
     }
@@ -206,9 +208,9 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             }
         }
         __syncwarp();
-    } else if (warp >= 6) {
+    } else if (warp >= 2 + kEpiWarps3) {
         // -------------------------------------------------------------- transform
-        const uint32_t r = (uint32_t)(warp - 6) * 32 + lane;  // tile row 0..127
+        const uint32_t r = (uint32_t)(warp - 2 - kEpiWarps3) * 32 + lane;  // tile row 0..127
         uint32_t stage = 0, phase = 0;
         for (int64_t u = blockIdx.x;; u += gridDim.x) {
             int32_t J, K;
@@ -238,14 +240,20 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         }
     } else {
         // -------------------------------------------------------------- epilogue
+        // Register-only drain (as in KB-2W): tcgen05.ld.16x256b gives a thread 2
+        // consecutive k of 4 rows j; each triple record is 32 B of tallies + 64 B of fp64
+        // CCC, i.e. whole L2 sectors written with 256-bit stores.
+        // 8 warps: warp w drains lanes [half*16, half*16+16) of TMEM quadrant w % 4
         const uint32_t quad = warp & 3;
-        const uint32_t row_in_tile = quad * 32 + lane;
+        const uint32_t half = (uint32_t)(warp - 2) >> 2;
         const int64_t n_v = args.n_v;
         const uint32_t fl = (uint32_t)args.out_flags;
         const bool want_t = fl & 1u, want_c64 = fl & 2u, want_c32 = fl & 4u, want_ck = fl & 8u;
+        const bool want_c = want_c64 | want_c32;
         const uint32_t eight_nf = 8u * (uint32_t)args.n_f;
         const double inv8nf = 1.0 / (8.0 * (double)args.n_f);
         const int64_t c3n = c3(n_v);
+        const int32_t cpair = 2 * (int32_t)(lane & 3);
         unsigned long long ck_lo = 0, ck_hi = 0;
         uint32_t acc = 0, acc_phase = 0;
         for (int64_t u = blockIdx.x;; u += gridDim.x) {
@@ -254,79 +262,102 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             if (!sch.get(u, J, K, i)) break;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            const int64_t j = (int64_t)J * kBM + row_in_tile;
-            const bool row_ok = j > i && j < n_v;
-            int32_t s_i = __ldg(args.s + i), s_j = 0, g_ij = 0;
-            const double wi0 = __ldg(args.w + 2 * i), wi1 = __ldg(args.w + 2 * i + 1);
-            double wij[4] = {0.0, 0.0, 0.0, 0.0};
-            int64_t rec_j = 0;
-            if (row_ok) {
-                s_j = __ldg(args.s + j);
-                g_ij = __ldg(args.G + i * n_v + j);
-                const double wj0 = __ldg(args.w + 2 * j), wj1 = __ldg(args.w + 2 * j + 1);
-                wij[0] = wi0 * wj0;  // (a,b) = (0,0)
-                wij[1] = wi0 * wj1;
-                wij[2] = wi1 * wj0;
-                wij[3] = wi1 * wj1;
-                rec_j = c3n - c3(n_v - i) + c2(n_v - i - 1) - c2(n_v - j) - j - 1 - args.rec_begin;
-            }
-            const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + acc * kBN;
-            for (int c = 0; c < kBN / 16; ++c) {
-                uint32_t v[16];
-                tmem_ld16(taddr + c * 16, v);
-                tmem_ld_wait();
-                const int64_t k0 = (int64_t)K * kBN + c * 16;
-#pragma unroll 4
-                for (int u2 = 0; u2 < 16; ++u2) {
-                    const int64_t k = k0 + u2;
-                    if (!(row_ok && k > j && k < n_v)) continue;
-                    const uint32_t g3 = v[u2];
-                    const uint32_t gij = (uint32_t)g_ij;
-                    const uint32_t gik = (uint32_t)__ldg(args.G + i * n_v + k);
-                    const uint32_t gjk = (uint32_t)__ldg(args.G + j * n_v + k);
-                    const uint32_t si = (uint32_t)s_i, sj = (uint32_t)s_j;
-                    const uint32_t sk = (uint32_t)__ldg(args.s + k);
-                    uint32_t t[8];
-                    t[7] = g3;                                       // (1,1,1)
-                    t[6] = 2u * gij - g3;                            // (1,1,0)
-                    t[5] = 2u * gik - g3;                            // (1,0,1)
-                    t[3] = 2u * gjk - g3;                            // (0,1,1)
-                    t[4] = 4u * si - 2u * gij - 2u * gik + g3;       // (1,0,0)
-                    t[2] = 4u * sj - 2u * gij - 2u * gjk + g3;       // (0,1,0)
-                    t[1] = 4u * sk - 2u * gik - 2u * gjk + g3;       // (0,0,1)
-                    t[0] = eight_nf - 4u * (si + sj + sk) + 2u * (gij + gik + gjk) - g3;
-                    const int64_t rec = rec_j + k;
-                    if (want_t) {
-                        uint32_t* p = args.tallies + 8 * rec;
-                        st_v4_u32(p, t[0], t[1], t[2], t[3]);
-                        st_v4_u32(p + 4, t[4], t[5], t[6], t[7]);
-                    }
-                    if (want_c64 | want_c32) {
-                        const double wk0 = __ldg(args.w + 2 * k), wk1 = __ldg(args.w + 2 * k + 1);
-                        double cc[8];
+            const uint32_t s_i = (uint32_t)__ldg(args.s + i);
+            const double wi0 = __ldg(args.w + 2 * i) * inv8nf, wi1 = __ldg(args.w + 2 * i + 1) * inv8nf;
+            // my 2 rows j = J*128 + quad*32 + half*16 + r*8 + lane/4
+            int64_t rec_r[2], j_r[2];
+            uint32_t s_j[2], g_ij[2];
+            double wij[2][4];
+            bool ok_r[2];
+            bool my_any = false;
 #pragma unroll
-                        for (int ab = 0; ab < 4; ++ab) {
-                            cc[2 * ab + 0] = (double)t[2 * ab + 0] * inv8nf * wij[ab] * wk0;
-                            cc[2 * ab + 1] = (double)t[2 * ab + 1] * inv8nf * wij[ab] * wk1;
+            for (int r = 0; r < 2; ++r) {
+                const int64_t j = (int64_t)J * kBM + quad * 32 + half * 16 + r * 8 + (lane >> 2);
+                j_r[r] = j;
+                ok_r[r] = j > i && j < n_v;
+                const int64_t jc = j < n_v ? j : n_v - 1;
+                s_j[r] = (uint32_t)__ldg(args.s + jc);
+                g_ij[r] = ok_r[r] ? (uint32_t)__ldg(args.G + i * n_v + j) : 0u;
+                const double wj0 = __ldg(args.w + 2 * jc), wj1 = __ldg(args.w + 2 * jc + 1);
+                wij[r][0] = wi0 * wj0;  // (a,b) = (0,0), includes 1/(8 n_f)
+                wij[r][1] = wi0 * wj1;
+                wij[r][2] = wi1 * wj0;
+                wij[r][3] = wi1 * wj1;
+                rec_r[r] = c3n - c3(n_v - i) + c2(n_v - i - 1) - c2(n_v - jc) - jc - 1 - args.rec_begin;
+                my_any |= ok_r[r];
+            }
+            const bool any_row = __any_sync(0xffffffffu, my_any);
+            const int64_t warp_jmin = __shfl_sync(0xffffffffu, j_r[0], 0);
+            const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + acc * kBN;
+            for (int c = 0; c < kBN / 8; ++c) {
+                const int64_t k0 = (int64_t)K * kBN + c * 8;
+                if (!any_row || k0 >= n_v || k0 + 8 <= warp_jmin + 1) continue;  // warp-uniform
+                uint32_t va[4];
+                tmem_ld_16x256(taddr + ((half * 16u) << 16) + c * 8, va);
+                const int64_t kA = k0 + cpair, kB = kA + 1;
+                const int64_t kAc = kA < n_v ? kA : n_v - 1, kBc = kB < n_v ? kB : n_v - 1;
+                const uint32_t sA = (uint32_t)__ldg(args.s + kAc), sB = (uint32_t)__ldg(args.s + kBc);
+                const uint32_t gikA = (uint32_t)__ldg(args.G + i * n_v + kAc);
+                const uint32_t gikB = (uint32_t)__ldg(args.G + i * n_v + kBc);
+                double wA0 = 0.0, wA1 = 0.0, wB0 = 0.0, wB1 = 0.0;
+                if (want_c) {
+                    wA0 = __ldg(args.w + 2 * kAc);
+                    wA1 = __ldg(args.w + 2 * kAc + 1);
+                    wB0 = __ldg(args.w + 2 * kBc);
+                    wB1 = __ldg(args.w + 2 * kBc + 1);
+                }
+                tmem_ld_wait();
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    if (!ok_r[r]) continue;
+                    const int64_t j = j_r[r];
+                    const uint32_t g3v[2] = {va[r * 2], va[r * 2 + 1]};
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int64_t k = h ? kB : kA;
+                        if (!(k > j && k < n_v)) continue;
+                        const uint32_t g3 = g3v[h];
+                        const uint32_t gij = g_ij[r], gik = h ? gikB : gikA;
+                        const uint32_t gjk = (uint32_t)__ldg(args.G + j * n_v + k);
+                        const uint32_t si = s_i, sj = s_j[r], sk = h ? sB : sA;
+                        uint32_t t[8];   // Eq.5 cells, index 4a+2b+c, by inclusion-exclusion
+                        t[7] = g3;                                       // (1,1,1)
+                        t[6] = 2u * gij - g3;                            // (1,1,0)
+                        t[5] = 2u * gik - g3;                            // (1,0,1)
+                        t[3] = 2u * gjk - g3;                            // (0,1,1)
+                        t[4] = 4u * si - 2u * gij - 2u * gik + g3;       // (1,0,0)
+                        t[2] = 4u * sj - 2u * gij - 2u * gjk + g3;       // (0,1,0)
+                        t[1] = 4u * sk - 2u * gik - 2u * gjk + g3;       // (0,0,1)
+                        t[0] = eight_nf - 4u * (si + sj + sk) + 2u * (gij + gik + gjk) - g3;
+                        const int64_t rec = rec_r[r] + k;
+                        if (want_t)
+                            stg_256_u32(args.tallies + 8 * rec, t[0], t[1], t[2], t[3], t[4], t[5],
+                                        t[6], t[7]);
+                        if (want_c) {
+                            // Eq.4: CCC = T / (8 n_f) * w_i(a) w_j(b) w_k(c)
+                            const double wk0 = h ? wB0 : wA0, wk1 = h ? wB1 : wA1;
+                            double cc[8];
+#pragma unroll
+                            for (int ab = 0; ab < 4; ++ab) {
+                                cc[2 * ab + 0] = (double)t[2 * ab + 0] * wij[r][ab] * wk0;
+                                cc[2 * ab + 1] = (double)t[2 * ab + 1] * wij[r][ab] * wk1;
+                            }
+                            if (want_c64) {
+                                double* p = reinterpret_cast<double*>(args.ccc) + 8 * rec;
+                                stg_256_f64(p, cc[0], cc[1], cc[2], cc[3]);
+                                stg_256_f64(p + 4, cc[4], cc[5], cc[6], cc[7]);
+                            } else {
+                                float* p = reinterpret_cast<float*>(args.ccc) + 8 * rec;
+                                stg_256_u32(p, __float_as_uint((float)cc[0]), __float_as_uint((float)cc[1]),
+                                            __float_as_uint((float)cc[2]), __float_as_uint((float)cc[3]),
+                                            __float_as_uint((float)cc[4]), __float_as_uint((float)cc[5]),
+                                            __float_as_uint((float)cc[6]), __float_as_uint((float)cc[7]));
+                            }
                         }
-                        if (want_c64) {
-                            double* p = reinterpret_cast<double*>(args.ccc) + 8 * rec;
-                            st_v2_f64(p, cc[0], cc[1]);
-                            st_v2_f64(p + 2, cc[2], cc[3]);
-                            st_v2_f64(p + 4, cc[4], cc[5]);
-                            st_v2_f64(p + 6, cc[6], cc[7]);
-                        } else {
-                            float* p = reinterpret_cast<float*>(args.ccc) + 8 * rec;
-                            st_v4_f32(p, (float)cc[0], (float)cc[1], (float)cc[2], (float)cc[3]);
-                            st_v4_f32(p + 4, (float)cc[4], (float)cc[5], (float)cc[6],
-                                      (float)cc[7]);
-                        }
+                        if (want_ck)
+                            ck_fold3(ck_lo, ck_hi,
+                                     (3ull << 60) | ((uint64_t)i << 40) | ((uint64_t)j << 20) | (uint64_t)k, t);
                     }
-                    if (want_ck)
-                        ck_fold3(ck_lo, ck_hi,
-                                 (3ull << 60) | ((uint64_t)i << 40) | ((uint64_t)j << 20) |
-                                     (uint64_t)k,
-                                 t);
                 }
             }
             tc_fence_before();
