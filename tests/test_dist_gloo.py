@@ -1,0 +1,122 @@
+"""World-size-2 (and 3, 4) gloo tests of the block-circulant ring orchestration on CPU.
+
+The ring logic of paper_1705_08213_b200.dist (which block is resident at which step, the
+A/B roles of every unit, record layouts, the 128-bit checksum reduction) runs unchanged;
+the kernels are replaced by an oracle-backed CPU backend defined here (test code only).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synthgen
+from paper_1705_08213_b200 import decomp
+
+
+class OracleBackend:
+    """CPU stand-in: 'packed' = the raw codes, 'expanded' = (codes, None, None)."""
+
+    def __init__(self, n_f):
+        self.n_f = n_f
+
+    def pack(self, codes, out=None):
+        if out is not None:
+            out.copy_(codes)
+            return out
+        return codes.clone()
+
+    def packed_empty(self, rows):
+        return torch.zeros((rows, self.n_f), dtype=torch.uint8)
+
+    def expand(self, packed, out=None):
+        return (packed.clone(), None, None)
+
+    def expanded_empty(self, rows):
+        return (torch.zeros((rows, self.n_f), dtype=torch.uint8), None, None)
+
+    def outputs(self, n_rec):
+        return (torch.zeros((n_rec, 4), dtype=torch.int64), torch.zeros((n_rec, 4), dtype=torch.float64))
+
+    def checksum_zero(self):
+        return torch.zeros(2, dtype=torch.int64)
+
+    def block(self, A, a_row0, a_lo, a_hi, B, b_row0, diag, out, ck, timed=False):
+        ca, cb = A[0].numpy(), B[0].numpy()
+        idx = []
+        for il in range(a_lo, a_hi):
+            for jl in range(il + 1 if diag else 0, cb.shape[0]):
+                idx.append((il, ca.shape[0] + jl))
+        both = np.concatenate([ca, cb])
+        T, C = oracle.pairs(both, np.array(idx, dtype=np.int64).reshape(-1, 2))
+        out[0][:] = torch.from_numpy(T)
+        out[1][:] = torch.from_numpy(C)
+        gidx = np.array([(a_row0 + i, b_row0 + j - ca.shape[0]) for i, j in idx]).reshape(-1, 2)
+        v = oracle.checksum(2, gidx, T)
+        lo, hi = v & ((1 << 64) - 1), v >> 64
+        cur_lo, cur_hi = (int(x) & ((1 << 64) - 1) for x in ck.tolist())
+        s = ((cur_hi << 64) | cur_lo) + ((hi << 64) | lo)
+        s &= (1 << 128) - 1
+        to_i64 = lambda u: u - (1 << 64) if u >= (1 << 63) else u
+        ck[0] = to_i64(s & ((1 << 64) - 1))
+        ck[1] = to_i64(s >> 64)
+        return 1
+
+
+def _worker(rank, world, port, n_v, n_f, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1705_08213_b200.dist import Ring2Way, checksum_total
+        bounds = decomp.block_bounds(n_v, world)
+        lo, hi = bounds[rank]
+        codes = synthgen.random_codes(hi - lo, n_f, seed=5, row0=lo)
+        ring = Ring2Way(OracleBackend(n_f), bounds, rank, world)
+        outs = ring.run(codes)
+        ck = checksum_total(ring.ck)
+        recs = []
+        for u, (T, C) in zip(ring.units, outs):
+            pairs = list(decomp.unit2_pairs(u, bounds))
+            recs.append((pairs, T.numpy(), C.numpy()))
+        q.put((rank, ck, recs))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_ring_2way_gloo(world):
+    n_v, n_f = 23, 37
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n_v, n_f, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    codes = synthgen.random_codes(n_v, n_f, seed=5)
+    To, Co = oracle.all_pairs(codes)
+    index = {tuple(p): r for r, p in enumerate(oracle.pair_list(n_v))}
+    seen = set()
+    for rank, ck, recs in res:
+        assert ck == oracle.checksum(2, oracle.pair_list(n_v), To)   # same on every rank
+        for pairs, T, C in recs:
+            for k, pr in enumerate(pairs):
+                assert pr not in seen
+                seen.add(pr)
+                np.testing.assert_array_equal(T[k], To[index[pr]])
+                np.testing.assert_allclose(C[k], Co[index[pr]], rtol=1e-15)
+    assert len(seen) == n_v * (n_v - 1) // 2
