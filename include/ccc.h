@@ -183,6 +183,40 @@ ccc_status ccc_3way_stage(int64_t n_v, int64_t n_f, int64_t n_stages, int64_t st
                           uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
                           uint64_t* checksum_d, void* ws_d, size_t ws_bytes, void* stream);
 
+/* One vector block as seen by the 3-way unit call: expanded rows (ccc_expand) and the
+ * global index of local row 0. */
+typedef struct {
+    const int8_t* N;      /* [rows][ccc_k_pad(n_f)], 128-B aligned (device) */
+    const int32_t* s;     /* [rows] allele-1 sums (device)                   */
+    const double* w;      /* [rows][2] frequency weights (device)            */
+    int64_t rows;
+    int64_t row0;         /* global index of local row 0; blocks are disjoint */
+} ccc_block;
+
+/* Records produced by ccc_3way_unit for these ranges (see its layouts); -1 if invalid. */
+int64_t ccc_3way_unit_records(const ccc_block* bp, int64_t p_lo, int64_t p_hi,
+                              const ccc_block* bm, int64_t m_lo, int64_t m_hi,
+                              const ccc_block* bn, int64_t n_lo, int64_t n_hi);
+
+/* One unit of the tetrahedral 3-way decomposition (§4): every
+ * unique triple {p, m, n} with pivot p in [p_lo,p_hi) of block bp, m in [m_lo,m_hi) of bm
+ * (GEMM rows) and n in [n_lo,n_hi) of bn (GEMM columns), where bp == bm implies m > p and
+ * bm == bn implies n > m (blocks are identified by row0).  `order` (0..5) says which role
+ * sits in each slot of the sorted triple (i<j<k): roles p=0, m=1, n=2, orders
+ * 0:(p,m,n) 1:(p,n,m) 2:(m,p,n) 3:(m,n,p) 4:(n,p,m) 5:(n,m,p); records hold the canonical
+ * (Eq.5-ordered) cells.  G_d: the pairwise G = N N^T by GLOBAL index, G[min*ldG + max]
+ * (upper triangle, e.g. from ccc_2way_block with g_d).  Record layouts:
+ *   bp==bm==bn : in-block lexicographic triple order, starting at the first pivot p_lo;
+ *   bp==bm     : record = (in-block pair index of (p,m) - that of (p_lo,p_lo+1)) * |N| + n-n_lo;
+ *   otherwise  : ((p-p_lo)*|M| + (m-m_lo))*|N| + (n-n_lo).
+ * Outputs and flags as in ccc_3way_stage; the checksum digest uses global canonical
+ * indices, so unit checksums of a decomposition add up to the single-GPU checksum. */
+ccc_status ccc_3way_unit(const ccc_block* bp, int64_t p_lo, int64_t p_hi, const ccc_block* bm,
+                         int64_t m_lo, int64_t m_hi, const ccc_block* bn, int64_t n_lo,
+                         int64_t n_hi, int order, const int32_t* G_d, int64_t ldG, int64_t n_f,
+                         uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
+                         uint64_t* checksum_d, void* stream);
+
 /* ccc_3way_prepare followed by ccc_3way_stage(n_stages, stage). */
 ccc_status ccc_3way(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
                     uint32_t out_flags, int64_t n_stages, int64_t stage, uint32_t* tallies_d,

@@ -28,6 +28,12 @@ class CCCError(RuntimeError):
         self.status = status
 
 
+class CccBlock(ctypes.Structure):
+    """struct ccc_block of include/ccc.h."""
+    _fields_ = [("N", ctypes.c_void_p), ("s", ctypes.c_void_p), ("w", ctypes.c_void_p),
+                ("rows", ctypes.c_int64), ("row0", ctypes.c_int64)]
+
+
 _lib = None
 _vp, _i64, _u32, _dbl, _int, _sz = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32,
                                     ctypes.c_double, ctypes.c_int, ctypes.c_size_t)
@@ -51,6 +57,9 @@ _SIGS = {
     "ccc_3way_prepare": (_int, [_vp, _i64, _i64, _dbl, _vp, _sz, _vp]),
     "ccc_3way_stage": (_int, [_i64, _i64, _i64, _i64, _u32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "ccc_3way": (_int, [_vp, _i64, _i64, _dbl, _u32, _i64, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "ccc_3way_unit_records": (_i64, [_vp, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _i64]),
+    "ccc_3way_unit": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _i64, _int, _vp, _i64,
+                             _i64, _u32, _vp, _vp, _vp, _vp]),
     "ccc_e2e_workspace_bytes": (_sz, [_i64, _i64, _u32]),
     "ccc_2way_host": (_int, [_vp, _i64, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _sz, _vp]),
 }
@@ -263,6 +272,37 @@ def ccc_3way(packed, n_f, gamma=GAMMA, out_flags=OUT_TALLY | OUT_CCC_F64, n_stag
         ws = workspace(3, n_v, n_f, packed.device)
     _check(lib().ccc_3way(_p(packed), n_v, n_f, gamma, out_flags, n_stages, stage, _p(tallies),
                           _p(ccc), _p(checksum), _p(ws), ws.numel(), _stream(stream)))
+    return tallies, ccc, checksum
+
+
+ORDERS = {("p", "m", "n"): 0, ("p", "n", "m"): 1, ("m", "p", "n"): 2, ("m", "n", "p"): 3,
+          ("n", "p", "m"): 4, ("n", "m", "p"): 5}
+
+
+def block(N, s, w, row0: int) -> CccBlock:
+    """ccc_block descriptor of an expanded block (keep the tensors alive)."""
+    _dev(N, torch.int8, "N"), _dev(s, torch.int32, "s"), _dev(w, torch.float64, "w")
+    return CccBlock(N.data_ptr(), s.data_ptr(), w.data_ptr(), N.shape[0], row0)
+
+
+def ccc_3way_unit_records(bp, p_lo, p_hi, bm, m_lo, m_hi, bn, n_lo, n_hi) -> int:
+    return lib().ccc_3way_unit_records(ctypes.byref(bp), p_lo, p_hi, ctypes.byref(bm), m_lo, m_hi,
+                                       ctypes.byref(bn), n_lo, n_hi)
+
+
+def ccc_3way_unit(bp, p_lo, p_hi, bm, m_lo, m_hi, bn, n_lo, n_hi, order, G, n_f,
+                  out_flags=OUT_TALLY | OUT_CCC_F64, tallies=None, ccc=None, checksum=None,
+                  stream=None):
+    """One tetrahedral 3-way unit; `order` is a role tuple like ("m", "p", "n") or 0..5."""
+    if not isinstance(order, int):
+        order = ORDERS[tuple(order)]
+    n_rec = ccc_3way_unit_records(bp, p_lo, p_hi, bm, m_lo, m_hi, bn, n_lo, n_hi)
+    if n_rec < 0:
+        raise ValueError("invalid unit ranges")
+    tallies, ccc, checksum = _outputs(n_rec, 8, out_flags, G.device, tallies, ccc, checksum)
+    _check(lib().ccc_3way_unit(ctypes.byref(bp), p_lo, p_hi, ctypes.byref(bm), m_lo, m_hi,
+                               ctypes.byref(bn), n_lo, n_hi, order, _p(G), G.shape[-1], n_f,
+                               out_flags, _p(tallies), _p(ccc), _p(checksum), _stream(stream)))
     return tallies, ccc, checksum
 
 

@@ -404,25 +404,121 @@ ccc_status ccc_3way_stage(int64_t n_v, int64_t n_f, int64_t n_stages, int64_t st
     CCC_CHECK(check_device(&sms));
     uint8_t* ws = static_cast<uint8_t*>(ws_d);
     const int64_t k_pad = kpad_of(n_f);
+    ccc::Blk3 b{reinterpret_cast<const int8_t*>(ws + L.N), reinterpret_cast<const int32_t*>(ws + L.s),
+                reinterpret_cast<const double*>(ws + L.w), n_v, 0};
     ccc::Tally3Args a{};
-    a.n_v = n_v;
-    a.i_begin = rng[0];
-    a.i_end = rng[1];
-    a.rec_begin = rng[2];
+    a.bp = a.bm = a.bn = b;
+    a.p_lo = rng[0];
+    a.p_hi = rng[1];
+    a.m_lo = 0;
+    a.m_hi = n_v;
+    a.n_lo = 0;
+    a.n_hi = n_v;
+    a.same_pm = a.same_mn = 1;
+    a.order = 0;
+    a.layout = 0;
+    a.G = reinterpret_cast<const int32_t*>(ws + L.G);
+    a.ldG = n_v;
+    a.rec_base = rng[2];
+    a.k_pad = k_pad;
     a.n_f = (int32_t)n_f;
     a.k_blocks = (int32_t)(k_pad / ccc::kBK);
     a.out_flags = (int32_t)out_flags;
-    a.N = reinterpret_cast<const int8_t*>(ws + L.N);
-    a.k_pad = k_pad;
-    a.s = reinterpret_cast<const int32_t*>(ws + L.s);
-    a.w = reinterpret_cast<const double*>(ws + L.w);
-    a.G = reinterpret_cast<const int32_t*>(ws + L.G);
     a.tallies = tallies_d;
     a.ccc = ccc_d;
     a.checksum = reinterpret_cast<unsigned long long*>(checksum_d);
     CUtensorMap tmA, tmB;
-    CCC_CHECK(make_tmap(&tmA, a.N, n_v, k_pad, ccc::kBM));
-    CCC_CHECK(make_tmap(&tmB, a.N, n_v, k_pad, ccc::kBN));
+    CCC_CHECK(make_tmap(&tmA, b.N, n_v, k_pad, ccc::kBM));
+    CCC_CHECK(make_tmap(&tmB, b.N, n_v, k_pad, ccc::kBN));
+    int64_t units = 0;
+    CCC_CUDA(ccc::launch_tally3(tmA, tmB, a, sms, (cudaStream_t)stream, &units), "tally3 launch");
+    if (units) g_launches = 1;
+    return CCC_OK;
+}
+
+int64_t ccc_3way_unit_records(const ccc_block* bp, int64_t p_lo, int64_t p_hi,
+                              const ccc_block* bm, int64_t m_lo, int64_t m_hi,
+                              const ccc_block* bn, int64_t n_lo, int64_t n_hi) {
+    if (!bp || !bm || !bn || p_lo < 0 || p_hi < p_lo || m_lo < 0 || m_hi < m_lo || n_lo < 0 ||
+        n_hi < n_lo)
+        return -1;
+    const bool spm = bp->row0 == bm->row0, smn = bm->row0 == bn->row0;
+    if (spm && smn) {   // one block, whole ranges for m and n: triples with p in [p_lo, p_hi)
+        const int64_t nb = bp->rows;
+        return c3(nb - p_lo) - c3(nb - p_hi);
+    }
+    if (spm) {          // pairs (p < m) of the block with p in [p_lo, p_hi), times |N|
+        const int64_t nb = bp->rows;
+        auto rs = [&](int64_t i) { return i * (2 * nb - i - 1) / 2; };
+        return (rs(p_hi) - rs(p_lo)) * (n_hi - n_lo);
+    }
+    return (p_hi - p_lo) * (m_hi - m_lo) * (n_hi - n_lo);
+}
+
+ccc_status ccc_3way_unit(const ccc_block* bp, int64_t p_lo, int64_t p_hi, const ccc_block* bm,
+                         int64_t m_lo, int64_t m_hi, const ccc_block* bn, int64_t n_lo,
+                         int64_t n_hi, int order, const int32_t* G_d, int64_t ldG, int64_t n_f,
+                         uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
+                         uint64_t* checksum_d, void* stream) {
+    g_launches = 0;
+    if (!bp || !bm || !bn) return fail(CCC_ERR_INVALID_ARGUMENT, "block descriptors must not be NULL");
+    CCC_CHECK(check_sizes(bp->rows, n_f));
+    CCC_CHECK(check_sizes(bm->rows, n_f));
+    CCC_CHECK(check_sizes(bn->rows, n_f));
+    if (out_flags & ~15u) return fail(CCC_ERR_INVALID_ARGUMENT, "unknown out_flags bits");
+    if (order < 0 || order > 5) return fail(CCC_ERR_INVALID_ARGUMENT, "order must be 0..5");
+    if (!(0 <= p_lo && p_lo <= p_hi && p_hi <= bp->rows && 0 <= m_lo && m_lo <= m_hi &&
+          m_hi <= bm->rows && 0 <= n_lo && n_lo <= n_hi && n_hi <= bn->rows))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "ranges must lie inside their blocks");
+    const bool spm = bp->row0 == bm->row0, smn = bm->row0 == bn->row0;
+    const bool spn = bp->row0 == bn->row0;
+    if ((spm && bp->N != bm->N) || (smn && bm->N != bn->N))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "blocks with equal row0 must be the same block");
+    if (spn && !spm) return fail(CCC_ERR_INVALID_ARGUMENT, "pivot and column block equal but row block differs");
+    if (smn && !(m_lo == 0 && n_lo == 0 && m_hi == bm->rows && n_hi == bn->rows))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "same row/column block needs whole ranges");
+    if (spm && !smn && !(m_lo == 0 && m_hi == bm->rows))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "same pivot/row block needs the whole row range");
+    const int64_t recs = ccc_3way_unit_records(bp, p_lo, p_hi, bm, m_lo, m_hi, bn, n_lo, n_hi);
+    if (recs == 0) return CCC_OK;
+    CCC_CHECK(check_outputs(out_flags, tallies_d, ccc_d, checksum_d));
+    if (!G_d || ldG <= 0) return fail(CCC_ERR_INVALID_ARGUMENT, "G_d must be a [ldG][ldG] pairwise G");
+    for (const ccc_block* b : {bp, bm, bn})
+        if (!b->N || !b->s || !b->w || !aligned(b->N, 128) || b->row0 < 0 || b->row0 + b->rows > ldG)
+            return fail(CCC_ERR_INVALID_ARGUMENT, "block N (128-B aligned), s, w, row0 + rows <= ldG");
+    int sms;
+    CCC_CHECK(check_device(&sms));
+    const int64_t k_pad = kpad_of(n_f);
+    ccc::Tally3Args a{};
+    a.bp = ccc::Blk3{bp->N, bp->s, bp->w, bp->rows, bp->row0};
+    a.bm = ccc::Blk3{bm->N, bm->s, bm->w, bm->rows, bm->row0};
+    a.bn = ccc::Blk3{bn->N, bn->s, bn->w, bn->rows, bn->row0};
+    a.p_lo = p_lo;
+    a.p_hi = p_hi;
+    a.m_lo = m_lo;
+    a.m_hi = m_hi;
+    a.n_lo = n_lo;
+    a.n_hi = n_hi;
+    a.same_pm = spm;
+    a.same_mn = smn;
+    a.order = order;
+    a.layout = (spm && smn) ? 0 : spm ? 1 : 2;
+    const int64_t nb = bp->rows;
+    if (a.layout == 0) a.rec_base = c3(nb) - c3(nb - p_lo);
+    else if (a.layout == 1) a.rec_base = (p_lo * (2 * nb - p_lo - 1) / 2) * (n_hi - n_lo);
+    else a.rec_base = 0;
+    a.G = G_d;
+    a.ldG = ldG;
+    a.k_pad = k_pad;
+    a.n_f = (int32_t)n_f;
+    a.k_blocks = (int32_t)(k_pad / ccc::kBK);
+    a.out_flags = (int32_t)out_flags;
+    a.tallies = tallies_d;
+    a.ccc = ccc_d;
+    a.checksum = reinterpret_cast<unsigned long long*>(checksum_d);
+    CUtensorMap tmA, tmB;
+    CCC_CHECK(make_tmap(&tmA, bm->N, bm->rows, k_pad, ccc::kBM));
+    CCC_CHECK(make_tmap(&tmB, bn->N, bn->rows, k_pad, ccc::kBN));
     int64_t units = 0;
     CCC_CUDA(ccc::launch_tally3(tmA, tmB, a, sms, (cudaStream_t)stream, &units), "tally3 launch");
     if (units) g_launches = 1;

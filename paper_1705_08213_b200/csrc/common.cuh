@@ -22,7 +22,7 @@ constexpr uint64_t kCkHi = 0x13198A2E03707344ull;
 // tiles, row-major inside) so that the ~148 concurrently active tiles share few A / B
 // panels in L2.
 struct TriSched {
-    int64_t a_lo, nA, nB;
+    int64_t a_lo, nA, nB, b_lo;   // rows [a_lo, a_lo+nA); cols [b_lo, b_lo+nB) (b_lo = 0 if diag)
     int32_t diag, bm_rows, sup_m, sup_n, nbm, nbn, SP, SQ;
     // cursor
     int32_t P, Q, cnt;
@@ -34,6 +34,7 @@ struct TriSched {
         a_lo = a_lo_;
         nA = nA_;
         nB = nB_;
+        b_lo = 0;
         diag = diag_;
         bm_rows = bm_rows_;
         sup_m = sup_rows / bm_rows > 0 ? sup_rows / bm_rows : 1;
@@ -123,22 +124,31 @@ struct Tally2Args {
     unsigned long long* trace; // optional per-tile %globaltimer trace (diagnostics)
 };
 
-// Kernel arguments of the fused 3-way pivot GEMM (KB-3W).
+// One vector block as seen by the 3-way kernel.
+struct Blk3 {
+    const int8_t* N;       // [rows][k_pad]
+    const int32_t* s;      // [rows]
+    const double* w;       // [rows][2]
+    int64_t rows;
+    int64_t row0;          // global index of local row 0
+};
+
+// Kernel arguments of the fused 3-way pivot GEMM (KB-3W).  A unit computes the triples
+// {p, m, n} with p in [p_lo,p_hi) of block bp (the pivot), m in [m_lo,m_hi) of bm (GEMM
+// rows), n in [n_lo,n_hi) of bn (GEMM columns); same_pm => m > p, same_mn => n > m.
+// `order` names the role (0 = p, 1 = m, 2 = n) in each canonical (sorted) slot.
 struct Tally3Args {
-    int64_t n_v;
-    int64_t i_begin, i_end;    // pivot range of the stage
-    int64_t rec_begin;         // record index of the stage's first triple
-    int32_t n_f;
-    int32_t k_blocks;
-    int32_t out_flags;
-    int32_t pad_;
-    const int8_t* N;           // [n_v][K_pad]  (pivot rows read directly)
+    Blk3 bp, bm, bn;
+    int64_t p_lo, p_hi, m_lo, m_hi, n_lo, n_hi;
+    int32_t same_pm, same_mn, order, layout;   // layout: 0 in-block lexicographic,
+                                               // 1 pair(p,m)-major x n, 2 dense box
+    const int32_t* G;          // global pairwise G: G[min * ldG + max] (i < j valid)
+    int64_t ldG;
+    int64_t rec_base;          // subtracted from every record index (stages)
     int64_t k_pad;
-    const int32_t* s;
-    const double* w;
-    const int32_t* G;          // [n_v][n_v] pairwise G (upper triangle valid)
-    uint32_t* tallies;         // [rec_count][8]
-    void* ccc;
+    int32_t n_f, k_blocks, out_flags, pad_;
+    uint32_t* tallies;         // [records][8]
+    void* ccc;                 // [records][8] double or float
     unsigned long long* checksum;
 };
 

@@ -130,7 +130,7 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 int32_t bm, bn;
                 if (!sch.get(t, bm, bn)) break;
                 const int32_t arow = (int32_t)(args.a_lo + (int64_t)bm * C::kTileM + rank * 128);
-                const int32_t brow = bn * kBN + (int32_t)rank * C::kBRows;
+                const int32_t brow = (int32_t)sch.b_lo + bn * kBN + (int32_t)rank * C::kBRows;
                 if (args.trace && rank == 0) args.trace[8 * t + 6] = globaltimer();
                 for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);

@@ -1,25 +1,25 @@
 // tally3.cu -- KB-3W: per-pivot Hadamard-weighted tcgen05 kind::i8 GEMM with the
-// fused 3-way CCC epilogue (stages a8).
+// fused 3-way CCC epilogue (stages a8, tetrahedral units §8(e)).
 //
-// Method (§2.2, Eq.4-5): for a pivot vector i (the FIRST index of the
-// triple, so that a stage = a contiguous i-range = a contiguous slice of the
-// lexicographic result array, cf. stages P:621-626),
-//     G3_ijk = sum_q n_iq n_jq n_kq = ((N_J o n_i) N_K^T)_jk,
-// one GEMM whose A operand is the Hadamard product of a row block of N with the
-// pivot row.  All eight cells follow from G3, the pairwise G (precomputed by KB-2W)
-// and s by inclusion-exclusion (rho(0) = 2 - rho(1)):
-//     T111 = G3, T110 = 2G_ij - G3, T101 = 2G_ik - G3, T011 = 2G_jk - G3,
-//     T100 = 4s_i - 2G_ij - 2G_ik + G3, T010 = 4s_j - 2G_ij - 2G_jk + G3,
-//     T001 = 4s_k - 2G_ik - 2G_jk + G3,
-//     T000 = 8n_f - 4(s_i+s_j+s_k) + 2(G_ij+G_ik+G_jk) - G3.
+// Method (§2.2, Eq.4-5): for a pivot vector p,
+//     G3_pmn = sum_q n_pq n_mq n_nq = ((N_M o n_p) N_N^T)_mn,
+// one GEMM whose A operand is the Hadamard product of a row block of N with the pivot
+// row.  With rho(0) = 2 - rho(1) all eight cells follow from G3, the pairwise
+// G (precomputed by KB-2W) and s by inclusion-exclusion, in role order (p, m, n):
+//     T111 = G3, T110 = 2G_pm - G3, T101 = 2G_pn - G3, T011 = 2G_mn - G3,
+//     T100 = 4s_p - 2G_pm - 2G_pn + G3, T010 = 4s_m - 2G_pm - 2G_mn + G3,
+//     T001 = 4s_n - 2G_pn - 2G_mn + G3,
+//     T000 = 8n_f - 4(s_p+s_m+s_n) + 2(G_pm+G_pn+G_mn) - G3,
+// then permuted to the canonical slot order of the sorted triple (Eq.5's (i,j,k)).
 // The paper instead runs three masked mGEMM3 per pivot (Table 1); this
 // needs one int8 MAC per unique 3-way comparison.
 //
-// Work unit = (row tile J of 128 j's, column tile K of 256 k's, pivot i); units are
-// ordered tile-outer / pivot-inner so the ~148 concurrent CTAs share the same N_J,
-// N_K panels in L2 and differ only in their 128-byte pivot rows.
+// A work unit is (row tile J of 128 m's, column tile K of 256 n's, pivot p); units are
+// ordered tile-outer / pivot-inner so the ~148 concurrent CTAs share the same N_M, N_N
+// panels in L2 and differ only in their 128-byte pivot rows.
 // Warp roles: 0 TMA producer (A, B tiles + pivot chunk), 1 TMEM alloc + MMA issuer,
-// 2..5 epilogue, 6..9 transform (A <- A o n_i in shared memory, in place).
+// 2..9 epilogue (2 per TMEM lane quadrant), 10..13 transform (A <- A o n_p in shared
+// memory, in place, then fence.proxy.async so the tensor core sees it).
 #include "sm100.cuh"
 #include "common.cuh"
 #include "internal.h"
@@ -31,31 +31,44 @@ constexpr int kABytes3 = kBM * kBK;  // 16 KB
 constexpr int kBBytes3 = kBN * kBK;  // 32 KB
 constexpr int kPivBytes = kBK;       // 128 B of the pivot row per stage
 constexpr int kEpiWarps3 = 8;                                 // 2 per TMEM lane quadrant
-constexpr int kXfWarps3 = 4;                                  // transform warps (1 row each lane)
-constexpr int kThreads3 = 32 * (2 + kEpiWarps3 + kXfWarps3);  // 448
+constexpr int kXfWarps3 = 2;                                  // transform warps (2 rows/lane)
+constexpr int kThreads3 = 32 * (2 + kEpiWarps3 + kXfWarps3);  // 384
 constexpr int kPivOff3 = kStages3 * (kABytes3 + kBBytes3);
 constexpr int kBarOff3 = kPivOff3 + kStages3 * kPivBytes;
 constexpr int kSmem3 = kBarOff3 + 256 + 1024;
 
+// Units: (m-tile, n-tile) in TriSched order (triangular when m and n share a block),
+// pivots innermost.
 struct PivotSched {
     TriSched tiles;
-    int64_t n_v, i_begin, i_end, tt, base, cnt;
-    int32_t J, K;
+    int64_t p_lo, p_hi, m_lo, m_hi, n_lo, n_hi, tt, base, cnt;
+    int32_t same_pm, same_mn, J, K;
 
     __host__ __device__ int64_t pivots(int32_t Jt, int32_t Kt) const {
-        int64_t jmax = (int64_t)Jt * kBM + kBM - 1;
-        if (jmax > n_v - 1) jmax = n_v - 1;
-        int64_t kmax = (int64_t)Kt * kBN + kBN - 1;
-        if (kmax > n_v - 1) kmax = n_v - 1;
-        int64_t imax = jmax < kmax - 1 ? jmax : kmax - 1;  // pivots i < imax
-        int64_t hi = i_end < imax ? i_end : imax;
-        return hi > i_begin ? hi - i_begin : 0;
+        int64_t m_max = tiles.a_lo + (int64_t)Jt * kBM + kBM - 1;
+        if (m_max > m_hi - 1) m_max = m_hi - 1;
+        int64_t n_max = tiles.b_lo + (int64_t)Kt * kBN + kBN - 1;
+        if (n_max > n_hi - 1) n_max = n_hi - 1;
+        int64_t hi = p_hi;
+        if (same_pm && hi > m_max) hi = m_max;                        // some m > p
+        if (same_pm && same_mn && hi > n_max - 1) hi = n_max - 1;     // some p < m < n
+        return hi > p_lo ? hi - p_lo : 0;
     }
-    __host__ __device__ void init(int64_t n_v_, int64_t ib, int64_t ie) {
-        n_v = n_v_;
-        i_begin = ib;
-        i_end = ie;
-        tiles.init(0, n_v, n_v, 1);
+    __host__ __device__ void init(const Tally3Args& a) {
+        p_lo = a.p_lo;
+        p_hi = a.p_hi;
+        m_lo = a.m_lo;
+        m_hi = a.m_hi;
+        n_lo = a.n_lo;
+        n_hi = a.n_hi;
+        same_pm = a.same_pm;
+        same_mn = a.same_mn;
+        if (same_mn) {
+            tiles.init(0, m_hi, n_hi, 1);           // m, n over the same [0, rows) range
+        } else {
+            tiles.init(m_lo, m_hi - m_lo, n_hi - n_lo, 0);
+            tiles.b_lo = n_lo;
+        }
         tt = 0;
         base = 0;
         cnt = 0;
@@ -63,7 +76,7 @@ struct PivotSched {
         if (tiles.get(0, J, K)) cnt = pivots(J, K);
         else tt = -1;
     }
-    __host__ __device__ bool get(int64_t u, int32_t& Jo, int32_t& Ko, int64_t& io) {
+    __host__ __device__ bool get(int64_t u, int32_t& Jo, int32_t& Ko, int64_t& po) {
         if (tt < 0) return false;
         while (u >= base + cnt) {
             base += cnt;
@@ -73,9 +86,11 @@ struct PivotSched {
         }
         Jo = J;
         Ko = K;
-        io = i_begin + (u - base);
+        po = p_lo + (u - base);
         return true;
     }
+    __host__ __device__ int64_t row0(int32_t Jt) const { return tiles.a_lo + (int64_t)Jt * kBM; }
+    __host__ __device__ int64_t col0(int32_t Kt) const { return tiles.b_lo + (int64_t)Kt * kBN; }
 };
 
 __device__ __forceinline__ void ck_fold3(unsigned long long& lo, unsigned long long& hi,
@@ -113,8 +128,40 @@ __device__ __forceinline__ uint32_t mul_012(uint32_t a, uint32_t b) {
     return (a & nz) + (a & two);
 }
 
-__device__ __forceinline__ int64_t c2(int64_t n) { return n * (n - 1) / 2; }
-__device__ __forceinline__ int64_t c3(int64_t n) { return n * (n - 1) * (n - 2) / 6; }
+__host__ __device__ __forceinline__ int64_t c2(int64_t n) { return n * (n - 1) / 2; }
+__host__ __device__ __forceinline__ int64_t c3(int64_t n) { return n * (n - 1) * (n - 2) / 6; }
+
+// Role-ordered cells (t = 4 a_p + 2 a_m + a_n) -> canonical cells (c = 4 a_s0 + 2 a_s1 + a_s2)
+// where slot s holds role R_s.
+template <int R0, int R1, int R2, typename T>
+__device__ __forceinline__ void perm_cells(const T (&in)[8], T (&out)[8]) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        const int a[3] = {(t >> 2) & 1, (t >> 1) & 1, t & 1};
+        out[4 * a[R0] + 2 * a[R1] + a[R2]] = in[t];
+    }
+}
+template <typename T>
+__device__ __forceinline__ void to_canonical(int order, const T (&in)[8], T (&out)[8]) {
+    switch (order) {
+        case 0: perm_cells<0, 1, 2>(in, out); break;
+        case 1: perm_cells<0, 2, 1>(in, out); break;
+        case 2: perm_cells<1, 0, 2>(in, out); break;
+        case 3: perm_cells<1, 2, 0>(in, out); break;
+        case 4: perm_cells<2, 0, 1>(in, out); break;
+        default: perm_cells<2, 1, 0>(in, out); break;
+    }
+}
+__host__ __device__ __forceinline__ void order_roles(int order, int& r0, int& r1, int& r2) {
+    const int tab[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    r0 = tab[order][0];
+    r1 = tab[order][1];
+    r2 = tab[order][2];
+}
+
+__device__ __forceinline__ uint32_t gpair(const int32_t* G, int64_t ld, int64_t x, int64_t y) {
+    return (uint32_t)__ldg(G + (x < y ? x * ld + y : y * ld + x));
+}
 
 __global__ void __launch_bounds__(kThreads3, 1)
 tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -140,7 +187,7 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         tma_prefetch_desc(&tmB);
         for (int s = 0; s < kStages3; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&xfull[s], 4);
+            mbar_init(&xfull[s], kXfWarps3);
             mbar_init(&empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
@@ -156,7 +203,7 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     const uint32_t tmem_base = *tmem_slot;
 
     PivotSched sch;
-    sch.init(args.n_v, args.i_begin, args.i_end);
+    sch.init(args);
 
     if (warp == 0) {
         if (lane == 0) {
@@ -165,14 +212,15 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             const uint64_t pol = policy_evict_last();
             for (int64_t u = blockIdx.x;; u += gridDim.x) {
                 int32_t J, K;
-                int64_t i;
-                if (!sch.get(u, J, K, i)) break;
-                const int8_t* prow = args.N + i * args.k_pad;
+                int64_t p;
+                if (!sch.get(u, J, K, p)) break;
+                const int8_t* prow = args.bp.N + p * args.k_pad;
+                const int32_t mrow = (int32_t)sch.row0(J), ncol = (int32_t)sch.col0(K);
                 for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&full[stage], kABytes3 + kBBytes3 + kPivBytes);
-                    tma_load_2d(smA + stage * kABytes3, &tmA, &full[stage], kb * kBK, J * kBM, pol);
-                    tma_load_2d(smB + stage * kBBytes3, &tmB, &full[stage], kb * kBK, K * kBN, pol);
+                    tma_load_2d(smA + stage * kABytes3, &tmA, &full[stage], kb * kBK, mrow, pol);
+                    tma_load_2d(smB + stage * kBBytes3, &tmB, &full[stage], kb * kBK, ncol, pol);
                     bulk_load(smP + stage * kPivBytes, prow + (int64_t)kb * kBK, kPivBytes,
                               &full[stage]);
                     if (++stage == kStages3) { stage = 0; phase ^= 1; }
@@ -187,8 +235,8 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             const uint32_t a0 = smem_u32(smA), b0 = smem_u32(smB);
             for (int64_t u = blockIdx.x;; u += gridDim.x) {
                 int32_t J, K;
-                int64_t i;
-                if (!sch.get(u, J, K, i)) break;
+                int64_t p;
+                if (!sch.get(u, J, K, p)) break;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + acc * kBN;
@@ -210,27 +258,30 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         __syncwarp();
     } else if (warp >= 2 + kEpiWarps3) {
         // -------------------------------------------------------------- transform
-        const uint32_t r = (uint32_t)(warp - 2 - kEpiWarps3) * 32 + lane;  // tile row 0..127
+        const uint32_t r_first = (uint32_t)(warp - 2 - kEpiWarps3) * 32 + lane;
         uint32_t stage = 0, phase = 0;
         for (int64_t u = blockIdx.x;; u += gridDim.x) {
             int32_t J, K;
-            int64_t i;
-            if (!sch.get(u, J, K, i)) break;
+            int64_t p;
+            if (!sch.get(u, J, K, p)) break;
             for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
                 mbar_wait(&full[stage], phase);
-                uint8_t* arow = smA + stage * kABytes3 + r * kBK;
                 const uint8_t* pv = smP + stage * kPivBytes;
 #pragma unroll
-                for (uint32_t c = 0; c < 8; ++c) {
-                    // 128-B swizzle: logical 16-B chunk c of row r sits at chunk c ^ (r & 7)
-                    uint4* pa = reinterpret_cast<uint4*>(arow + ((c ^ (r & 7u)) << 4));
-                    const uint4 y = *reinterpret_cast<const uint4*>(pv + (c << 4));
-                    uint4 x = *pa;
-                    x.x = mul_012(x.x, y.x);
-                    x.y = mul_012(x.y, y.y);
-                    x.z = mul_012(x.z, y.z);
-                    x.w = mul_012(x.w, y.w);
-                    *pa = x;
+                for (uint32_t r = r_first; r < (uint32_t)kBM; r += 32 * kXfWarps3) {
+                    uint8_t* arow = smA + stage * kABytes3 + r * kBK;
+#pragma unroll
+                    for (uint32_t c = 0; c < 8; ++c) {
+                        // 128-B swizzle: logical 16-B chunk c of row r sits at chunk c ^ (r & 7)
+                        uint4* pa = reinterpret_cast<uint4*>(arow + ((c ^ (r & 7u)) << 4));
+                        const uint4 y = *reinterpret_cast<const uint4*>(pv + (c << 4));
+                        uint4 x = *pa;
+                        x.x = mul_012(x.x, y.x);
+                        x.y = mul_012(x.y, y.y);
+                        x.z = mul_012(x.z, y.z);
+                        x.w = mul_012(x.w, y.w);
+                        *pa = x;
+                    }
                 }
                 fence_proxy_async_smem();
                 __syncwarp();
@@ -240,123 +291,141 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         }
     } else {
         // -------------------------------------------------------------- epilogue
-        // Register-only drain (as in KB-2W): tcgen05.ld.16x256b gives a thread 2
-        // consecutive k of 4 rows j; each triple record is 32 B of tallies + 64 B of fp64
-        // CCC, i.e. whole L2 sectors written with 256-bit stores.
-        // 8 warps: warp w drains lanes [half*16, half*16+16) of TMEM quadrant w % 4
+        // Register-only drain: tcgen05.ld.16x256b gives a thread 2 consecutive n of 2 rows
+        // m; a record is 32 B of tallies + 64 B of fp64 CCC = whole L2 sectors, written
+        // with 256-bit stores.  Warp w drains lanes [half*16, +16) of TMEM quadrant w % 4.
         const uint32_t quad = warp & 3;
         const uint32_t half = (uint32_t)(warp - 2) >> 2;
-        const int64_t n_v = args.n_v;
         const uint32_t fl = (uint32_t)args.out_flags;
         const bool want_t = fl & 1u, want_c64 = fl & 2u, want_c32 = fl & 4u, want_ck = fl & 8u;
         const bool want_c = want_c64 | want_c32;
         const uint32_t eight_nf = 8u * (uint32_t)args.n_f;
         const double inv8nf = 1.0 / (8.0 * (double)args.n_f);
-        const int64_t c3n = c3(n_v);
+        const int order = args.order;
+        int r0, r1, r2;
+        order_roles(order, r0, r1, r2);
+        const int64_t nbp = args.bp.rows, nN = args.n_hi - args.n_lo, nM = args.m_hi - args.m_lo;
         const int32_t cpair = 2 * (int32_t)(lane & 3);
         unsigned long long ck_lo = 0, ck_hi = 0;
         uint32_t acc = 0, acc_phase = 0;
         for (int64_t u = blockIdx.x;; u += gridDim.x) {
             int32_t J, K;
-            int64_t i;
-            if (!sch.get(u, J, K, i)) break;
+            int64_t p;
+            if (!sch.get(u, J, K, p)) break;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            const uint32_t s_i = (uint32_t)__ldg(args.s + i);
-            const double wi0 = __ldg(args.w + 2 * i) * inv8nf, wi1 = __ldg(args.w + 2 * i + 1) * inv8nf;
-            // my 2 rows j = J*128 + quad*32 + half*16 + r*8 + lane/4
-            int64_t rec_r[2], j_r[2];
-            uint32_t s_j[2], g_ij[2];
-            double wij[2][4];
+            const int64_t gp = args.bp.row0 + p;
+            const uint32_t s_p = (uint32_t)__ldg(args.bp.s + p);
+            const double wp0 = __ldg(args.bp.w + 2 * p) * inv8nf;
+            const double wp1 = __ldg(args.bp.w + 2 * p + 1) * inv8nf;
+            // my 2 rows m = row0(J) + quad*32 + half*16 + r*8 + lane/4
+            int64_t rec_r[2], m_r[2];
+            uint32_t s_m[2], g_pm[2];
+            double wpm[2][4];
             bool ok_r[2];
             bool my_any = false;
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
-                const int64_t j = (int64_t)J * kBM + quad * 32 + half * 16 + r * 8 + (lane >> 2);
-                j_r[r] = j;
-                ok_r[r] = j > i && j < n_v;
-                const int64_t jc = j < n_v ? j : n_v - 1;
-                s_j[r] = (uint32_t)__ldg(args.s + jc);
-                g_ij[r] = ok_r[r] ? (uint32_t)__ldg(args.G + i * n_v + j) : 0u;
-                const double wj0 = __ldg(args.w + 2 * jc), wj1 = __ldg(args.w + 2 * jc + 1);
-                wij[r][0] = wi0 * wj0;  // (a,b) = (0,0), includes 1/(8 n_f)
-                wij[r][1] = wi0 * wj1;
-                wij[r][2] = wi1 * wj0;
-                wij[r][3] = wi1 * wj1;
-                rec_r[r] = c3n - c3(n_v - i) + c2(n_v - i - 1) - c2(n_v - jc) - jc - 1 - args.rec_begin;
+                const int64_t m = sch.row0(J) + quad * 32 + half * 16 + r * 8 + (lane >> 2);
+                m_r[r] = m;
+                ok_r[r] = m >= args.m_lo && m < args.m_hi && (!args.same_pm || m > p);
+                const int64_t mc = m < args.m_hi ? m : args.m_hi - 1;
+                s_m[r] = (uint32_t)__ldg(args.bm.s + mc);
+                g_pm[r] = ok_r[r] ? gpair(args.G, args.ldG, gp, args.bm.row0 + m) : 0u;
+                const double wm0 = __ldg(args.bm.w + 2 * mc), wm1 = __ldg(args.bm.w + 2 * mc + 1);
+                wpm[r][0] = wp0 * wm0;  // (a_p, a_m) = (0,0), includes 1/(8 n_f)
+                wpm[r][1] = wp0 * wm1;
+                wpm[r][2] = wp1 * wm0;
+                wpm[r][3] = wp1 * wm1;
+                if (args.layout == 0)
+                    rec_r[r] = c3(nbp) - c3(nbp - p) + c2(nbp - p - 1) - c2(nbp - mc) - mc - 1 -
+                               args.rec_base;
+                else if (args.layout == 1)
+                    rec_r[r] = (p * (2 * nbp - p - 1) / 2 + mc - p - 1) * nN - args.n_lo - args.rec_base;
+                else
+                    rec_r[r] = ((p - args.p_lo) * nM + (mc - args.m_lo)) * nN - args.n_lo;
                 my_any |= ok_r[r];
             }
             const bool any_row = __any_sync(0xffffffffu, my_any);
-            const int64_t warp_jmin = __shfl_sync(0xffffffffu, j_r[0], 0);
-            const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + acc * kBN;
+            const uint32_t taddr = tmem_base + ((quad * 32u + half * 16u) << 16) + acc * kBN;
             for (int c = 0; c < kBN / 8; ++c) {
-                const int64_t k0 = (int64_t)K * kBN + c * 8;
-                if (!any_row || k0 >= n_v || k0 + 8 <= warp_jmin + 1) continue;  // warp-uniform
+                const int64_t n0 = sch.col0(K) + c * 8;
+                if (!any_row || n0 >= args.n_hi) continue;  // warp-uniform
                 uint32_t va[4];
-                tmem_ld_16x256(taddr + ((half * 16u) << 16) + c * 8, va);
-                const int64_t kA = k0 + cpair, kB = kA + 1;
-                const int64_t kAc = kA < n_v ? kA : n_v - 1, kBc = kB < n_v ? kB : n_v - 1;
-                const uint32_t sA = (uint32_t)__ldg(args.s + kAc), sB = (uint32_t)__ldg(args.s + kBc);
-                const uint32_t gikA = (uint32_t)__ldg(args.G + i * n_v + kAc);
-                const uint32_t gikB = (uint32_t)__ldg(args.G + i * n_v + kBc);
+                tmem_ld_16x256(taddr + c * 8, va);
+                const int64_t nA = n0 + cpair, nB = nA + 1;
+                const int64_t nAc = nA < args.n_hi ? nA : args.n_hi - 1;
+                const int64_t nBc = nB < args.n_hi ? nB : args.n_hi - 1;
+                const uint32_t sA = (uint32_t)__ldg(args.bn.s + nAc);
+                const uint32_t sB = (uint32_t)__ldg(args.bn.s + nBc);
+                const int64_t gnA = args.bn.row0 + nAc, gnB = args.bn.row0 + nBc;
+                const uint32_t gpnA = gpair(args.G, args.ldG, gp, gnA);
+                const uint32_t gpnB = gpair(args.G, args.ldG, gp, gnB);
                 double wA0 = 0.0, wA1 = 0.0, wB0 = 0.0, wB1 = 0.0;
                 if (want_c) {
-                    wA0 = __ldg(args.w + 2 * kAc);
-                    wA1 = __ldg(args.w + 2 * kAc + 1);
-                    wB0 = __ldg(args.w + 2 * kBc);
-                    wB1 = __ldg(args.w + 2 * kBc + 1);
+                    wA0 = __ldg(args.bn.w + 2 * nAc);
+                    wA1 = __ldg(args.bn.w + 2 * nAc + 1);
+                    wB0 = __ldg(args.bn.w + 2 * nBc);
+                    wB1 = __ldg(args.bn.w + 2 * nBc + 1);
                 }
                 tmem_ld_wait();
 #pragma unroll
                 for (int r = 0; r < 2; ++r) {
                     if (!ok_r[r]) continue;
-                    const int64_t j = j_r[r];
-                    const uint32_t g3v[2] = {va[r * 2], va[r * 2 + 1]};
+                    const int64_t m = m_r[r], gm = args.bm.row0 + m;
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        const int64_t k = h ? kB : kA;
-                        if (!(k > j && k < n_v)) continue;
-                        const uint32_t g3 = g3v[h];
-                        const uint32_t gij = g_ij[r], gik = h ? gikB : gikA;
-                        const uint32_t gjk = (uint32_t)__ldg(args.G + j * n_v + k);
-                        const uint32_t si = s_i, sj = s_j[r], sk = h ? sB : sA;
-                        uint32_t t[8];   // Eq.5 cells, index 4a+2b+c, by inclusion-exclusion
-                        t[7] = g3;                                       // (1,1,1)
-                        t[6] = 2u * gij - g3;                            // (1,1,0)
-                        t[5] = 2u * gik - g3;                            // (1,0,1)
-                        t[3] = 2u * gjk - g3;                            // (0,1,1)
-                        t[4] = 4u * si - 2u * gij - 2u * gik + g3;       // (1,0,0)
-                        t[2] = 4u * sj - 2u * gij - 2u * gjk + g3;       // (0,1,0)
-                        t[1] = 4u * sk - 2u * gik - 2u * gjk + g3;       // (0,0,1)
-                        t[0] = eight_nf - 4u * (si + sj + sk) + 2u * (gij + gik + gjk) - g3;
-                        const int64_t rec = rec_r[r] + k;
+                        const int64_t n = h ? nB : nA;
+                        if (!(n >= args.n_lo && n < args.n_hi && (!args.same_mn || n > m))) continue;
+                        const int64_t gn = h ? gnB : gnA;
+                        const uint32_t g3 = va[r * 2 + h];
+                        const uint32_t gpm = g_pm[r], gpn = h ? gpnB : gpnA;
+                        const uint32_t gmn = gpair(args.G, args.ldG, gm, gn);
+                        const uint32_t sp = s_p, sm = s_m[r], sn = h ? sB : sA;
+                        uint32_t t[8];   // role order: index 4 a_p + 2 a_m + a_n
+                        t[7] = g3;
+                        t[6] = 2u * gpm - g3;
+                        t[5] = 2u * gpn - g3;
+                        t[3] = 2u * gmn - g3;
+                        t[4] = 4u * sp - 2u * gpm - 2u * gpn + g3;
+                        t[2] = 4u * sm - 2u * gpm - 2u * gmn + g3;
+                        t[1] = 4u * sn - 2u * gpn - 2u * gmn + g3;
+                        t[0] = eight_nf - 4u * (sp + sm + sn) + 2u * (gpm + gpn + gmn) - g3;
+                        uint32_t tc[8];
+                        to_canonical(order, t, tc);
+                        const int64_t rec = rec_r[r] + n;
                         if (want_t)
-                            stg_256_u32(args.tallies + 8 * rec, t[0], t[1], t[2], t[3], t[4], t[5],
-                                        t[6], t[7]);
+                            stg_256_u32(args.tallies + 8 * rec, tc[0], tc[1], tc[2], tc[3], tc[4],
+                                        tc[5], tc[6], tc[7]);
                         if (want_c) {
-                            // Eq.4: CCC = T / (8 n_f) * w_i(a) w_j(b) w_k(c)
-                            const double wk0 = h ? wB0 : wA0, wk1 = h ? wB1 : wA1;
-                            double cc[8];
+                            // Eq.4: CCC = T / (8 n_f) * w_p(a_p) w_m(a_m) w_n(a_n)
+                            const double wn0 = h ? wB0 : wA0, wn1 = h ? wB1 : wA1;
+                            double cr[8], cc[8];
 #pragma unroll
                             for (int ab = 0; ab < 4; ++ab) {
-                                cc[2 * ab + 0] = (double)t[2 * ab + 0] * wij[r][ab] * wk0;
-                                cc[2 * ab + 1] = (double)t[2 * ab + 1] * wij[r][ab] * wk1;
+                                cr[2 * ab + 0] = (double)t[2 * ab + 0] * wpm[r][ab] * wn0;
+                                cr[2 * ab + 1] = (double)t[2 * ab + 1] * wpm[r][ab] * wn1;
                             }
+                            to_canonical(order, cr, cc);
                             if (want_c64) {
-                                double* p = reinterpret_cast<double*>(args.ccc) + 8 * rec;
-                                stg_256_f64(p, cc[0], cc[1], cc[2], cc[3]);
-                                stg_256_f64(p + 4, cc[4], cc[5], cc[6], cc[7]);
+                                double* q = reinterpret_cast<double*>(args.ccc) + 8 * rec;
+                                stg_256_f64(q, cc[0], cc[1], cc[2], cc[3]);
+                                stg_256_f64(q + 4, cc[4], cc[5], cc[6], cc[7]);
                             } else {
-                                float* p = reinterpret_cast<float*>(args.ccc) + 8 * rec;
-                                stg_256_u32(p, __float_as_uint((float)cc[0]), __float_as_uint((float)cc[1]),
+                                float* q = reinterpret_cast<float*>(args.ccc) + 8 * rec;
+                                stg_256_u32(q, __float_as_uint((float)cc[0]), __float_as_uint((float)cc[1]),
                                             __float_as_uint((float)cc[2]), __float_as_uint((float)cc[3]),
                                             __float_as_uint((float)cc[4]), __float_as_uint((float)cc[5]),
                                             __float_as_uint((float)cc[6]), __float_as_uint((float)cc[7]));
                             }
                         }
-                        if (want_ck)
+                        if (want_ck) {
+                            const int64_t g[3] = {gp, gm, gn};
                             ck_fold3(ck_lo, ck_hi,
-                                     (3ull << 60) | ((uint64_t)i << 40) | ((uint64_t)j << 20) | (uint64_t)k, t);
+                                     (3ull << 60) | ((uint64_t)g[r0] << 40) | ((uint64_t)g[r1] << 20) |
+                                         (uint64_t)g[r2],
+                                     tc);
+                        }
                     }
                 }
             }
@@ -374,17 +443,23 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     if (warp == 1) tmem_dealloc<512>(tmem_base);
 }
 
+int64_t tally3_units(const Tally3Args& a) {
+    PivotSched sch;
+    sch.init(a);
+    if (sch.tt < 0) return 0;
+    TriSched t = sch.tiles;
+    t.P = t.Q = 0;
+    t.base = 0;
+    t.cnt = (t.SP > 0 && t.SQ > 0) ? t.super_count(0, 0) : 0;
+    int64_t units = 0;
+    int32_t J, K;
+    for (int64_t tt = 0; t.get(tt, J, K); ++tt) units += sch.pivots(J, K);
+    return units;
+}
+
 cudaError_t launch_tally3(const CUtensorMap& tmA, const CUtensorMap& tmB, const Tally3Args& a,
                           int num_sms, cudaStream_t stream, int64_t* n_units_out) {
-    PivotSched sch;
-    sch.init(a.n_v, a.i_begin, a.i_end);
-    int64_t units = 0;
-    if (sch.tt >= 0) {
-        TriSched t;
-        t.init(0, a.n_v, a.n_v, 1);
-        int32_t J, K;
-        for (int64_t tt = 0; t.get(tt, J, K); ++tt) units += sch.pivots(J, K);
-    }
+    const int64_t units = tally3_units(a);
     if (n_units_out) *n_units_out = units;
     if (units == 0) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(tally3_kernel,

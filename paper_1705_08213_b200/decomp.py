@@ -161,13 +161,15 @@ def unit3_triples(u: Unit3, bounds):
 
 
 def unit3_count(u: Unit3, bounds) -> int:
-    """Number of canonical triples of a unit (closed form per case)."""
+    """Number of canonical triples of a unit (closed form per case; the pivot range may be
+    a sub-range -- a stage -- while same-block row / column ranges are whole blocks)."""
     np_, nm, nn = u.p_hi - u.p_lo, u.m_hi - u.m_lo, u.n_hi - u.n_lo
-    same_pm, same_mn, same_pn = u.pb == u.mb, u.mb == u.nb, u.pb == u.nb
-    if same_pm and same_mn:
-        return comb(np_, 3)
-    if same_pm:
-        return comb(np_, 2) * nn
+    nb = bounds[u.pb][1] - bounds[u.pb][0]
+    if u.pb == u.mb and u.mb == u.nb:          # sum_p C(nb-1-p, 2)
+        return comb(nb - u.p_lo, 3) - comb(nb - u.p_hi, 3)
+    if u.pb == u.mb:                           # sum_p (nb-1-p) * |N|
+        rs = lambda i: i * (2 * nb - i - 1) // 2
+        return (rs(u.p_hi) - rs(u.p_lo)) * nn
     return np_ * nm * nn
 
 

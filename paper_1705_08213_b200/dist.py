@@ -68,6 +68,53 @@ class CudaBackend:
     def checksum_zero(self):
         return torch.zeros(2, dtype=torch.int64, device=self.device)
 
+    # ---- 3-way (Ring3Way) ------------------------------------------------------------
+    def g_empty(self, n_v):
+        return torch.zeros((n_v, n_v), dtype=torch.int32, device=self.device)
+
+    def expand_into(self, packed, full, lo, hi):
+        N, s, w = full
+        return self.ccc.ccc_expand(packed, self.n_f, self.gamma, N[lo:hi], s[lo:hi], w[lo:hi])
+
+    def g_block(self, ring, a, b):
+        """Pairwise G of blocks a == b (own block) into the global G."""
+        N, s, w = ring.full
+        lo, hi = ring.bounds[a]
+        n_v = ring.n_v
+        Gv = ring.G.view(-1)[lo * n_v + lo:]
+        self.ccc.ccc_2way_block(N[lo:hi], s[lo:hi], w[lo:hi], lo, 0, hi - lo, N[lo:hi], s[lo:hi],
+                                w[lo:hi], lo, True, self.n_f, 0, g=Gv, ldg=n_v)
+
+    def g_full(self, ring):
+        N, s, w = ring.full
+        self.ccc.ccc_2way_block(N, s, w, 0, 0, ring.n_v, N, s, w, 0, True, self.n_f, 0,
+                                g=ring.G, ldg=ring.n_v)
+
+    def _blk(self, ring, b):
+        N, s, w = ring.full
+        lo, hi = ring.bounds[b]
+        return self.ccc.block(N[lo:hi], s[lo:hi], w[lo:hi], lo)
+
+    def unit_records(self, ring, u, p_lo, p_hi):
+        return decomp.unit3_count(decomp.Unit3(u.pb, p_lo, p_hi, u.mb, u.m_lo, u.m_hi, u.nb,
+                                               u.n_lo, u.n_hi, u.order), ring.bounds)
+
+    def unit(self, ring, u, p_lo, p_hi, ck):
+        f = self.out_flags
+        n_rec = self.unit_records(ring, u, p_lo, p_hi)
+        if not hasattr(self, "_buf3") or self._buf3[0] < n_rec:
+            T = torch.empty((n_rec, 8), dtype=torch.int32, device=self.device) if f & 1 else None
+            C = (torch.empty((n_rec, 8), dtype=torch.float64, device=self.device) if f & 2 else
+                 torch.empty((n_rec, 8), dtype=torch.float32, device=self.device) if f & 4 else None)
+            self._buf3 = (n_rec, T, C)
+        _, T, C = self._buf3
+        T = T[:n_rec] if T is not None else None
+        C = C[:n_rec] if C is not None else None
+        self.ccc.ccc_3way_unit(self._blk(ring, u.pb), p_lo, p_hi, self._blk(ring, u.mb), u.m_lo,
+                               u.m_hi, self._blk(ring, u.nb), u.n_lo, u.n_hi, u.order, ring.G,
+                               self.n_f, f, T, C, ck)
+        return T, C
+
     def block(self, A, a_row0, a_lo, a_hi, B, b_row0, diag, out, ck, timed=False):
         N_a, s_a, w_a = A
         N_b, s_b, w_b = B
@@ -147,6 +194,88 @@ class Ring2Way:
         return self.out
 
 
+class Ring3Way:
+    """Per-rank tetrahedral 3-way computation.  Every rank
+    needs every block: a ring all-gather *with retention* of the packed blocks (P-1
+    steps, NCCL send/recv) fills a full expanded N in place (blocks are contiguous
+    rows), overlapped with the rank's {A,A,A} unit, which needs only its own block and
+    the own-block part of G.  Then the pairwise G over all vectors (KB-2W, ~1/n_f of the
+    3-way work) and the remaining units.  Each unit is cut into pivot sub-ranges so
+    that no output buffer exceeds `max_records` (the paper's stages)."""
+
+    def __init__(self, backend, bounds, rank: int, world: int, max_records: int, group=None):
+        self.be = backend
+        self.bounds = bounds
+        self.rank = rank
+        self.P = world
+        self.group = group
+        self.n_v = bounds[-1][1]
+        self.units = decomp.plan_3way(world, rank, bounds)
+        self.full = backend.expanded_empty(self.n_v)
+        self.G = backend.g_empty(self.n_v)
+        self.recv = [backend.packed_empty(max(hi - lo for lo, hi in bounds)) for _ in range(2)]
+        self.held = [None] * world
+        self.max_records = max_records
+        self.ck = backend.checksum_zero()
+        self.launches = 0
+
+    def _pieces(self, u):
+        """Split a unit into pivot sub-ranges of <= max_records records."""
+        out, lo = [], u.p_lo
+        while lo < u.p_hi:
+            hi = lo + 1
+            while hi < u.p_hi and self.be.unit_records(self, u, lo, hi + 1) <= self.max_records:
+                hi += 1
+            out.append((lo, hi))
+            lo = hi
+        return out
+
+    def run(self, packed_own, sink=None):
+        """One pass; sink(unit, p_lo, p_hi, outputs) receives each piece's records (on the
+        device; the default drops them after the checksum fold)."""
+        be, r, P = self.be, self.rank, self.P
+        lo, hi = self.bounds[r]
+        be.expand_into(packed_own, self.full, lo, hi)
+        be.g_block(self, r, r)
+        self.launches = 2
+        cur = packed_own
+        reqs = []
+        for d in range(P):
+            nxt = None
+            if d < P - 1:
+                nb = (r + d + 1) % P
+                nxt = self.recv[d % 2][: self.bounds[nb][1] - self.bounds[nb][0]]
+                ops = [dist.P2POp(dist.isend, cur.contiguous(), (r - 1) % P, self.group),
+                       dist.P2POp(dist.irecv, nxt, (r + 1) % P, self.group)]
+                reqs = dist.batch_isend_irecv(ops)
+            if d == 0:   # own-block unit overlaps the gather
+                self.launches += self._run_units(lambda u: u.pb == u.mb == u.nb, sink)
+            for q in reqs:
+                q.wait()
+            reqs = []
+            if nxt is not None:
+                nb = (r + d + 1) % P
+                be.expand_into(nxt, self.full, *self.bounds[nb])
+                self.launches += 1
+                cur = nxt
+        be.g_full(self)
+        self.launches += 1
+        self.launches += self._run_units(lambda u: not (u.pb == u.mb == u.nb), sink)
+        return self.ck
+
+    def _run_units(self, pick, sink):
+        n = 0
+        for u in self.units:
+            if not pick(u):
+                continue
+            for plo, phi in self._pieces(u):
+                out = self.be.unit(self, u, plo, phi, self.ck)
+                n += 1
+                if sink is not None:
+                    sink(u, plo, phi, out)
+        return n
+
+
 def checksum_total(ck_local: torch.Tensor, group=None) -> int:
     """Sum of the ranks' 128-bit checksums mod 2^128 (host-side, exact)."""
     world = dist.get_world_size(group)
@@ -176,8 +305,8 @@ def bench_main(args, wl, metric, unit):
     import synthgen
     from . import ccc
 
-    if wl["way"] != 2:
-        raise SystemExit("multi-GPU bench covers the 2-way path (3-way: see DESIGN.md)")
+    if wl["way"] == 3:
+        return bench_main_3way(args, wl, metric, unit)
     dist.init_process_group("nccl")
     rank, P = dist.get_rank(), dist.get_world_size()
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -279,6 +408,75 @@ def bench_main(args, wl, metric, unit):
         }
         if e2e:
             out["e2e"] = e2e
+        print(json.dumps(out))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def weak_scaled_nv3(n_v1: int, P: int, align: int = 256) -> int:
+    """n_v at P GPUs with the same per-GPU triple count as n_v1 on one GPU."""
+    if P == 1:
+        return n_v1
+    q = align * P
+    return max(q, int(round(n_v1 * P ** (1.0 / 3.0) / q)) * q)
+
+
+def bench_main_3way(args, wl, metric, unit):
+    """bench.py --workload c4 at N > 1: tetrahedral 3-way, weak-scaled from C4."""
+    import json
+
+    import synthgen
+    from . import ccc
+
+    dist.init_process_group("nccl")
+    rank, P = dist.get_rank(), dist.get_world_size()
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    n_f = wl["n_f"]
+    n_v = weak_scaled_nv3(wl["n_v"], P)
+    bounds = decomp.block_bounds(n_v, P, align=256)
+    lo, hi = bounds[rank]
+    flags = ccc.OUT_TALLY | ccc.OUT_CCC_F64 | ccc.OUT_CHECKSUM
+    be = CudaBackend(n_f, ccc.GAMMA, flags)
+    max_rec = int(os.environ.get("CCC_3WAY_STAGE_RECORDS", 700_000_000))   # ~67 GB / stage
+    ring = Ring3Way(be, bounds, rank, P, max_records=max_rec)
+    codes = synthgen.random_codes(hi - lo, n_f, seed=1, device="cuda", row0=lo)
+    packed = be.packed_empty(hi - lo)
+
+    def step():
+        be.pack(codes, packed)
+        ring.ck.zero_()
+        ring.run(packed)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    from bench import ClockSampler
+    clk = ClockSampler(local)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with clk:
+        t0.record()
+        for _ in range(args.steps):
+            step()
+        t1.record()
+        torch.cuda.synchronize()
+    tmax = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ck = checksum_total(ring.ck)
+    comps = n_f * (n_v * (n_v - 1) * (n_v - 2) // 6)
+    ms_step = float(tmax.item()) / args.steps
+    if rank == 0:
+        out = {"metric": metric, "value": comps / (ms_step / 1e3), "unit": unit, "n_gpus": P,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+               "dtype": "int8", "data": "synthetic",
+               "config": {"workload": f"3-way CCC tetrahedral, {n_v} SNP vectors x {n_f} "
+                                      f"individuals over {P} GPUs (per-GPU load = configs[3])",
+                          "n_v": n_v, "n_f": n_f, "parallelism": f"tetrahedral dp{P}",
+                          "output": "FULL, staged", "l2": "outputs larger than L2"},
+               "gpu_launches": args.steps * (1 + ring.launches), "checksum": f"{ck:032x}",
+               "clocks": clk.summary()}
         print(json.dumps(out))
     dist.barrier()
     dist.destroy_process_group()

@@ -74,3 +74,13 @@ def test_block_bounds_alignment():
     assert b[0][0] == 0 and b[-1][1] == 56568
     assert all(lo % 256 == 0 for lo, _ in b)
     assert all(hi > lo for lo, hi in b)
+
+
+def test_unit3_count_pivot_subranges():
+    bounds = decomp.block_bounds(30, 3)
+    for r in range(3):
+        for u in decomp.plan_3way(3, r, bounds):
+            for lo in range(u.p_lo, u.p_hi):
+                for hi in range(lo, u.p_hi + 1):
+                    sub = decomp.Unit3(u.pb, lo, hi, u.mb, u.m_lo, u.m_hi, u.nb, u.n_lo, u.n_hi, u.order)
+                    assert decomp.unit3_count(sub, bounds) == len(list(decomp.unit3_triples(sub, bounds)))

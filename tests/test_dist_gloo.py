@@ -120,3 +120,84 @@ def test_ring_2way_gloo(world):
                 np.testing.assert_array_equal(T[k], To[index[pr]])
                 np.testing.assert_allclose(C[k], Co[index[pr]], rtol=1e-15)
     assert len(seen) == n_v * (n_v - 1) // 2
+
+
+class Oracle3Backend(OracleBackend):
+    """CPU stand-in for the 3-way ring: 'expanded' full matrix = the raw codes."""
+
+    def expanded_empty(self, rows):
+        return (torch.zeros((rows, self.n_f), dtype=torch.uint8), None, None)
+
+    def g_empty(self, n_v):
+        return None
+
+    def expand_into(self, packed, full, lo, hi):
+        full[0][lo:hi] = packed
+
+    def g_block(self, ring, a, b):
+        pass
+
+    def g_full(self, ring):
+        pass
+
+    def unit_records(self, ring, u, p_lo, p_hi):
+        return decomp.unit3_count(decomp.Unit3(u.pb, p_lo, p_hi, u.mb, u.m_lo, u.m_hi, u.nb,
+                                               u.n_lo, u.n_hi, u.order), ring.bounds)
+
+    def unit(self, ring, u, p_lo, p_hi, ck):
+        sub = decomp.Unit3(u.pb, p_lo, p_hi, u.mb, u.m_lo, u.m_hi, u.nb, u.n_lo, u.n_hi, u.order)
+        tr = np.array(list(decomp.unit3_triples(sub, ring.bounds)), dtype=np.int64).reshape(-1, 3)
+        codes = ring.full[0].numpy()
+        T, C = oracle.triples(codes, tr)
+        v = oracle.checksum(3, tr, T)
+        cur_lo, cur_hi = (int(x) & ((1 << 64) - 1) for x in ck.tolist())
+        tot = (((cur_hi << 64) | cur_lo) + v) & ((1 << 128) - 1)
+        to_i64 = lambda x: x - (1 << 64) if x >= (1 << 63) else x
+        ck[0] = to_i64(tot & ((1 << 64) - 1))
+        ck[1] = to_i64(tot >> 64)
+        return tr, T
+
+
+def _worker3(rank, world, port, n_v, n_f, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1705_08213_b200.dist import Ring3Way, checksum_total
+        bounds = decomp.block_bounds(n_v, world)
+        lo, hi = bounds[rank]
+        codes = synthgen.random_codes(hi - lo, n_f, seed=6, row0=lo)
+        ring = Ring3Way(Oracle3Backend(n_f), bounds, rank, world, max_records=150)
+        got = []
+        ring.run(codes, sink=lambda u, plo, phi, out: got.append((phi - plo,) + tuple(out)))
+        q.put((rank, checksum_total(ring.ck), got))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ring_3way_gloo(world):
+    n_v, n_f = 17, 29
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker3, args=(r, world, port, n_v, n_f, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    codes = synthgen.random_codes(n_v, n_f, seed=6)
+    To, _ = oracle.all_triples(codes)
+    index = {tuple(t): r for r, t in enumerate(oracle.triple_list(n_v))}
+    seen = set()
+    for rank, ck, got in res:
+        assert ck == oracle.checksum(3, oracle.triple_list(n_v), To)
+        for npiv, tr, T in got:
+            assert len(tr) <= 150 or npiv == 1         # stage pieces respect the bound
+            for k, t in enumerate(map(tuple, tr)):
+                assert t not in seen
+                seen.add(t)
+                np.testing.assert_array_equal(T[k], To[index[t]])
+    assert len(seen) == len(To)

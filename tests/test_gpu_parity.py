@@ -351,3 +351,114 @@ def test_ring_nccl_two_gpus():
     [p.join(timeout=60) for p in ps]
     To, _ = oracle.all_pairs(synthgen.random_codes(n_v, n_f, seed=5))
     assert cks[0] == cks[1] == oracle.checksum(2, oracle.pair_list(n_v), To)
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4])
+def test_tetrahedral_units_on_one_gpu(P):
+    """Every rank's tetrahedral 3-way units ({A,A,A}, {D,D,S} both orders, the three
+    parts of {A<B<C}) through ccc_3way_unit on per-block expanded data; union equals the
+    single-GPU result triple for triple and the unit checksums add up."""
+    from paper_1705_08213_b200 import decomp
+    n_v, n_f = 150, 197
+    codes = _codes("random", n_v, n_f, seed=31)
+    To, Co = oracle.all_triples(codes)
+    # global pairwise G by the 2-way kernel on the whole matrix (what each rank builds
+    # after the all-gather)
+    N, s, w = ccc.ccc_expand(ccc.ccc_pack(codes.cuda()), n_f)
+    G = torch.zeros((n_v, n_v), dtype=torch.int32, device="cuda")
+    ccc.ccc_2way_block(N, s, w, 0, 0, n_v, N, s, w, 0, True, n_f, 0, g=G, ldg=n_v)
+    bounds = decomp.block_bounds(n_v, P)
+    exp = [ccc.ccc_expand(ccc.ccc_pack(codes[lo:hi].contiguous().cuda()), n_f) for lo, hi in bounds]
+    blks = [ccc.block(*exp[b], bounds[b][0]) for b in range(P)]
+    seen = np.zeros(len(To), dtype=np.int64)
+    total_ck = 0
+    for r in range(P):
+        for u in decomp.plan_3way(P, r, bounds):
+            ck = torch.zeros(2, dtype=torch.int64, device="cuda")
+            T, C, ck = ccc.ccc_3way_unit(blks[u.pb], u.p_lo, u.p_hi, blks[u.mb], u.m_lo, u.m_hi,
+                                         blks[u.nb], u.n_lo, u.n_hi, u.order, G, n_f,
+                                         TAL | F64 | CK, checksum=ck)
+            tr = list(decomp.unit3_triples(u, bounds))
+            assert T.shape[0] == len(tr) == decomp.unit3_count(u, bounds)
+            if not tr:
+                continue
+            rows = np.array([ccc.ccc_triple_index(n_v, *t) for t in tr], dtype=np.int64)
+            np.testing.assert_array_equal(_t(T), To[rows])
+            _ccc_close(C.cpu().numpy(), Co[rows])
+            seen[rows] += 1
+            total_ck = (total_ck + ccc.checksum_int(ck)) % (1 << 128)
+    assert np.all(seen == 1)
+    assert total_ck == oracle.checksum(3, oracle.triple_list(n_v), To)
+
+
+def test_3way_unit_pivot_subranges_as_stages():
+    """A distinct-block unit and a {D,D,S} unit split into pivot sub-ranges (stages) give
+    the same records as the whole unit."""
+    from paper_1705_08213_b200 import decomp
+    n_v, n_f = 120, 300
+    codes = _codes("hwe", n_v, n_f)
+    N, s, w = ccc.ccc_expand(ccc.ccc_pack(codes.cuda()), n_f)
+    G = torch.zeros((n_v, n_v), dtype=torch.int32, device="cuda")
+    ccc.ccc_2way_block(N, s, w, 0, 0, n_v, N, s, w, 0, True, n_f, 0, g=G, ldg=n_v)
+    bounds = decomp.block_bounds(n_v, 3)
+    exp = [ccc.ccc_expand(ccc.ccc_pack(codes[lo:hi].contiguous().cuda()), n_f) for lo, hi in bounds]
+    b = [ccc.block(*exp[i], bounds[i][0]) for i in range(3)]
+    for (pb, mb, nb, order) in [(1, 0, 2, ("m", "p", "n")), (2, 2, 0, ("n", "p", "m"))]:
+        n_p = bounds[pb][1] - bounds[pb][0]
+        full, _, _ = ccc.ccc_3way_unit(b[pb], 0, n_p, b[mb], 0, b[mb].rows, b[nb], 0, b[nb].rows,
+                                       order, G, n_f, TAL)
+        parts = []
+        for lo, hi in [(0, 7), (7, 20), (20, n_p)]:
+            T, _, _ = ccc.ccc_3way_unit(b[pb], lo, hi, b[mb], 0, b[mb].rows, b[nb], 0,
+                                        b[nb].rows, order, G, n_f, TAL)
+            parts.append(_t(T))
+        np.testing.assert_array_equal(np.concatenate(parts), _t(full))
+
+
+def _ring_world1(q, n_v2, n_v3, n_f):
+    import os
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(q.get()))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    from paper_1705_08213_b200 import decomp, dist as cdist
+    res = {}
+    be = cdist.CudaBackend(n_f, ccc.GAMMA, TAL | CK)
+    codes = synthgen.random_codes(n_v2, n_f, seed=9, device="cuda")
+    r2 = cdist.Ring2Way(be, decomp.block_bounds(n_v2, 1), 0, 1)
+    r2.run(be.pack(codes))
+    res["ck2"] = cdist.checksum_total(r2.ck)
+    codes = synthgen.random_codes(n_v3, n_f, seed=9, device="cuda")
+    r3 = cdist.Ring3Way(be, decomp.block_bounds(n_v3, 1), 0, 1, max_records=5000)
+    pieces = []
+    r3.run(be.pack(codes), sink=lambda u, lo, hi, out: pieces.append((lo, hi, _t(out[0]).tolist())))
+    res["ck3"] = cdist.checksum_total(r3.ck)
+    res["pieces"] = pieces
+    dist.destroy_process_group()
+    q.put(res)
+
+
+def test_rings_world1_nccl():
+    """The CUDA backend methods of Ring2Way / Ring3Way (expand into the full buffer, own-block
+    and full G, staged units) under a 1-rank NCCL group."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    n_v2, n_v3, n_f = 300, 90, 211
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    q.put(port)
+    p = ctx.Process(target=_ring_world1, args=(q, n_v2, n_v3, n_f))
+    p.start()
+    import time
+    time.sleep(1)
+    res = q.get(timeout=300)
+    p.join(timeout=60)
+    T2, _ = oracle.all_pairs(synthgen.random_codes(n_v2, n_f, seed=9))
+    assert res["ck2"] == oracle.checksum(2, oracle.pair_list(n_v2), T2)
+    T3, _ = oracle.all_triples(synthgen.random_codes(n_v3, n_f, seed=9))
+    assert res["ck3"] == oracle.checksum(3, oracle.triple_list(n_v3), T3)
+    got = np.concatenate([np.array(t, dtype=np.int64).reshape(-1, 8) for _, _, t in res["pieces"]])
+    np.testing.assert_array_equal(got, T3)
+    assert len(res["pieces"]) > 1                     # the stage split was exercised
