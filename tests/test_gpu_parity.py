@@ -415,10 +415,10 @@ def test_3way_unit_pivot_subranges_as_stages():
         np.testing.assert_array_equal(np.concatenate(parts), _t(full))
 
 
-def _ring_world1(q, n_v2, n_v3, n_f):
+def _ring_world1(q, port, n_v2, n_v3, n_f):
     import os
     import torch.distributed as dist
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(q.get()))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("nccl", rank=0, world_size=1)
     from paper_1705_08213_b200 import decomp, dist as cdist
     res = {}
@@ -448,11 +448,8 @@ def test_rings_world1_nccl():
     n_v2, n_v3, n_f = 300, 90, 211
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    q.put(port)
-    p = ctx.Process(target=_ring_world1, args=(q, n_v2, n_v3, n_f))
+    p = ctx.Process(target=_ring_world1, args=(q, port, n_v2, n_v3, n_f))
     p.start()
-    import time
-    time.sleep(1)
     res = q.get(timeout=300)
     p.join(timeout=60)
     T2, _ = oracle.all_pairs(synthgen.random_codes(n_v2, n_f, seed=9))
