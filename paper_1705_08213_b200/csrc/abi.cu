@@ -428,8 +428,8 @@ ccc_status ccc_3way_stage(int64_t n_v, int64_t n_f, int64_t n_stages, int64_t st
     a.ccc = ccc_d;
     a.checksum = reinterpret_cast<unsigned long long*>(checksum_d);
     CUtensorMap tmA, tmB;
-    CCC_CHECK(make_tmap(&tmA, b.N, n_v, k_pad, ccc::kBM));
-    CCC_CHECK(make_tmap(&tmB, b.N, n_v, k_pad, ccc::kBN));
+    CCC_CHECK(make_tmap(&tmA, b.N, n_v, k_pad, 128));
+    CCC_CHECK(make_tmap(&tmB, b.N, n_v, k_pad, 128));   // per-CTA halves of the pair tile
     int64_t units = 0;
     CCC_CUDA(ccc::launch_tally3(tmA, tmB, a, sms, (cudaStream_t)stream, &units), "tally3 launch");
     if (units) g_launches = 1;
@@ -517,8 +517,8 @@ ccc_status ccc_3way_unit(const ccc_block* bp, int64_t p_lo, int64_t p_hi, const 
     a.ccc = ccc_d;
     a.checksum = reinterpret_cast<unsigned long long*>(checksum_d);
     CUtensorMap tmA, tmB;
-    CCC_CHECK(make_tmap(&tmA, bm->N, bm->rows, k_pad, ccc::kBM));
-    CCC_CHECK(make_tmap(&tmB, bn->N, bn->rows, k_pad, ccc::kBN));
+    CCC_CHECK(make_tmap(&tmA, bm->N, bm->rows, k_pad, 128));
+    CCC_CHECK(make_tmap(&tmB, bn->N, bn->rows, k_pad, 128));   // per-CTA halves of the pair tile
     int64_t units = 0;
     CCC_CUDA(ccc::launch_tally3(tmA, tmB, a, sms, (cudaStream_t)stream, &units), "tally3 launch");
     if (units) g_launches = 1;

@@ -150,6 +150,7 @@ struct Tally3Args {
     uint32_t* tallies;         // [records][8]
     void* ccc;                 // [records][8] double or float
     unsigned long long* checksum;
+    unsigned long long* trace; // optional per-unit %globaltimer trace (diagnostics)
 };
 
 }  // namespace ccc

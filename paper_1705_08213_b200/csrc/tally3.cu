@@ -18,24 +18,31 @@
 // ordered tile-outer / pivot-inner so the ~148 concurrent CTAs share the same N_M, N_N
 // panels in L2 and differ only in their 128-byte pivot rows.
 // Warp roles: 0 TMA producer (A, B tiles + pivot chunk), 1 TMEM alloc + MMA issuer,
-// 2..9 epilogue (2 per TMEM lane quadrant), 10..13 transform (A <- A o n_p in shared
+// 2..9 epilogue (2 per TMEM lane quadrant), 10..11 transform (A <- A o n_p in shared
 // memory, in place, then fence.proxy.async so the tensor core sees it).
 #include "sm100.cuh"
 #include "common.cuh"
 #include "internal.h"
 
+#include <cstdlib>
+
 namespace ccc {
 
-constexpr int kStages3 = 4;
-constexpr int kABytes3 = kBM * kBK;  // 16 KB
-constexpr int kBBytes3 = kBN * kBK;  // 32 KB
+constexpr int kTileM3 = 256;         // pair tile rows (UMMA M = 256, cta_group::2)
+constexpr int kStages3 = 6;
+constexpr int kABytes3 = 128 * kBK;  // 16 KB: this CTA's 128 rows of A
+constexpr int kBBytes3 = 128 * kBK;  // 16 KB: this CTA's 128 rows of B
+constexpr int kEpiWarps3 = 8;        // 2 per TMEM lane quadrant
+#ifndef CCC_XF_WARPS
+#define CCC_XF_WARPS 4
+#endif
+constexpr int kXfWarps3 = CCC_XF_WARPS;                       // transform warps
+constexpr int kThreads3 = 32 * (2 + kEpiWarps3 + kXfWarps3);
 constexpr int kPivBytes = kBK;       // 128 B of the pivot row per stage
-constexpr int kEpiWarps3 = 8;                                 // 2 per TMEM lane quadrant
-constexpr int kXfWarps3 = 2;                                  // transform warps (2 rows/lane)
-constexpr int kThreads3 = 32 * (2 + kEpiWarps3 + kXfWarps3);  // 384
 constexpr int kPivOff3 = kStages3 * (kABytes3 + kBBytes3);
-constexpr int kBarOff3 = kPivOff3 + kStages3 * kPivBytes;
-constexpr int kSmem3 = kBarOff3 + 256 + 1024;
+constexpr int kMaskOff3 = kPivOff3 + kStages3 * kPivBytes;   // per transform warp: 2 x 128 B
+constexpr int kBarOff3 = kMaskOff3 + kXfWarps3 * 2 * kPivBytes;
+constexpr int kSmem3 = kBarOff3 + 512 + 1024;
 
 // Units: (m-tile, n-tile) in TriSched order (triangular when m and n share a block),
 // pivots innermost.
@@ -45,7 +52,7 @@ struct PivotSched {
     int32_t same_pm, same_mn, J, K;
 
     __host__ __device__ int64_t pivots(int32_t Jt, int32_t Kt) const {
-        int64_t m_max = tiles.a_lo + (int64_t)Jt * kBM + kBM - 1;
+        int64_t m_max = tiles.a_lo + (int64_t)Jt * kTileM3 + kTileM3 - 1;
         if (m_max > m_hi - 1) m_max = m_hi - 1;
         int64_t n_max = tiles.b_lo + (int64_t)Kt * kBN + kBN - 1;
         if (n_max > n_hi - 1) n_max = n_hi - 1;
@@ -64,9 +71,9 @@ struct PivotSched {
         same_pm = a.same_pm;
         same_mn = a.same_mn;
         if (same_mn) {
-            tiles.init(0, m_hi, n_hi, 1);           // m, n over the same [0, rows) range
+            tiles.init(0, m_hi, n_hi, 1, kTileM3);  // m, n over the same [0, rows) range
         } else {
-            tiles.init(m_lo, m_hi - m_lo, n_hi - n_lo, 0);
+            tiles.init(m_lo, m_hi - m_lo, n_hi - n_lo, 0, kTileM3);
             tiles.b_lo = n_lo;
         }
         tt = 0;
@@ -89,7 +96,7 @@ struct PivotSched {
         po = p_lo + (u - base);
         return true;
     }
-    __host__ __device__ int64_t row0(int32_t Jt) const { return tiles.a_lo + (int64_t)Jt * kBM; }
+    __host__ __device__ int64_t row0(int32_t Jt) const { return tiles.a_lo + (int64_t)Jt * kTileM3; }
     __host__ __device__ int64_t col0(int32_t Kt) const { return tiles.b_lo + (int64_t)Kt * kBN; }
 };
 
@@ -121,13 +128,6 @@ __device__ __forceinline__ void ck_flush3(unsigned long long lo, unsigned long l
     }
 }
 
-// bytewise a * b for a, b in {0,1,2} packed 4 per word: a*[b!=0] + a*[b==2].
-__device__ __forceinline__ uint32_t mul_012(uint32_t a, uint32_t b) {
-    const uint32_t nz = ((b | (b >> 1)) & 0x01010101u) * 0xFFu;
-    const uint32_t two = ((b >> 1) & 0x01010101u) * 0xFFu;
-    return (a & nz) + (a & two);
-}
-
 __host__ __device__ __forceinline__ int64_t c2(int64_t n) { return n * (n - 1) / 2; }
 __host__ __device__ __forceinline__ int64_t c3(int64_t n) { return n * (n - 1) * (n - 2) / 6; }
 
@@ -141,66 +141,70 @@ __device__ __forceinline__ void perm_cells(const T (&in)[8], T (&out)[8]) {
         out[4 * a[R0] + 2 * a[R1] + a[R2]] = in[t];
     }
 }
-template <typename T>
-__device__ __forceinline__ void to_canonical(int order, const T (&in)[8], T (&out)[8]) {
-    switch (order) {
-        case 0: perm_cells<0, 1, 2>(in, out); break;
-        case 1: perm_cells<0, 2, 1>(in, out); break;
-        case 2: perm_cells<1, 0, 2>(in, out); break;
-        case 3: perm_cells<1, 2, 0>(in, out); break;
-        case 4: perm_cells<2, 0, 1>(in, out); break;
-        default: perm_cells<2, 1, 0>(in, out); break;
-    }
-}
-__host__ __device__ __forceinline__ void order_roles(int order, int& r0, int& r1, int& r2) {
-    const int tab[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
-    r0 = tab[order][0];
-    r1 = tab[order][1];
-    r2 = tab[order][2];
-}
-
 __device__ __forceinline__ uint32_t gpair(const int32_t* G, int64_t ld, int64_t x, int64_t y) {
     return (uint32_t)__ldg(G + (x < y ? x * ld + y : y * ld + x));
 }
 
+// Compile-time view of an order: slot position of each role (p=0, m=1, n=2).  Within a
+// unit the canonical order is fixed, so G(x, y) = G[min][max] needs no comparison.
+template <int kOrder>
+struct Ord {
+    static constexpr int R0 = kOrder == 0 || kOrder == 1 ? 0 : kOrder == 2 || kOrder == 3 ? 1 : 2;
+    static constexpr int R1 = kOrder == 0 ? 1 : kOrder == 1 ? 2 : kOrder == 2 ? 0 : kOrder == 3 ? 2
+                              : kOrder == 4 ? 0 : 1;
+    static constexpr int R2 = 3 - R0 - R1;
+    __host__ __device__ static constexpr int pos(int role) { return role == R0 ? 0 : role == R1 ? 1 : 2; }
+};
+template <int kOrder, int RoleX, int RoleY>
+__device__ __forceinline__ uint32_t gord(const int32_t* G, int64_t ld, int64_t gx, int64_t gy) {
+    if constexpr (Ord<kOrder>::pos(RoleX) < Ord<kOrder>::pos(RoleY)) return (uint32_t)__ldg(G + gx * ld + gy);
+    else return (uint32_t)__ldg(G + gy * ld + gx);
+}
+
+template <int kOrder>
 __global__ void __launch_bounds__(kThreads3, 1)
 tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const Tally3Args args) {
+    using O = Ord<kOrder>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
     uint8_t* smem = smem_raw + pad;
     uint8_t* smA = smem;
     uint8_t* smB = smem + kStages3 * kABytes3;
     uint8_t* smP = smem + kPivOff3;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBarOff3);
-    uint64_t* xfull = full + kStages3;
-    uint64_t* empty = xfull + kStages3;
+    uint64_t* aload = reinterpret_cast<uint64_t*>(smem + kBarOff3);  // own A half + pivot landed
+    uint64_t* ready = aload + kStages3;    // leader: both B halves + both transforms done
+    uint64_t* empty = ready + kStages3;    // both: the pair's MMAs consumed the stage
     uint64_t* tfull = empty + kStages3;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();      // 0 = leader CTA of the pair
+    const int64_t unit0 = blockIdx.x / 2, units = gridDim.x / 2;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
         for (int s = 0; s < kStages3; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&xfull[s], kXfWarps3);
+            mbar_init(&aload[s], 1);
+            mbar_init(&ready[s], 2 + 2 * kXfWarps3);   // 2 producers + transform warps
             mbar_init(&empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], kEpiWarps3);
+            mbar_init(&tempty[s], 2 * kEpiWarps3);
         }
         fence_mbar_init();
     }
-    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
     tc_fence_before();
-    __syncthreads();
+    cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const uint32_t ready_leader = mapa_shared(smem_u32(&ready[0]), 0);
+    const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), 0);
 
     PivotSched sch;
     sch.init(args);
@@ -210,82 +214,107 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             // ---------------------------------------------------------- TMA producer
             uint32_t stage = 0, phase = 0;
             const uint64_t pol = policy_evict_last();
-            for (int64_t u = blockIdx.x;; u += gridDim.x) {
+            for (int64_t u = unit0;; u += units) {
                 int32_t J, K;
                 int64_t p;
                 if (!sch.get(u, J, K, p)) break;
                 const int8_t* prow = args.bp.N + p * args.k_pad;
-                const int32_t mrow = (int32_t)sch.row0(J), ncol = (int32_t)sch.col0(K);
+                const int32_t mrow = (int32_t)(sch.row0(J) + rank * 128);
+                const int32_t ncol = (int32_t)(sch.col0(K) + rank * 128);
                 for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_arrive_expect_tx(&full[stage], kABytes3 + kBBytes3 + kPivBytes);
-                    tma_load_2d(smA + stage * kABytes3, &tmA, &full[stage], kb * kBK, mrow, pol);
-                    tma_load_2d(smB + stage * kBBytes3, &tmB, &full[stage], kb * kBK, ncol, pol);
+                    // own A half + pivot chunk -> local barrier (the transform warps wait)
+                    mbar_arrive_expect_tx(&aload[stage], kABytes3 + kPivBytes);
+                    tma_load_2d(smA + stage * kABytes3, &tmA, &aload[stage], kb * kBK, mrow, pol);
                     bulk_load(smP + stage * kPivBytes, prow + (int64_t)kb * kBK, kPivBytes,
-                              &full[stage]);
+                              &aload[stage]);
+                    // B half -> the leader's ready barrier
+                    const uint32_t rb = ready_leader + stage * 8u;
+                    if (rank == 0) mbar_arrive_expect_tx(&ready[stage], 2 * kBBytes3);
+                    else mbar_arrive_cluster(rb);
+                    tma_load_2d_pair(smB + stage * kBBytes3, &tmB, rb, kb * kBK, ncol, pol);
                     if (++stage == kStages3) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (lane == 0 && rank == 0) {
             // ---------------------------------------------------------- MMA issuer
-            constexpr uint32_t idesc = idesc_i8(kBM, kBN);
+            constexpr uint32_t idesc = idesc_i8(kTileM3, kBN);
             uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
             const uint32_t a0 = smem_u32(smA), b0 = smem_u32(smB);
-            for (int64_t u = blockIdx.x;; u += gridDim.x) {
+            for (int64_t u = unit0;; u += units) {
                 int32_t J, K;
                 int64_t p;
                 if (!sch.get(u, J, K, p)) break;
+                unsigned long long* tr = args.trace ? args.trace + 8 * u : nullptr;
+                if (tr) tr[0] = globaltimer();
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
+                if (tr) tr[1] = globaltimer();
                 const uint32_t d = tmem_base + acc * kBN;
                 for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
-                    mbar_wait(&xfull[stage], phase);
+                    mbar_wait(&ready[stage], phase);
                     tc_fence_after();
                     const uint32_t sa = a0 + stage * kABytes3, sb = b0 + stage * kBBytes3;
 #pragma unroll
                     for (int k = 0; k < kBK / kUMMA_K; ++k)
-                        mma_i8(d, smem_desc_sw128(sa + k * kUMMA_K),
-                               smem_desc_sw128(sb + k * kUMMA_K), idesc, (kb | k) != 0);
-                    mma_commit(&empty[stage]);
+                        mma_i8_pair(d, smem_desc_sw128(sa + k * kUMMA_K),
+                                    smem_desc_sw128(sb + k * kUMMA_K), idesc, (kb | k) != 0);
+                    mma_commit_pair(&empty[stage], 3);
                     if (++stage == kStages3) { stage = 0; phase ^= 1; }
                 }
-                mma_commit(&tfull[acc]);
+                mma_commit_pair(&tfull[acc], 3);
+                if (tr) tr[2] = globaltimer();
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
         __syncwarp();
     } else if (warp >= 2 + kEpiWarps3) {
         // -------------------------------------------------------------- transform
-        const uint32_t r_first = (uint32_t)(warp - 2 - kEpiWarps3) * 32 + lane;
+        // A <- A o n_p in place: per stage each warp turns the pivot chunk into byte masks
+        // M1 = [n_p >= 1], M2 = [n_p == 2] once, then a * n_p = (a & M1) + (a & M2).
+        const uint32_t xw = (uint32_t)(warp - 2 - kEpiWarps3);
+        const uint32_t r_first = xw * 32 + lane;
+        uint32_t* mk = reinterpret_cast<uint32_t*>(smem + kMaskOff3 + xw * 2 * kPivBytes);
         uint32_t stage = 0, phase = 0;
-        for (int64_t u = blockIdx.x;; u += gridDim.x) {
+        for (int64_t u = unit0;; u += units) {
             int32_t J, K;
             int64_t p;
             if (!sch.get(u, J, K, p)) break;
             for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
-                mbar_wait(&full[stage], phase);
-                const uint8_t* pv = smP + stage * kPivBytes;
+                mbar_wait(&aload[stage], phase);
+                {
+                    const uint32_t b = reinterpret_cast<const uint32_t*>(smP + stage * kPivBytes)[lane];
+                    const uint32_t lo = b & 0x01010101u, hi = (b >> 1) & 0x01010101u;
+                    mk[lane] = (lo | hi) * 0xFFu;
+                    mk[32 + lane] = hi * 0xFFu;
+                }
+                __syncwarp();
 #pragma unroll
-                for (uint32_t r = r_first; r < (uint32_t)kBM; r += 32 * kXfWarps3) {
+                for (uint32_t r = r_first; r < 128u; r += 32 * kXfWarps3) {
                     uint8_t* arow = smA + stage * kABytes3 + r * kBK;
 #pragma unroll
                     for (uint32_t c = 0; c < 8; ++c) {
                         // 128-B swizzle: logical 16-B chunk c of row r sits at chunk c ^ (r & 7)
                         uint4* pa = reinterpret_cast<uint4*>(arow + ((c ^ (r & 7u)) << 4));
-                        const uint4 y = *reinterpret_cast<const uint4*>(pv + (c << 4));
+                        const uint4 m1 = reinterpret_cast<const uint4*>(mk)[c];
+                        const uint4 m2 = reinterpret_cast<const uint4*>(mk + 32)[c];
                         uint4 x = *pa;
-                        x.x = mul_012(x.x, y.x);
-                        x.y = mul_012(x.y, y.y);
-                        x.z = mul_012(x.z, y.z);
-                        x.w = mul_012(x.w, y.w);
+                        x.x = (x.x & m1.x) + (x.x & m2.x);
+                        x.y = (x.y & m1.y) + (x.y & m2.y);
+                        x.z = (x.z & m1.z) + (x.z & m2.z);
+                        x.w = (x.w & m1.w) + (x.w & m2.w);
                         *pa = x;
                     }
                 }
+                __syncwarp();
                 fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&xfull[stage]);
+                if (lane == 0) {
+                    if (rank == 0) mbar_arrive(&ready[stage]);
+                    else mbar_arrive_cluster(ready_leader + stage * 8u);
+                }
                 if (++stage == kStages3) { stage = 0; phase ^= 1; }
             }
         }
@@ -301,24 +330,24 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         const bool want_c = want_c64 | want_c32;
         const uint32_t eight_nf = 8u * (uint32_t)args.n_f;
         const double inv8nf = 1.0 / (8.0 * (double)args.n_f);
-        const int order = args.order;
-        int r0, r1, r2;
-        order_roles(order, r0, r1, r2);
         const int64_t nbp = args.bp.rows, nN = args.n_hi - args.n_lo, nM = args.m_hi - args.m_lo;
         const int32_t cpair = 2 * (int32_t)(lane & 3);
         unsigned long long ck_lo = 0, ck_hi = 0;
         uint32_t acc = 0, acc_phase = 0;
-        for (int64_t u = blockIdx.x;; u += gridDim.x) {
+        for (int64_t u = unit0;; u += units) {
             int32_t J, K;
             int64_t p;
             if (!sch.get(u, J, K, p)) break;
+            unsigned long long* tr = (args.trace && warp == 2 && rank == 0) ? args.trace + 8 * u : nullptr;
+            if (tr && lane == 0) tr[3] = globaltimer();
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
+            if (tr && lane == 0) tr[4] = globaltimer();
             const int64_t gp = args.bp.row0 + p;
             const uint32_t s_p = (uint32_t)__ldg(args.bp.s + p);
             const double wp0 = __ldg(args.bp.w + 2 * p) * inv8nf;
             const double wp1 = __ldg(args.bp.w + 2 * p + 1) * inv8nf;
-            // my 2 rows m = row0(J) + quad*32 + half*16 + r*8 + lane/4
+            // my 2 rows m = row0(J) + rank*128 + quad*32 + half*16 + r*8 + lane/4
             int64_t rec_r[2], m_r[2];
             uint32_t s_m[2], g_pm[2];
             double wpm[2][4];
@@ -326,12 +355,12 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             bool my_any = false;
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
-                const int64_t m = sch.row0(J) + quad * 32 + half * 16 + r * 8 + (lane >> 2);
+                const int64_t m = sch.row0(J) + rank * 128 + quad * 32 + half * 16 + r * 8 + (lane >> 2);
                 m_r[r] = m;
                 ok_r[r] = m >= args.m_lo && m < args.m_hi && (!args.same_pm || m > p);
                 const int64_t mc = m < args.m_hi ? m : args.m_hi - 1;
                 s_m[r] = (uint32_t)__ldg(args.bm.s + mc);
-                g_pm[r] = ok_r[r] ? gpair(args.G, args.ldG, gp, args.bm.row0 + m) : 0u;
+                g_pm[r] = ok_r[r] ? gord<kOrder, 0, 1>(args.G, args.ldG, gp, args.bm.row0 + m) : 0u;
                 const double wm0 = __ldg(args.bm.w + 2 * mc), wm1 = __ldg(args.bm.w + 2 * mc + 1);
                 wpm[r][0] = wp0 * wm0;  // (a_p, a_m) = (0,0), includes 1/(8 n_f)
                 wpm[r][1] = wp0 * wm1;
@@ -359,8 +388,8 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 const uint32_t sA = (uint32_t)__ldg(args.bn.s + nAc);
                 const uint32_t sB = (uint32_t)__ldg(args.bn.s + nBc);
                 const int64_t gnA = args.bn.row0 + nAc, gnB = args.bn.row0 + nBc;
-                const uint32_t gpnA = gpair(args.G, args.ldG, gp, gnA);
-                const uint32_t gpnB = gpair(args.G, args.ldG, gp, gnB);
+                const uint32_t gpnA = gord<kOrder, 0, 2>(args.G, args.ldG, gp, gnA);
+                const uint32_t gpnB = gord<kOrder, 0, 2>(args.G, args.ldG, gp, gnB);
                 double wA0 = 0.0, wA1 = 0.0, wB0 = 0.0, wB1 = 0.0;
                 if (want_c) {
                     wA0 = __ldg(args.bn.w + 2 * nAc);
@@ -380,7 +409,7 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         const int64_t gn = h ? gnB : gnA;
                         const uint32_t g3 = va[r * 2 + h];
                         const uint32_t gpm = g_pm[r], gpn = h ? gpnB : gpnA;
-                        const uint32_t gmn = gpair(args.G, args.ldG, gm, gn);
+                        const uint32_t gmn = gord<kOrder, 1, 2>(args.G, args.ldG, gm, gn);
                         const uint32_t sp = s_p, sm = s_m[r], sn = h ? sB : sA;
                         uint32_t t[8];   // role order: index 4 a_p + 2 a_m + a_n
                         t[7] = g3;
@@ -392,7 +421,7 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         t[1] = 4u * sn - 2u * gpn - 2u * gmn + g3;
                         t[0] = eight_nf - 4u * (sp + sm + sn) + 2u * (gpm + gpn + gmn) - g3;
                         uint32_t tc[8];
-                        to_canonical(order, t, tc);
+                        perm_cells<O::R0, O::R1, O::R2>(t, tc);
                         const int64_t rec = rec_r[r] + n;
                         if (want_t)
                             stg_256_u32(args.tallies + 8 * rec, tc[0], tc[1], tc[2], tc[3], tc[4],
@@ -406,7 +435,7 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                                 cr[2 * ab + 0] = (double)t[2 * ab + 0] * wpm[r][ab] * wn0;
                                 cr[2 * ab + 1] = (double)t[2 * ab + 1] * wpm[r][ab] * wn1;
                             }
-                            to_canonical(order, cr, cc);
+                            perm_cells<O::R0, O::R1, O::R2>(cr, cc);
                             if (want_c64) {
                                 double* q = reinterpret_cast<double*>(args.ccc) + 8 * rec;
                                 stg_256_f64(q, cc[0], cc[1], cc[2], cc[3]);
@@ -422,8 +451,8 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         if (want_ck) {
                             const int64_t g[3] = {gp, gm, gn};
                             ck_fold3(ck_lo, ck_hi,
-                                     (3ull << 60) | ((uint64_t)g[r0] << 40) | ((uint64_t)g[r1] << 20) |
-                                         (uint64_t)g[r2],
+                                     (3ull << 60) | ((uint64_t)g[O::R0] << 40) |
+                                         ((uint64_t)g[O::R1] << 20) | (uint64_t)g[O::R2],
                                      tc);
                         }
                     }
@@ -431,16 +460,20 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (tr && lane == 0) tr[5] = globaltimer();
+            if (lane == 0) {
+                if (rank == 0) mbar_arrive(&tempty[acc]);
+                else mbar_arrive_cluster(tempty_leader + acc * 8u);
+            }
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
         if (want_ck) ck_flush3(ck_lo, ck_hi, args.checksum);
     }
 
     tc_fence_before();
-    __syncthreads();
+    cluster_sync();
     tc_fence_after();
-    if (warp == 1) tmem_dealloc<512>(tmem_base);
+    if (warp == 1) tmem_dealloc_pair<512>(tmem_base);
 }
 
 int64_t tally3_units(const Tally3Args& a) {
@@ -457,17 +490,43 @@ int64_t tally3_units(const Tally3Args& a) {
     return units;
 }
 
-cudaError_t launch_tally3(const CUtensorMap& tmA, const CUtensorMap& tmB, const Tally3Args& a,
+cudaError_t launch_tally3(const CUtensorMap& tmA, const CUtensorMap& tmB, const Tally3Args& a0,
                           int num_sms, cudaStream_t stream, int64_t* n_units_out) {
+    Tally3Args a = a0;
+    {
+        const char* tre = getenv("CCC_TRACE_PTR");   // diagnostics: device pointer (decimal)
+        a.trace = tre ? reinterpret_cast<unsigned long long*>(strtoull(tre, nullptr, 10)) : nullptr;
+    }
     const int64_t units = tally3_units(a);
     if (n_units_out) *n_units_out = units;
     if (units == 0) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(tally3_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem3);
-    if (e != cudaSuccess) return e;
-    const int grid = (int)(units < num_sms ? units : num_sms);
-    tally3_kernel<<<grid, kThreads3, kSmem3, stream>>>(tmA, tmB, a);
-    return cudaGetLastError();
+    const int64_t pairs = num_sms / 2;
+    const int grid = (int)(2 * (units < pairs ? units : pairs));
+    auto go = [&](auto kern) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem3);
+        if (e != cudaSuccess) return e;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3(kThreads3);
+        cfg.dynamicSmemBytes = kSmem3;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, a);
+    };
+    switch (a.order) {
+        case 0: return go(tally3_kernel<0>);
+        case 1: return go(tally3_kernel<1>);
+        case 2: return go(tally3_kernel<2>);
+        case 3: return go(tally3_kernel<3>);
+        case 4: return go(tally3_kernel<4>);
+        default: return go(tally3_kernel<5>);
+    }
 }
 
 }  // namespace ccc
