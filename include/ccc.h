@@ -154,11 +154,15 @@ ccc_status ccc_2way(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double ga
  *             canonical (i < j globally).
  * Output buffers / flags as in ccc_2way.  N_a, N_b: [rows][ccc_k_pad(n_f)], 128-B
  * aligned.  If g_d != NULL the raw int32 G_ij = sum_q n_iq n_jq of every computed
- * tile is also stored at g_d[i*ldg + j] (local indices; used by the 3-way path). */
+ * tile is also stored at g_d[i*ldg + j] (local indices; used by the 3-way path).
+ * gamma: the constant w_a / w_b were expanded with (ccc_expand).  For the paper's
+ * gamma = 2/3 (compared with ==, pass 2.0/3.0) the epilogue uses the equivalent
+ * integer form w(0) = (n_f + s)/(3n_f), w(1) = (3n_f - s)/(3n_f) and does not read w
+ * (fewer FP64 multiplies, same result within 2 ulp); any other gamma reads w. */
 ccc_status ccc_2way_block(const int8_t* N_a, const int32_t* s_a, const double* w_a,
                           int64_t n_a, int64_t a_row0, int64_t a_lo, int64_t a_hi,
                           const int8_t* N_b, const int32_t* s_b, const double* w_b,
-                          int64_t n_b, int64_t b_row0, int diag, int64_t n_f,
+                          int64_t n_b, int64_t b_row0, int diag, int64_t n_f, double gamma,
                           uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
                           uint64_t* checksum_d, int32_t* g_d, int64_t ldg, void* stream);
 
@@ -178,8 +182,9 @@ ccc_status ccc_3way_prepare(const uint8_t* packed_d, int64_t n_v, int64_t n_f, d
  *   CCC(a,b,c) = T/(8n_f) * w_i(a) w_j(b) w_k(c)                 (Eq.4-5)
  * writing record t = ccc_triple_index(n_v,i,j,k) - rec_begin of every triple of the
  * stage: tallies_d uint32 [rec_count][8], ccc_d double/float [rec_count][8],
- * checksum_d as in ccc_2way. */
-ccc_status ccc_3way_stage(int64_t n_v, int64_t n_f, int64_t n_stages, int64_t stage,
+ * checksum_d as in ccc_2way.  gamma: the value given to ccc_3way_prepare (selects the
+ * integer form for gamma = 2/3 as in ccc_2way_block; n_f <= 500000). */
+ccc_status ccc_3way_stage(int64_t n_v, int64_t n_f, double gamma, int64_t n_stages, int64_t stage,
                           uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
                           uint64_t* checksum_d, void* ws_d, size_t ws_bytes, void* stream);
 
@@ -209,12 +214,12 @@ int64_t ccc_3way_unit_records(const ccc_block* bp, int64_t p_lo, int64_t p_hi,
  *   bp==bm==bn : in-block lexicographic triple order, starting at the first pivot p_lo;
  *   bp==bm     : record = (in-block pair index of (p,m) - that of (p_lo,p_lo+1)) * |N| + n-n_lo;
  *   otherwise  : ((p-p_lo)*|M| + (m-m_lo))*|N| + (n-n_lo).
- * Outputs and flags as in ccc_3way_stage; the checksum digest uses global canonical
+ * Outputs, flags and gamma as in ccc_3way_stage; the checksum digest uses global canonical
  * indices, so unit checksums of a decomposition add up to the single-GPU checksum. */
 ccc_status ccc_3way_unit(const ccc_block* bp, int64_t p_lo, int64_t p_hi, const ccc_block* bm,
                          int64_t m_lo, int64_t m_hi, const ccc_block* bn, int64_t n_lo,
                          int64_t n_hi, int order, const int32_t* G_d, int64_t ldG, int64_t n_f,
-                         uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
+                         double gamma, uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
                          uint64_t* checksum_d, void* stream);
 
 /* ccc_3way_prepare followed by ccc_3way_stage(n_stages, stage). */

@@ -53,13 +53,13 @@ _SIGS = {
     "ccc_expand": (_int, [_vp, _i64, _i64, _dbl, _vp, _vp, _vp, _vp]),
     "ccc_2way": (_int, [_vp, _i64, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "ccc_2way_block": (_int, [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _i64, _i64,
-                              _int, _i64, _u32, _vp, _vp, _vp, _vp, _i64, _vp]),
+                              _int, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _i64, _vp]),
     "ccc_3way_prepare": (_int, [_vp, _i64, _i64, _dbl, _vp, _sz, _vp]),
-    "ccc_3way_stage": (_int, [_i64, _i64, _i64, _i64, _u32, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "ccc_3way_stage": (_int, [_i64, _i64, _dbl, _i64, _i64, _u32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "ccc_3way": (_int, [_vp, _i64, _i64, _dbl, _u32, _i64, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
     "ccc_3way_unit_records": (_i64, [_vp, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _i64]),
     "ccc_3way_unit": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _i64, _int, _vp, _i64,
-                             _i64, _u32, _vp, _vp, _vp, _vp]),
+                             _i64, _dbl, _u32, _vp, _vp, _vp, _vp]),
     "ccc_e2e_workspace_bytes": (_sz, [_i64, _i64, _u32]),
     "ccc_2way_host": (_int, [_vp, _i64, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _sz, _vp]),
 }
@@ -232,12 +232,13 @@ def ccc_2way(packed: torch.Tensor, n_f: int, gamma: float = GAMMA,
 
 def ccc_2way_block(N_a, s_a, w_a, a_row0, a_lo, a_hi, N_b, s_b, w_b, b_row0, diag: bool, n_f,
                    out_flags, tallies=None, ccc=None, checksum=None, g=None, ldg=0,
-                   stream=None):
+                   stream=None, gamma=GAMMA):
+    """gamma: the value the w arrays were expanded with (selects the kernel's arithmetic)."""
     n_a, n_b = N_a.shape[0], N_b.shape[0]
     for t, n in ((N_a, "N_a"), (N_b, "N_b")):
         _dev(t, torch.int8, n)
     _check(lib().ccc_2way_block(_p(N_a), _p(s_a), _p(w_a), n_a, a_row0, a_lo, a_hi, _p(N_b),
-                                _p(s_b), _p(w_b), n_b, b_row0, int(bool(diag)), n_f, out_flags,
+                                _p(s_b), _p(w_b), n_b, b_row0, int(bool(diag)), n_f, gamma, out_flags,
                                 _p(tallies), _p(ccc), _p(checksum), _p(g), ldg, _stream(stream)))
     return tallies, ccc, checksum
 
@@ -253,10 +254,11 @@ def ccc_3way_prepare(packed, n_f, gamma=GAMMA, ws=None, stream=None):
 
 
 def ccc_3way_stage(n_v, n_f, n_stages, stage, ws, out_flags=OUT_TALLY | OUT_CCC_F64,
-                   tallies=None, ccc=None, checksum=None, stream=None):
+                   tallies=None, ccc=None, checksum=None, stream=None, gamma=GAMMA):
+    """gamma: the value given to ccc_3way_prepare for this workspace."""
     _, _, _, rec_count = ccc_stage_range(n_v, n_stages, stage)
     tallies, ccc, checksum = _outputs(rec_count, 8, out_flags, ws.device, tallies, ccc, checksum)
-    _check(lib().ccc_3way_stage(n_v, n_f, n_stages, stage, out_flags, _p(tallies), _p(ccc),
+    _check(lib().ccc_3way_stage(n_v, n_f, gamma, n_stages, stage, out_flags, _p(tallies), _p(ccc),
                                 _p(checksum), _p(ws), ws.numel(), _stream(stream)))
     return tallies, ccc, checksum
 
@@ -292,8 +294,9 @@ def ccc_3way_unit_records(bp, p_lo, p_hi, bm, m_lo, m_hi, bn, n_lo, n_hi) -> int
 
 def ccc_3way_unit(bp, p_lo, p_hi, bm, m_lo, m_hi, bn, n_lo, n_hi, order, G, n_f,
                   out_flags=OUT_TALLY | OUT_CCC_F64, tallies=None, ccc=None, checksum=None,
-                  stream=None):
-    """One tetrahedral 3-way unit; `order` is a role tuple like ("m", "p", "n") or 0..5."""
+                  stream=None, gamma=GAMMA):
+    """One tetrahedral 3-way unit; `order` is a role tuple like ("m", "p", "n") or 0..5;
+    gamma: the value the blocks' w were expanded with."""
     if not isinstance(order, int):
         order = ORDERS[tuple(order)]
     n_rec = ccc_3way_unit_records(bp, p_lo, p_hi, bm, m_lo, m_hi, bn, n_lo, n_hi)
@@ -302,7 +305,7 @@ def ccc_3way_unit(bp, p_lo, p_hi, bm, m_lo, m_hi, bn, n_lo, n_hi, order, G, n_f,
     tallies, ccc, checksum = _outputs(n_rec, 8, out_flags, G.device, tallies, ccc, checksum)
     _check(lib().ccc_3way_unit(ctypes.byref(bp), p_lo, p_hi, ctypes.byref(bm), m_lo, m_hi,
                                ctypes.byref(bn), n_lo, n_hi, order, _p(G), G.shape[-1], n_f,
-                               out_flags, _p(tallies), _p(ccc), _p(checksum), _stream(stream)))
+                               gamma, out_flags, _p(tallies), _p(ccc), _p(checksum), _stream(stream)))
     return tallies, ccc, checksum
 
 

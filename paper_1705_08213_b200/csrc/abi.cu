@@ -164,11 +164,25 @@ WsLayout ws_layout(int way, int64_t n_v, int64_t n_f) {
     return L;
 }
 
+// gamma == 2/3 exactly as the caller computed it (2.0/3.0 in C, 2/3 in Python): the
+// weights are then w(a) = U(a) / (3 n_f) with integer U, and the epilogues form CCC
+// from integer products instead of the stored doubles (K-2).
+bool is_gamma23(double gamma) { return gamma == 2.0 / 3.0; }
+
+// 3-way: CCC = (T U_p U_m) U_n / (216 n_f^4); T U_p U_m <= 72 n_f^3 stays below 2^63
+// (and exact in double below 2^53, n_f <= 50000) for n_f <= 500000.
+void set_exact3(ccc::Tally3Args& a, int64_t n_f, double gamma) {
+    a.exact23 = (is_gamma23(gamma) && n_f <= 500000) ? 1 : 0;
+    const double nf = (double)n_f;
+    a.inv_d = 1.0 / (216.0 * nf * nf * nf * nf);
+}
+
 ccc_status block_impl(const int8_t* N_a, const int32_t* s_a, const double* w_a, int64_t n_a,
                       int64_t a_row0, int64_t a_lo, int64_t a_hi, const int8_t* N_b,
                       const int32_t* s_b, const double* w_b, int64_t n_b, int64_t b_row0,
-                      int diag, int64_t n_f, uint32_t flags, uint32_t* tallies, void* ccc,
-                      uint64_t* ck, int32_t* g, int64_t ldg, cudaStream_t stream, int num_sms) {
+                      int diag, int64_t n_f, double gamma, uint32_t flags, uint32_t* tallies,
+                      void* ccc, uint64_t* ck, int32_t* g, int64_t ldg, cudaStream_t stream,
+                      int num_sms) {
     const int64_t k_pad = kpad_of(n_f);
     CUtensorMap tmA, tmB;
     CCC_CHECK(make_tmap(&tmA, N_a, n_a, k_pad, ccc::kBM));
@@ -183,6 +197,9 @@ ccc_status block_impl(const int8_t* N_a, const int32_t* s_a, const double* w_a, 
     a.n_f = (int32_t)n_f;
     a.k_blocks = (int32_t)(k_pad / ccc::kBK);
     a.out_flags = (int32_t)flags;
+    // gamma = 2/3: CCC = (T U_i(a)) U_j(b) / (36 n_f^3) from integers (K-2)
+    a.exact23 = is_gamma23(gamma) ? 1 : 0;
+    a.inv_d = 1.0 / (36.0 * (double)n_f * (double)n_f * (double)n_f);
     a.s_a = s_a;
     a.s_b = s_b;
     a.w_a = w_a;
@@ -310,7 +327,7 @@ ccc_status ccc_expand(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double 
 ccc_status ccc_2way_block(const int8_t* N_a, const int32_t* s_a, const double* w_a, int64_t n_a,
                           int64_t a_row0, int64_t a_lo, int64_t a_hi, const int8_t* N_b,
                           const int32_t* s_b, const double* w_b, int64_t n_b, int64_t b_row0,
-                          int diag, int64_t n_f, uint32_t out_flags, uint32_t* tallies_d,
+                          int diag, int64_t n_f, double gamma, uint32_t out_flags, uint32_t* tallies_d,
                           void* ccc_d, uint64_t* checksum_d, int32_t* g_d, int64_t ldg,
                           void* stream) {
     g_launches = 0;
@@ -331,7 +348,7 @@ ccc_status ccc_2way_block(const int8_t* N_a, const int32_t* s_a, const double* w
     int sms;
     CCC_CHECK(check_device(&sms));
     return block_impl(N_a, s_a, w_a, n_a, a_row0, a_lo, a_hi, N_b, s_b, w_b, n_b, b_row0, diag,
-                      n_f, out_flags, tallies_d, ccc_d, checksum_d, g_d, ldg,
+                      n_f, gamma, out_flags, tallies_d, ccc_d, checksum_d, g_d, ldg,
                       (cudaStream_t)stream, sms);
 }
 
@@ -356,7 +373,7 @@ ccc_status ccc_2way(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double ga
     double* w = reinterpret_cast<double*>(ws + L.w);
     cudaStream_t st = (cudaStream_t)stream;
     CCC_CUDA(ccc::launch_expand(packed_d, n_v, n_f, gamma, N, s, w, sms, st), "expand launch");
-    CCC_CHECK(block_impl(N, s, w, n_v, 0, 0, n_v, N, s, w, n_v, 0, 1, n_f, out_flags, tallies_d,
+    CCC_CHECK(block_impl(N, s, w, n_v, 0, 0, n_v, N, s, w, n_v, 0, 1, n_f, gamma, out_flags, tallies_d,
                          ccc_d, checksum_d, nullptr, 0, st, sms));
     g_launches += 1;
     return CCC_OK;
@@ -381,13 +398,13 @@ ccc_status ccc_3way_prepare(const uint8_t* packed_d, int64_t n_v, int64_t n_f, d
     int32_t* G = reinterpret_cast<int32_t*>(ws + L.G);
     cudaStream_t st = (cudaStream_t)stream;
     CCC_CUDA(ccc::launch_expand(packed_d, n_v, n_f, gamma, N, s, w, sms, st), "expand launch");
-    CCC_CHECK(block_impl(N, s, w, n_v, 0, 0, n_v, N, s, w, n_v, 0, 1, n_f, 0, nullptr, nullptr,
+    CCC_CHECK(block_impl(N, s, w, n_v, 0, 0, n_v, N, s, w, n_v, 0, 1, n_f, gamma, 0, nullptr, nullptr,
                          nullptr, G, n_v, st, sms));
     g_launches += 1;
     return CCC_OK;
 }
 
-ccc_status ccc_3way_stage(int64_t n_v, int64_t n_f, int64_t n_stages, int64_t stage,
+ccc_status ccc_3way_stage(int64_t n_v, int64_t n_f, double gamma, int64_t n_stages, int64_t stage,
                           uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
                           uint64_t* checksum_d, void* ws_d, size_t ws_bytes, void* stream) {
     g_launches = 0;
@@ -424,6 +441,7 @@ ccc_status ccc_3way_stage(int64_t n_v, int64_t n_f, int64_t n_stages, int64_t st
     a.n_f = (int32_t)n_f;
     a.k_blocks = (int32_t)(k_pad / ccc::kBK);
     a.out_flags = (int32_t)out_flags;
+    set_exact3(a, n_f, gamma);
     a.tallies = tallies_d;
     a.ccc = ccc_d;
     a.checksum = reinterpret_cast<unsigned long long*>(checksum_d);
@@ -458,7 +476,7 @@ int64_t ccc_3way_unit_records(const ccc_block* bp, int64_t p_lo, int64_t p_hi,
 ccc_status ccc_3way_unit(const ccc_block* bp, int64_t p_lo, int64_t p_hi, const ccc_block* bm,
                          int64_t m_lo, int64_t m_hi, const ccc_block* bn, int64_t n_lo,
                          int64_t n_hi, int order, const int32_t* G_d, int64_t ldG, int64_t n_f,
-                         uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
+                         double gamma, uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
                          uint64_t* checksum_d, void* stream) {
     g_launches = 0;
     if (!bp || !bm || !bn) return fail(CCC_ERR_INVALID_ARGUMENT, "block descriptors must not be NULL");
@@ -513,6 +531,7 @@ ccc_status ccc_3way_unit(const ccc_block* bp, int64_t p_lo, int64_t p_hi, const 
     a.n_f = (int32_t)n_f;
     a.k_blocks = (int32_t)(k_pad / ccc::kBK);
     a.out_flags = (int32_t)out_flags;
+    set_exact3(a, n_f, gamma);
     a.tallies = tallies_d;
     a.ccc = ccc_d;
     a.checksum = reinterpret_cast<unsigned long long*>(checksum_d);
@@ -532,7 +551,7 @@ ccc_status ccc_3way(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double ga
     if (n_v >= 3) CCC_CHECK(check_outputs(out_flags, tallies_d, ccc_d, checksum_d));
     CCC_CHECK(ccc_3way_prepare(packed_d, n_v, n_f, gamma, ws_d, ws_bytes, stream));
     const int64_t n1 = g_launches;
-    CCC_CHECK(ccc_3way_stage(n_v, n_f, n_stages, stage, out_flags, tallies_d, ccc_d, checksum_d,
+    CCC_CHECK(ccc_3way_stage(n_v, n_f, gamma, n_stages, stage, out_flags, tallies_d, ccc_d, checksum_d,
                              ws_d, ws_bytes, stream));
     g_launches += n1;
     return CCC_OK;
@@ -646,7 +665,7 @@ ccc_status ccc_2way_host(const uint8_t* codes_h, int64_t n_v, int64_t n_f, doubl
         }
         uint32_t* bt = reinterpret_cast<uint32_t*>(base + L.band_t[b]);
         void* bc = base + L.band_c[b];
-        rc = block_impl(N, s, w, n_v, 0, r0, r1, N, s, w, n_v, 0, 1, n_f, out_flags, bt, bc, ck,
+        rc = block_impl(N, s, w, n_v, 0, r0, r1, N, s, w, n_v, 0, 1, n_f, gamma, out_flags, bt, bc, ck,
                         nullptr, 0, st, sms);
         if (rc != CCC_OK) break;
         ++launches;

@@ -121,6 +121,9 @@ struct Tally2Args {
     int64_t ldg;
     int64_t rec_row_base;      // diag: record index of row a_lo's first pair
     int32_t sup_rows, sup_cols;  // super-tile shape (elements) of the tile raster
+    int32_t k_alternate;         // odd waves of tiles walk K backwards (L2 reuse across waves)
+    int32_t exact23;             // gamma == 2/3: CCC = double(T*U_i(a)) * (U_j(b)/D), D = 36 n_f^3
+    double inv_d;                // 1 / (36 n_f^3)
     unsigned long long* trace; // optional per-tile %globaltimer trace (diagnostics)
 };
 
@@ -142,6 +145,9 @@ struct Tally3Args {
     int64_t p_lo, p_hi, m_lo, m_hi, n_lo, n_hi;
     int32_t same_pm, same_mn, order, layout;   // layout: 0 in-block lexicographic,
                                                // 1 pair(p,m)-major x n, 2 dense box
+    int32_t exact23;           // gamma == 2/3: CCC = double(T*U_p*U_m) * (U_n/D), D = 216 n_f^4
+    int32_t pad3_;
+    double inv_d;              // 1 / (216 n_f^4)
     const int32_t* G;          // global pairwise G: G[min * ldG + max] (i < j valid)
     int64_t ldG;
     int64_t rec_base;          // subtracted from every record index (stages)

@@ -161,7 +161,7 @@ __device__ __forceinline__ uint32_t gord(const int32_t* G, int64_t ld, int64_t g
     else return (uint32_t)__ldg(G + gy * ld + gx);
 }
 
-template <int kOrder>
+template <int kOrder, bool kExact>
 __global__ void __launch_bounds__(kThreads3, 1)
 tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const Tally3Args args) {
@@ -330,6 +330,7 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         const bool want_c = want_c64 | want_c32;
         const uint32_t eight_nf = 8u * (uint32_t)args.n_f;
         const double inv8nf = 1.0 / (8.0 * (double)args.n_f);
+        const uint32_t nf = (uint32_t)args.n_f;
         const int64_t nbp = args.bp.rows, nN = args.n_hi - args.n_lo, nM = args.m_hi - args.m_lo;
         const int32_t cpair = 2 * (int32_t)(lane & 3);
         unsigned long long ck_lo = 0, ck_hi = 0;
@@ -345,12 +346,14 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             if (tr && lane == 0) tr[4] = globaltimer();
             const int64_t gp = args.bp.row0 + p;
             const uint32_t s_p = (uint32_t)__ldg(args.bp.s + p);
-            const double wp0 = __ldg(args.bp.w + 2 * p) * inv8nf;
-            const double wp1 = __ldg(args.bp.w + 2 * p + 1) * inv8nf;
+            // general gamma: w_p(a) / (8 n_f); gamma = 2/3: integer U_p(a) = 3 n_f - S_p(a)
+            const double wp0 = kExact ? 0.0 : __ldg(args.bp.w + 2 * p) * inv8nf;
+            const double wp1 = kExact ? 0.0 : __ldg(args.bp.w + 2 * p + 1) * inv8nf;
+            const uint64_t up0 = nf + s_p, up1 = 3u * nf - s_p;
             // my 2 rows m = row0(J) + rank*128 + quad*32 + half*16 + r*8 + lane/4
             int64_t rec_r[2], m_r[2];
             uint32_t s_m[2], g_pm[2];
-            double wpm[2][4];
+            double wpm[2][4];      // general: w_p(a_p) w_m(a_m) / (8 n_f); exact: U_p U_m (integer)
             bool ok_r[2];
             bool my_any = false;
 #pragma unroll
@@ -361,11 +364,19 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 const int64_t mc = m < args.m_hi ? m : args.m_hi - 1;
                 s_m[r] = (uint32_t)__ldg(args.bm.s + mc);
                 g_pm[r] = ok_r[r] ? gord<kOrder, 0, 1>(args.G, args.ldG, gp, args.bm.row0 + m) : 0u;
-                const double wm0 = __ldg(args.bm.w + 2 * mc), wm1 = __ldg(args.bm.w + 2 * mc + 1);
-                wpm[r][0] = wp0 * wm0;  // (a_p, a_m) = (0,0), includes 1/(8 n_f)
-                wpm[r][1] = wp0 * wm1;
-                wpm[r][2] = wp1 * wm0;
-                wpm[r][3] = wp1 * wm1;
+                if constexpr (kExact) {
+                    const uint64_t um0 = nf + s_m[r], um1 = 3u * nf - s_m[r];
+                    wpm[r][0] = __longlong_as_double((long long)(up0 * um0));   // bit-carried ints
+                    wpm[r][1] = __longlong_as_double((long long)(up0 * um1));
+                    wpm[r][2] = __longlong_as_double((long long)(up1 * um0));
+                    wpm[r][3] = __longlong_as_double((long long)(up1 * um1));
+                } else {
+                    const double wm0 = __ldg(args.bm.w + 2 * mc), wm1 = __ldg(args.bm.w + 2 * mc + 1);
+                    wpm[r][0] = wp0 * wm0;  // (a_p, a_m) = (0,0), includes 1/(8 n_f)
+                    wpm[r][1] = wp0 * wm1;
+                    wpm[r][2] = wp1 * wm0;
+                    wpm[r][3] = wp1 * wm1;
+                }
                 if (args.layout == 0)
                     rec_r[r] = c3(nbp) - c3(nbp - p) + c2(nbp - p - 1) - c2(nbp - mc) - mc - 1 -
                                args.rec_base;
@@ -392,10 +403,17 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 const uint32_t gpnB = gord<kOrder, 0, 2>(args.G, args.ldG, gp, gnB);
                 double wA0 = 0.0, wA1 = 0.0, wB0 = 0.0, wB1 = 0.0;
                 if (want_c) {
-                    wA0 = __ldg(args.bn.w + 2 * nAc);
-                    wA1 = __ldg(args.bn.w + 2 * nAc + 1);
-                    wB0 = __ldg(args.bn.w + 2 * nBc);
-                    wB1 = __ldg(args.bn.w + 2 * nBc + 1);
+                    if constexpr (kExact) {   // U_n(c) / (216 n_f^4)
+                        wA0 = (double)(nf + sA) * args.inv_d;
+                        wA1 = (double)(3u * nf - sA) * args.inv_d;
+                        wB0 = (double)(nf + sB) * args.inv_d;
+                        wB1 = (double)(3u * nf - sB) * args.inv_d;
+                    } else {
+                        wA0 = __ldg(args.bn.w + 2 * nAc);
+                        wA1 = __ldg(args.bn.w + 2 * nAc + 1);
+                        wB0 = __ldg(args.bn.w + 2 * nBc);
+                        wB1 = __ldg(args.bn.w + 2 * nBc + 1);
+                    }
                 }
                 tmem_ld_wait();
 #pragma unroll
@@ -432,8 +450,15 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                             double cr[8], cc[8];
 #pragma unroll
                             for (int ab = 0; ab < 4; ++ab) {
-                                cr[2 * ab + 0] = (double)t[2 * ab + 0] * wpm[r][ab] * wn0;
-                                cr[2 * ab + 1] = (double)t[2 * ab + 1] * wpm[r][ab] * wn1;
+                                if constexpr (kExact) {
+                                    // CCC = T U_p U_m U_n / (216 n_f^4); T U_p U_m < 2^53 is exact
+                                    const uint64_t upm = (uint64_t)__double_as_longlong(wpm[r][ab]);
+                                    cr[2 * ab + 0] = (double)(t[2 * ab + 0] * upm) * wn0;
+                                    cr[2 * ab + 1] = (double)(t[2 * ab + 1] * upm) * wn1;
+                                } else {
+                                    cr[2 * ab + 0] = (double)t[2 * ab + 0] * wpm[r][ab] * wn0;
+                                    cr[2 * ab + 1] = (double)t[2 * ab + 1] * wpm[r][ab] * wn1;
+                                }
                             }
                             perm_cells<O::R0, O::R1, O::R2>(cr, cc);
                             if (want_c64) {
@@ -519,13 +544,23 @@ cudaError_t launch_tally3(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
         cfg.numAttrs = 1;
         return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, a);
     };
+    if (a.exact23) {
+        switch (a.order) {
+            case 0: return go(tally3_kernel<0, true>);
+            case 1: return go(tally3_kernel<1, true>);
+            case 2: return go(tally3_kernel<2, true>);
+            case 3: return go(tally3_kernel<3, true>);
+            case 4: return go(tally3_kernel<4, true>);
+            default: return go(tally3_kernel<5, true>);
+        }
+    }
     switch (a.order) {
-        case 0: return go(tally3_kernel<0>);
-        case 1: return go(tally3_kernel<1>);
-        case 2: return go(tally3_kernel<2>);
-        case 3: return go(tally3_kernel<3>);
-        case 4: return go(tally3_kernel<4>);
-        default: return go(tally3_kernel<5>);
+        case 0: return go(tally3_kernel<0, false>);
+        case 1: return go(tally3_kernel<1, false>);
+        case 2: return go(tally3_kernel<2, false>);
+        case 3: return go(tally3_kernel<3, false>);
+        case 4: return go(tally3_kernel<4, false>);
+        default: return go(tally3_kernel<5, false>);
     }
 }
 

@@ -112,7 +112,7 @@ class CudaBackend:
         C = C[:n_rec] if C is not None else None
         self.ccc.ccc_3way_unit(self._blk(ring, u.pb), p_lo, p_hi, self._blk(ring, u.mb), u.m_lo,
                                u.m_hi, self._blk(ring, u.nb), u.n_lo, u.n_hi, u.order, ring.G,
-                               self.n_f, f, T, C, ck)
+                               self.n_f, f, T, C, ck, gamma=self.gamma)
         return T, C
 
     def block(self, A, a_row0, a_lo, a_hi, B, b_row0, diag, out, ck, timed=False):
@@ -124,7 +124,7 @@ class CudaBackend:
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             ev[0].record()
         self.ccc.ccc_2way_block(N_a, s_a, w_a, a_row0, a_lo, a_hi, N_b, s_b, w_b, b_row0, diag,
-                                self.n_f, self.out_flags, T, C, ck)
+                                self.n_f, self.out_flags, T, C, ck, gamma=self.gamma)
         if timed:
             ev[1].record()
             self.kernel_events.append(ev)

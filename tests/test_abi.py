@@ -109,7 +109,7 @@ def test_validation_before_launch():
     assert lib.ccc_last_launch_count() == 0
     # diag block requires A == B
     st = lib.ccc_2way_block(ctypes.c_void_p(256), null, null, 8, 0, 0, 8, ctypes.c_void_p(512),
-                            null, null, 8, 0, 1, 10, 0, null, null, null, null, 0, null)
+                            null, null, 8, 0, 1, 10, 2 / 3, 0, null, null, null, null, 0, null)
     assert st == ccc.ERR_INVALID_ARGUMENT
 
 

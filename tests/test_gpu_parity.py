@@ -103,6 +103,7 @@ def test_2way_f32_and_gamma():
     codes = _codes("random", 150, 300, seed=5)
     _check_2way_full(codes, flags=TAL | F32)
     _check_2way_full(codes, flags=F64, gamma=0.0)
+    _check_2way_full(codes, flags=F32 | CK, gamma=0.5)
 
 
 def test_2way_checksum_only_and_tally_only():
@@ -210,14 +211,14 @@ def test_2way_C2_full_size_sampled_and_invariants():
 
 
 # ------------------------------------------------------------------- 3-way
-def _check_3way_full(codes, n_stages=1, flags=TAL | F64 | CK):
+def _check_3way_full(codes, n_stages=1, flags=TAL | F64 | CK, gamma=oracle.GAMMA):
     n_v, n_f = codes.shape
-    To, Co = oracle.all_triples(codes)
+    To, Co = oracle.all_triples(codes, gamma)
     packed = ccc.ccc_pack(codes.cuda())
-    ws = ccc.ccc_3way_prepare(packed, n_f)
+    ws = ccc.ccc_3way_prepare(packed, n_f, gamma)
     Ts, Cs, cks = [], [], 0
     for st in range(n_stages):
-        T, C, ck = ccc.ccc_3way_stage(n_v, n_f, n_stages, st, ws, out_flags=flags)
+        T, C, ck = ccc.ccc_3way_stage(n_v, n_f, n_stages, st, ws, out_flags=flags, gamma=gamma)
         if flags & TAL:
             Ts.append(_t(T))
         if flags & (F64 | F32):
@@ -246,6 +247,14 @@ def test_3way_stages_and_variants():
     _check_3way_full(codes, n_stages=3, flags=TAL | F32)
     _check_3way_full(_codes("planted", 90, 250), n_stages=2)
     _check_3way_full(torch.full((70, 130), 3, dtype=torch.uint8))
+
+
+@pytest.mark.parametrize("gamma", [0.0, 0.5, 1.0])
+def test_3way_general_gamma(gamma):
+    """gamma != 2/3 takes the epilogue that reads the stored weights w (the integer form
+    only holds for the paper's 2/3)."""
+    _check_3way_full(_codes("hwe", 140, 301), n_stages=2, flags=TAL | F64, gamma=gamma)
+    _check_3way_full(_codes("random", 70, 97), flags=F32, gamma=gamma)
 
 
 def test_3way_C4_full_size_stage_sampled():
@@ -353,22 +362,24 @@ def test_ring_nccl_two_gpus():
     assert cks[0] == cks[1] == oracle.checksum(2, oracle.pair_list(n_v), To)
 
 
-@pytest.mark.parametrize("P", [1, 2, 3, 4])
-def test_tetrahedral_units_on_one_gpu(P):
+@pytest.mark.parametrize("P,gamma", [(1, oracle.GAMMA), (2, oracle.GAMMA), (3, oracle.GAMMA),
+                                     (4, oracle.GAMMA), (3, 0.25)])
+def test_tetrahedral_units_on_one_gpu(P, gamma):
     """Every rank's tetrahedral 3-way units ({A,A,A}, {D,D,S} both orders, the three
     parts of {A<B<C}) through ccc_3way_unit on per-block expanded data; union equals the
     single-GPU result triple for triple and the unit checksums add up."""
     from paper_1705_08213_b200 import decomp
     n_v, n_f = 150, 197
     codes = _codes("random", n_v, n_f, seed=31)
-    To, Co = oracle.all_triples(codes)
+    To, Co = oracle.all_triples(codes, gamma)
     # global pairwise G by the 2-way kernel on the whole matrix (what each rank builds
     # after the all-gather)
     N, s, w = ccc.ccc_expand(ccc.ccc_pack(codes.cuda()), n_f)
     G = torch.zeros((n_v, n_v), dtype=torch.int32, device="cuda")
     ccc.ccc_2way_block(N, s, w, 0, 0, n_v, N, s, w, 0, True, n_f, 0, g=G, ldg=n_v)
     bounds = decomp.block_bounds(n_v, P)
-    exp = [ccc.ccc_expand(ccc.ccc_pack(codes[lo:hi].contiguous().cuda()), n_f) for lo, hi in bounds]
+    exp = [ccc.ccc_expand(ccc.ccc_pack(codes[lo:hi].contiguous().cuda()), n_f, gamma)
+           for lo, hi in bounds]
     blks = [ccc.block(*exp[b], bounds[b][0]) for b in range(P)]
     seen = np.zeros(len(To), dtype=np.int64)
     total_ck = 0
@@ -377,7 +388,7 @@ def test_tetrahedral_units_on_one_gpu(P):
             ck = torch.zeros(2, dtype=torch.int64, device="cuda")
             T, C, ck = ccc.ccc_3way_unit(blks[u.pb], u.p_lo, u.p_hi, blks[u.mb], u.m_lo, u.m_hi,
                                          blks[u.nb], u.n_lo, u.n_hi, u.order, G, n_f,
-                                         TAL | F64 | CK, checksum=ck)
+                                         TAL | F64 | CK, checksum=ck, gamma=gamma)
             tr = list(decomp.unit3_triples(u, bounds))
             assert T.shape[0] == len(tr) == decomp.unit3_count(u, bounds)
             if not tr:
