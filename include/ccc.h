@@ -118,6 +118,27 @@ size_t ccc_workspace_bytes(int num_way, int64_t n_v, int64_t n_f);
 ccc_status ccc_pack(const uint8_t* codes_d, int64_t n_v, int64_t n_f, uint8_t* packed_d,
                     void* stream);
 
+/* Threshold-compacted output ("very few of the elements
+ * are actually needed -- only those above a certain threshold").  Passed as the
+ * `compact` argument of ccc_2way, ccc_2way_block, ccc_3way_stage, ccc_3way_unit and
+ * ccc_3way; NULL selects the dense record layout.  When non-NULL, a record is kept iff
+ * the largest of its 4 (8) CCC cells is > threshold (computed in fp64 whatever the
+ * output precision), and every kept record is appended at an arbitrary free slot:
+ *   keys_d[slot]    = i * 2^20 + j (2-way) or i * 2^40 + j * 2^20 + k (3-way), GLOBAL
+ *                     indices, i < j < k
+ *   tallies_d[slot] = its 4 (8) tallies (if CCC_OUT_TALLY), ccc_d[slot] = its CCC cells
+ *                     (if CCC_OUT_CCC_F64 / _F32), both [capacity][cells]
+ * *count_d (zeroed by the caller; accumulates across calls) is increased by the number
+ * of kept records.  If it ends above `capacity`, only `capacity` of the kept records
+ * (an arbitrary subset) were stored: re-run with a larger buffer.  The checksum, if
+ * requested, still covers every record.  Slot order is nondeterministic. */
+typedef struct {
+    double threshold;
+    int64_t capacity;     /* records keys_d / tallies_d / ccc_d can hold */
+    uint64_t* keys_d;     /* [capacity], 8-B aligned (device) */
+    uint64_t* count_d;    /* one counter (device), 8-B aligned */
+} ccc_compact;
+
 /* KB-expand (§8(a) a2; Eq.1): packed_d -> N_d int8 [n_v][ccc_k_pad(n_f)] with
  * N[i][q] = rho_{i,q}(1) in {0,1,2} (0 for q >= n_f), s_d int32 [n_v] with
  * s_i = sum_q rho_{i,q}(1) = S_i(1), and w_d double [n_v][2] with
@@ -137,10 +158,10 @@ ccc_status ccc_expand(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double 
  *   checksum_d uint64 [2] (lo, hi) += sum of record digests (CCC_OUT_CHECKSUM; the
  *              caller zeroes it first).
  * Outputs not selected may be NULL.  ws_d: >= ccc_workspace_bytes(2,...) bytes,
- * 256-B aligned. */
+ * 256-B aligned.  compact: NULL, or the threshold-compacted layout (ccc_compact). */
 ccc_status ccc_2way(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
                     uint32_t out_flags, uint32_t* tallies_d, void* ccc_d, uint64_t* checksum_d,
-                    void* ws_d, size_t ws_bytes, void* stream);
+                    void* ws_d, size_t ws_bytes, const ccc_compact* compact, void* stream);
 
 /* One block of the block-circulant 2-way decomposition (§4; §8(e)):
  * rows [a_lo, a_hi) of block A (expanded N_a / s_a / w_a, n_a rows, global index of
@@ -164,7 +185,8 @@ ccc_status ccc_2way_block(const int8_t* N_a, const int32_t* s_a, const double* w
                           const int8_t* N_b, const int32_t* s_b, const double* w_b,
                           int64_t n_b, int64_t b_row0, int diag, int64_t n_f, double gamma,
                           uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
-                          uint64_t* checksum_d, int32_t* g_d, int64_t ldg, void* stream);
+                          uint64_t* checksum_d, int32_t* g_d, int64_t ldg,
+                          const ccc_compact* compact, void* stream);
 
 /* 3-way preparation (§8(a) a2, a5 prerequisites): expand packed_d into the workspace
  * and compute the pairwise G = N N^T (upper triangle) that the 3-way epilogue needs. */
@@ -186,7 +208,8 @@ ccc_status ccc_3way_prepare(const uint8_t* packed_d, int64_t n_v, int64_t n_f, d
  * integer form for gamma = 2/3 as in ccc_2way_block; n_f <= 500000). */
 ccc_status ccc_3way_stage(int64_t n_v, int64_t n_f, double gamma, int64_t n_stages, int64_t stage,
                           uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
-                          uint64_t* checksum_d, void* ws_d, size_t ws_bytes, void* stream);
+                          uint64_t* checksum_d, void* ws_d, size_t ws_bytes,
+                          const ccc_compact* compact, void* stream);
 
 /* One vector block as seen by the 3-way unit call: expanded rows (ccc_expand) and the
  * global index of local row 0. */
@@ -220,13 +243,13 @@ ccc_status ccc_3way_unit(const ccc_block* bp, int64_t p_lo, int64_t p_hi, const 
                          int64_t m_lo, int64_t m_hi, const ccc_block* bn, int64_t n_lo,
                          int64_t n_hi, int order, const int32_t* G_d, int64_t ldG, int64_t n_f,
                          double gamma, uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
-                         uint64_t* checksum_d, void* stream);
+                         uint64_t* checksum_d, const ccc_compact* compact, void* stream);
 
 /* ccc_3way_prepare followed by ccc_3way_stage(n_stages, stage). */
 ccc_status ccc_3way(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
                     uint32_t out_flags, int64_t n_stages, int64_t stage, uint32_t* tallies_d,
                     void* ccc_d, uint64_t* checksum_d, void* ws_d, size_t ws_bytes,
-                    void* stream);
+                    const ccc_compact* compact, void* stream);
 
 /* End-to-end 2-way with HOST buffers (the e2e measurement of bench.py): copies
  * codes_h (uint8 [n_v][n_f], pinned for full speed) to the device, packs, runs

@@ -34,6 +34,57 @@ class CccBlock(ctypes.Structure):
                 ("rows", ctypes.c_int64), ("row0", ctypes.c_int64)]
 
 
+class CccCompact(ctypes.Structure):
+    """struct ccc_compact of include/ccc.h."""
+    _fields_ = [("threshold", ctypes.c_double), ("capacity", ctypes.c_int64),
+                ("keys_d", ctypes.c_void_p), ("count_d", ctypes.c_void_p)]
+
+
+class Compact:
+    """Threshold-compacted output buffers (ccc_compact): records whose
+    largest CCC cell exceeds `threshold` land in keys / tallies / ccc[:count] in arbitrary
+    order.  Pass as `compact=` to ccc_2way / ccc_2way_block / ccc_3way_stage /
+    ccc_3way_unit / ccc_3way; `count` accumulates across calls until reset()."""
+
+    def __init__(self, threshold: float, capacity: int, cells: int,
+                 out_flags: int = OUT_TALLY | OUT_CCC_F64, device="cuda"):
+        self.threshold, self.capacity, self.cells = float(threshold), int(capacity), cells
+        self.keys = torch.empty(self.capacity, dtype=torch.int64, device=device)
+        self.count = torch.zeros(1, dtype=torch.int64, device=device)
+        self.tallies = (torch.empty((self.capacity, cells), dtype=torch.int32, device=device)
+                        if out_flags & OUT_TALLY else None)
+        self.ccc = None
+        if out_flags & OUT_CCC_F64:
+            self.ccc = torch.empty((self.capacity, cells), dtype=torch.float64, device=device)
+        elif out_flags & OUT_CCC_F32:
+            self.ccc = torch.empty((self.capacity, cells), dtype=torch.float32, device=device)
+        self._c = CccCompact(self.threshold, self.capacity, self.keys.data_ptr(),
+                             self.count.data_ptr())
+
+    def reset(self):
+        self.count.zero_()
+
+    def kept(self) -> int:
+        return int(self.count.item())
+
+    def result(self):
+        """(count, keys, tallies, ccc) of the stored records (synchronises)."""
+        n = self.kept()
+        m = min(n, self.capacity)
+        sl = lambda t: None if t is None else t[:m]
+        return n, self.keys[:m], sl(self.tallies), sl(self.ccc)
+
+
+
+
+def decode_keys(keys: torch.Tensor, num_way: int) -> torch.Tensor:
+    """Compacted keys -> global indices [n][num_way]."""
+    k = keys.to(torch.int64)
+    if num_way == 2:
+        return torch.stack([k >> 20, k & 0xFFFFF], 1)
+    return torch.stack([k >> 40, (k >> 20) & 0xFFFFF, k & 0xFFFFF], 1)
+
+
 _lib = None
 _vp, _i64, _u32, _dbl, _int, _sz = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32,
                                     ctypes.c_double, ctypes.c_int, ctypes.c_size_t)
@@ -51,15 +102,17 @@ _SIGS = {
     "ccc_workspace_bytes": (_sz, [_int, _i64, _i64]),
     "ccc_pack": (_int, [_vp, _i64, _i64, _vp, _vp]),
     "ccc_expand": (_int, [_vp, _i64, _i64, _dbl, _vp, _vp, _vp, _vp]),
-    "ccc_2way": (_int, [_vp, _i64, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "ccc_2way": (_int, [_vp, _i64, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _sz, _vp, _vp]),
     "ccc_2way_block": (_int, [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _i64, _i64,
-                              _int, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _i64, _vp]),
+                              _int, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "ccc_3way_prepare": (_int, [_vp, _i64, _i64, _dbl, _vp, _sz, _vp]),
-    "ccc_3way_stage": (_int, [_i64, _i64, _dbl, _i64, _i64, _u32, _vp, _vp, _vp, _vp, _sz, _vp]),
-    "ccc_3way": (_int, [_vp, _i64, _i64, _dbl, _u32, _i64, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "ccc_3way_stage": (_int, [_i64, _i64, _dbl, _i64, _i64, _u32, _vp, _vp, _vp, _vp, _sz, _vp,
+                              _vp]),
+    "ccc_3way": (_int, [_vp, _i64, _i64, _dbl, _u32, _i64, _i64, _vp, _vp, _vp, _vp, _sz, _vp,
+                        _vp]),
     "ccc_3way_unit_records": (_i64, [_vp, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _i64]),
     "ccc_3way_unit": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _i64, _int, _vp, _i64,
-                             _i64, _dbl, _u32, _vp, _vp, _vp, _vp]),
+                             _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _vp]),
     "ccc_e2e_workspace_bytes": (_sz, [_i64, _i64, _u32]),
     "ccc_2way_host": (_int, [_vp, _i64, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _sz, _vp]),
 }
@@ -215,31 +268,45 @@ def _outputs(n_rec: int, width: int, out_flags: int, device, tallies=None, ccc=N
     return tallies, ccc, checksum
 
 
+def _outs(n_rec, width, out_flags, device, tallies, ccc, checksum, compact):
+    """Dense record buffers, or the compacted ones of `compact` (+ the checksum)."""
+    if compact is None:
+        return (None,) + _outputs(n_rec, width, out_flags, device, tallies, ccc, checksum)
+    _, _, checksum = _outputs(0, width, out_flags & OUT_CHECKSUM, device, None, None, checksum)
+    return ctypes.byref(compact._c), compact.tallies, compact.ccc, checksum
+
+
 def ccc_2way(packed: torch.Tensor, n_f: int, gamma: float = GAMMA,
              out_flags: int = OUT_TALLY | OUT_CCC_F64, tallies=None, ccc=None, checksum=None,
-             ws=None, stream=None):
-    """Tallies (uint32 bit patterns in an int32 tensor) [C(n_v,2)][4], CCC, checksum[2]."""
+             ws=None, stream=None, compact: Compact | None = None):
+    """Tallies (uint32 bit patterns in an int32 tensor) [C(n_v,2)][4], CCC, checksum[2]
+    (with `compact`: the compacted buffers of that object instead)."""
     _dev(packed, torch.uint8, "packed")
     n_v = packed.shape[0]
-    tallies, ccc, checksum = _outputs(ccc_num_unique(2, n_v), 4, out_flags, packed.device,
-                                      tallies, ccc, checksum)
+    cp, tallies, ccc, checksum = _outs(ccc_num_unique(2, n_v), 4, out_flags, packed.device,
+                                       tallies, ccc, checksum, compact)
     if ws is None:
         ws = workspace(2, n_v, n_f, packed.device)
     _check(lib().ccc_2way(_p(packed), n_v, n_f, gamma, out_flags, _p(tallies), _p(ccc),
-                          _p(checksum), _p(ws), ws.numel(), _stream(stream)))
+                          _p(checksum), _p(ws), ws.numel(), cp, _stream(stream)))
     return tallies, ccc, checksum
 
 
 def ccc_2way_block(N_a, s_a, w_a, a_row0, a_lo, a_hi, N_b, s_b, w_b, b_row0, diag: bool, n_f,
                    out_flags, tallies=None, ccc=None, checksum=None, g=None, ldg=0,
-                   stream=None, gamma=GAMMA):
-    """gamma: the value the w arrays were expanded with (selects the kernel's arithmetic)."""
+                   stream=None, gamma=GAMMA, compact: Compact | None = None):
+    """gamma: the value the w arrays were expanded with (selects the kernel's arithmetic).
+    Output buffers are the caller's (dense layout) or those of `compact`."""
+    cp = None
+    if compact is not None:
+        cp, tallies, ccc = ctypes.byref(compact._c), compact.tallies, compact.ccc
     n_a, n_b = N_a.shape[0], N_b.shape[0]
     for t, n in ((N_a, "N_a"), (N_b, "N_b")):
         _dev(t, torch.int8, n)
     _check(lib().ccc_2way_block(_p(N_a), _p(s_a), _p(w_a), n_a, a_row0, a_lo, a_hi, _p(N_b),
                                 _p(s_b), _p(w_b), n_b, b_row0, int(bool(diag)), n_f, gamma, out_flags,
-                                _p(tallies), _p(ccc), _p(checksum), _p(g), ldg, _stream(stream)))
+                                _p(tallies), _p(ccc), _p(checksum), _p(g), ldg, cp,
+                                _stream(stream)))
     return tallies, ccc, checksum
 
 
@@ -254,26 +321,29 @@ def ccc_3way_prepare(packed, n_f, gamma=GAMMA, ws=None, stream=None):
 
 
 def ccc_3way_stage(n_v, n_f, n_stages, stage, ws, out_flags=OUT_TALLY | OUT_CCC_F64,
-                   tallies=None, ccc=None, checksum=None, stream=None, gamma=GAMMA):
+                   tallies=None, ccc=None, checksum=None, stream=None, gamma=GAMMA,
+                   compact: Compact | None = None):
     """gamma: the value given to ccc_3way_prepare for this workspace."""
     _, _, _, rec_count = ccc_stage_range(n_v, n_stages, stage)
-    tallies, ccc, checksum = _outputs(rec_count, 8, out_flags, ws.device, tallies, ccc, checksum)
+    cp, tallies, ccc, checksum = _outs(rec_count, 8, out_flags, ws.device, tallies, ccc,
+                                       checksum, compact)
     _check(lib().ccc_3way_stage(n_v, n_f, gamma, n_stages, stage, out_flags, _p(tallies), _p(ccc),
-                                _p(checksum), _p(ws), ws.numel(), _stream(stream)))
+                                _p(checksum), _p(ws), ws.numel(), cp, _stream(stream)))
     return tallies, ccc, checksum
 
 
 def ccc_3way(packed, n_f, gamma=GAMMA, out_flags=OUT_TALLY | OUT_CCC_F64, n_stages=1, stage=0,
-             tallies=None, ccc=None, checksum=None, ws=None, stream=None):
+             tallies=None, ccc=None, checksum=None, ws=None, stream=None,
+             compact: Compact | None = None):
     _dev(packed, torch.uint8, "packed")
     n_v = packed.shape[0]
     _, _, _, rec_count = ccc_stage_range(n_v, n_stages, stage)
-    tallies, ccc, checksum = _outputs(rec_count, 8, out_flags, packed.device, tallies, ccc,
-                                      checksum)
+    cp, tallies, ccc, checksum = _outs(rec_count, 8, out_flags, packed.device, tallies, ccc,
+                                       checksum, compact)
     if ws is None:
         ws = workspace(3, n_v, n_f, packed.device)
     _check(lib().ccc_3way(_p(packed), n_v, n_f, gamma, out_flags, n_stages, stage, _p(tallies),
-                          _p(ccc), _p(checksum), _p(ws), ws.numel(), _stream(stream)))
+                          _p(ccc), _p(checksum), _p(ws), ws.numel(), cp, _stream(stream)))
     return tallies, ccc, checksum
 
 
@@ -294,7 +364,7 @@ def ccc_3way_unit_records(bp, p_lo, p_hi, bm, m_lo, m_hi, bn, n_lo, n_hi) -> int
 
 def ccc_3way_unit(bp, p_lo, p_hi, bm, m_lo, m_hi, bn, n_lo, n_hi, order, G, n_f,
                   out_flags=OUT_TALLY | OUT_CCC_F64, tallies=None, ccc=None, checksum=None,
-                  stream=None, gamma=GAMMA):
+                  stream=None, gamma=GAMMA, compact: Compact | None = None):
     """One tetrahedral 3-way unit; `order` is a role tuple like ("m", "p", "n") or 0..5;
     gamma: the value the blocks' w were expanded with."""
     if not isinstance(order, int):
@@ -302,10 +372,12 @@ def ccc_3way_unit(bp, p_lo, p_hi, bm, m_lo, m_hi, bn, n_lo, n_hi, order, G, n_f,
     n_rec = ccc_3way_unit_records(bp, p_lo, p_hi, bm, m_lo, m_hi, bn, n_lo, n_hi)
     if n_rec < 0:
         raise ValueError("invalid unit ranges")
-    tallies, ccc, checksum = _outputs(n_rec, 8, out_flags, G.device, tallies, ccc, checksum)
+    cp, tallies, ccc, checksum = _outs(n_rec, 8, out_flags, G.device, tallies, ccc, checksum,
+                                       compact)
     _check(lib().ccc_3way_unit(ctypes.byref(bp), p_lo, p_hi, ctypes.byref(bm), m_lo, m_hi,
                                ctypes.byref(bn), n_lo, n_hi, order, _p(G), G.shape[-1], n_f,
-                               gamma, out_flags, _p(tallies), _p(ccc), _p(checksum), _stream(stream)))
+                               gamma, out_flags, _p(tallies), _p(ccc), _p(checksum), cp,
+                               _stream(stream)))
     return tallies, ccc, checksum
 
 

@@ -129,6 +129,28 @@ ccc_status check_sizes(int64_t n_v, int64_t n_f) {
     return CCC_OK;
 }
 
+ccc_status check_compact(const ccc_compact* c) {
+    if (!c) return CCC_OK;
+    if (c->capacity < 0) return fail(CCC_ERR_INVALID_ARGUMENT, "compact capacity must be >= 0");
+    if (!c->count_d || !aligned(c->count_d, 8))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "compact count_d must be a non-NULL 8-B aligned pointer");
+    if (c->capacity > 0 && (!c->keys_d || !aligned(c->keys_d, 8)))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "compact keys_d must be a non-NULL 8-B aligned pointer");
+    if (c->threshold != c->threshold) return fail(CCC_ERR_INVALID_ARGUMENT, "compact threshold is NaN");
+    return CCC_OK;
+}
+
+ccc::Compact to_compact(const ccc_compact* c) {
+    ccc::Compact k{};
+    if (c) {
+        k.thr = c->threshold;
+        k.cap = c->capacity;
+        k.keys = reinterpret_cast<unsigned long long*>(c->keys_d);
+        k.count = reinterpret_cast<unsigned long long*>(c->count_d);
+    }
+    return k;
+}
+
 ccc_status check_outputs(uint32_t flags, const uint32_t* tallies, const void* ccc,
                          const uint64_t* ck) {
     if (flags & ~15u) return fail(CCC_ERR_INVALID_ARGUMENT, "unknown out_flags bits");
@@ -181,8 +203,8 @@ ccc_status block_impl(const int8_t* N_a, const int32_t* s_a, const double* w_a, 
                       int64_t a_row0, int64_t a_lo, int64_t a_hi, const int8_t* N_b,
                       const int32_t* s_b, const double* w_b, int64_t n_b, int64_t b_row0,
                       int diag, int64_t n_f, double gamma, uint32_t flags, uint32_t* tallies,
-                      void* ccc, uint64_t* ck, int32_t* g, int64_t ldg, cudaStream_t stream,
-                      int num_sms) {
+                      void* ccc, uint64_t* ck, int32_t* g, int64_t ldg,
+                      const ccc_compact* cmp, cudaStream_t stream, int num_sms) {
     const int64_t k_pad = kpad_of(n_f);
     CUtensorMap tmA, tmB;
     CCC_CHECK(make_tmap(&tmA, N_a, n_a, k_pad, ccc::kBM));
@@ -200,6 +222,8 @@ ccc_status block_impl(const int8_t* N_a, const int32_t* s_a, const double* w_a, 
     // gamma = 2/3: CCC = (T U_i(a)) U_j(b) / (36 n_f^3) from integers (K-2)
     a.exact23 = is_gamma23(gamma) ? 1 : 0;
     a.inv_d = 1.0 / (36.0 * (double)n_f * (double)n_f * (double)n_f);
+    a.compact = cmp ? 1 : 0;
+    a.cmp = to_compact(cmp);
     a.s_a = s_a;
     a.s_b = s_b;
     a.w_a = w_a;
@@ -329,7 +353,8 @@ ccc_status ccc_2way_block(const int8_t* N_a, const int32_t* s_a, const double* w
                           const int32_t* s_b, const double* w_b, int64_t n_b, int64_t b_row0,
                           int diag, int64_t n_f, double gamma, uint32_t out_flags, uint32_t* tallies_d,
                           void* ccc_d, uint64_t* checksum_d, int32_t* g_d, int64_t ldg,
-                          void* stream) {
+                          const ccc_compact* compact, void* stream) {
+    CCC_CHECK(check_compact(compact));
     g_launches = 0;
     CCC_CHECK(check_sizes(n_a, n_f));
     CCC_CHECK(check_sizes(n_b, n_f));
@@ -348,13 +373,14 @@ ccc_status ccc_2way_block(const int8_t* N_a, const int32_t* s_a, const double* w
     int sms;
     CCC_CHECK(check_device(&sms));
     return block_impl(N_a, s_a, w_a, n_a, a_row0, a_lo, a_hi, N_b, s_b, w_b, n_b, b_row0, diag,
-                      n_f, gamma, out_flags, tallies_d, ccc_d, checksum_d, g_d, ldg,
+                      n_f, gamma, out_flags, tallies_d, ccc_d, checksum_d, g_d, ldg, compact,
                       (cudaStream_t)stream, sms);
 }
 
 ccc_status ccc_2way(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
                     uint32_t out_flags, uint32_t* tallies_d, void* ccc_d, uint64_t* checksum_d,
-                    void* ws_d, size_t ws_bytes, void* stream) {
+                    void* ws_d, size_t ws_bytes, const ccc_compact* compact, void* stream) {
+    CCC_CHECK(check_compact(compact));
     g_launches = 0;
     CCC_CHECK(check_sizes(n_v, n_f));
     if (out_flags & ~15u) return fail(CCC_ERR_INVALID_ARGUMENT, "unknown out_flags bits");
@@ -374,7 +400,7 @@ ccc_status ccc_2way(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double ga
     cudaStream_t st = (cudaStream_t)stream;
     CCC_CUDA(ccc::launch_expand(packed_d, n_v, n_f, gamma, N, s, w, sms, st), "expand launch");
     CCC_CHECK(block_impl(N, s, w, n_v, 0, 0, n_v, N, s, w, n_v, 0, 1, n_f, gamma, out_flags, tallies_d,
-                         ccc_d, checksum_d, nullptr, 0, st, sms));
+                         ccc_d, checksum_d, nullptr, 0, compact, st, sms));
     g_launches += 1;
     return CCC_OK;
 }
@@ -399,14 +425,15 @@ ccc_status ccc_3way_prepare(const uint8_t* packed_d, int64_t n_v, int64_t n_f, d
     cudaStream_t st = (cudaStream_t)stream;
     CCC_CUDA(ccc::launch_expand(packed_d, n_v, n_f, gamma, N, s, w, sms, st), "expand launch");
     CCC_CHECK(block_impl(N, s, w, n_v, 0, 0, n_v, N, s, w, n_v, 0, 1, n_f, gamma, 0, nullptr, nullptr,
-                         nullptr, G, n_v, st, sms));
+                         nullptr, G, n_v, nullptr, st, sms));
     g_launches += 1;
     return CCC_OK;
 }
 
 ccc_status ccc_3way_stage(int64_t n_v, int64_t n_f, double gamma, int64_t n_stages, int64_t stage,
                           uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
-                          uint64_t* checksum_d, void* ws_d, size_t ws_bytes, void* stream) {
+                          uint64_t* checksum_d, void* ws_d, size_t ws_bytes, const ccc_compact* compact, void* stream) {
+    CCC_CHECK(check_compact(compact));
     g_launches = 0;
     CCC_CHECK(check_sizes(n_v, n_f));
     if (out_flags & ~15u) return fail(CCC_ERR_INVALID_ARGUMENT, "unknown out_flags bits");
@@ -442,6 +469,8 @@ ccc_status ccc_3way_stage(int64_t n_v, int64_t n_f, double gamma, int64_t n_stag
     a.k_blocks = (int32_t)(k_pad / ccc::kBK);
     a.out_flags = (int32_t)out_flags;
     set_exact3(a, n_f, gamma);
+    a.compact = compact ? 1 : 0;
+    a.cmp = to_compact(compact);
     a.tallies = tallies_d;
     a.ccc = ccc_d;
     a.checksum = reinterpret_cast<unsigned long long*>(checksum_d);
@@ -477,7 +506,8 @@ ccc_status ccc_3way_unit(const ccc_block* bp, int64_t p_lo, int64_t p_hi, const 
                          int64_t m_lo, int64_t m_hi, const ccc_block* bn, int64_t n_lo,
                          int64_t n_hi, int order, const int32_t* G_d, int64_t ldG, int64_t n_f,
                          double gamma, uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
-                         uint64_t* checksum_d, void* stream) {
+                         uint64_t* checksum_d, const ccc_compact* compact, void* stream) {
+    CCC_CHECK(check_compact(compact));
     g_launches = 0;
     if (!bp || !bm || !bn) return fail(CCC_ERR_INVALID_ARGUMENT, "block descriptors must not be NULL");
     CCC_CHECK(check_sizes(bp->rows, n_f));
@@ -532,6 +562,8 @@ ccc_status ccc_3way_unit(const ccc_block* bp, int64_t p_lo, int64_t p_hi, const 
     a.k_blocks = (int32_t)(k_pad / ccc::kBK);
     a.out_flags = (int32_t)out_flags;
     set_exact3(a, n_f, gamma);
+    a.compact = compact ? 1 : 0;
+    a.cmp = to_compact(compact);
     a.tallies = tallies_d;
     a.ccc = ccc_d;
     a.checksum = reinterpret_cast<unsigned long long*>(checksum_d);
@@ -547,12 +579,13 @@ ccc_status ccc_3way_unit(const ccc_block* bp, int64_t p_lo, int64_t p_hi, const 
 ccc_status ccc_3way(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
                     uint32_t out_flags, int64_t n_stages, int64_t stage, uint32_t* tallies_d,
                     void* ccc_d, uint64_t* checksum_d, void* ws_d, size_t ws_bytes,
-                    void* stream) {
+                    const ccc_compact* compact, void* stream) {
+    CCC_CHECK(check_compact(compact));
     if (n_v >= 3) CCC_CHECK(check_outputs(out_flags, tallies_d, ccc_d, checksum_d));
     CCC_CHECK(ccc_3way_prepare(packed_d, n_v, n_f, gamma, ws_d, ws_bytes, stream));
     const int64_t n1 = g_launches;
     CCC_CHECK(ccc_3way_stage(n_v, n_f, gamma, n_stages, stage, out_flags, tallies_d, ccc_d, checksum_d,
-                             ws_d, ws_bytes, stream));
+                             ws_d, ws_bytes, compact, stream));
     g_launches += n1;
     return CCC_OK;
 }
@@ -666,7 +699,7 @@ ccc_status ccc_2way_host(const uint8_t* codes_h, int64_t n_v, int64_t n_f, doubl
         uint32_t* bt = reinterpret_cast<uint32_t*>(base + L.band_t[b]);
         void* bc = base + L.band_c[b];
         rc = block_impl(N, s, w, n_v, 0, r0, r1, N, s, w, n_v, 0, 1, n_f, gamma, out_flags, bt, bc, ck,
-                        nullptr, 0, st, sms);
+                        nullptr, 0, nullptr, st, sms);
         if (rc != CCC_OK) break;
         ++launches;
         if ((e = cudaEventRecord(done[b], st)) != cudaSuccess ||

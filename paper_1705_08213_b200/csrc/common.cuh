@@ -3,6 +3,7 @@
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
 
 namespace ccc {
 
@@ -103,6 +104,26 @@ struct TriSched {
 };
 
 // Kernel arguments of the fused 2-way tally GEMM (KB-2W).
+// Threshold-compacted output: instead of the dense record
+// arrays, every record whose largest CCC cell exceeds `thr` is appended at
+// slot = atomicAdd(count, 1) (warp-aggregated): keys[slot] = global index key,
+// tallies[slot][cells], ccc[slot][cells].  Slots >= cap are counted but not stored.
+struct Compact {
+    double thr;
+    int64_t cap;
+    unsigned long long* keys;
+    unsigned long long* count;
+};
+
+// Next free slot of a compacted output: one atomic per group of converged threads.
+__device__ __forceinline__ unsigned long long compact_slot(unsigned long long* count) {
+    namespace cg = cooperative_groups;
+    cg::coalesced_group g = cg::coalesced_threads();
+    unsigned long long base = 0;
+    if (g.thread_rank() == 0) base = atomicAdd(count, (unsigned long long)g.size());
+    return g.shfl(base, 0) + g.thread_rank();
+}
+
 struct Tally2Args {
     int64_t a_lo, nA, nB;      // A rows [a_lo, a_lo+nA) (local), B rows [0, nB)
     int64_t a_row0, b_row0;    // global index of local row 0 of A / B (checksum)
@@ -124,6 +145,8 @@ struct Tally2Args {
     int32_t k_alternate;         // odd waves of tiles walk K backwards (L2 reuse across waves)
     int32_t exact23;             // gamma == 2/3: CCC = double(T*U_i(a)) * (U_j(b)/D), D = 36 n_f^3
     double inv_d;                // 1 / (36 n_f^3)
+    Compact cmp;                 // used when compact != 0
+    int32_t compact;
     unsigned long long* trace; // optional per-tile %globaltimer trace (diagnostics)
 };
 
@@ -156,6 +179,8 @@ struct Tally3Args {
     uint32_t* tallies;         // [records][8]
     void* ccc;                 // [records][8] double or float
     unsigned long long* checksum;
+    Compact cmp;               // used when compact != 0
+    int32_t compact, pad4_;
     unsigned long long* trace; // optional per-unit %globaltimer trace (diagnostics)
 };
 

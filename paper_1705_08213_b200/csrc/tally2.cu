@@ -74,7 +74,22 @@ struct Cfg2 {
     static constexpr int kSmem = kBarOff + 256 + 1024;
 };
 
-template <int kPair>
+// f2 compaction: append one kept record (2-way key = i * 2^20 + j, global indices).
+__device__ __forceinline__ void emit2(const Tally2Args& a, uint64_t key, uint32_t t00, uint32_t t01,
+                                      uint32_t t10, uint32_t t11, double c00, double c01,
+                                      double c10, double c11) {
+    const unsigned long long slot = compact_slot(a.cmp.count);
+    if (slot >= (unsigned long long)a.cmp.cap) return;
+    a.cmp.keys[slot] = key;
+    const uint32_t fl = (uint32_t)a.out_flags;
+    if (fl & 1u) stg_128_u32(a.tallies + 4 * slot, t00, t01, t10, t11);
+    if (fl & 2u) stg_256_f64(reinterpret_cast<double*>(a.ccc) + 4 * slot, c00, c01, c10, c11);
+    else if (fl & 4u)
+        stg_128_u32(reinterpret_cast<float*>(a.ccc) + 4 * slot, __float_as_uint((float)c00),
+                    __float_as_uint((float)c01), __float_as_uint((float)c10), __float_as_uint((float)c11));
+}
+
+template <int kPair, bool kCompact>
 __global__ void __launch_bounds__(kThreads2, 1)
 tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const Tally2Args args) {
@@ -265,7 +280,7 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 // column factors: general gamma -> w_j(b); gamma = 2/3 -> U_j(b) / (36 n_f^3)
                 // with the integer U_j(0) = n_f + s_j, U_j(1) = 3 n_f - s_j
                 double wA0 = 0.0, wA1 = 0.0, wB0 = 0.0, wB1 = 0.0;
-                if (want_c) {
+                if (want_c || kCompact) {
                     if (exact23) {
                         const uint32_t sAj = two_sA >> 1, sBj = two_sB >> 1;
                         wA0 = (double)(nf + sAj) * args.inv_d;
@@ -293,21 +308,12 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     const uint32_t b11 = gB, b10 = two_si[r] - gB, b01 = two_sB - gB;
                     const uint32_t b00 = four_nf - two_si[r] - two_sB + gB;
                     const int64_t recA = rec_r[r] + jA;
-                    if (want_t) {
-                        uint32_t* p = args.tallies + 4 * recA;
-                        if (okA && okB && !(recA & 1)) {
-                            stg_256_u32(p, a00, a01, a10, a11, b00, b01, b10, b11);
-                        } else {
-                            if (okA) stg_128_u32(p, a00, a01, a10, a11);
-                            if (okB) stg_128_u32(p + 4, b00, b01, b10, b11);
-                        }
-                    }
-                    if (want_c) {
-                        // Eq.3: CCC(a,b) = T(a,b) / (4 n_f) * w_i(a) * w_j(b).  For gamma = 2/3,
-                        // w(a) = U(a) / (3 n_f) with integer U, so CCC = T U_i(a) U_j(b) / (36 n_f^3):
-                        // T * U_i(a) < 2^53 is exact in a double and one DMUL per cell remains
-                        // (FP64 issue rate is the scarce resource of this epilogue on B200).
-                        double ca00, ca01, ca10, ca11, cb00, cb01, cb10, cb11;
+                    // Eq.3: CCC(a,b) = T(a,b) / (4 n_f) * w_i(a) * w_j(b).  For gamma = 2/3,
+                    // w(a) = U(a) / (3 n_f) with integer U, so CCC = T U_i(a) U_j(b) / (36 n_f^3):
+                    // T * U_i(a) < 2^53 is exact in a double and one DMUL per cell remains
+                    // (FP64 issue rate is the scarce resource of this epilogue on B200).
+                    double ca00 = 0, ca01 = 0, ca10 = 0, ca11 = 0, cb00 = 0, cb01 = 0, cb10 = 0, cb11 = 0;
+                    if (want_c || kCompact) {
                         if (exact23) {
                             const uint64_t u0 = ui0[r], u1 = ui1[r];
                             ca00 = (double)(a00 * u0) * wA0;
@@ -328,6 +334,29 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                             cb10 = (double)b10 * wi1[r] * wB0;
                             cb11 = (double)b11 * wi1[r] * wB1;
                         }
+                    }
+                    if constexpr (kCompact) {
+                        // f2: keep a record iff its largest CCC cell exceeds the threshold
+                        const Compact& cm = args.cmp;
+                        const double mA = fmax(fmax(ca00, ca01), fmax(ca10, ca11));
+                        const double mB = fmax(fmax(cb00, cb01), fmax(cb10, cb11));
+                        if (okA && mA > cm.thr)
+                            emit2(args, (gi[r] << 20) | (uint64_t)(args.b_row0 + jA), a00, a01, a10, a11,
+                                  ca00, ca01, ca10, ca11);
+                        if (okB && mB > cm.thr)
+                            emit2(args, (gi[r] << 20) | (uint64_t)(args.b_row0 + jB), b00, b01, b10, b11,
+                                  cb00, cb01, cb10, cb11);
+                    } else {
+                    if (want_t) {
+                        uint32_t* p = args.tallies + 4 * recA;
+                        if (okA && okB && !(recA & 1)) {
+                            stg_256_u32(p, a00, a01, a10, a11, b00, b01, b10, b11);
+                        } else {
+                            if (okA) stg_128_u32(p, a00, a01, a10, a11);
+                            if (okB) stg_128_u32(p + 4, b00, b01, b10, b11);
+                        }
+                    }
+                    if (want_c) {
                         if (want_c64) {
                             double* p = reinterpret_cast<double*>(args.ccc) + 4 * recA;
                             if (okA) stg_256_f64(p, ca00, ca01, ca10, ca11);
@@ -348,6 +377,7 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                                                 __float_as_uint((float)cb10), __float_as_uint((float)cb11));
                             }
                         }
+                    }
                     }
                     if (args.g_out) {
                         const int64_t row = (int64_t)(gi[r] - (uint64_t)args.a_row0);
@@ -419,16 +449,16 @@ cudaError_t launch_tally2(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
     if (n_tiles_out) *n_tiles_out = tiles;
     if (tiles == 0) return cudaSuccess;
     if (pm == 1) {
-        cudaError_t e = cudaFuncSetAttribute(tally2_kernel<1>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+        auto kern = a.compact ? tally2_kernel<1, true> : tally2_kernel<1, false>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              Cfg2<1>::kSmem);
         if (e != cudaSuccess) return e;
         const int grid = (int)(tiles < num_sms ? tiles : num_sms);
-        tally2_kernel<1><<<grid, kThreads2, Cfg2<1>::kSmem, stream>>>(tmA, tmB, a2);
+        kern<<<grid, kThreads2, Cfg2<1>::kSmem, stream>>>(tmA, tmB, a2);
         return cudaGetLastError();
     }
-    cudaError_t e = cudaFuncSetAttribute(tally2_kernel<2>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+    auto kern = a.compact ? tally2_kernel<2, true> : tally2_kernel<2, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg2<2>::kSmem);
     if (e != cudaSuccess) return e;
     const int64_t pairs = num_sms / 2;
@@ -444,7 +474,7 @@ cudaError_t launch_tally2(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, tally2_kernel<2>, tmA, tmB, a2);
+    return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, a2);
 }
 
 }  // namespace ccc

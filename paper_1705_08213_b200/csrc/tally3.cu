@@ -25,6 +25,7 @@
 #include "internal.h"
 
 #include <cstdlib>
+#include <type_traits>
 
 namespace ccc {
 
@@ -161,7 +162,27 @@ __device__ __forceinline__ uint32_t gord(const int32_t* G, int64_t ld, int64_t g
     else return (uint32_t)__ldg(G + gy * ld + gx);
 }
 
-template <int kOrder, bool kExact>
+// f2 compaction: append one kept record (3-way key = i * 2^40 + j * 2^20 + k, canonical).
+__device__ __forceinline__ void emit3(const Tally3Args& a, uint64_t key, const uint32_t (&t)[8],
+                                      const double (&c)[8]) {
+    const unsigned long long slot = compact_slot(a.cmp.count);
+    if (slot >= (unsigned long long)a.cmp.cap) return;
+    a.cmp.keys[slot] = key;
+    const uint32_t fl = (uint32_t)a.out_flags;
+    if (fl & 1u) stg_256_u32(a.tallies + 8 * slot, t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]);
+    if (fl & 2u) {
+        double* q = reinterpret_cast<double*>(a.ccc) + 8 * slot;
+        stg_256_f64(q, c[0], c[1], c[2], c[3]);
+        stg_256_f64(q + 4, c[4], c[5], c[6], c[7]);
+    } else if (fl & 4u) {
+        stg_256_u32(reinterpret_cast<float*>(a.ccc) + 8 * slot, __float_as_uint((float)c[0]),
+                    __float_as_uint((float)c[1]), __float_as_uint((float)c[2]), __float_as_uint((float)c[3]),
+                    __float_as_uint((float)c[4]), __float_as_uint((float)c[5]), __float_as_uint((float)c[6]),
+                    __float_as_uint((float)c[7]));
+    }
+}
+
+template <int kOrder, bool kExact, bool kCompact>
 __global__ void __launch_bounds__(kThreads3, 1)
 tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const Tally3Args args) {
@@ -402,7 +423,7 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 const uint32_t gpnA = gord<kOrder, 0, 2>(args.G, args.ldG, gp, gnA);
                 const uint32_t gpnB = gord<kOrder, 0, 2>(args.G, args.ldG, gp, gnB);
                 double wA0 = 0.0, wA1 = 0.0, wB0 = 0.0, wB1 = 0.0;
-                if (want_c) {
+                if (want_c || kCompact) {
                     if constexpr (kExact) {   // U_n(c) / (216 n_f^4)
                         wA0 = (double)(nf + sA) * args.inv_d;
                         wA1 = (double)(3u * nf - sA) * args.inv_d;
@@ -441,10 +462,10 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         uint32_t tc[8];
                         perm_cells<O::R0, O::R1, O::R2>(t, tc);
                         const int64_t rec = rec_r[r] + n;
-                        if (want_t)
+                        if (!kCompact && want_t)
                             stg_256_u32(args.tallies + 8 * rec, tc[0], tc[1], tc[2], tc[3], tc[4],
                                         tc[5], tc[6], tc[7]);
-                        if (want_c) {
+                        if (want_c || kCompact) {
                             // Eq.4: CCC = T / (8 n_f) * w_p(a_p) w_m(a_m) w_n(a_n)
                             const double wn0 = h ? wB0 : wA0, wn1 = h ? wB1 : wA1;
                             double cr[8], cc[8];
@@ -461,7 +482,17 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                                 }
                             }
                             perm_cells<O::R0, O::R1, O::R2>(cr, cc);
-                            if (want_c64) {
+                            if constexpr (kCompact) {
+                                // f2: keep a record iff its largest CCC cell exceeds the threshold
+                                double mx = cc[0];
+#pragma unroll
+                                for (int q = 1; q < 8; ++q) mx = fmax(mx, cc[q]);
+                                if (mx > args.cmp.thr) {
+                                    const int64_t g[3] = {gp, gm, gn};
+                                    emit3(args, ((uint64_t)g[O::R0] << 40) | ((uint64_t)g[O::R1] << 20) |
+                                                    (uint64_t)g[O::R2], tc, cc);
+                                }
+                            } else if (want_c64) {
                                 double* q = reinterpret_cast<double*>(args.ccc) + 8 * rec;
                                 stg_256_f64(q, cc[0], cc[1], cc[2], cc[3]);
                                 stg_256_f64(q + 4, cc[4], cc[5], cc[6], cc[7]);
@@ -544,24 +575,22 @@ cudaError_t launch_tally3(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
         cfg.numAttrs = 1;
         return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, a);
     };
-    if (a.exact23) {
+    // 6 canonical orders x {general gamma, gamma = 2/3} x {dense, compacted} instantiations
+    auto pick = [&](auto ex, auto cp) {
+        constexpr bool E = decltype(ex)::value, Cp = decltype(cp)::value;
         switch (a.order) {
-            case 0: return go(tally3_kernel<0, true>);
-            case 1: return go(tally3_kernel<1, true>);
-            case 2: return go(tally3_kernel<2, true>);
-            case 3: return go(tally3_kernel<3, true>);
-            case 4: return go(tally3_kernel<4, true>);
-            default: return go(tally3_kernel<5, true>);
+            case 0: return go(tally3_kernel<0, E, Cp>);
+            case 1: return go(tally3_kernel<1, E, Cp>);
+            case 2: return go(tally3_kernel<2, E, Cp>);
+            case 3: return go(tally3_kernel<3, E, Cp>);
+            case 4: return go(tally3_kernel<4, E, Cp>);
+            default: return go(tally3_kernel<5, E, Cp>);
         }
-    }
-    switch (a.order) {
-        case 0: return go(tally3_kernel<0, false>);
-        case 1: return go(tally3_kernel<1, false>);
-        case 2: return go(tally3_kernel<2, false>);
-        case 3: return go(tally3_kernel<3, false>);
-        case 4: return go(tally3_kernel<4, false>);
-        default: return go(tally3_kernel<5, false>);
-    }
+    };
+    using T = std::true_type;
+    using F = std::false_type;
+    if (a.exact23) return a.compact ? pick(T{}, T{}) : pick(T{}, F{});
+    return a.compact ? pick(F{}, T{}) : pick(F{}, F{});
 }
 
 }  // namespace ccc

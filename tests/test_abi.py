@@ -88,15 +88,15 @@ def test_validation_before_launch():
     assert "non-NULL" in lib.ccc_last_error().decode()
     # exclusive CCC flags
     st = lib.ccc_2way(ctypes.c_void_p(256), 4, 10, 2 / 3, ccc.OUT_CCC_F64 | ccc.OUT_CCC_F32,
-                      null, ctypes.c_void_p(256), null, ctypes.c_void_p(256), 1 << 20, null)
+                      null, ctypes.c_void_p(256), null, ctypes.c_void_p(256), 1 << 20, null, null)
     assert st == ccc.ERR_INVALID_ARGUMENT
     # missing tally buffer
     st = lib.ccc_2way(ctypes.c_void_p(256), 4, 10, 2 / 3, ccc.OUT_TALLY, null, null, null,
-                      ctypes.c_void_p(256), 1 << 20, null)
+                      ctypes.c_void_p(256), 1 << 20, null, null)
     assert st == ccc.ERR_INVALID_ARGUMENT
     # workspace too small
     st = lib.ccc_2way(ctypes.c_void_p(256), 40, 10, 2 / 3, 0, null, null, null,
-                      ctypes.c_void_p(256), 16, null)
+                      ctypes.c_void_p(256), 16, null, null)
     assert st == ccc.ERR_WORKSPACE
     # bad stage
     out = (ctypes.c_int64 * 4)()
@@ -104,13 +104,22 @@ def test_validation_before_launch():
     with pytest.raises(ValueError):
         ccc.ccc_stage_range(10, 0, 0)
     # empty problems are valid and launch nothing
-    assert lib.ccc_2way(null, 1, 10, 2 / 3, 0, null, null, null, null, 0, null) == ccc.OK
-    assert lib.ccc_3way(null, 2, 10, 2 / 3, 0, 1, 0, null, null, null, null, 0, null) == ccc.OK
+    assert lib.ccc_2way(null, 1, 10, 2 / 3, 0, null, null, null, null, 0, null, null) == ccc.OK
+    assert lib.ccc_3way(null, 2, 10, 2 / 3, 0, 1, 0, null, null, null, null, 0, null, null) == ccc.OK
     assert lib.ccc_last_launch_count() == 0
     # diag block requires A == B
     st = lib.ccc_2way_block(ctypes.c_void_p(256), null, null, 8, 0, 0, 8, ctypes.c_void_p(512),
-                            null, null, 8, 0, 1, 10, 2 / 3, 0, null, null, null, null, 0, null)
+                            null, null, 8, 0, 1, 10, 2 / 3, 0, null, null, null, null, 0, null, null)
     assert st == ccc.ERR_INVALID_ARGUMENT
+    # compacted output: counter required, NaN threshold refused
+    cmp = ccc.CccCompact(0.5, 10, 256, None)
+    st = lib.ccc_2way(ctypes.c_void_p(256), 40, 10, 2 / 3, 0, null, null, null,
+                      ctypes.c_void_p(256), 1 << 30, ctypes.byref(cmp), null)
+    assert st == ccc.ERR_INVALID_ARGUMENT and "count_d" in lib.ccc_last_error().decode()
+    cmp = ccc.CccCompact(float("nan"), 10, 256, 512)
+    st = lib.ccc_2way(ctypes.c_void_p(256), 40, 10, 2 / 3, 0, null, null, null,
+                      ctypes.c_void_p(256), 1 << 30, ctypes.byref(cmp), null)
+    assert st == ccc.ERR_INVALID_ARGUMENT and "NaN" in lib.ccc_last_error().decode()
 
 
 def test_workspace_sizes():
