@@ -68,6 +68,8 @@ def lib():
             getattr(L, name).argtypes = [p, i64, i64, p, ctypes.c_double, p, i64, p, p]
         for name in ("oracle_all_pairs", "oracle_all_triples"):
             getattr(L, name).argtypes = [p, i64, i64, p, ctypes.c_double, p, p]
+        L.oracle_sparse_sums.argtypes = [p, i64, i64, p, p]
+        L.oracle_sparse_pairs.argtypes = [p, i64, i64, p, p, ctypes.c_double, p, i64, p, p, p]
         _lib = L
     return _lib
 
@@ -152,6 +154,40 @@ def all_triples(codes, gamma: float = GAMMA):
     if m:
         lib().oracle_all_triples(_ptr(c), n, c.shape[1], _ptr(S), gamma, _ptr(T), _ptr(C))
     return T, C
+
+
+# ----------------------------------------------------------------------------------
+# Sparse (missing-data) mode, P:1028-1043 under reading A-17 (see ccc_oracle.c)
+# ----------------------------------------------------------------------------------
+MISSING = 2   # code of the element (1,0), the missing-entry marker
+
+
+def sparse_sums(codes):
+    """(S int64 [n_v][2] over present entries, c int64 [n_v] = #present entries)."""
+    c = _codes_np(codes)
+    S = np.zeros((c.shape[0], 2), dtype=np.int64)
+    cnt = np.zeros(c.shape[0], dtype=np.int64)
+    lib().oracle_sparse_sums(_ptr(c), c.shape[0], c.shape[1], _ptr(S), _ptr(cnt))
+    return S, cnt
+
+
+def sparse_pairs(codes, idx, gamma: float = GAMMA):
+    """Sparse-mode tallies [m][4], CCC [m][4] and c_ij [m] for the pairs idx [m][2]."""
+    c = _codes_np(codes)
+    idx = np.ascontiguousarray(idx, dtype=np.int64).reshape(-1, 2)
+    S, cnt = sparse_sums(c)
+    T = np.zeros((len(idx), 4), dtype=np.int64)
+    C = np.zeros((len(idx), 4), dtype=np.float64)
+    cij = np.zeros(len(idx), dtype=np.int64)
+    if len(idx):
+        lib().oracle_sparse_pairs(_ptr(c), c.shape[0], c.shape[1], _ptr(S), _ptr(cnt), gamma,
+                                  _ptr(idx), len(idx), _ptr(T), _ptr(C), _ptr(cij))
+    return T, C, cij
+
+
+def sparse_all_pairs(codes, gamma: float = GAMMA):
+    """Every unique pair i<j, lexicographic: sparse (T, CCC, c_ij)."""
+    return sparse_pairs(codes, pair_list(_codes_np(codes).shape[0]), gamma)
 
 
 def pair_list(n_v: int) -> np.ndarray:

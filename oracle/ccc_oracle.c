@@ -178,3 +178,88 @@ void oracle_all_triples(const uint8_t* codes, int64_t n_v, int64_t n_f, const in
             }
     }
 }
+
+/*
+ * ---- Sparse (missing-data) mode, §7 item 1 -------------------
+ * "the value (1,0) can be set aside as a marker to denote a missing entry ... skipping
+ * calculations for missing entries".  Reading A-17:
+ *   present_{i,q} = [v_{i,q} != (1,0)],  c_i = sum_q present_{i,q}
+ *   S_i(a)  = sum over present q of rho_{i,q}(a),   f_i(a) = S_i(a) / (2 c_i)
+ *   T_ij(a,b) = the Fig.1 enumeration over the fields where BOTH entries are present,
+ *   c_ij = that number of fields,  f_ij = T_ij / (4 c_ij)
+ *   CCC_ij(a,b) = f_ij(a,b) (1 - g f_i(a)) (1 - g f_j(b))          (Eq.3 with these)
+ * Degenerate cases: c_ij = 0 -> T = 0 and CCC = 0; c_i = 0 -> f_i(a) = 0.
+ */
+static int elem_missing(uint8_t code) { return elem_r1(code) == 1 && elem_r2(code) == 0; }
+
+/* S[i*2 + a] over present entries, cnt[i] = c_i. */
+void oracle_sparse_sums(const uint8_t* codes, int64_t n_v, int64_t n_f, int64_t* S,
+                        int64_t* cnt)
+{
+    for (int64_t i = 0; i < n_v; ++i) {
+        int64_t s0 = 0, s1 = 0, c = 0;
+        for (int64_t q = 0; q < n_f; ++q) {
+            uint8_t e = codes[i * n_f + q];
+            if (elem_missing(e)) continue;
+            c += 1;
+            int r[2] = {elem_r1(e), elem_r2(e)};
+            for (int t = 0; t < 2; ++t) {
+                if (r[t] == 0) s0 += 1;
+                if (r[t] == 1) s1 += 1;
+            }
+        }
+        S[i * 2 + 0] = s0;
+        S[i * 2 + 1] = s1;
+        cnt[i] = c;
+    }
+}
+
+static void tally2_sparse_one(const uint8_t* vi, const uint8_t* vj, int64_t n_f, int64_t T[4],
+                              int64_t* c_ij)
+{
+    T[0] = T[1] = T[2] = T[3] = 0;
+    *c_ij = 0;
+    for (int64_t q = 0; q < n_f; ++q) {
+        if (elem_missing(vi[q]) || elem_missing(vj[q])) continue;   /* skipped field */
+        *c_ij += 1;
+        int ri[2] = {elem_r1(vi[q]), elem_r2(vi[q])};
+        int rj[2] = {elem_r1(vj[q]), elem_r2(vj[q])};
+        for (int s = 0; s < 2; ++s)
+            for (int t = 0; t < 2; ++t)
+                T[2 * ri[s] + rj[t]] += 1;
+    }
+}
+
+static void ccc2_sparse_one(const int64_t T[4], const int64_t* Si, const int64_t* Sj,
+                            int64_t c_i, int64_t c_j, int64_t c_ij, double gamma, double out[4])
+{
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) {
+            if (c_ij == 0) {
+                out[2 * a + b] = 0.0;
+                continue;
+            }
+            double f_ij = (double)T[2 * a + b] / (4.0 * (double)c_ij);
+            double f_ia = c_i ? (double)Si[a] / (2.0 * (double)c_i) : 0.0;
+            double f_jb = c_j ? (double)Sj[b] / (2.0 * (double)c_j) : 0.0;
+            out[2 * a + b] = f_ij * (1.0 - gamma * f_ia) * (1.0 - gamma * f_jb);
+        }
+}
+
+/* Sparse tallies, CCC and c_ij for an explicit pair list idx[m][2]; S, cnt from
+ * oracle_sparse_sums.  ccc / cij may be NULL. */
+void oracle_sparse_pairs(const uint8_t* codes, int64_t n_v, int64_t n_f, const int64_t* S,
+                         const int64_t* cnt, double gamma, const int64_t* idx, int64_t m,
+                         int64_t* T, double* ccc, int64_t* cij)
+{
+    (void)n_v;
+    #pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t r = 0; r < m; ++r) {
+        int64_t i = idx[2 * r], j = idx[2 * r + 1], c;
+        tally2_sparse_one(codes + i * n_f, codes + j * n_f, n_f, T + 4 * r, &c);
+        if (cij) cij[r] = c;
+        if (ccc)
+            ccc2_sparse_one(T + 4 * r, S + 2 * i, S + 2 * j, cnt[i], cnt[j], c, gamma,
+                            ccc + 4 * r);
+    }
+}

@@ -109,6 +109,35 @@ def hwe_codes(n_v: int, n_f: int, seed: int = 2, device="cpu",
     return out
 
 
+def sparse_codes(n_v: int, n_f: int, seed: int = 4, device="cpu", row0: int = 0,
+                 miss_max: float = 0.3, chunk_rows: int = 256) -> torch.Tensor:
+    """Type-3 sparse-mode data (§7 item 1): Hardy-Weinberg
+    genotypes as in hwe_codes with the heterozygote always stored as (0,1) = code 1, and
+    each entry missing -- the marker (1,0) = code 2 -- with a per-vector probability
+    m_i ~ U(0, miss_max)."""
+    out = torch.empty((n_v, n_f), dtype=torch.uint8, device=device)
+    q = torch.arange(n_f, dtype=torch.int64, device=device)
+    two53 = float(1 << 53)
+    for r0 in range(0, n_v, chunk_rows):
+        r1 = min(n_v, r0 + chunk_rows)
+        rows = torch.arange(row0 + r0, row0 + r1, dtype=torch.int64, device=device)
+        h = _row_hash(seed, rows)
+        u_row = _lsr(_splitmix64(h ^ 0x5bd1e995), 11).to(torch.float64) / two53
+        u_mis = _lsr(_splitmix64(h ^ 0x27d4eb2f), 11).to(torch.float64) / two53
+        p = (0.05 + 0.45 * u_row)[:, None]
+        m = (miss_max * u_mis)[:, None]
+        z1 = _splitmix64(h[:, None] + 3 * q[None, :])
+        z2 = _splitmix64(h[:, None] + 3 * q[None, :] + 1)
+        z3 = _splitmix64(h[:, None] + 3 * q[None, :] + 2)
+        u1 = _lsr(z1, 11).to(torch.float64) / two53
+        u2 = _lsr(z2, 11).to(torch.float64) / two53
+        u3 = _lsr(z3, 11).to(torch.float64) / two53
+        a1, a2 = (u1 < p), (u2 < p)
+        code = torch.where(a1 & a2, 3, torch.where(a1 ^ a2, 1, 0))
+        out[r0:r1] = torch.where(u3 < m, 2, code).to(torch.uint8)
+    return out
+
+
 def planted_lengths(n_v: int, n_f: int, seed: int = 3):
     """Interval lengths (L_i, H_i) of the planted type-2 design (L_i + H_i <= n_f)."""
     L, H = [], []
@@ -155,6 +184,8 @@ def make_codes(kind: str, n_v: int, n_f: int, seed: int | None = None, device="c
         return random_codes(n_v, n_f, 1 if seed is None else seed, device, row0)
     if kind == "hwe":
         return hwe_codes(n_v, n_f, 2 if seed is None else seed, device, row0)
+    if kind == "sparse":
+        return sparse_codes(n_v, n_f, 4 if seed is None else seed, device, row0)
     if kind == "planted":
         if row0:
             raise ValueError("planted data is generated whole")

@@ -291,3 +291,70 @@ def test_synthgen_scalar_vs_tensor_and_tiling():
     big = synthgen.random_codes(64, 4096, seed=1).numpy()
     freq = np.bincount(big.ravel(), minlength=4) / big.size
     assert np.all(np.abs(freq - 0.25) < 0.01)
+
+
+# ------------------------------------------------------------ sparse mode (f1, A-17)
+def test_sparse_no_missing_equals_dense():
+    """with no missing entry the sparse tally equals the dense one, c_ij = n_f
+    (and so does CCC: every divisor reduces to n_f)."""
+    c = synthgen.random_codes(12, 77, seed=9).numpy()
+    c[c == oracle.MISSING] = 1                      # (1,0) -> (0,1): same heterozygote
+    Ts, Cs, cij = oracle.sparse_all_pairs(c)
+    Td, Cd = oracle.all_pairs(c)
+    np.testing.assert_array_equal(Ts, Td)
+    np.testing.assert_allclose(Cs, Cd, rtol=1e-15, atol=0)
+    assert np.all(cij == 77)
+
+
+def test_sparse_all_missing_vector():
+    """a vector with every entry missing has zero tallies, count 0, CCC 0."""
+    c = synthgen.sparse_codes(6, 50, seed=10).numpy()
+    c[2, :] = oracle.MISSING
+    T, C, cij = oracle.sparse_all_pairs(c)
+    for r, (i, j) in enumerate(oracle.pair_list(6)):
+        if 2 in (i, j):
+            assert cij[r] == 0 and not T[r].any() and not C[r].any()
+    S, cnt = oracle.sparse_sums(c)
+    assert cnt[2] == 0 and not S[2].any()
+
+
+def test_sparse_equals_dense_on_present_columns():
+    """Independent pin (column deletion): T_ij over the fields where both entries are
+    present is the DENSE tally of the two vectors restricted to those fields; c_ij is
+    that field count; the per-vector frequencies are the dense frequencies of the vector
+    with its missing entries deleted."""
+    c = synthgen.sparse_codes(9, 240, seed=11).numpy()
+    T, C, cij = oracle.sparse_all_pairs(c)
+    S, cnt = oracle.sparse_sums(c)
+    for i in range(9):
+        keep = c[i] != oracle.MISSING
+        assert cnt[i] == keep.sum()
+        if keep.any():
+            np.testing.assert_array_equal(S[i], oracle.allele_sums(c[i:i + 1, keep])[0])
+    for r, (i, j) in enumerate(oracle.pair_list(9)):
+        keep = (c[i] != oracle.MISSING) & (c[j] != oracle.MISSING)
+        assert cij[r] == keep.sum() and T[r].sum() == 4 * cij[r]
+        Td, _ = oracle.pairs(c[[i, j]][:, keep], [[0, 1]])
+        np.testing.assert_array_equal(T[r], Td[0])
+
+
+def test_sparse_ccc_exact_rational():
+    """CCC in fp64 against exact rationals built from the column-deleted dense pieces."""
+    c = synthgen.sparse_codes(5, 31, seed=12).numpy()
+    T, C, cij = oracle.sparse_all_pairs(c)
+    g = Fraction(2, 3)
+    for r, (i, j) in enumerate(oracle.pair_list(5)):
+        fi = [Fraction(int(x), 2 * int((c[i] != 2).sum())) for x in oracle.sparse_sums(c)[0][i]]
+        fj = [Fraction(int(x), 2 * int((c[j] != 2).sum())) for x in oracle.sparse_sums(c)[0][j]]
+        for a in range(2):
+            for b in range(2):
+                exact = Fraction(int(T[r, 2 * a + b]), 4 * int(cij[r])) * (1 - g * fi[a]) * (1 - g * fj[b])
+                assert abs(C[r, 2 * a + b] - float(exact)) <= 2e-15 * float(exact) + 1e-300
+
+
+def test_sparse_codes_generator():
+    c = synthgen.sparse_codes(64, 2000, seed=4).numpy()
+    frac = (c == 2).mean(1)
+    assert frac.max() < 0.35 and frac.min() >= 0.0 and frac.mean() > 0.05
+    np.testing.assert_array_equal(synthgen.sparse_codes(8, 100, seed=4, row0=5).numpy(),
+                                  synthgen.sparse_codes(13, 100, seed=4).numpy()[5:])
