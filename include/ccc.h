@@ -268,6 +268,49 @@ ccc_status ccc_2way_host(const uint8_t* codes_h, int64_t n_v, int64_t n_f, doubl
  * bench's gpu_launches count). */
 int64_t ccc_last_launch_count(void);
 
+/* ---------------------------------------------------------------------------------
+ * Sparse (missing-data) mode (§7 item 1: "the
+ * value (1,0) can be set aside as a marker to denote a missing entry ... skipping
+ * calculations for missing entries").  Reading A-17:
+ *   present_{iq} = [code != 2],  c_i = #present,  S_i(a) over present entries,
+ *   f_i(a) = S_i(a) / (2 c_i)  (0 if c_i = 0),  w_i(a) = 1 - gamma f_i(a)
+ *   T_ij(a,b) over the fields where both entries are present, c_ij = their number,
+ *   CCC_ij(a,b) = T_ij(a,b) / (4 c_ij) * w_i(a) * w_j(b)   (0 if c_ij = 0).
+ * Records as in dense mode (lexicographic i<j, cells a-major, sum T = 4 c_ij).  On the
+ * tensor pipe each pair costs four int8 MACs per field instead of one: with n = rho(1)
+ * (0 if missing) and v = present, rho(0) = 2v - n, so T needs n.n, n.v, v.n and v.v.
+ * --------------------------------------------------------------------------------- */
+
+/* Rows of the sparse operand X for n_v vectors: 2 * ceil(n_v / 16) * 16. */
+int64_t ccc_sparse_rows(int64_t n_v);
+
+/* Workspace of ccc_2way_sparse (X, s, c, w); 0 if invalid. */
+size_t ccc_sparse_workspace_bytes(int64_t n_v, int64_t n_f);
+
+/* Sparse KB-expand: packed_d (ccc_pack layout) -> X_d int8 [ccc_sparse_rows(n_v)][K_pad],
+ * 128-B aligned, group-interleaved: for the group g of vectors 16g..16g+15, rows
+ * 32g + r hold n_{16g+r,q} (rho(1) on present entries, 0 if missing) and rows 32g + 16 + r
+ * hold present_{16g+r,q} (0 on the K padding and on padding vectors >= n_v);
+ * s_d int32 [n_v] = S_i(1), c_d int32 [n_v] = c_i, w_d double [n_v][2] = w_i(0), w_i(1). */
+ccc_status ccc_expand_sparse(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
+                             int8_t* X_d, int32_t* s_d, int32_t* c_d, double* w_d, void* stream);
+
+/* Sparse 2-way block (rows [a_lo, a_hi) of block A x all n_b vectors of block B), the
+ * same record layouts, diag semantics, flags, checksum and compaction as ccc_2way_block;
+ * X_a / X_b and w_a / w_b from ccc_expand_sparse of each block. */
+ccc_status ccc_2way_sparse_block(const int8_t* X_a, const double* w_a, int64_t n_a, int64_t a_row0,
+                                 int64_t a_lo, int64_t a_hi, const int8_t* X_b, const double* w_b,
+                                 int64_t n_b, int64_t b_row0, int diag, int64_t n_f,
+                                 uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
+                                 uint64_t* checksum_d, const ccc_compact* compact, void* stream);
+
+/* Whole sparse 2-way problem: ccc_expand_sparse into ws_d (>= ccc_sparse_workspace_bytes,
+ * 256-B aligned) then ccc_2way_sparse_block over the upper triangle; outputs as ccc_2way. */
+ccc_status ccc_2way_sparse(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
+                           uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
+                           uint64_t* checksum_d, void* ws_d, size_t ws_bytes,
+                           const ccc_compact* compact, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -113,6 +113,12 @@ _SIGS = {
     "ccc_3way_unit_records": (_i64, [_vp, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _i64]),
     "ccc_3way_unit": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _i64, _int, _vp, _i64,
                              _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _vp]),
+    "ccc_sparse_rows": (_i64, [_i64]),
+    "ccc_sparse_workspace_bytes": (_sz, [_i64, _i64]),
+    "ccc_expand_sparse": (_int, [_vp, _i64, _i64, _dbl, _vp, _vp, _vp, _vp, _vp]),
+    "ccc_2way_sparse_block": (_int, [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _i64, _int,
+                                     _i64, _u32, _vp, _vp, _vp, _vp, _vp]),
+    "ccc_2way_sparse": (_int, [_vp, _i64, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _sz, _vp, _vp]),
     "ccc_e2e_workspace_bytes": (_sz, [_i64, _i64, _u32]),
     "ccc_2way_host": (_int, [_vp, _i64, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _sz, _vp]),
 }
@@ -411,6 +417,54 @@ def checksum_int(ck: torch.Tensor) -> int:
     """checksum tensor [2] (lo, hi as int64 bit patterns) -> Python int mod 2^128."""
     lo, hi = (int(x) & ((1 << 64) - 1) for x in ck.cpu().tolist())
     return (hi << 64) | lo
+
+
+# ----------------------------------------------------------------------- sparse mode (f1)
+def ccc_sparse_rows(n_v: int) -> int:
+    return lib().ccc_sparse_rows(n_v)
+
+
+def ccc_expand_sparse(packed: torch.Tensor, n_f: int, gamma: float = GAMMA, stream=None):
+    """packed -> (X int8 [ccc_sparse_rows(n_v)][K_pad], s, c int32 [n_v], w f64 [n_v][2])."""
+    _dev(packed, torch.uint8, "packed")
+    n_v = packed.shape[0]
+    dev = packed.device
+    X = torch.empty((ccc_sparse_rows(n_v), ccc_k_pad(n_f)), dtype=torch.int8, device=dev)
+    s = torch.empty(n_v, dtype=torch.int32, device=dev)
+    c = torch.empty(n_v, dtype=torch.int32, device=dev)
+    w = torch.empty((n_v, 2), dtype=torch.float64, device=dev)
+    _check(lib().ccc_expand_sparse(_p(packed), n_v, n_f, gamma, _p(X), _p(s), _p(c), _p(w),
+                                   _stream(stream)))
+    return X, s, c, w
+
+
+def ccc_2way_sparse_block(X_a, w_a, n_a, a_row0, a_lo, a_hi, X_b, w_b, n_b, b_row0, diag, n_f,
+                          out_flags, tallies=None, ccc=None, checksum=None, stream=None,
+                          compact: Compact | None = None):
+    cp = None
+    if compact is not None:
+        cp, tallies, ccc = ctypes.byref(compact._c), compact.tallies, compact.ccc
+    _dev(X_a, torch.int8, "X_a"), _dev(X_b, torch.int8, "X_b")
+    _check(lib().ccc_2way_sparse_block(_p(X_a), _p(w_a), n_a, a_row0, a_lo, a_hi, _p(X_b),
+                                       _p(w_b), n_b, b_row0, int(bool(diag)), n_f, out_flags,
+                                       _p(tallies), _p(ccc), _p(checksum), cp, _stream(stream)))
+    return tallies, ccc, checksum
+
+
+def ccc_2way_sparse(packed: torch.Tensor, n_f: int, gamma: float = GAMMA,
+                    out_flags: int = OUT_TALLY | OUT_CCC_F64, tallies=None, ccc=None,
+                    checksum=None, ws=None, stream=None, compact: Compact | None = None):
+    """Sparse-mode 2-way (code 2 = (1,0) marks a missing entry): records as ccc_2way."""
+    _dev(packed, torch.uint8, "packed")
+    n_v = packed.shape[0]
+    cp, tallies, ccc, checksum = _outs(ccc_num_unique(2, n_v), 4, out_flags, packed.device,
+                                       tallies, ccc, checksum, compact)
+    if ws is None:
+        ws = torch.empty(max(lib().ccc_sparse_workspace_bytes(n_v, n_f), 256), dtype=torch.uint8,
+                         device=packed.device)
+    _check(lib().ccc_2way_sparse(_p(packed), n_v, n_f, gamma, out_flags, _p(tallies), _p(ccc),
+                                 _p(checksum), _p(ws), ws.numel(), cp, _stream(stream)))
+    return tallies, ccc, checksum
 
 
 def two_way(codes: torch.Tensor, gamma: float = GAMMA, out_flags: int = OUT_TALLY | OUT_CCC_F64,

@@ -731,4 +731,120 @@ ccc_status ccc_2way_host(const uint8_t* codes_h, int64_t n_v, int64_t n_f, doubl
     return rc;
 }
 
+// ------------------------------------------------------------------ sparse mode (f1)
+int64_t ccc_sparse_rows(int64_t n_v) { return n_v < 0 ? -1 : 2 * ((n_v + 15) / 16 * 16); }
+
+size_t ccc_sparse_workspace_bytes(int64_t n_v, int64_t n_f) {
+    if (n_v < 0 || n_f < 1) return 0;
+    size_t off = al256((size_t)ccc_sparse_rows(n_v) * (size_t)kpad_of(n_f));   // X
+    off += al256((size_t)n_v * 4) * 2;                                           // s, c
+    off += al256((size_t)n_v * 16);                                              // w
+    return off + 256;
+}
+
+ccc_status ccc_expand_sparse(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
+                             int8_t* X_d, int32_t* s_d, int32_t* c_d, double* w_d, void* stream) {
+    g_launches = 0;
+    CCC_CHECK(check_sizes(n_v, n_f));
+    if (n_v == 0) return CCC_OK;
+    if (!packed_d || !X_d || !s_d || !c_d || !w_d || !aligned(packed_d, 16) || !aligned(X_d, 128) ||
+        !aligned(s_d, 4) || !aligned(c_d, 4) || !aligned(w_d, 8))
+        return fail(CCC_ERR_INVALID_ARGUMENT,
+                    "packed_d (16-B), X_d (128-B), s_d, c_d, w_d must be non-NULL and aligned");
+    int sms;
+    CCC_CHECK(check_device(&sms));
+    CCC_CUDA(ccc::launch_expand_sparse(packed_d, n_v, n_f, gamma, X_d, s_d, c_d, w_d, sms,
+                                       (cudaStream_t)stream), "expand_sparse launch");
+    g_launches = 1;
+    return CCC_OK;
+}
+
+ccc_status ccc_2way_sparse_block(const int8_t* X_a, const double* w_a, int64_t n_a, int64_t a_row0,
+                                 int64_t a_lo, int64_t a_hi, const int8_t* X_b, const double* w_b,
+                                 int64_t n_b, int64_t b_row0, int diag, int64_t n_f,
+                                 uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
+                                 uint64_t* checksum_d, const ccc_compact* compact, void* stream) {
+    g_launches = 0;
+    CCC_CHECK(check_compact(compact));
+    CCC_CHECK(check_sizes(n_a, n_f));
+    CCC_CHECK(check_sizes(n_b, n_f));
+    if (out_flags & ~15u) return fail(CCC_ERR_INVALID_ARGUMENT, "unknown out_flags bits");
+    if (!(0 <= a_lo && a_lo <= a_hi && a_hi <= n_a))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "need 0 <= a_lo <= a_hi <= n_a");
+    if (diag && (X_a != X_b || n_a != n_b || a_row0 != b_row0))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "diag block needs A == B");
+    if (a_row0 < 0 || b_row0 < 0 || a_row0 + n_a > CCC_MAX_NV || b_row0 + n_b > CCC_MAX_NV)
+        return fail(CCC_ERR_INVALID_ARGUMENT, "global row indices out of range");
+    if (a_hi == a_lo || n_b == 0) return CCC_OK;
+    CCC_CHECK(check_outputs(out_flags, tallies_d, ccc_d, checksum_d));
+    if (!X_a || !X_b || !w_a || !w_b || !aligned(X_a, 128) || !aligned(X_b, 128))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "X_a/X_b (128-B aligned), w must be non-NULL");
+    int sms;
+    CCC_CHECK(check_device(&sms));
+    const int64_t k_pad = kpad_of(n_f);
+    CUtensorMap tmA, tmB;
+    CCC_CHECK(make_tmap(&tmA, X_a, ccc_sparse_rows(n_a), k_pad, 128));
+    CCC_CHECK(make_tmap(&tmB, X_b, ccc_sparse_rows(n_b), k_pad, 128));
+    ccc::Tally2Args a{};
+    const int64_t v_lo16 = a_lo / 16 * 16, v_hi16 = (a_hi + 15) / 16 * 16;
+    a.sparse = 1;
+    a.a_lo = 2 * v_lo16;                 // scheduler / TMA coordinates: rows of X
+    a.nA = 2 * (v_hi16 - v_lo16);
+    a.nB = ccc_sparse_rows(n_b);
+    a.v_lo = a_lo;                       // records: vectors
+    a.v_hi = a_hi;
+    a.nBv = n_b;
+    a.a_row0 = a_row0;
+    a.b_row0 = b_row0;
+    a.diag = diag ? 1 : 0;
+    a.n_f = (int32_t)n_f;
+    a.k_blocks = (int32_t)(k_pad / ccc::kBK);
+    a.out_flags = (int32_t)out_flags;
+    a.w_a = w_a;
+    a.w_b = w_b;
+    a.tallies = tallies_d;
+    a.ccc = ccc_d;
+    a.checksum = reinterpret_cast<unsigned long long*>(checksum_d);
+    a.rec_row_base = diag ? (a_lo * (2 * n_b - a_lo - 1)) / 2 : 0;
+    a.sup_rows = 2048;
+    a.sup_cols = 2048;
+    a.compact = compact ? 1 : 0;
+    a.cmp = to_compact(compact);
+    int64_t tiles = 0;
+    CCC_CUDA(ccc::launch_tally2(tmA, tmB, a, sms, (cudaStream_t)stream, &tiles), "tally2 sparse launch");
+    if (tiles) g_launches = 1;
+    return CCC_OK;
+}
+
+ccc_status ccc_2way_sparse(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
+                           uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
+                           uint64_t* checksum_d, void* ws_d, size_t ws_bytes,
+                           const ccc_compact* compact, void* stream) {
+    g_launches = 0;
+    CCC_CHECK(check_compact(compact));
+    CCC_CHECK(check_sizes(n_v, n_f));
+    if (out_flags & ~15u) return fail(CCC_ERR_INVALID_ARGUMENT, "unknown out_flags bits");
+    if (n_v < 2) return CCC_OK;
+    CCC_CHECK(check_outputs(out_flags, tallies_d, ccc_d, checksum_d));
+    if (!packed_d || !aligned(packed_d, 16))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "packed_d must be non-NULL and 16-B aligned");
+    if (!ws_d || !aligned(ws_d, 256)) return fail(CCC_ERR_INVALID_ARGUMENT, "ws_d must be 256-B aligned");
+    if (ws_bytes < ccc_sparse_workspace_bytes(n_v, n_f))
+        return fail(CCC_ERR_WORKSPACE, "workspace too small (see ccc_sparse_workspace_bytes)");
+    uint8_t* ws = static_cast<uint8_t*>(ws_d);
+    size_t off = 0;
+    int8_t* X = reinterpret_cast<int8_t*>(ws);
+    off += al256((size_t)ccc_sparse_rows(n_v) * (size_t)kpad_of(n_f));
+    int32_t* sv = reinterpret_cast<int32_t*>(ws + off);
+    off += al256((size_t)n_v * 4);
+    int32_t* cv = reinterpret_cast<int32_t*>(ws + off);
+    off += al256((size_t)n_v * 4);
+    double* w = reinterpret_cast<double*>(ws + off);
+    CCC_CHECK(ccc_expand_sparse(packed_d, n_v, n_f, gamma, X, sv, cv, w, stream));
+    CCC_CHECK(ccc_2way_sparse_block(X, w, n_v, 0, 0, n_v, X, w, n_v, 0, 1, n_f, out_flags,
+                                    tallies_d, ccc_d, checksum_d, compact, stream));
+    g_launches += 1;
+    return CCC_OK;
+}
+
 }  // extern "C"

@@ -147,6 +147,12 @@ struct Tally2Args {
     double inv_d;                // 1 / (36 n_f^3)
     Compact cmp;                 // used when compact != 0
     int32_t compact;
+    // sparse mode (f1): a_lo / nA / nB above are in rows of the group-interleaved X;
+    // the records cover vectors [v_lo, v_hi) of A (local) x [0, nBv) of B
+    int32_t sparse;
+    int64_t v_lo, v_hi, nBv;
+    const int32_t* c_a;          // present-entry counts c_i
+    const int32_t* c_b;
     unsigned long long* trace; // optional per-tile %globaltimer trace (diagnostics)
 };
 

@@ -89,7 +89,7 @@ __device__ __forceinline__ void emit2(const Tally2Args& a, uint64_t key, uint32_
                     __float_as_uint((float)c01), __float_as_uint((float)c10), __float_as_uint((float)c11));
 }
 
-template <int kPair, bool kCompact>
+template <int kPair, bool kCompact, bool kSparse>
 __global__ void __launch_bounds__(kThreads2, 1)
 tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const Tally2Args args) {
@@ -209,6 +209,96 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             }
         }
         __syncwarp();
+    } else if constexpr (kSparse) {
+        // ------------------------------------------------------ sparse epilogue (f1)
+        // X is group-interleaved (16 rows n, then 16 rows v per group of 16 vectors), so
+        // each epilogue warp's TMEM quadrant is one group of vectors i: lanes 0-15 hold
+        // rows n_i, lanes 16-31 rows v_i.  Per 32-column group (vectors j: columns 0-15
+        // n_j, 16-31 v_j) lane t < 16 holds G = n_i.n_j, H = n_i.v_j and lane t + 16
+        // H' = v_i.n_j, C = v_i.v_j = c_ij; one shuffle round hands thread t < 16 all four
+        // for j = 0..7 and thread t + 16 for j = 8..15.  With rho(1) = n, rho(0) = 2v - n:
+        //   T11 = G, T10 = 2H - G, T01 = 2H' - G, T00 = 4C - 2H - 2H' + G
+        //   CCC(a,b) = T(a,b) / (4 c_ij) * w_i(a) * w_j(b)   (reading A-17; 0 if c_ij = 0)
+        const uint32_t quad = warp & 3;
+        const bool low = lane < 16;
+        const uint32_t fl = (uint32_t)args.out_flags;
+        const bool want_t = fl & 1u, want_c64 = fl & 2u, want_c32 = fl & 4u, want_ck = fl & 8u;
+        const bool want_c = want_c64 | want_c32;
+        const int64_t nBv = args.nBv;
+        const uint32_t tempty_leader = kPair == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
+        unsigned long long ck_lo = 0, ck_hi = 0;
+        uint32_t acc = 0, acc_phase = 0;
+        for (int64_t t = unit0;; t += units) {
+            int32_t bm, bn;
+            if (!sch.get(t, bm, bn)) break;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int64_t xrow = args.a_lo + (int64_t)bm * C::kTileM + rank * 128 + quad * 32;
+            const int64_t i_w = xrow >> 1;                    // first vector of my group
+            const int64_t i = i_w + (lane & 15);
+            const bool row_ok = i >= args.v_lo && i < args.v_hi;
+            const int64_t ic = row_ok ? i : args.v_lo;
+            const double wi0 = __ldg(args.w_a + 2 * ic), wi1 = __ldg(args.w_a + 2 * ic + 1);
+            const int64_t rec_i = args.diag ? (i * (2 * nBv - i - 1)) / 2 - i - 1 - args.rec_row_base
+                                            : (i - args.v_lo) * nBv;
+            const uint64_t gi = (uint64_t)(args.a_row0 + i);
+            const bool any_row = __any_sync(0xffffffffu, row_ok);
+            const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + acc * kBN;
+            for (int cg = 0; cg < kBN / 32; ++cg) {
+                const int64_t j0 = ((int64_t)bn * kBN + cg * 32) >> 1;   // first vector j
+                if (!any_row || j0 >= nBv || (args.diag && j0 + 15 <= i_w)) continue;  // uniform
+                uint32_t v[32];
+                tmem_ld16(taddr + cg * 32, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+                tmem_ld16(taddr + cg * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+                tmem_ld_wait();
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t r0 = __shfl_xor_sync(0xffffffffu, low ? v[8 + k] : v[k], 16);
+                    const uint32_t r1 = __shfl_xor_sync(0xffffffffu, low ? v[24 + k] : v[16 + k], 16);
+                    const uint32_t G = low ? v[k] : r0, H = low ? v[16 + k] : r1;
+                    const uint32_t Hp = low ? r0 : v[8 + k], Cc = low ? r1 : v[24 + k];
+                    const int64_t j = j0 + (low ? k : 8 + k);
+                    if (!(row_ok && j < nBv && (!args.diag || j > i))) continue;
+                    const uint32_t t11 = G, t10 = 2u * H - G, t01 = 2u * Hp - G;
+                    const uint32_t t00 = 4u * Cc - 2u * H - 2u * Hp + G;
+                    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+                    if ((want_c || kCompact) && Cc != 0u) {
+                        const double inv = 1.0 / (4.0 * (double)Cc);
+                        const double wj0 = __ldg(args.w_b + 2 * j), wj1 = __ldg(args.w_b + 2 * j + 1);
+                        const double a0 = wi0 * inv, a1 = wi1 * inv;
+                        c00 = (double)t00 * a0 * wj0;
+                        c01 = (double)t01 * a0 * wj1;
+                        c10 = (double)t10 * a1 * wj0;
+                        c11 = (double)t11 * a1 * wj1;
+                    }
+                    const uint64_t gj = (uint64_t)(args.b_row0 + j);
+                    if constexpr (kCompact) {
+                        if (fmax(fmax(c00, c01), fmax(c10, c11)) > args.cmp.thr)
+                            emit2(args, (gi << 20) | gj, t00, t01, t10, t11, c00, c01, c10, c11);
+                    } else {
+                        const int64_t rec = rec_i + j;
+                        if (want_t) stg_128_u32(args.tallies + 4 * rec, t00, t01, t10, t11);
+                        if (want_c64)
+                            stg_256_f64(reinterpret_cast<double*>(args.ccc) + 4 * rec, c00, c01, c10, c11);
+                        else if (want_c32)
+                            stg_128_u32(reinterpret_cast<float*>(args.ccc) + 4 * rec,
+                                        __float_as_uint((float)c00), __float_as_uint((float)c01),
+                                        __float_as_uint((float)c10), __float_as_uint((float)c11));
+                    }
+                    if (want_ck)
+                        ck_fold(ck_lo, ck_hi, (2ull << 60) | (gi << 40) | (gj << 20),
+                                (uint64_t)t00 | ((uint64_t)t01 << 32), (uint64_t)t10 | ((uint64_t)t11 << 32));
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (kPair == 2 && rank != 0) mbar_arrive_cluster(tempty_leader + acc * 8u);
+                else mbar_arrive(&tempty[acc]);
+            }
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+        if (want_ck) ck_flush(ck_lo, ck_hi, args.checksum);
     } else {
         // ---------------------------------------------------------------- epilogue
         // Each warp drains its 32-lane TMEM quadrant with tcgen05.ld.16x256b: per 8-column
@@ -444,12 +534,13 @@ cudaError_t launch_tally2(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
         const char* tre = getenv("CCC_TRACE_PTR");   // diagnostics: device pointer (decimal)
         a2.trace = tre ? reinterpret_cast<unsigned long long*>(strtoull(tre, nullptr, 10)) : nullptr;
     }
-    sch.init(a.a_lo, a.nA, a.nB, a.diag, pm == 2 ? Cfg2<2>::kTileM : Cfg2<1>::kTileM, a2.sup_rows, a2.sup_cols);
+    sch.init(a.a_lo, a.nA, a.nB, a.diag, (pm == 2 || a.sparse) ? Cfg2<2>::kTileM : Cfg2<1>::kTileM,
+             a2.sup_rows, a2.sup_cols);
     const int64_t tiles = sch.total();
     if (n_tiles_out) *n_tiles_out = tiles;
     if (tiles == 0) return cudaSuccess;
-    if (pm == 1) {
-        auto kern = a.compact ? tally2_kernel<1, true> : tally2_kernel<1, false>;
+    if (pm == 1 && !a.sparse) {
+        auto kern = a.compact ? tally2_kernel<1, true, false> : tally2_kernel<1, false, false>;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              Cfg2<1>::kSmem);
         if (e != cudaSuccess) return e;
@@ -457,7 +548,8 @@ cudaError_t launch_tally2(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
         kern<<<grid, kThreads2, Cfg2<1>::kSmem, stream>>>(tmA, tmB, a2);
         return cudaGetLastError();
     }
-    auto kern = a.compact ? tally2_kernel<2, true> : tally2_kernel<2, false>;
+    auto kern = a.sparse ? (a.compact ? tally2_kernel<2, true, true> : tally2_kernel<2, false, true>)
+                         : (a.compact ? tally2_kernel<2, true, false> : tally2_kernel<2, false, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg2<2>::kSmem);
     if (e != cudaSuccess) return e;
