@@ -1,13 +1,15 @@
 """bench.py -- CCC comparisons/s of the B200 hot path.
 
 python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                [--workload c2|c4|c1] [--no-e2e] [--no-cpu]
+                [--workload c2|c4|c1|c2s] [--no-e2e] [--no-cpu]
 
 One step = one pass of the whole hot path over one synthetic batch resident in HBM:
   2-way (default, BASELINE configs[1] = C2: 20,000 vectors x 50,000 individuals):
       ccc_pack -> ccc_expand -> ccc_2way_block (fused tally GEMM + CCC epilogue,
       every unique pair's uint32 tallies + fp64 CCC written to HBM)
   3-way (--workload c4: 4,096 x 16,384, 16 stages, FULL output, buffer reused)
+  sparse 2-way (--workload c2s: C2's shape, ~15% missing entries):
+      ccc_pack -> ccc_expand_sparse -> ccc_2way_sparse_block
 At N > 1 (torchrun), the 2-way path runs the block-circulant decomposition with the
 packed vector blocks passed round a ring over NCCL send/recv; per-GPU load is kept at
 C2's (weak scaling: n_v = 20,000 * sqrt(N)).
@@ -33,6 +35,8 @@ WORKLOADS = {
     "c1": dict(way=2, n_v=64, n_f=1024, label="2-way CCC, 64 x 1,024 (configs[0])"),
     "c2": dict(way=2, n_v=20000, n_f=50000,
                label="2-way CCC, 20,000 SNP vectors x 50,000 individuals (configs[1])"),
+    "c2s": dict(way=2, n_v=20000, n_f=50000, sparse=True,
+                label="2-way sparse-mode CCC (missing entries, SURVEY f1), 20,000 x 50,000"),
     "c4": dict(way=3, n_v=4096, n_f=16384, n_st=16,
                label="3-way CCC, 4,096 SNP vectors x 16,384 individuals, 16 stages (configs[3])"),
 }
@@ -137,6 +141,8 @@ def cpu_baseline(way, n_v, n_f, target_s=12.0, kind="random"):  # noqa: C901
     if way == 2:
         allidx = np.array([(a, b) for a in range(m_local) for b in range(a + 1, m_local)])
         f = oracle.pairs
+        if kind == "sparse":
+            f = lambda c, idx, S=None: oracle.sparse_pairs(c, idx)   # noqa: E731
     else:
         allidx = np.array([(a, b, c) for a in range(m_local) for b in range(a + 1, m_local)
                            for c in range(b + 1, m_local)])
@@ -168,13 +174,19 @@ def run_2way_single(args, wl):
     import synthgen
     from paper_1705_08213_b200 import ccc
     n_v, n_f = wl["n_v"], wl["n_f"]
+    sparse = wl.get("sparse", False)
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     flags = ccc.OUT_TALLY | ccc.OUT_CCC_F64
-    codes = synthgen.random_codes(n_v, n_f, seed=1, device=dev)        # resident in HBM
+    if sparse:
+        codes = synthgen.sparse_codes(n_v, n_f, seed=4, device=dev)    # resident in HBM
+    else:
+        codes = synthgen.random_codes(n_v, n_f, seed=1, device=dev)    # resident in HBM
     packed = torch.empty((n_v, ccc.ccc_packed_stride(n_f)), dtype=torch.uint8, device=dev)
-    N = torch.empty((n_v, ccc.ccc_k_pad(n_f)), dtype=torch.int8, device=dev)
+    N = torch.empty((ccc.ccc_sparse_rows(n_v) if sparse else n_v, ccc.ccc_k_pad(n_f)),
+                    dtype=torch.int8, device=dev)
     s = torch.empty(n_v, dtype=torch.int32, device=dev)
+    cnt = torch.empty(n_v, dtype=torch.int32, device=dev)
     w = torch.empty((n_v, 2), dtype=torch.float64, device=dev)
     m = ccc.ccc_num_unique(2, n_v)
     T = torch.empty((m, 4), dtype=torch.int32, device=dev)
@@ -185,11 +197,17 @@ def run_2way_single(args, wl):
     def step(ev=None):
         ccc.ccc_pack(codes, packed)
         launches[0] += ccc.ccc_last_launch_count()
-        ccc.ccc_expand(packed, n_f, ccc.GAMMA, N, s, w)
+        if sparse:
+            ccc.ccc_expand_sparse(packed, n_f, ccc.GAMMA, (N, s, cnt, w))
+        else:
+            ccc.ccc_expand(packed, n_f, ccc.GAMMA, N, s, w)
         launches[0] += ccc.ccc_last_launch_count()
         if ev:
             ev[0].record(stream)
-        ccc.ccc_2way_block(N, s, w, 0, 0, n_v, N, s, w, 0, True, n_f, flags, T, C)
+        if sparse:
+            ccc.ccc_2way_sparse_block(N, w, n_v, 0, 0, n_v, N, w, n_v, 0, True, n_f, flags, T, C)
+        else:
+            ccc.ccc_2way_block(N, s, w, 0, 0, n_v, N, s, w, 0, True, n_f, flags, T, C)
         launches[0] += ccc.ccc_last_launch_count()
         if ev:
             ev[1].record(stream)
@@ -218,7 +236,7 @@ def run_2way_single(args, wl):
     }
     del T, C
     torch.cuda.empty_cache()
-    if args.e2e:
+    if args.e2e and not sparse:
         res["e2e"] = run_2way_e2e(args, wl, codes)
     return res
 
@@ -324,7 +342,8 @@ def main():
         # exists for this paper): a bounded sample of the same workload per step.
         vals = []
         for _ in range(args.warmup + args.steps):
-            vals.append(cpu_baseline(wl["way"], wl["n_v"], wl["n_f"], target_s=4.0))
+            vals.append(cpu_baseline(wl["way"], wl["n_v"], wl["n_f"], target_s=4.0,
+                                     kind="sparse" if wl.get("sparse") else "random"))
         vals = vals[args.warmup:]
         v = sorted(x["value"] for x in vals)[len(vals) // 2]
         cb = dict(vals[0])
@@ -341,6 +360,8 @@ def main():
         return
 
     if world > 1 or args.gpus > 1:
+        if wl.get("sparse"):
+            raise SystemExit("--workload c2s is a single-GPU measurement")
         from paper_1705_08213_b200 import dist
         return dist.bench_main(args, wl, METRIC, UNIT)
 
@@ -354,7 +375,8 @@ def main():
     # roofline of the dominant kernel (the fused tally GEMM): 2 int8 ops per comparison
     k_s = r["kernel_ms"] / 1e3
     if wl["way"] == 2:
-        ops = 2.0 * r["comparisons"]
+        # sparse mode: 4 int8 MACs per comparison (n.n, n.v, v.n, v.v)
+        ops = (8.0 if wl.get("sparse") else 2.0) * r["comparisons"]
     else:
         ops = 2.0 * r["comparisons"] / wl["n_st"]
     # int8 dense = 2 x bf16 dense (the guide's nominal ratio, 4.5 vs 2.25 PFLOP/s); the
@@ -365,7 +387,8 @@ def main():
             "frac": achieved / int8_peak, "traffic": ncu_traffic(r["kernel"]),
             "kernel": r["kernel"], "kernel_ms": r["kernel_ms"],
             "peak_source": f"2 x bf16_tflops (burst) of MEASURED_PEAKS.json ({pk_kind}); "
-                           "int8 ops = 2 per MAC = 2 per comparison",
+                           "int8 ops = 2 per MAC = %d per comparison" % (
+                               8 if wl.get("sparse") else 2),
             "nominal_int8_frac": achieved / 4500.0}
     hbm_write = r["out_bytes"] / (ms_step / 1e3) / 1e9
     roof["out_write_GBps"] = hbm_write
@@ -384,7 +407,9 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "int8",
         "data": "synthetic",
         "config": {"workload": wl["label"], "n_v": wl["n_v"], "n_f": wl["n_f"],
-                   "input": "type-1 uniform random 2-bit codes, seed 1 (P:657)",
+                   "input": ("type-3 sparse HWE codes, seed 4, missing marker (1,0) with "
+                             "per-vector rate U(0, 0.3) (P:1028-1043)") if wl.get("sparse") else
+                            "type-1 uniform random 2-bit codes, seed 1 (P:657)",
                    "output": "FULL: uint32 tallies + fp64 CCC for every unique record",
                    "l2": "inputs larger than L2 (codes %.2f GB, N %.2f GB)" % (
                        wl["n_v"] * wl["n_f"] / 1e9, wl["n_v"] * wl["n_f"] / 1e9),
@@ -396,7 +421,8 @@ def main():
     if "e2e" in r:
         out["e2e"] = r["e2e"]
     if args.cpu:
-        out["cpu_baseline"] = cpu_baseline(wl["way"], wl["n_v"], wl["n_f"])
+        out["cpu_baseline"] = cpu_baseline(wl["way"], wl["n_v"], wl["n_f"],
+                                           kind="sparse" if wl.get("sparse") else "random")
     print(json.dumps(out))
 
 

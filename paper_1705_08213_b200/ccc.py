@@ -424,15 +424,22 @@ def ccc_sparse_rows(n_v: int) -> int:
     return lib().ccc_sparse_rows(n_v)
 
 
-def ccc_expand_sparse(packed: torch.Tensor, n_f: int, gamma: float = GAMMA, stream=None):
-    """packed -> (X int8 [ccc_sparse_rows(n_v)][K_pad], s, c int32 [n_v], w f64 [n_v][2])."""
+def ccc_expand_sparse(packed: torch.Tensor, n_f: int, gamma: float = GAMMA, out=None,
+                      stream=None):
+    """packed -> (X int8 [ccc_sparse_rows(n_v)][K_pad], s, c int32 [n_v], w f64 [n_v][2])
+    (written into `out` = (X, s, c, w) if given)."""
     _dev(packed, torch.uint8, "packed")
     n_v = packed.shape[0]
     dev = packed.device
-    X = torch.empty((ccc_sparse_rows(n_v), ccc_k_pad(n_f)), dtype=torch.int8, device=dev)
-    s = torch.empty(n_v, dtype=torch.int32, device=dev)
-    c = torch.empty(n_v, dtype=torch.int32, device=dev)
-    w = torch.empty((n_v, 2), dtype=torch.float64, device=dev)
+    if out is None:
+        X = torch.empty((ccc_sparse_rows(n_v), ccc_k_pad(n_f)), dtype=torch.int8, device=dev)
+        s = torch.empty(n_v, dtype=torch.int32, device=dev)
+        c = torch.empty(n_v, dtype=torch.int32, device=dev)
+        w = torch.empty((n_v, 2), dtype=torch.float64, device=dev)
+    else:
+        X, s, c, w = out
+    _dev(X, torch.int8, "X"), _dev(s, torch.int32, "s"), _dev(c, torch.int32, "c")
+    _dev(w, torch.float64, "w")
     _check(lib().ccc_expand_sparse(_p(packed), n_v, n_f, gamma, _p(X), _p(s), _p(c), _p(w),
                                    _stream(stream)))
     return X, s, c, w
