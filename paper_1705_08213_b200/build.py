@@ -30,13 +30,16 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    """Compile every csrc/*.cu into one shared library.  `out`/`defines` build diagnostic
+    variants (e.g. -DCCC_D3_NOXF) next to the product library; they are never loaded
+    unless CCC_LIB points at them."""
+    if not force and out == LIB and not defines and up_to_date():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = out + f".tmp{os.getpid()}"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
            "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
-           "-I", os.path.join(ROOT, "include"), "-I", CSRC] + EXTRA + [
+           "-I", os.path.join(ROOT, "include"), "-I", CSRC] + EXTRA + [f"-D{d}" for d in defines] + [
            "-Xptxas", "-v" if verbose else "-O3",
            "-o", tmp] + sources()
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -45,10 +48,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed building libccc.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    args = sys.argv[1:]
+    out = LIB
+    if "--out" in args:
+        out = os.path.abspath(args[args.index("--out") + 1])
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    print(build(force="--force" in args or out != LIB, verbose="-v" in args, out=out, defines=defs))

@@ -195,6 +195,9 @@ bool is_gamma23(double gamma) { return gamma == 2.0 / 3.0; }
 // (and exact in double below 2^53, n_f <= 50000) for n_f <= 500000.
 void set_exact3(ccc::Tally3Args& a, int64_t n_f, double gamma) {
     a.exact23 = (is_gamma23(gamma) && n_f <= 500000) ? 1 : 0;
+    // T U_p U_m <= 8 n_f (3 n_f)^2 = 72 n_f^3 < 2^52 (n_f <= 38,000): the FULL epilogue
+    // builds 2^52 + T U_p U_m as a double's bit pattern and needs one DFMA per cell
+    a.exact52 = (a.exact23 && 72.0 * (double)n_f * (double)n_f * (double)n_f < 4503599627370496.0) ? 1 : 0;
     const double nf = (double)n_f;
     a.inv_d = 1.0 / (216.0 * nf * nf * nf * nf);
 }

@@ -175,7 +175,7 @@ struct Tally3Args {
     int32_t same_pm, same_mn, order, layout;   // layout: 0 in-block lexicographic,
                                                // 1 pair(p,m)-major x n, 2 dense box
     int32_t exact23;           // gamma == 2/3: CCC = double(T*U_p*U_m) * (U_n/D), D = 216 n_f^4
-    int32_t pad3_;
+    int32_t exact52;           // exact23 and 72 n_f^3 < 2^52: T*U_p*U_m fits a double's mantissa
     double inv_d;              // 1 / (216 n_f^4)
     const int32_t* G;          // global pairwise G: G[min * ldG + max] (i < j valid)
     int64_t ldG;

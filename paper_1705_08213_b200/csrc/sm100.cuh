@@ -49,6 +49,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // ---------------------------------------------------------------- TMA
+// Same, with a suspend-time hint: a waiting warp sleeps in the barrier unit instead of
+// re-issuing try_wait (frees issue slots for the warps that have work).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
+        "r"(parity), "r"(0x989680)
+        : "memory");
+}
+
 __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
 }
@@ -169,8 +182,72 @@ __device__ __forceinline__ void tmem_ld_16x256(uint32_t taddr, uint32_t (&v)[4])
                  : "r"(taddr));
 }
 
+// .x2 / .x4: the 16x256b pattern repeated over 16 / 32 consecutive columns; registers
+// 4r..4r+3 hold repetition r (columns 8r..8r+7).
+__device__ __forceinline__ void tmem_ld_16x256_x(uint32_t taddr, uint32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                   "=r"(v[7])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_16x256_x(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.16x256b.x4.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_16x256_x(uint32_t taddr, uint32_t (&v)[4]) { tmem_ld_16x256(taddr, v); }
+__device__ __forceinline__ void tmem_ld_wait_keep(uint32_t (&v)[8]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]),
+                   "+r"(v[7])
+                 :
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld_wait_keep(uint32_t (&v)[16]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]),
+                   "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]),
+                   "+r"(v[14]), "+r"(v[15])
+                 :
+                 : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld_wait() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Wait for outstanding tcgen05.ld and tie the destination registers to the wait, so the
+// compiler cannot read them before it (used when the next load is issued early).
+__device__ __forceinline__ void tmem_ld_wait_keep(uint32_t (&v)[4]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3])
+                 :
+                 : "memory");
+}
+
+// Named barrier among `threads` threads (id 1..15; id 0 is __syncthreads).
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// Exact uint32 -> double on the FP64 pipe (2^52 + x, minus 2^52) instead of I2F.
+// 2^52 + x as a double, for integer 0 <= x < 2^52 (bit pattern only, no FP64 op).
+__device__ __forceinline__ double magic52(uint64_t x) {
+    double d;
+    asm("mov.b64 %0, %1;" : "=d"(d) : "l"(x | 0x4330000000000000ull));
+    return d;
+}
+
+// (The bit pattern is built in asm: written as __hiloint2double the compiler folds the
+// pair back into an I2F.F64, which issues on the narrow XU pipe.)
+__device__ __forceinline__ double u32_to_f64(uint32_t x) {
+    double d;
+    asm("mov.b64 %0, {%1, %2};" : "=d"(d) : "r"(x), "r"(0x43300000));
+    return d - 4503599627370496.0;
 }
 
 // UMMA shared-memory matrix descriptor: K-major operand, 128-byte swizzle, rows of
@@ -276,6 +353,13 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t mask) {
         : "memory");
 }
 
+// Output stores do not allocate in L1: the records are never re-read by the SM, and
+// allocating them competes with the operand traffic of the mainloop (measured: the 3-way
+// FULL stage went from 25.0 to 20.8 ms).
+#ifndef CCC_ST_HINT
+#define CCC_ST_HINT ".L1::no_allocate"
+#endif
+
 // ---------------------------------------------------------------- shared-memory staging
 __device__ __forceinline__ void sts_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(p)), "r"(a), "r"(b),
@@ -307,16 +391,33 @@ __device__ __forceinline__ void stg_v4(void* p, uint4 v) {
 // 256-bit global stores (sm_100): 32-B aligned, one full L2 sector per thread.
 __device__ __forceinline__ void stg_256_u32(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
                                             uint32_t e, uint32_t f, uint32_t g, uint32_t h) {
-    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a), "r"(b),
+    asm volatile("st.global" CCC_ST_HINT ".v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a), "r"(b),
                  "r"(c), "r"(d), "r"(e), "r"(f), "r"(g), "r"(h)
                  : "memory");
 }
+// Predicated forms: the store is skipped when ok == 0, without a branch.
+
+__device__ __forceinline__ void stg_256_u32_if(bool ok, void* p, uint32_t a, uint32_t b, uint32_t c,
+                                               uint32_t d, uint32_t e, uint32_t f, uint32_t g, uint32_t h) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %9, 0;\n\t"
+        "@q st.global" CCC_ST_HINT ".v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n\t}" ::"l"(p),
+        "r"(a), "r"(b), "r"(c), "r"(d), "r"(e), "r"(f), "r"(g), "r"(h), "r"((uint32_t)ok)
+        : "memory");
+}
+__device__ __forceinline__ void stg_256_f64_if(bool ok, void* p, double a, double b, double c, double d) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+        "@q st.global" CCC_ST_HINT ".v4.f64 [%0], {%1,%2,%3,%4};\n\t}" ::"l"(p),
+        "d"(a), "d"(b), "d"(c), "d"(d), "r"((uint32_t)ok)
+        : "memory");
+}
 __device__ __forceinline__ void stg_256_f64(void* p, double a, double b, double c, double d) {
-    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+    asm volatile("st.global" CCC_ST_HINT ".v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
                  : "memory");
 }
 __device__ __forceinline__ void stg_128_u32(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
+    asm volatile("st.global" CCC_ST_HINT ".v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
                  : "memory");
 }
 

@@ -41,9 +41,16 @@ constexpr int kXfWarps3 = CCC_XF_WARPS;                       // transform warps
 constexpr int kThreads3 = 32 * (2 + kEpiWarps3 + kXfWarps3);
 constexpr int kPivBytes = kBK;       // 128 B of the pivot row per stage
 constexpr int kPivOff3 = kStages3 * (kABytes3 + kBBytes3);
-constexpr int kMaskOff3 = kPivOff3 + kStages3 * kPivBytes;   // per transform warp: 2 x 128 B
-constexpr int kBarOff3 = kMaskOff3 + kXfWarps3 * 2 * kPivBytes;
+// per-unit column terms (s_n, G_pn, n-side weights), one table per TMEM accumulator
+struct ColT3 {
+    uint32_t gpn2, cn, en, sn;   // 2 G_pn, 4 s_n - 2 G_pn, 2 G_pn - 4 s_n, s_n (mod 2^32)
+    double w0, w1;               // n-side weights (exact: U_n(c) / (216 n_f^4))
+    double m0, m1;               // -2^52 w0, -2^52 w1 (kFull cell formula)
+};
+constexpr int kColOff3 = kPivOff3 + kStages3 * kPivBytes;
+constexpr int kBarOff3 = kColOff3 + 2 * kBN * (int)sizeof(ColT3);
 constexpr int kSmem3 = kBarOff3 + 512 + 1024;
+static_assert(kSmem3 <= 232448, "3-way shared memory");
 
 // Units: (m-tile, n-tile) in TriSched order (triangular when m and n share a block),
 // pivots innermost.
@@ -182,7 +189,7 @@ __device__ __forceinline__ void emit3(const Tally3Args& a, uint64_t key, const u
     }
 }
 
-template <int kOrder, bool kExact, bool kCompact>
+template <int kOrder, bool kExact, bool kCompact, bool kFull>
 __global__ void __launch_bounds__(kThreads3, 1)
 tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const Tally3Args args) {
@@ -243,7 +250,14 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 const int32_t mrow = (int32_t)(sch.row0(J) + rank * 128);
                 const int32_t ncol = (int32_t)(sch.col0(K) + rank * 128);
                 for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_wait_sleep(&empty[stage], phase ^ 1);
+#ifdef CCC_D3_NOTMA
+                    mbar_arrive(&aload[stage]);
+                    if (rank == 0) mbar_arrive(&ready[stage]);
+                    else mbar_arrive_cluster(ready_leader + stage * 8u);
+                    if (++stage == kStages3) { stage = 0; phase ^= 1; }
+                    continue;
+#endif
                     // own A half + pivot chunk -> local barrier (the transform warps wait)
                     mbar_arrive_expect_tx(&aload[stage], kABytes3 + kPivBytes);
                     tma_load_2d(smA + stage * kABytes3, &tmA, &aload[stage], kb * kBK, mrow, pol);
@@ -270,18 +284,20 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 if (!sch.get(u, J, K, p)) break;
                 unsigned long long* tr = args.trace ? args.trace + 8 * u : nullptr;
                 if (tr) tr[0] = globaltimer();
-                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                mbar_wait_sleep(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 if (tr) tr[1] = globaltimer();
                 const uint32_t d = tmem_base + acc * kBN;
                 for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
-                    mbar_wait(&ready[stage], phase);
+                    mbar_wait_sleep(&ready[stage], phase);
                     tc_fence_after();
                     const uint32_t sa = a0 + stage * kABytes3, sb = b0 + stage * kBBytes3;
+#ifndef CCC_D3_NOMMA
 #pragma unroll
                     for (int k = 0; k < kBK / kUMMA_K; ++k)
                         mma_i8_pair(d, smem_desc_sw128(sa + k * kUMMA_K),
                                     smem_desc_sw128(sb + k * kUMMA_K), idesc, (kb | k) != 0);
+#endif
                     mma_commit_pair(&empty[stage], 3);
                     if (++stage == kStages3) { stage = 0; phase ^= 1; }
                 }
@@ -293,44 +309,55 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         __syncwarp();
     } else if (warp >= 2 + kEpiWarps3) {
         // -------------------------------------------------------------- transform
-        // A <- A o n_p in place: per stage each warp turns the pivot chunk into byte masks
-        // M1 = [n_p >= 1], M2 = [n_p == 2] once, then a * n_p = (a & M1) + (a & M2).
+        // A <- A o n_p in place.  Thread (warp xw, lane) owns logical 16-B chunk c = lane % 8
+        // of rows xw*32 + lane/8 + 4k (k < 8): its byte masks M1 = [n_p >= 1], M2 = [n_p == 2]
+        // come from one broadcast load of pivot chunk c, and a * n_p = (a & M1) + (a & M2).
+        // Each warp instruction covers 4 whole 128-B rows (8 lanes per row on 8 different
+        // swizzled chunk positions): 4 wavefronts, no bank conflicts.
+        static_assert(kXfWarps3 * 32 == 128, "transform covers 128 rows with 4 warps");
         const uint32_t xw = (uint32_t)(warp - 2 - kEpiWarps3);
-        const uint32_t r_first = xw * 32 + lane;
-        uint32_t* mk = reinterpret_cast<uint32_t*>(smem + kMaskOff3 + xw * 2 * kPivBytes);
+        const uint32_t cl = lane & 7u, r0 = xw * 32 + (lane >> 3);
         uint32_t stage = 0, phase = 0;
         for (int64_t u = unit0;; u += units) {
             int32_t J, K;
             int64_t p;
             if (!sch.get(u, J, K, p)) break;
             for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
-                mbar_wait(&aload[stage], phase);
+                mbar_wait_sleep(&aload[stage], phase);
+#ifndef CCC_D3_NOXF
                 {
-                    const uint32_t b = reinterpret_cast<const uint32_t*>(smP + stage * kPivBytes)[lane];
-                    const uint32_t lo = b & 0x01010101u, hi = (b >> 1) & 0x01010101u;
-                    mk[lane] = (lo | hi) * 0xFFu;
-                    mk[32 + lane] = hi * 0xFFu;
-                }
-                __syncwarp();
+                    const uint4 pv = lds_v4(smP + stage * kPivBytes + cl * 16);
+                    uint4 m1, m2;
+                    m1.x = ((pv.x | (pv.x >> 1)) & 0x01010101u) * 0xFFu;
+                    m1.y = ((pv.y | (pv.y >> 1)) & 0x01010101u) * 0xFFu;
+                    m1.z = ((pv.z | (pv.z >> 1)) & 0x01010101u) * 0xFFu;
+                    m1.w = ((pv.w | (pv.w >> 1)) & 0x01010101u) * 0xFFu;
+                    m2.x = ((pv.x >> 1) & 0x01010101u) * 0xFFu;
+                    m2.y = ((pv.y >> 1) & 0x01010101u) * 0xFFu;
+                    m2.z = ((pv.z >> 1) & 0x01010101u) * 0xFFu;
+                    m2.w = ((pv.w >> 1) & 0x01010101u) * 0xFFu;
+                    uint8_t* abase = smA + stage * kABytes3;
+                    uint4 x[8];
 #pragma unroll
-                for (uint32_t r = r_first; r < 128u; r += 32 * kXfWarps3) {
-                    uint8_t* arow = smA + stage * kABytes3 + r * kBK;
+                    for (int k = 0; k < 8; ++k) {
+                        const uint32_t r = r0 + 4 * k;   // 128-B swizzle: chunk c at c ^ (r & 7)
+                        x[k] = lds_v4(abase + r * kBK + ((cl ^ (r & 7u)) << 4));
+                    }
 #pragma unroll
-                    for (uint32_t c = 0; c < 8; ++c) {
-                        // 128-B swizzle: logical 16-B chunk c of row r sits at chunk c ^ (r & 7)
-                        uint4* pa = reinterpret_cast<uint4*>(arow + ((c ^ (r & 7u)) << 4));
-                        const uint4 m1 = reinterpret_cast<const uint4*>(mk)[c];
-                        const uint4 m2 = reinterpret_cast<const uint4*>(mk + 32)[c];
-                        uint4 x = *pa;
-                        x.x = (x.x & m1.x) + (x.x & m2.x);
-                        x.y = (x.y & m1.y) + (x.y & m2.y);
-                        x.z = (x.z & m1.z) + (x.z & m2.z);
-                        x.w = (x.w & m1.w) + (x.w & m2.w);
-                        *pa = x;
+                    for (int k = 0; k < 8; ++k) {
+                        const uint32_t r = r0 + 4 * k;
+                        x[k].x = (x[k].x & m1.x) + (x[k].x & m2.x);
+                        x[k].y = (x[k].y & m1.y) + (x[k].y & m2.y);
+                        x[k].z = (x[k].z & m1.z) + (x[k].z & m2.z);
+                        x[k].w = (x[k].w & m1.w) + (x[k].w & m2.w);
+                        sts_v4(abase + r * kBK + ((cl ^ (r & 7u)) << 4), x[k].x, x[k].y, x[k].z, x[k].w);
                     }
                 }
+#endif
                 __syncwarp();
+#ifndef CCC_D3_NOFENCE
                 fence_proxy_async_smem();
+#endif
                 __syncwarp();
                 if (lane == 0) {
                     if (rank == 0) mbar_arrive(&ready[stage]);
@@ -344,16 +371,26 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         // Register-only drain: tcgen05.ld.16x256b gives a thread 2 consecutive n of 2 rows
         // m; a record is 32 B of tallies + 64 B of fp64 CCC = whole L2 sectors, written
         // with 256-bit stores.  Warp w drains lanes [half*16, +16) of TMEM quadrant w % 4.
+        // Everything that depends only on the row (m) or only on the column (n) of a unit is
+        // hoisted: the column terms are staged in shared memory by all 256 epilogue threads
+        // before the accumulator is waited on, the row terms live in registers, and a record
+        // costs the 8 inclusion-exclusion cells, 8 x (convert, 2 DMUL) and 3 stores.  The
+        // next TMEM load and the next G_mn loads are in flight while a group is computed.
+        const uint32_t et = threadIdx.x - 64u;          // 0..255 among the epilogue warps
         const uint32_t quad = warp & 3;
         const uint32_t half = (uint32_t)(warp - 2) >> 2;
         const uint32_t fl = (uint32_t)args.out_flags;
-        const bool want_t = fl & 1u, want_c64 = fl & 2u, want_c32 = fl & 4u, want_ck = fl & 8u;
+        // kFull: out_flags == tallies + fp64 CCC (the FULL headline mode), no runtime tests
+        const bool want_t = kFull || (fl & 1u), want_c64 = kFull || (fl & 2u);
+        const bool want_c32 = !kFull && (fl & 4u), want_ck = !kFull && (fl & 8u);
         const bool want_c = want_c64 | want_c32;
         const uint32_t eight_nf = 8u * (uint32_t)args.n_f;
         const double inv8nf = 1.0 / (8.0 * (double)args.n_f);
         const uint32_t nf = (uint32_t)args.n_f;
         const int64_t nbp = args.bp.rows, nN = args.n_hi - args.n_lo, nM = args.m_hi - args.m_lo;
-        const int32_t cpair = 2 * (int32_t)(lane & 3);
+        const uint32_t cpair = 2u * (lane & 3u);
+        constexpr bool kRowG = O::pos(1) < O::pos(2);   // G_mn = G[gm][gn]: a row of G per m
+        ColT3* coltab = reinterpret_cast<ColT3*>(smem + kColOff3);
         unsigned long long ck_lo = 0, ck_hi = 0;
         uint32_t acc = 0, acc_phase = 0;
         for (int64_t u = unit0;; u += units) {
@@ -362,35 +399,74 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             if (!sch.get(u, J, K, p)) break;
             unsigned long long* tr = (args.trace && warp == 2 && rank == 0) ? args.trace + 8 * u : nullptr;
             if (tr && lane == 0) tr[3] = globaltimer();
-            mbar_wait(&tfull[acc], acc_phase);
-            tc_fence_after();
-            if (tr && lane == 0) tr[4] = globaltimer();
             const int64_t gp = args.bp.row0 + p;
+            const int64_t col0 = sch.col0(K);
+            const int64_t gcol0 = args.bn.row0 + col0;       // global index of column 0
+            // valid columns of this unit: local index < nval (warp-uniform)
+            const int64_t ncols = args.n_hi - col0;
+            const int32_t nval = ncols >= kBN ? kBN : (int32_t)ncols;
+            const int32_t gn_max = (int32_t)(args.n_hi - 1 - col0);   // clamp for loads
+            ColT3* ct = coltab + acc * kBN;
             const uint32_t s_p = (uint32_t)__ldg(args.bp.s + p);
+            {
+                // column terms of this unit: thread et <- column col0 + et
+                const int64_t nc = col0 + (et < (uint32_t)nval ? et : (uint32_t)(nval - 1));
+                const uint32_t sn = (uint32_t)__ldg(args.bn.s + nc);
+                const uint32_t gpn = gord<kOrder, 0, 2>(args.G, args.ldG, gp, args.bn.row0 + nc);
+                ColT3 v;
+                v.gpn2 = 2u * gpn;
+                v.cn = 4u * sn - 2u * gpn;
+                v.en = 2u * gpn - 4u * sn;
+                v.sn = sn;
+                if constexpr (kExact) {   // U_n(c) / (216 n_f^4)
+                    v.w0 = (double)(nf + sn) * args.inv_d;
+                    v.w1 = (double)(3u * nf - sn) * args.inv_d;
+                    v.m0 = -4503599627370496.0 * v.w0;
+                    v.m1 = -4503599627370496.0 * v.w1;
+                } else {
+                    v.w0 = __ldg(args.bn.w + 2 * nc);
+                    v.w1 = __ldg(args.bn.w + 2 * nc + 1);
+                }
+                ct[et] = v;
+            }
             // general gamma: w_p(a) / (8 n_f); gamma = 2/3: integer U_p(a) = 3 n_f - S_p(a)
             const double wp0 = kExact ? 0.0 : __ldg(args.bp.w + 2 * p) * inv8nf;
             const double wp1 = kExact ? 0.0 : __ldg(args.bp.w + 2 * p + 1) * inv8nf;
             const uint64_t up0 = nf + s_p, up1 = 3u * nf - s_p;
             // my 2 rows m = row0(J) + rank*128 + quad*32 + half*16 + r*8 + lane/4
-            int64_t rec_r[2], m_r[2];
-            uint32_t s_m[2], g_pm[2];
-            double wpm[2][4];      // general: w_p(a_p) w_m(a_m) / (8 n_f); exact: U_p U_m (integer)
-            bool ok_r[2];
+            int64_t rec_r[2], gm_r[2];
+            int32_t lo_r[2];             // record (r, local n) valid iff lo_r < n < nval
+            uint32_t gpm2[2], A_r[2], B_r[2], D_r[2], s_m[2], g_pm[2];
+            double wpm[2][4];            // general: w_p(a_p) w_m(a_m) / (8 n_f); exact: U_p U_m
+            uint64_t upm[2][4];          // kFull: U_p(a_p) U_m(a_m) as integers
+            const int32_t* grow[2];      // kRowG: &G[gm][gcol0]
             bool my_any = false;
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
                 const int64_t m = sch.row0(J) + rank * 128 + quad * 32 + half * 16 + r * 8 + (lane >> 2);
-                m_r[r] = m;
-                ok_r[r] = m >= args.m_lo && m < args.m_hi && (!args.same_pm || m > p);
+                const bool ok = m >= args.m_lo && m < args.m_hi && (!args.same_pm || m > p);
                 const int64_t mc = m < args.m_hi ? m : args.m_hi - 1;
+                gm_r[r] = args.bm.row0 + mc;
                 s_m[r] = (uint32_t)__ldg(args.bm.s + mc);
-                g_pm[r] = ok_r[r] ? gord<kOrder, 0, 1>(args.G, args.ldG, gp, args.bm.row0 + m) : 0u;
+                const uint32_t gpm = ok ? gord<kOrder, 0, 1>(args.G, args.ldG, gp, gm_r[r]) : 0u;
+                g_pm[r] = gpm;
+                gpm2[r] = 2u * gpm;
+                A_r[r] = 4u * s_p - 2u * gpm;
+                B_r[r] = 4u * s_m[r] - 2u * gpm;
+                D_r[r] = eight_nf - 4u * s_p - 4u * s_m[r] + 2u * gpm;
                 if constexpr (kExact) {
                     const uint64_t um0 = nf + s_m[r], um1 = 3u * nf - s_m[r];
-                    wpm[r][0] = __longlong_as_double((long long)(up0 * um0));   // bit-carried ints
-                    wpm[r][1] = __longlong_as_double((long long)(up0 * um1));
-                    wpm[r][2] = __longlong_as_double((long long)(up1 * um0));
-                    wpm[r][3] = __longlong_as_double((long long)(up1 * um1));
+                    if constexpr (kFull) {
+                        upm[r][0] = up0 * um0;
+                        upm[r][1] = up0 * um1;
+                        upm[r][2] = up1 * um0;
+                        upm[r][3] = up1 * um1;
+                    } else {
+                        wpm[r][0] = (double)(up0 * um0);   // < 2^53: exact
+                        wpm[r][1] = (double)(up0 * um1);
+                        wpm[r][2] = (double)(up1 * um0);
+                        wpm[r][3] = (double)(up1 * um1);
+                    }
                 } else {
                     const double wm0 = __ldg(args.bm.w + 2 * mc), wm1 = __ldg(args.bm.w + 2 * mc + 1);
                     wpm[r][0] = wp0 * wm0;  // (a_p, a_m) = (0,0), includes 1/(8 n_f)
@@ -405,80 +481,101 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     rec_r[r] = (p * (2 * nbp - p - 1) / 2 + mc - p - 1) * nN - args.n_lo - args.rec_base;
                 else
                     rec_r[r] = ((p - args.p_lo) * nM + (mc - args.m_lo)) * nN - args.n_lo;
-                my_any |= ok_r[r];
+                rec_r[r] += col0;   // record of local column 0
+                // n > m is needed only when m and n share a block
+                const int64_t lo = args.same_mn ? m - col0 : -1;
+                lo_r[r] = !ok ? kBN : lo < -1 ? -1 : lo > kBN ? kBN : (int32_t)lo;
+                grow[r] = args.G + gm_r[r] * args.ldG + gcol0;
+                my_any |= ok;
             }
+#ifdef CCC_D3_NOEPI
+            const bool any_row = false;
+#else
             const bool any_row = __any_sync(0xffffffffu, my_any);
-            const uint32_t taddr = tmem_base + ((quad * 32u + half * 16u) << 16) + acc * kBN;
-            for (int c = 0; c < kBN / 8; ++c) {
-                const int64_t n0 = sch.col0(K) + c * 8;
-                if (!any_row || n0 >= args.n_hi) continue;  // warp-uniform
-                uint32_t va[4];
-                tmem_ld_16x256(taddr + c * 8, va);
-                const int64_t nA = n0 + cpair, nB = nA + 1;
-                const int64_t nAc = nA < args.n_hi ? nA : args.n_hi - 1;
-                const int64_t nBc = nB < args.n_hi ? nB : args.n_hi - 1;
-                const uint32_t sA = (uint32_t)__ldg(args.bn.s + nAc);
-                const uint32_t sB = (uint32_t)__ldg(args.bn.s + nBc);
-                const int64_t gnA = args.bn.row0 + nAc, gnB = args.bn.row0 + nBc;
-                const uint32_t gpnA = gord<kOrder, 0, 2>(args.G, args.ldG, gp, gnA);
-                const uint32_t gpnB = gord<kOrder, 0, 2>(args.G, args.ldG, gp, gnB);
-                double wA0 = 0.0, wA1 = 0.0, wB0 = 0.0, wB1 = 0.0;
-                if (want_c || kCompact) {
-                    if constexpr (kExact) {   // U_n(c) / (216 n_f^4)
-                        wA0 = (double)(nf + sA) * args.inv_d;
-                        wA1 = (double)(3u * nf - sA) * args.inv_d;
-                        wB0 = (double)(nf + sB) * args.inv_d;
-                        wB1 = (double)(3u * nf - sB) * args.inv_d;
-                    } else {
-                        wA0 = __ldg(args.bn.w + 2 * nAc);
-                        wA1 = __ldg(args.bn.w + 2 * nAc + 1);
-                        wB0 = __ldg(args.bn.w + 2 * nBc);
-                        wB1 = __ldg(args.bn.w + 2 * nBc + 1);
+#endif
+            // column groups of 8 that hold any valid n (warp-uniform)
+            const int c_end = !any_row ? 0 : (nval + 7) / 8;
+            // G_mn for column group c: g[r][h] = G(m_r, col0 + 8c + cpair + h), clamped
+            auto load_gmn = [&](int c, uint32_t (&g)[2][2]) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    int32_t nl = c * 8 + (int32_t)cpair + h;
+                    nl = nl < gn_max ? nl : gn_max;
+#pragma unroll
+                    for (int r = 0; r < 2; ++r) {
+                        if constexpr (kRowG) g[r][h] = (uint32_t)__ldg(grow[r] + nl);
+                        else g[r][h] = (uint32_t)__ldg(args.G + (gcol0 + nl) * args.ldG + gm_r[r]);
                     }
                 }
-                tmem_ld_wait();
+            };
+            uint32_t gnext[2][2] = {{0u, 0u}, {0u, 0u}};
+            if (c_end > 0) load_gmn(0, gnext);
+            named_bar_sync(1, 32 * kEpiWarps3);   // column table of this unit is complete
+            mbar_wait_sleep(&tfull[acc], acc_phase);
+            tc_fence_after();
+            if (tr && lane == 0) tr[4] = globaltimer();
+            const uint32_t taddr = tmem_base + ((quad * 32u + half * 16u) << 16) + acc * kBN;
+            uint32_t vnext[4];
+            if (c_end > 0) tmem_ld_16x256(taddr, vnext);
+            for (int c = 0; c < c_end; ++c) {
+                tmem_ld_wait_keep(vnext);
+                const uint32_t va[4] = {vnext[0], vnext[1], vnext[2], vnext[3]};
+                const uint32_t gcur[2][2] = {{gnext[0][0], gnext[0][1]}, {gnext[1][0], gnext[1][1]}};
+                if (c + 1 < c_end) {
+                    tmem_ld_16x256(taddr + (c + 1) * 8, vnext);
+                    load_gmn(c + 1, gnext);
+                }
+                const int32_t nA = c * 8 + (int32_t)cpair;    // local column of h = 0
+                const ColT3 cA = ct[nA], cB = ct[nA + 1];
 #pragma unroll
                 for (int r = 0; r < 2; ++r) {
-                    if (!ok_r[r]) continue;
-                    const int64_t m = m_r[r], gm = args.bm.row0 + m;
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        const int64_t n = h ? nB : nA;
-                        if (!(n >= args.n_lo && n < args.n_hi && (!args.same_mn || n > m))) continue;
-                        const int64_t gn = h ? gnB : gnA;
+                        // every record is computed; invalid ones (tile edges, j <= i) are
+                        // only not stored, so the loop body has no branches
+                        const int32_t nl = nA + h;
+                        const bool ok = nl > lo_r[r] && nl < nval;
+                        const ColT3& cn = h ? cB : cA;
                         const uint32_t g3 = va[r * 2 + h];
-                        const uint32_t gpm = g_pm[r], gpn = h ? gpnB : gpnA;
-                        const uint32_t gmn = gord<kOrder, 1, 2>(args.G, args.ldG, gm, gn);
-                        const uint32_t sp = s_p, sm = s_m[r], sn = h ? sB : sA;
+                        const uint32_t gmn2 = 2u * gcur[r][h];
                         uint32_t t[8];   // role order: index 4 a_p + 2 a_m + a_n
                         t[7] = g3;
-                        t[6] = 2u * gpm - g3;
-                        t[5] = 2u * gpn - g3;
-                        t[3] = 2u * gmn - g3;
-                        t[4] = 4u * sp - 2u * gpm - 2u * gpn + g3;
-                        t[2] = 4u * sm - 2u * gpm - 2u * gmn + g3;
-                        t[1] = 4u * sn - 2u * gpn - 2u * gmn + g3;
-                        t[0] = eight_nf - 4u * (sp + sm + sn) + 2u * (gpm + gpn + gmn) - g3;
+                        t[6] = gpm2[r] - g3;
+                        t[5] = cn.gpn2 - g3;
+                        t[3] = gmn2 - g3;
+                        t[4] = A_r[r] - cn.gpn2 + g3;
+                        t[2] = B_r[r] - gmn2 + g3;
+                        t[1] = cn.cn - gmn2 + g3;
+                        t[0] = D_r[r] + cn.en + gmn2 - g3;
                         uint32_t tc[8];
                         perm_cells<O::R0, O::R1, O::R2>(t, tc);
-                        const int64_t rec = rec_r[r] + n;
+                        const int64_t rec = rec_r[r] + nl;
+#ifdef CCC_D3_NOSTORE
+                        const bool st_ok = ok && rec < 0;
+#else
+                        const bool st_ok = ok;
+#endif
                         if (!kCompact && want_t)
-                            stg_256_u32(args.tallies + 8 * rec, tc[0], tc[1], tc[2], tc[3], tc[4],
-                                        tc[5], tc[6], tc[7]);
+                            stg_256_u32_if(st_ok, args.tallies + 8 * rec, tc[0], tc[1], tc[2], tc[3], tc[4],
+                                           tc[5], tc[6], tc[7]);
                         if (want_c || kCompact) {
                             // Eq.4: CCC = T / (8 n_f) * w_p(a_p) w_m(a_m) w_n(a_n)
-                            const double wn0 = h ? wB0 : wA0, wn1 = h ? wB1 : wA1;
+                            const double wn0 = cn.w0, wn1 = cn.w1;
                             double cr[8], cc[8];
 #pragma unroll
                             for (int ab = 0; ab < 4; ++ab) {
-                                if constexpr (kExact) {
-                                    // CCC = T U_p U_m U_n / (216 n_f^4); T U_p U_m < 2^53 is exact
-                                    const uint64_t upm = (uint64_t)__double_as_longlong(wpm[r][ab]);
-                                    cr[2 * ab + 0] = (double)(t[2 * ab + 0] * upm) * wn0;
-                                    cr[2 * ab + 1] = (double)(t[2 * ab + 1] * upm) * wn1;
+                                if constexpr (kFull) {
+                                    // P = T U_p U_m < 2^52 in integers; the double 2^52 + P is
+                                    // P's bits under exponent 0x433, so CCC = P w_n =
+                                    // fma(2^52 + P, w_n, -2^52 w_n): one rounding, one FP64 op
+                                    // (FP64 shares its issue pipe with the tensor core)
+                                    cr[2 * ab + 0] = __fma_rn(magic52(t[2 * ab + 0] * upm[r][ab]), wn0, cn.m0);
+                                    cr[2 * ab + 1] = __fma_rn(magic52(t[2 * ab + 1] * upm[r][ab]), wn1, cn.m1);
                                 } else {
-                                    cr[2 * ab + 0] = (double)t[2 * ab + 0] * wpm[r][ab] * wn0;
-                                    cr[2 * ab + 1] = (double)t[2 * ab + 1] * wpm[r][ab] * wn1;
+                                    // exact: T U_p U_m rounded once (same as the 64-bit integer
+                                    // product converted), times U_n / (216 n_f^4)
+                                    cr[2 * ab + 0] = u32_to_f64(t[2 * ab + 0]) * wpm[r][ab] * wn0;
+                                    cr[2 * ab + 1] = u32_to_f64(t[2 * ab + 1]) * wpm[r][ab] * wn1;
                                 }
                             }
                             perm_cells<O::R0, O::R1, O::R2>(cr, cc);
@@ -487,25 +584,25 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                                 double mx = cc[0];
 #pragma unroll
                                 for (int q = 1; q < 8; ++q) mx = fmax(mx, cc[q]);
-                                if (mx > args.cmp.thr) {
-                                    const int64_t g[3] = {gp, gm, gn};
+                                if (ok && mx > args.cmp.thr) {
+                                    const int64_t g[3] = {gp, gm_r[r], gcol0 + nl};
                                     emit3(args, ((uint64_t)g[O::R0] << 40) | ((uint64_t)g[O::R1] << 20) |
                                                     (uint64_t)g[O::R2], tc, cc);
                                 }
                             } else if (want_c64) {
                                 double* q = reinterpret_cast<double*>(args.ccc) + 8 * rec;
-                                stg_256_f64(q, cc[0], cc[1], cc[2], cc[3]);
-                                stg_256_f64(q + 4, cc[4], cc[5], cc[6], cc[7]);
+                                stg_256_f64_if(st_ok, q, cc[0], cc[1], cc[2], cc[3]);
+                                stg_256_f64_if(st_ok, q + 4, cc[4], cc[5], cc[6], cc[7]);
                             } else {
                                 float* q = reinterpret_cast<float*>(args.ccc) + 8 * rec;
-                                stg_256_u32(q, __float_as_uint((float)cc[0]), __float_as_uint((float)cc[1]),
-                                            __float_as_uint((float)cc[2]), __float_as_uint((float)cc[3]),
-                                            __float_as_uint((float)cc[4]), __float_as_uint((float)cc[5]),
-                                            __float_as_uint((float)cc[6]), __float_as_uint((float)cc[7]));
+                                stg_256_u32_if(st_ok, q, __float_as_uint((float)cc[0]), __float_as_uint((float)cc[1]),
+                                               __float_as_uint((float)cc[2]), __float_as_uint((float)cc[3]),
+                                               __float_as_uint((float)cc[4]), __float_as_uint((float)cc[5]),
+                                               __float_as_uint((float)cc[6]), __float_as_uint((float)cc[7]));
                             }
                         }
-                        if (want_ck) {
-                            const int64_t g[3] = {gp, gm, gn};
+                        if (want_ck && ok) {
+                            const int64_t g[3] = {gp, gm_r[r], gcol0 + nl};
                             ck_fold3(ck_lo, ck_hi,
                                      (3ull << 60) | ((uint64_t)g[O::R0] << 40) |
                                          ((uint64_t)g[O::R1] << 20) | (uint64_t)g[O::R2],
@@ -576,21 +673,26 @@ cudaError_t launch_tally3(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
         return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, a);
     };
     // 6 canonical orders x {general gamma, gamma = 2/3} x {dense, compacted} instantiations
-    auto pick = [&](auto ex, auto cp) {
-        constexpr bool E = decltype(ex)::value, Cp = decltype(cp)::value;
+    auto pick = [&](auto ex, auto cp, auto fu) {
+        constexpr bool E = decltype(ex)::value, Cp = decltype(cp)::value, Fu = decltype(fu)::value;
         switch (a.order) {
-            case 0: return go(tally3_kernel<0, E, Cp>);
-            case 1: return go(tally3_kernel<1, E, Cp>);
-            case 2: return go(tally3_kernel<2, E, Cp>);
-            case 3: return go(tally3_kernel<3, E, Cp>);
-            case 4: return go(tally3_kernel<4, E, Cp>);
-            default: return go(tally3_kernel<5, E, Cp>);
+            case 0: return go(tally3_kernel<0, E, Cp, Fu>);
+            case 1: return go(tally3_kernel<1, E, Cp, Fu>);
+            case 2: return go(tally3_kernel<2, E, Cp, Fu>);
+            case 3: return go(tally3_kernel<3, E, Cp, Fu>);
+            case 4: return go(tally3_kernel<4, E, Cp, Fu>);
+            default: return go(tally3_kernel<5, E, Cp, Fu>);
         }
     };
     using T = std::true_type;
     using F = std::false_type;
-    if (a.exact23) return a.compact ? pick(T{}, T{}) : pick(T{}, F{});
-    return a.compact ? pick(F{}, T{}) : pick(F{}, F{});
+    // FULL with gamma = 2/3 (tallies + fp64 CCC, no checksum) gets a flag-free epilogue
+    const bool full = !a.compact && a.out_flags == 3 && a.exact52;
+    if (a.exact23) {
+        if (a.compact) return pick(T{}, T{}, F{});
+        return full ? pick(T{}, F{}, T{}) : pick(T{}, F{}, F{});
+    }
+    return a.compact ? pick(F{}, T{}, F{}) : pick(F{}, F{}, F{});
 }
 
 }  // namespace ccc
