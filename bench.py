@@ -1,7 +1,7 @@
 """bench.py -- CCC comparisons/s of the B200 hot path.
 
 python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                [--workload c2|c4|c1|c2s] [--no-e2e] [--no-cpu]
+                [--workload c2|c4|c1|c2s|c2pop] [--no-e2e] [--no-cpu]
 
 One step = one pass of the whole hot path over one synthetic batch resident in HBM:
   2-way (default, BASELINE configs[1] = C2: 20,000 vectors x 50,000 individuals):
@@ -10,6 +10,8 @@ One step = one pass of the whole hot path over one synthetic batch resident in H
   3-way (--workload c4: 4,096 x 16,384, 16 stages, FULL output, buffer reused)
   sparse 2-way (--workload c2s: C2's shape, ~15% missing entries):
       ccc_pack -> ccc_expand_sparse -> ccc_2way_sparse_block
+  popcount baseline (--workload c2pop: C2 through ccc_2way_popcount, the paper's
+      AND + popcount tally on CUDA cores): ccc_pack -> ccc_2way_popcount
 At N > 1 (torchrun), the 2-way path runs the block-circulant decomposition with the
 packed vector blocks passed round a ring over NCCL send/recv; per-GPU load is kept at
 C2's (weak scaling: n_v = 20,000 * sqrt(N)).
@@ -37,6 +39,9 @@ WORKLOADS = {
                label="2-way CCC, 20,000 SNP vectors x 50,000 individuals (configs[1])"),
     "c2s": dict(way=2, n_v=20000, n_f=50000, sparse=True,
                 label="2-way sparse-mode CCC (missing entries, SURVEY f1), 20,000 x 50,000"),
+    "c2pop": dict(way=2, n_v=20000, n_f=50000, popcount=True,
+                  label="2-way CCC, 20,000 x 50,000, the paper's popcount tally on CUDA cores "
+                        "(SURVEY f4 baseline)"),
     "c4": dict(way=3, n_v=4096, n_f=16384, n_st=16,
                label="3-way CCC, 4,096 SNP vectors x 16,384 individuals, 16 stages (configs[3])"),
 }
@@ -175,6 +180,7 @@ def run_2way_single(args, wl):
     from paper_1705_08213_b200 import ccc
     n_v, n_f = wl["n_v"], wl["n_f"]
     sparse = wl.get("sparse", False)
+    popcount = wl.get("popcount", False)
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     flags = ccc.OUT_TALLY | ccc.OUT_CCC_F64
@@ -193,10 +199,19 @@ def run_2way_single(args, wl):
     C = torch.empty((m, 4), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream()
     launches = [0]
+    ws = ccc.workspace(2, n_v, n_f, dev) if popcount else None
 
     def step(ev=None):
         ccc.ccc_pack(codes, packed)
         launches[0] += ccc.ccc_last_launch_count()
+        if popcount:
+            if ev:
+                ev[0].record(stream)
+            ccc.ccc_2way_popcount(packed, n_f, ccc.GAMMA, flags, T, C, None, ws)
+            launches[0] += ccc.ccc_last_launch_count()
+            if ev:
+                ev[1].record(stream)
+            return
         if sparse:
             ccc.ccc_expand_sparse(packed, n_f, ccc.GAMMA, (N, s, cnt, w))
         else:
@@ -231,12 +246,12 @@ def run_2way_single(args, wl):
     comps = comparisons(2, n_v, n_f)
     res = {
         "ms": ms, "kernel_ms": k_ms, "comparisons": comps, "launches": launches[0],
-        "clocks": clk.summary(), "kernel": "tally2_kernel",
+        "clocks": clk.summary(), "kernel": "popc_tally2_kernel" if popcount else "tally2_kernel",
         "out_bytes": m * 48,
     }
     del T, C
     torch.cuda.empty_cache()
-    if args.e2e and not sparse:
+    if args.e2e and not sparse and not popcount:
         res["e2e"] = run_2way_e2e(args, wl, codes)
     return res
 
@@ -393,6 +408,18 @@ def main():
     hbm_write = r["out_bytes"] / (ms_step / 1e3) / 1e9
     roof["out_write_GBps"] = hbm_write
     roof["out_write_frac_of_hbm"] = hbm_write / pk["hbm_gbs"]
+    if wl.get("popcount"):
+        # CUDA-core path: 2 POPC per 16 comparisons; peak = 148 SMs x 16 POPC/clk (the
+        # CUDA C throughput table's population-count rate) x the sampled SM clock
+        mhz = (r["clocks"].get("sm_mhz") or pk.get("sm_max_mhz", 1965.0))
+        popc = 2.0 * r["comparisons"] / 16.0
+        roof = {"bound": "alu", "achieved": popc / k_s / 1e12,
+                "peak": 148 * 16 * mhz * 1e6 / 1e12, "unit": "TPOPC/s",
+                "traffic": ncu_traffic(r["kernel"]), "kernel": r["kernel"],
+                "kernel_ms": r["kernel_ms"],
+                "peak_source": "148 SMs x 16 POPC/clk/SM x sampled SM clock (DESIGN.md §6)",
+                "tensor_path_equiv_frac_of_int8_peak": 2.0 * r["comparisons"] / k_s / 1e12 / int8_peak}
+        roof["frac"] = roof["achieved"] / roof["peak"]
     if wl["way"] == 3:
         roof["bound"] = "hbm"
         roof["achieved"] = r["out_bytes"] / wl["n_st"] / k_s / 1e9
@@ -404,7 +431,8 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int8",
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32 (bitwise AND + popcount)" if wl.get("popcount") else "int8",
         "data": "synthetic",
         "config": {"workload": wl["label"], "n_v": wl["n_v"], "n_f": wl["n_f"],
                    "input": ("type-3 sparse HWE codes, seed 4, missing marker (1,0) with "

@@ -163,6 +163,19 @@ ccc_status ccc_2way(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double ga
                     uint32_t out_flags, uint32_t* tallies_d, void* ccc_d, uint64_t* checksum_d,
                     void* ws_d, size_t ws_bytes, const ccc_compact* compact, void* stream);
 
+/* The paper's own 2-way tally method on CUDA cores (§3.1
+ * mGEMM2): the same problem and outputs as ccc_2way, computed from the
+ * packed 2-bit rows with bitwise AND + population count instead of tensor-core MACs,
+ *   G_ij = sum_w popc(x & y) + popc((xs & y) | ((x & ys) << 1)),  xs = (x >> 1) & 0x55..,
+ * then the Eq.2-3 epilogue of ccc_2way (general-gamma form: CCC = T * (w_i(a)/(4n_f)) *
+ * w_j(b) with w from Eq.1).  An on-device comparison baseline, not the product path.
+ * packed_d as produced by ccc_pack; ws_d >= ccc_workspace_bytes(2, n_v, n_f) bytes,
+ * 256-B aligned (only the s / w part is used); other arguments and errors as ccc_2way
+ * (no compaction). */
+ccc_status ccc_2way_popcount(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
+                             uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
+                             uint64_t* checksum_d, void* ws_d, size_t ws_bytes, void* stream);
+
 /* One block of the block-circulant 2-way decomposition (§4; §8(e)):
  * rows [a_lo, a_hi) of block A (expanded N_a / s_a / w_a, n_a rows, global index of
  * its row 0 = a_row0) against all n_b rows of block B (global row0 b_row0).

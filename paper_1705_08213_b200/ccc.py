@@ -103,6 +103,7 @@ _SIGS = {
     "ccc_pack": (_int, [_vp, _i64, _i64, _vp, _vp]),
     "ccc_expand": (_int, [_vp, _i64, _i64, _dbl, _vp, _vp, _vp, _vp]),
     "ccc_2way": (_int, [_vp, _i64, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _sz, _vp, _vp]),
+    "ccc_2way_popcount": (_int, [_vp, _i64, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "ccc_2way_block": (_int, [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _i64, _i64,
                               _int, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "ccc_3way_prepare": (_int, [_vp, _i64, _i64, _dbl, _vp, _sz, _vp]),
@@ -296,6 +297,21 @@ def ccc_2way(packed: torch.Tensor, n_f: int, gamma: float = GAMMA,
     _check(lib().ccc_2way(_p(packed), n_v, n_f, gamma, out_flags, _p(tallies), _p(ccc),
                           _p(checksum), _p(ws), ws.numel(), cp, _stream(stream)))
     return tallies, ccc, checksum
+
+
+def ccc_2way_popcount(packed: torch.Tensor, n_f: int, gamma: float = GAMMA,
+                      out_flags: int = OUT_TALLY | OUT_CCC_F64, tallies=None, ccc=None, checksum=None,
+                      ws=None, stream=None):
+    """The paper's popcount tally (mGEMM2 idea) on CUDA cores: a comparison
+    baseline with the outputs of ccc_2way."""
+    n_v = packed.shape[0]
+    dev = packed.device
+    T, C, ck = _outputs(ccc_num_unique(2, n_v), 4, out_flags, dev, tallies, ccc, checksum)
+    if ws is None:
+        ws = workspace(2, n_v, n_f, dev)
+    _check(lib().ccc_2way_popcount(_p(packed), n_v, n_f, gamma, out_flags, _p(T), _p(C),
+                                   _p(ck), _p(ws), ws.numel(), _stream(stream)))
+    return T, C, ck
 
 
 def ccc_2way_block(N_a, s_a, w_a, a_row0, a_lo, a_hi, N_b, s_b, w_b, b_row0, diag: bool, n_f,

@@ -408,6 +408,31 @@ ccc_status ccc_2way(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double ga
     return CCC_OK;
 }
 
+ccc_status ccc_2way_popcount(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
+                             uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
+                             uint64_t* checksum_d, void* ws_d, size_t ws_bytes, void* stream) {
+    g_launches = 0;
+    CCC_CHECK(check_sizes(n_v, n_f));
+    if (out_flags & ~15u) return fail(CCC_ERR_INVALID_ARGUMENT, "unknown out_flags bits");
+    if (n_v < 2) return CCC_OK;
+    CCC_CHECK(check_outputs(out_flags, tallies_d, ccc_d, checksum_d));
+    if (!packed_d || !aligned(packed_d, 16))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "packed_d must be non-NULL and 16-B aligned");
+    const WsLayout L = ws_layout(2, n_v, n_f);
+    if (!ws_d || !aligned(ws_d, 256)) return fail(CCC_ERR_INVALID_ARGUMENT, "ws_d must be 256-B aligned");
+    if (ws_bytes < L.total) return fail(CCC_ERR_WORKSPACE, "workspace too small (see ccc_workspace_bytes)");
+    int sms;
+    CCC_CHECK(check_device(&sms));
+    uint8_t* ws = static_cast<uint8_t*>(ws_d);
+    CCC_CUDA(ccc::launch_popc_2way(packed_d, n_v, n_f, gamma, out_flags, tallies_d, ccc_d,
+                                   reinterpret_cast<unsigned long long*>(checksum_d),
+                                   reinterpret_cast<int32_t*>(ws + L.s), reinterpret_cast<double*>(ws + L.w),
+                                   sms, (cudaStream_t)stream),
+             "popcount launch");
+    g_launches = 2;
+    return CCC_OK;
+}
+
 ccc_status ccc_3way_prepare(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
                             void* ws_d, size_t ws_bytes, void* stream) {
     g_launches = 0;

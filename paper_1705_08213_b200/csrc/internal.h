@@ -21,4 +21,8 @@ cudaError_t launch_tally2(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
 cudaError_t launch_tally3(const CUtensorMap& tmA, const CUtensorMap& tmB, const Tally3Args& a,
                           int num_sms, cudaStream_t stream, int64_t* n_units_out);
 
+cudaError_t launch_popc_2way(const uint8_t* packed, int64_t n_v, int64_t n_f, double gamma, uint32_t flags,
+                             uint32_t* tallies, void* ccc, unsigned long long* checksum, int32_t* s,
+                             double* w, int num_sms, cudaStream_t stream);
+
 }  // namespace ccc

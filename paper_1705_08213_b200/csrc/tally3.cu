@@ -510,6 +510,10 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             };
             uint32_t gnext[2][2] = {{0u, 0u}, {0u, 0u}};
             if (c_end > 0) load_gmn(0, gnext);
+#ifdef CCC_G2AHEAD
+            uint32_t gnext2[2][2] = {{0u, 0u}, {0u, 0u}};
+            if (c_end > 1) load_gmn(1, gnext2);
+#endif
             named_bar_sync(1, 32 * kEpiWarps3);   // column table of this unit is complete
             mbar_wait_sleep(&tfull[acc], acc_phase);
             tc_fence_after();
@@ -521,10 +525,17 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 tmem_ld_wait_keep(vnext);
                 const uint32_t va[4] = {vnext[0], vnext[1], vnext[2], vnext[3]};
                 const uint32_t gcur[2][2] = {{gnext[0][0], gnext[0][1]}, {gnext[1][0], gnext[1][1]}};
+#ifdef CCC_G2AHEAD
+                if (c + 1 < c_end) tmem_ld_16x256(taddr + (c + 1) * 8, vnext);
+#pragma unroll
+                for (int x = 0; x < 4; ++x) gnext[x >> 1][x & 1] = gnext2[x >> 1][x & 1];
+                if (c + 2 < c_end) load_gmn(c + 2, gnext2);
+#else
                 if (c + 1 < c_end) {
                     tmem_ld_16x256(taddr + (c + 1) * 8, vnext);
                     load_gmn(c + 1, gnext);
                 }
+#endif
                 const int32_t nA = c * 8 + (int32_t)cpair;    // local column of h = 0
                 const ColT3 cA = ct[nA], cB = ct[nA + 1];
 #pragma unroll
