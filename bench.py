@@ -1,7 +1,7 @@
 """bench.py -- CCC comparisons/s of the B200 hot path.
 
 python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                [--workload c2|c4|c1|c2s|c2pop] [--no-e2e] [--no-cpu]
+                [--workload c2|c4|c1|c2s|c2pop|c2fs] [--no-e2e] [--no-cpu]
 
 One step = one pass of the whole hot path over one synthetic batch resident in HBM:
   2-way (default, BASELINE configs[1] = C2: 20,000 vectors x 50,000 individuals):
@@ -12,6 +12,9 @@ One step = one pass of the whole hot path over one synthetic batch resident in H
       ccc_pack -> ccc_expand_sparse -> ccc_2way_sparse_block
   popcount baseline (--workload c2pop: C2 through ccc_2way_popcount, the paper's
       AND + popcount tally on CUDA cores): ccc_pack -> ccc_2way_popcount
+  field split (--workload c2fs: C2 split into 4 field slices, all slices
+      on one GPU): per slice ccc_pack -> ccc_expand -> ccc_2way_fs_export (tally GEMM whose
+      epilogue stores partial tiles into the owners' slots), then per owner ccc_2way_fs_finish
 At N > 1 (torchrun), the 2-way path runs the block-circulant decomposition with the
 packed vector blocks passed round a ring over NCCL send/recv; per-GPU load is kept at
 C2's (weak scaling: n_v = 20,000 * sqrt(N)).
@@ -42,6 +45,9 @@ WORKLOADS = {
     "c2pop": dict(way=2, n_v=20000, n_f=50000, popcount=True,
                   label="2-way CCC, 20,000 x 50,000, the paper's popcount tally on CUDA cores "
                         "(SURVEY f4 baseline)"),
+    "c2fs": dict(way=2, n_v=20000, n_f=50000, fieldsplit=4,
+                 label="2-way CCC, 20,000 x 50,000, field-axis split into 4 slices (SURVEY f3), "
+                       "all slices simulated on one GPU"),
     "c4": dict(way=3, n_v=4096, n_f=16384, n_st=16,
                label="3-way CCC, 4,096 SNP vectors x 16,384 individuals, 16 stages (configs[3])"),
 }
@@ -311,6 +317,78 @@ def run_2way_e2e(args, wl, codes_dev):
             "api": "ccc_2way_host (pinned host codes in, pinned host tallies+fp64 CCC out)"}
 
 
+def run_fieldsplit_single(args, wl):
+    """f3 on one GPU: the slices' export GEMMs and the owners' reduce + epilogue."""
+    import torch
+
+    import synthgen
+    from paper_1705_08213_b200 import ccc, fieldsplit
+    n_v, n_f, P = wl["n_v"], wl["n_f"], wl["fieldsplit"]
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    flags = ccc.OUT_TALLY | ccc.OUT_CCC_F64
+    codes = synthgen.random_codes(n_v, n_f, seed=1, device=dev)
+    sl = fieldsplit.field_slices(n_f, P)
+    cs = [codes[:, a:b].contiguous() for a, b in sl]
+    del codes
+    packed = [torch.empty((n_v, ccc.ccc_packed_stride(b - a)), dtype=torch.uint8, device=dev) for a, b in sl]
+    Ns = [(torch.empty((n_v, ccc.ccc_k_pad(b - a)), dtype=torch.int8, device=dev),
+           torch.empty(n_v, dtype=torch.int32, device=dev),
+           torch.empty((n_v, 2), dtype=torch.float64, device=dev)) for a, b in sl]
+    total = ccc.ccc_2way_fs_tiles(n_v)
+    nbytes = ccc.ccc_2way_fs_slot_bytes(P, 0, total)
+    slots = [torch.empty(nbytes // 4, dtype=torch.int32, device=dev) for _ in range(P)]
+    ptrs = torch.tensor([t.data_ptr() for t in slots], dtype=torch.int64, device=dev)
+    m = ccc.ccc_num_unique(2, n_v)
+    T = torch.empty((m, 4), dtype=torch.int32, device=dev)
+    C = torch.empty((m, 4), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+    launches = [0]
+
+    def step(ev=None):
+        for r, (a, b) in enumerate(sl):
+            ccc.ccc_pack(cs[r], packed[r])
+            launches[0] += ccc.ccc_last_launch_count()
+            N, s, w = Ns[r]
+            ccc.ccc_expand(packed[r], b - a, ccc.GAMMA, N, s, w)
+            launches[0] += ccc.ccc_last_launch_count()
+        s_full = Ns[0][1].clone()
+        for r in range(1, P):
+            s_full += Ns[r][1]                 # the s all-reduce of the multi-GPU run
+        if ev:
+            ev[0].record(stream)
+        for r, (a, b) in enumerate(sl):
+            ccc.ccc_2way_fs_export(Ns[r][0], Ns[r][1], b - a, ptrs, r, P, 0, total)
+            launches[0] += ccc.ccc_last_launch_count()
+        if ev:
+            ev[1].record(stream)
+        for r in range(P):
+            ccc.ccc_2way_fs_finish(slots[r], s_full, n_f, r, P, 0, total, flags, T, C)
+            launches[0] += ccc.ccc_last_launch_count()
+        if ev:
+            ev[2].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches[0] = 0
+    kev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for k in range(args.steps):
+            step(kev[k])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    k_ms = sum(e[0].elapsed_time(e[1]) for e in kev) / args.steps
+    f_ms = sum(e[1].elapsed_time(e[2]) for e in kev) / args.steps
+    return {"ms": ms, "kernel_ms": k_ms, "finish_ms": f_ms, "comparisons": comparisons(2, n_v, n_f),
+            "launches": launches[0], "clocks": clk.summary(), "kernel": "tally2_kernel",
+            "out_bytes": m * 48, "slot_bytes_per_pair_in": 4 * P}
+
+
 def run_3way_single(args, wl):
     import torch
 
@@ -409,7 +487,9 @@ def main():
         return dist.bench_main(args, wl, METRIC, UNIT)
 
     pk, pk_kind = peaks()
-    if wl["way"] == 2:
+    if wl.get("fieldsplit"):
+        r = run_fieldsplit_single(args, wl)
+    elif wl["way"] == 2:
         r = run_2way_single(args, wl)
     else:
         r = run_3way_single(args, wl)
@@ -436,6 +516,13 @@ def main():
     hbm_write = r["out_bytes"] / (ms_step / 1e3) / 1e9
     roof["out_write_GBps"] = hbm_write
     roof["out_write_frac_of_hbm"] = hbm_write / pk["hbm_gbs"]
+    if wl.get("fieldsplit"):
+        # the export GEMMs of all slices (tensor) + the owners' reduce/epilogue (HBM)
+        pairs = r["comparisons"] / wl["n_f"]
+        roof["kernel_ms"] = r["kernel_ms"]
+        roof["finish_ms"] = r["finish_ms"]
+        roof["finish_GBps"] = pairs * (r["slot_bytes_per_pair_in"] + 48) / (r["finish_ms"] / 1e3) / 1e9
+        roof["finish_frac_of_hbm"] = roof["finish_GBps"] / pk["hbm_gbs"]
     if wl.get("popcount"):
         # CUDA-core path: 2 POPC per 16 comparisons; peak = 148 SMs x 16 POPC/clk (the
         # CUDA C throughput table's population-count rate) x the sampled SM clock

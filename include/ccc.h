@@ -176,6 +176,46 @@ ccc_status ccc_2way_popcount(const uint8_t* packed_d, int64_t n_v, int64_t n_f, 
                              uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
                              uint64_t* checksum_d, void* ws_d, size_t ws_bytes, void* stream);
 
+/* ---- f3: field-axis split with the reduce-scatter fused onto the GEMM (
+ * PAPER.md §4: n_pf > 1 processors share the fields of every vector).
+ * `world` ranks each hold all n_v vectors over a slice of the fields (any split; each
+ * slice is packed / expanded on its own with its own n_f_slice).  Per wave of tiles
+ * [t_lo, t_hi) of the 2-way schedule (0 <= t_lo <= t_hi <= ccc_2way_fs_tiles(n_v)):
+ *   1. every rank: ccc_2way_fs_export -- the tcgen05 tally GEMM of its slice; each
+ *      partial tile G_f = N_f N_f^T is stored by the GEMM epilogue straight into the
+ *      slot buffer of the tile's owner (owner(t) = t mod world), i.e. over NVLink when
+ *      slots_d[owner] is a peer mapping (ccc_ipc_*), overlapped with later tiles;
+ *   2. a stream-ordered barrier across ranks (the caller's, e.g. an NCCL all-reduce);
+ *   3. every rank r: ccc_2way_fs_finish -- sums the `world` partials of its own tiles
+ *      (exact int32) and writes their records exactly as ccc_2way (Eq.2-3), with the
+ *      full allele sums s_d (the caller sums the slices' s, e.g. all-reduce) and the full
+ *      n_f; general-gamma CCC form, w(a) = 1 - gamma S(a)/(2 n_f) computed inline.
+ * Slot buffer of one owner: ccc_2way_fs_slot_bytes(world, t_lo, t_hi) bytes (int32
+ * [owned tiles][world][256][256]); slots_d: DEVICE array of `world` device pointers (the
+ * owners' buffers as this rank sees them).  A slot buffer may be reused by a later wave
+ * once every owner's finish of the earlier wave is ordered before the new exports.
+ * Records of a rank's own tiles only are written (tallies/ccc/checksum as ccc_2way;
+ * per-rank checksums add up mod 2^128 to ccc_2way's). */
+#define CCC_IPC_HANDLE_BYTES 64
+int64_t    ccc_2way_fs_tiles(int64_t n_v);
+size_t     ccc_2way_fs_slot_bytes(int world, int64_t t_lo, int64_t t_hi);
+ccc_status ccc_2way_fs_export(const int8_t* N_d, const int32_t* s_d, int64_t n_v, int64_t n_f_slice,
+                              int32_t* const* slots_d, int rank, int world, int64_t t_lo, int64_t t_hi,
+                              void* stream);
+ccc_status ccc_2way_fs_finish(const int32_t* slots_d, const int32_t* s_d, int64_t n_v, int64_t n_f,
+                              double gamma, int rank, int world, int64_t t_lo, int64_t t_hi,
+                              uint32_t out_flags, uint32_t* tallies_d, void* ccc_d, uint64_t* checksum_d,
+                              void* stream);
+/* Peer-shareable device buffers for the slots (one process per GPU): cudaMalloc'd here
+ * (a CUDA IPC handle must name a whole allocation; these are the only buffers the
+ * library allocates, and only on request), exported as a CCC_IPC_HANDLE_BYTES handle,
+ * opened in a peer process (peer access enabled lazily), closed / freed by the caller. */
+ccc_status ccc_ipc_malloc(size_t bytes, void** dptr);
+ccc_status ccc_ipc_free(void* dptr);
+ccc_status ccc_ipc_get_handle(void* dptr, void* handle);
+ccc_status ccc_ipc_open(const void* handle, void** dptr);
+ccc_status ccc_ipc_close(void* dptr);
+
 /* One block of the block-circulant 2-way decomposition (§4; §8(e)):
  * rows [a_lo, a_hi) of block A (expanded N_a / s_a / w_a, n_a rows, global index of
  * its row 0 = a_row0) against all n_b rows of block B (global row0 b_row0).

@@ -104,6 +104,16 @@ _SIGS = {
     "ccc_expand": (_int, [_vp, _i64, _i64, _dbl, _vp, _vp, _vp, _vp]),
     "ccc_2way": (_int, [_vp, _i64, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _sz, _vp, _vp]),
     "ccc_2way_popcount": (_int, [_vp, _i64, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "ccc_2way_fs_tiles": (_i64, [_i64]),
+    "ccc_2way_fs_slot_bytes": (_sz, [_int, _i64, _i64]),
+    "ccc_2way_fs_export": (_int, [_vp, _vp, _i64, _i64, _vp, _int, _int, _i64, _i64, _vp]),
+    "ccc_2way_fs_finish": (_int, [_vp, _vp, _i64, _i64, _dbl, _int, _int, _i64, _i64, _u32, _vp, _vp,
+                                  _vp, _vp]),
+    "ccc_ipc_malloc": (_int, [_sz, _vp]),
+    "ccc_ipc_free": (_int, [_vp]),
+    "ccc_ipc_get_handle": (_int, [_vp, _vp]),
+    "ccc_ipc_open": (_int, [_vp, _vp]),
+    "ccc_ipc_close": (_int, [_vp]),
     "ccc_2way_block": (_int, [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _i64, _i64,
                               _int, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "ccc_3way_prepare": (_int, [_vp, _i64, _i64, _dbl, _vp, _sz, _vp]),
@@ -312,6 +322,65 @@ def ccc_2way_popcount(packed: torch.Tensor, n_f: int, gamma: float = GAMMA,
     _check(lib().ccc_2way_popcount(_p(packed), n_v, n_f, gamma, out_flags, _p(T), _p(C),
                                    _p(ck), _p(ws), ws.numel(), _stream(stream)))
     return T, C, ck
+
+
+# ------------------------------------------------------------- f3: field-axis split
+def ccc_2way_fs_tiles(n_v: int) -> int:
+    return lib().ccc_2way_fs_tiles(n_v)
+
+
+def ccc_2way_fs_slot_bytes(world: int, t_lo: int, t_hi: int) -> int:
+    return lib().ccc_2way_fs_slot_bytes(world, t_lo, t_hi)
+
+
+def ccc_2way_fs_export(N, s, n_f_slice: int, slot_ptrs: torch.Tensor, rank: int, world: int,
+                       t_lo: int, t_hi: int, stream=None):
+    """GEMM of this field slice; partial tiles go to the owners' slots (slot_ptrs: int64
+    device tensor of `world` device addresses)."""
+    _dev(N, torch.int8, "N")
+    _check(lib().ccc_2way_fs_export(_p(N), _p(s), N.shape[0], n_f_slice, _p(slot_ptrs), rank, world,
+                                    t_lo, t_hi, _stream(stream)))
+
+
+def ccc_2way_fs_finish(slots: torch.Tensor, s, n_f: int, rank: int, world: int, t_lo: int, t_hi: int,
+                       out_flags: int, tallies=None, ccc=None, checksum=None, gamma: float = GAMMA,
+                       stream=None):
+    """Reduce this owner's partial tiles and write their records (ccc_2way layout)."""
+    n_v = s.shape[0]
+    T, C, ck = _outputs(ccc_num_unique(2, n_v), 4, out_flags, s.device, tallies, ccc, checksum)
+    _check(lib().ccc_2way_fs_finish(_p(slots), _p(s), n_v, n_f, gamma, rank, world, t_lo, t_hi,
+                                    out_flags, _p(T), _p(C), _p(ck), _stream(stream)))
+    return T, C, ck
+
+
+class IpcBuffer:
+    """A peer-shareable device buffer (ccc_ipc_malloc) with its CUDA IPC handle."""
+
+    def __init__(self, nbytes: int):
+        p = ctypes.c_void_p()
+        _check(lib().ccc_ipc_malloc(nbytes, ctypes.byref(p)))
+        self.ptr = p.value
+        self.nbytes = nbytes
+
+    def handle(self) -> bytes:
+        h = ctypes.create_string_buffer(64)
+        _check(lib().ccc_ipc_get_handle(self.ptr, h))
+        return h.raw
+
+    def free(self):
+        if self.ptr:
+            _check(lib().ccc_ipc_free(self.ptr))
+            self.ptr = None
+
+
+def ipc_open(handle: bytes) -> int:
+    p = ctypes.c_void_p()
+    _check(lib().ccc_ipc_open(ctypes.create_string_buffer(handle, 64), ctypes.byref(p)))
+    return p.value
+
+
+def ipc_close(ptr: int):
+    _check(lib().ccc_ipc_close(ptr))
 
 
 def ccc_2way_block(N_a, s_a, w_a, a_row0, a_lo, a_hi, N_b, s_b, w_b, b_row0, diag: bool, n_f,

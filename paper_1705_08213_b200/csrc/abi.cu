@@ -433,6 +433,105 @@ ccc_status ccc_2way_popcount(const uint8_t* packed_d, int64_t n_v, int64_t n_f, 
     return CCC_OK;
 }
 
+// ---------------------------------------------------------------- f3: field split
+int64_t ccc_2way_fs_tiles(int64_t n_v) { return n_v < 2 ? 0 : ccc::fs_total_tiles(n_v); }
+
+size_t ccc_2way_fs_slot_bytes(int world, int64_t t_lo, int64_t t_hi) {
+    if (world < 1 || t_hi <= t_lo) return 0;
+    const int64_t owned = (t_hi - t_lo + world - 1) / world;
+    return (size_t)owned * (size_t)world * 65536u * sizeof(int32_t);
+}
+
+ccc_status ccc_2way_fs_export(const int8_t* N_d, const int32_t* s_d, int64_t n_v, int64_t n_f_slice,
+                              int32_t* const* slots_d, int rank, int world, int64_t t_lo, int64_t t_hi,
+                              void* stream) {
+    g_launches = 0;
+    CCC_CHECK(check_sizes(n_v, n_f_slice));
+    if (world < 1 || rank < 0 || rank >= world) return fail(CCC_ERR_INVALID_ARGUMENT, "need 0 <= rank < world");
+    if (t_lo < 0 || t_hi < t_lo) return fail(CCC_ERR_INVALID_ARGUMENT, "need 0 <= t_lo <= t_hi");
+    if (n_v < 2 || t_hi == t_lo) return CCC_OK;
+    if (!N_d || !aligned(N_d, 128) || !s_d || !slots_d)
+        return fail(CCC_ERR_INVALID_ARGUMENT, "N_d (128-B aligned), s_d and slots_d must be non-NULL");
+    int sms;
+    CCC_CHECK(check_device(&sms));
+    const int64_t k_pad = kpad_of(n_f_slice);
+    CUtensorMap tmA, tmB;
+    CCC_CHECK(make_tmap(&tmA, N_d, n_v, k_pad, ccc::kBM));
+    CCC_CHECK(make_tmap(&tmB, N_d, n_v, k_pad, (uint32_t)ccc::tally2_b_box_rows()));
+    ccc::Tally2Args a{};
+    a.a_lo = 0;
+    a.nA = a.nB = n_v;
+    a.diag = 1;
+    a.n_f = (int32_t)n_f_slice;
+    a.k_blocks = (int32_t)(k_pad / ccc::kBK);
+    a.out_flags = 0;
+    a.exact23 = 1;          // the per-row setup then reads s only (no w)
+    a.s_a = a.s_b = s_d;
+    a.sup_rows = a.sup_cols = 2048;   // the schedule ccc_2way_fs_finish walks
+    a.t_lo = t_lo;
+    a.t_hi = t_hi;
+    a.xp_ptrs = slots_d;
+    a.xp_rank = rank;
+    a.xp_world = world;
+    int64_t tiles = 0;
+    CCC_CUDA(ccc::launch_tally2(tmA, tmB, a, sms, (cudaStream_t)stream, &tiles), "fs export launch");
+    if (tiles) ++g_launches;
+    return CCC_OK;
+}
+
+ccc_status ccc_2way_fs_finish(const int32_t* slots_d, const int32_t* s_d, int64_t n_v, int64_t n_f,
+                              double gamma, int rank, int world, int64_t t_lo, int64_t t_hi,
+                              uint32_t out_flags, uint32_t* tallies_d, void* ccc_d, uint64_t* checksum_d,
+                              void* stream) {
+    g_launches = 0;
+    CCC_CHECK(check_sizes(n_v, n_f));
+    if (out_flags & ~15u) return fail(CCC_ERR_INVALID_ARGUMENT, "unknown out_flags bits");
+    if (world < 1 || rank < 0 || rank >= world) return fail(CCC_ERR_INVALID_ARGUMENT, "need 0 <= rank < world");
+    if (t_lo < 0 || t_hi < t_lo) return fail(CCC_ERR_INVALID_ARGUMENT, "need 0 <= t_lo <= t_hi");
+    if (n_v < 2 || t_hi == t_lo) return CCC_OK;
+    CCC_CHECK(check_outputs(out_flags, tallies_d, ccc_d, checksum_d));
+    if (!slots_d || !s_d) return fail(CCC_ERR_INVALID_ARGUMENT, "slots_d and s_d must be non-NULL");
+    int sms;
+    CCC_CHECK(check_device(&sms));
+    CCC_CUDA(ccc::launch_fs_finish(slots_d, s_d, n_v, n_f, gamma, rank, world, t_lo, t_hi, out_flags,
+                                   tallies_d, ccc_d, reinterpret_cast<unsigned long long*>(checksum_d),
+                                   sms, (cudaStream_t)stream),
+             "fs finish launch");
+    ++g_launches;
+    return CCC_OK;
+}
+
+ccc_status ccc_ipc_malloc(size_t bytes, void** dptr) {
+    if (!dptr || bytes == 0) return fail(CCC_ERR_INVALID_ARGUMENT, "dptr non-NULL, bytes > 0");
+    CCC_CUDA(cudaMalloc(dptr, bytes), "cudaMalloc (ipc buffer)");
+    return CCC_OK;
+}
+
+ccc_status ccc_ipc_free(void* dptr) {
+    CCC_CUDA(cudaFree(dptr), "cudaFree (ipc buffer)");
+    return CCC_OK;
+}
+
+ccc_status ccc_ipc_get_handle(void* dptr, void* handle) {
+    if (!dptr || !handle) return fail(CCC_ERR_INVALID_ARGUMENT, "dptr and handle must be non-NULL");
+    static_assert(sizeof(cudaIpcMemHandle_t) == CCC_IPC_HANDLE_BYTES, "ipc handle size");
+    CCC_CUDA(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle), dptr), "cudaIpcGetMemHandle");
+    return CCC_OK;
+}
+
+ccc_status ccc_ipc_open(const void* handle, void** dptr) {
+    if (!dptr || !handle) return fail(CCC_ERR_INVALID_ARGUMENT, "dptr and handle must be non-NULL");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    CCC_CUDA(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    return CCC_OK;
+}
+
+ccc_status ccc_ipc_close(void* dptr) {
+    CCC_CUDA(cudaIpcCloseMemHandle(dptr), "cudaIpcCloseMemHandle");
+    return CCC_OK;
+}
+
 ccc_status ccc_3way_prepare(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
                             void* ws_d, size_t ws_bytes, void* stream) {
     g_launches = 0;

@@ -154,6 +154,10 @@ struct Tally2Args {
     const int32_t* c_a;          // present-entry counts c_i
     const int32_t* c_b;
     unsigned long long* trace; // optional per-tile %globaltimer trace (diagnostics)
+    // f3 field split: schedule range and partial-G export (no records are written)
+    int64_t t_lo, t_hi;          // tiles [t_lo, t_hi) of the schedule; t_hi = 0: all
+    int32_t* const* xp_ptrs;     // [xp_world] owner slot buffers (device-visible), or NULL
+    int32_t xp_rank, xp_world;   // this field slice; number of slices (= owners)
 };
 
 // One vector block as seen by the 3-way kernel.

@@ -108,7 +108,8 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t rank = kPair == 2 ? cluster_ctarank() : 0u;  // 0 = leader CTA
-    const int64_t unit0 = blockIdx.x / kPair, units = gridDim.x / kPair;
+    // tiles [t_lo, t_hi) of the schedule (t_hi = 0: all); f3 field-split waves use a range
+    const int64_t unit0 = args.t_lo + blockIdx.x / kPair, units = gridDim.x / kPair;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
@@ -143,7 +144,7 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             const uint64_t pol = policy_evict_last();
             for (int64_t t = unit0;; t += units) {
                 int32_t bm, bn;
-                if (!sch.get(t, bm, bn)) break;
+                if ((args.t_hi > 0 && t >= args.t_hi) || !sch.get(t, bm, bn)) break;
                 const int32_t arow = (int32_t)(args.a_lo + (int64_t)bm * C::kTileM + rank * 128);
                 const int32_t brow = (int32_t)sch.b_lo + bn * kBN + (int32_t)rank * C::kBRows;
                 if (args.trace && rank == 0) args.trace[8 * t + 6] = globaltimer();
@@ -180,7 +181,7 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             const uint32_t a0 = smem_u32(smA), b0 = smem_u32(smB);
             for (int64_t t = unit0;; t += units) {
                 int32_t bm, bn;
-                if (!sch.get(t, bm, bn)) break;
+                if ((args.t_hi > 0 && t >= args.t_hi) || !sch.get(t, bm, bn)) break;
                 unsigned long long* tr = args.trace ? args.trace + 8 * t : nullptr;
                 if (tr) tr[0] = globaltimer();
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -230,7 +231,7 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         uint32_t acc = 0, acc_phase = 0;
         for (int64_t t = unit0;; t += units) {
             int32_t bm, bn;
-            if (!sch.get(t, bm, bn)) break;
+            if ((args.t_hi > 0 && t >= args.t_hi) || !sch.get(t, bm, bn)) break;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int64_t xrow = args.a_lo + (int64_t)bm * C::kTileM + rank * 128 + quad * 32;
@@ -323,7 +324,7 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         uint32_t acc = 0, acc_phase = 0;
         for (int64_t t = unit0;; t += units) {
             int32_t bm, bn;
-            if (!sch.get(t, bm, bn)) break;
+            if ((args.t_hi > 0 && t >= args.t_hi) || !sch.get(t, bm, bn)) break;
             unsigned long long* tr = (args.trace && warp == 2 && rank == 0) ? args.trace + 8 * t : nullptr;
             if (tr && lane == 0) tr[3] = globaltimer();
             mbar_wait(&tfull[acc], acc_phase);
@@ -391,6 +392,19 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     const uint32_t gB = (r >> 1) ? vb[(r & 1) * 2 + 1] : va[(r & 1) * 2 + 1];
                     const bool okA = jA >= jlo_r[r] && jA < jhi_r[r];
                     const bool okB = jB >= jlo_r[r] && jB < jhi_r[r];
+                    if (args.xp_ptrs && (okA | okB)) {
+                        // f3 field split: this field slice's partial G of the tile goes
+                        // straight to the owner's slot (a peer-mapped pointer over NVLink
+                        // on a multi-GPU run), overlapped with the MMAs of later tiles
+                        const int64_t world = args.xp_world;
+                        const int64_t slot = (t - args.t_lo) / world;
+                        int32_t* dst = args.xp_ptrs[t % world] + ((slot * world + args.xp_rank) << 16);
+                        const int32_t trow = (int32_t)(rank * 128 + quad * 32 + (r >> 1) * 16 + (r & 1) * 8 +
+                                                       (lane >> 2));
+                        const int32_t tcol = c * 8 + cpair;
+                        *reinterpret_cast<int2*>(dst + trow * kBN + tcol) = make_int2((int32_t)gA, (int32_t)gB);
+                        continue;
+                    }
                     if (!(okA | okB)) continue;
                     // Eq.2 tallies from G (rho(0) = 2 - rho(1))
                     const uint32_t a11 = gA, a10 = two_si[r] - gA, a01 = two_sA - gA;
@@ -536,7 +550,9 @@ cudaError_t launch_tally2(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
     }
     sch.init(a.a_lo, a.nA, a.nB, a.diag, (pm == 2 || a.sparse) ? Cfg2<2>::kTileM : Cfg2<1>::kTileM,
              a2.sup_rows, a2.sup_cols);
-    const int64_t tiles = sch.total();
+    const int64_t all_tiles = sch.total();
+    const int64_t t_end = (a.t_hi > 0 && a.t_hi < all_tiles) ? a.t_hi : all_tiles;
+    const int64_t tiles = t_end > a.t_lo ? t_end - a.t_lo : 0;   // f3 waves: a range
     if (n_tiles_out) *n_tiles_out = tiles;
     if (tiles == 0) return cudaSuccess;
     if (pm == 1 && !a.sparse) {
