@@ -16,7 +16,8 @@ PROF = os.path.join(ROOT, "profiles")
 
 
 def short(name):
-    for k in ("tally2_kernel", "tally3_kernel", "pack_kernel", "expand_kernel"):
+    for k in ("popc_tally2_kernel", "popc_stats_kernel", "fs_finish_kernel", "tally2_kernel",
+              "tally3_kernel", "pack_kernel", "expand_kernel"):
         if k in name:
             return k
     return name.split("(")[0][:60]
@@ -40,7 +41,8 @@ def launches(path):
         k = short(r["Kernel Name"])
         agg[k][0] += 1
         agg[k][1] += ns
-    ours = {"tally2_kernel", "tally3_kernel", "pack_kernel", "expand_kernel"}
+    ours = {"tally2_kernel", "tally3_kernel", "pack_kernel", "expand_kernel", "popc_tally2_kernel",
+            "popc_stats_kernel", "fs_finish_kernel"}
     tot = sum(v[1] for k, v in agg.items() if k in ours)   # the step = our kernels only
     res = {k: {"launches": c, "total_ms": t / 1e6, "mean_ms": t / 1e6 / c, "share_of_step": t / tot}
            for k, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]) if k in ours}
@@ -86,11 +88,12 @@ def main():
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     summary = {}
-    for wl in ("c2", "c4"):
+    WLS = ("c2", "c4", "c2pop", "c2fs", "c2s")
+    for wl in WLS:
         p = os.path.join(OUT, f"launches_{wl}.csv")
         if os.path.exists(p):
             summary[f"launch_list_{wl}"] = launches(p)
-    for wl in ("c2", "c4"):
+    for wl in WLS:
         p = os.path.join(OUT, f"metrics_{wl}.csv")
         if os.path.exists(p):
             summary[f"metrics_{wl}"] = metrics(p)
@@ -110,7 +113,7 @@ def main():
         json.dump(summary, f, indent=1, sort_keys=True)
     with open(os.path.join(PROF, "ncu_summary.json"), "w") as f:
         json.dump(traffic, f, indent=1, sort_keys=True)
-    for wl in ("c2", "c4"):
+    for wl in WLS:
         p = os.path.join(OUT, f"launches_{wl}.csv")
         if os.path.exists(p):
             os.replace(p, os.path.join(PROF, f"r{a.round}_launches_{wl}.csv")) if False else \
