@@ -353,9 +353,10 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t mask) {
         : "memory");
 }
 
-// Output stores do not allocate in L1: the records are never re-read by the SM, and
-// allocating them competes with the operand traffic of the mainloop (measured: the 3-way
-// FULL stage went from 25.0 to 20.8 ms).
+// The predicated record stores of the 3-way epilogue (the _if forms below) do not allocate
+// in L1: the records are never re-read by the SM, and allocating them competes with the
+// operand traffic of the mainloop (measured: a C4 FULL stage went from 25.0 to 20.8 ms).
+// The 2-way kernel keeps plain stores (the hint raised its cold-L2 DRAM reads 14 -> 20 GB).
 #ifndef CCC_ST_HINT
 #define CCC_ST_HINT ".L1::no_allocate"
 #endif
@@ -391,7 +392,7 @@ __device__ __forceinline__ void stg_v4(void* p, uint4 v) {
 // 256-bit global stores (sm_100): 32-B aligned, one full L2 sector per thread.
 __device__ __forceinline__ void stg_256_u32(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
                                             uint32_t e, uint32_t f, uint32_t g, uint32_t h) {
-    asm volatile("st.global" CCC_ST_HINT ".v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a), "r"(b),
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a), "r"(b),
                  "r"(c), "r"(d), "r"(e), "r"(f), "r"(g), "r"(h)
                  : "memory");
 }
@@ -413,11 +414,11 @@ __device__ __forceinline__ void stg_256_f64_if(bool ok, void* p, double a, doubl
         : "memory");
 }
 __device__ __forceinline__ void stg_256_f64(void* p, double a, double b, double c, double d) {
-    asm volatile("st.global" CCC_ST_HINT ".v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
                  : "memory");
 }
 __device__ __forceinline__ void stg_128_u32(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-    asm volatile("st.global" CCC_ST_HINT ".v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
                  : "memory");
 }
 
