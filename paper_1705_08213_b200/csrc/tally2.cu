@@ -318,6 +318,8 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         const uint32_t four_nf = 4u * nf;
         const double inv4nf = 1.0 / (4.0 * (double)args.n_f);
         const bool exact23 = args.exact23 != 0;
+        // gamma = 2/3 and 12 n_f^2 < 2^52: the single-DFMA cell form below
+        const bool exact52 = exact23 && (uint64_t)12 * nf * nf < (1ull << 52);
         const uint32_t tempty_leader = kPair == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
         const int32_t cpair = 2 * (int32_t)(lane & 3);   // my 2 columns within a chunk
         unsigned long long ck_lo = 0, ck_hi = 0;
@@ -361,8 +363,12 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 const int32_t j0 = bn * kBN + c * 8;
                 if (!any_row || j0 >= nB || j0 + 8 <= warp_jlo) continue;  // warp-uniform
                 uint32_t va[4], vb[4];
+#ifdef CCC_D2_NOTMEMLD
+                for (int x = 0; x < 4; ++x) { va[x] = lane + x + c; vb[x] = lane * 3 + x; }   // diagnostics
+#else
                 tmem_ld_16x256(taddr + c * 8, va);                  // lanes +0..15
                 tmem_ld_16x256(taddr + (16u << 16) + c * 8, vb);    // lanes +16..31
+#endif
                 const int32_t jA = j0 + cpair, jB = jA + 1;
                 const int32_t jAc = jA < nB ? jA : (int32_t)nB - 1;
                 const int32_t jBc = jB < nB ? jB : (int32_t)nB - 1;
@@ -371,13 +377,22 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 // column factors: general gamma -> w_j(b); gamma = 2/3 -> U_j(b) / (36 n_f^3)
                 // with the integer U_j(0) = n_f + s_j, U_j(1) = 3 n_f - s_j
                 double wA0 = 0.0, wA1 = 0.0, wB0 = 0.0, wB1 = 0.0;
+                double mA0 = 0.0, mA1 = 0.0, mB0 = 0.0, mB1 = 0.0;
                 if (want_c || kCompact) {
+#ifdef CCC_D2_NOFP64
+                    if (false) {
+#else
                     if (exact23) {
+#endif
                         const uint32_t sAj = two_sA >> 1, sBj = two_sB >> 1;
-                        wA0 = (double)(nf + sAj) * args.inv_d;
-                        wA1 = (double)(3u * nf - sAj) * args.inv_d;
-                        wB0 = (double)(nf + sBj) * args.inv_d;
-                        wB1 = (double)(3u * nf - sBj) * args.inv_d;
+                        wA0 = u32_to_f64(nf + sAj) * args.inv_d;
+                        wA1 = u32_to_f64(3u * nf - sAj) * args.inv_d;
+                        wB0 = u32_to_f64(nf + sBj) * args.inv_d;
+                        wB1 = u32_to_f64(3u * nf - sBj) * args.inv_d;
+                        mA0 = -4503599627370496.0 * wA0;
+                        mA1 = -4503599627370496.0 * wA1;
+                        mB0 = -4503599627370496.0 * wB0;
+                        mB1 = -4503599627370496.0 * wB1;
                     } else {
                         wA0 = __ldg(args.w_b + 2 * jAc);
                         wA1 = __ldg(args.w_b + 2 * jAc + 1);
@@ -418,7 +433,30 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     // (FP64 issue rate is the scarce resource of this epilogue on B200).
                     double ca00 = 0, ca01 = 0, ca10 = 0, ca11 = 0, cb00 = 0, cb01 = 0, cb10 = 0, cb11 = 0;
                     if (want_c || kCompact) {
-                        if (exact23) {
+#ifdef CCC_D2_NOFP64
+                        if (true) {   // diagnostics: integer-only stand-in for the CCC cells
+                            const uint32_t u0 = ui0[r], u1 = ui1[r];
+                            ca00 = magic52((uint64_t)a00 * u0); ca01 = magic52((uint64_t)a01 * u0);
+                            ca10 = magic52((uint64_t)a10 * u1); ca11 = magic52((uint64_t)a11 * u1);
+                            cb00 = magic52((uint64_t)b00 * u0); cb01 = magic52((uint64_t)b01 * u0);
+                            cb10 = magic52((uint64_t)b10 * u1); cb11 = magic52((uint64_t)b11 * u1);
+                        } else
+#endif
+                        if (exact52) {
+                            // P = T U_i(a) < 12 n_f^2 < 2^52: the double 2^52 + P is P's bits
+                            // under exponent 0x433, so CCC = P w = fma(2^52 + P, w, -2^52 w):
+                            // one rounding (as before), one FP64 op and no I2F (the XU pipe
+                            // was the limiter of this epilogue)
+                            const uint32_t u0 = ui0[r], u1 = ui1[r];
+                            ca00 = __fma_rn(magic52((uint64_t)a00 * u0), wA0, mA0);
+                            ca01 = __fma_rn(magic52((uint64_t)a01 * u0), wA1, mA1);
+                            ca10 = __fma_rn(magic52((uint64_t)a10 * u1), wA0, mA0);
+                            ca11 = __fma_rn(magic52((uint64_t)a11 * u1), wA1, mA1);
+                            cb00 = __fma_rn(magic52((uint64_t)b00 * u0), wB0, mB0);
+                            cb01 = __fma_rn(magic52((uint64_t)b01 * u0), wB1, mB1);
+                            cb10 = __fma_rn(magic52((uint64_t)b10 * u1), wB0, mB0);
+                            cb11 = __fma_rn(magic52((uint64_t)b11 * u1), wB1, mB1);
+                        } else if (exact23) {
                             const uint64_t u0 = ui0[r], u1 = ui1[r];
                             ca00 = (double)(a00 * u0) * wA0;
                             ca01 = (double)(a01 * u0) * wA1;
@@ -451,32 +489,37 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                             emit2(args, (gi[r] << 20) | (uint64_t)(args.b_row0 + jB), b00, b01, b10, b11,
                                   cb00, cb01, cb10, cb11);
                     } else {
+#ifdef CCC_D2_NOSTORE
+                    const bool stA = okA && recA < 0, stB = okB && recA < 0;   // diagnostics
+#else
+                    const bool stA = okA, stB = okB;
+#endif
                     if (want_t) {
                         uint32_t* p = args.tallies + 4 * recA;
-                        if (okA && okB && !(recA & 1)) {
+                        if (stA && stB && !(recA & 1)) {
                             stg_256_u32(p, a00, a01, a10, a11, b00, b01, b10, b11);
                         } else {
-                            if (okA) stg_128_u32(p, a00, a01, a10, a11);
-                            if (okB) stg_128_u32(p + 4, b00, b01, b10, b11);
+                            if (stA) stg_128_u32(p, a00, a01, a10, a11);
+                            if (stB) stg_128_u32(p + 4, b00, b01, b10, b11);
                         }
                     }
                     if (want_c) {
                         if (want_c64) {
                             double* p = reinterpret_cast<double*>(args.ccc) + 4 * recA;
-                            if (okA) stg_256_f64(p, ca00, ca01, ca10, ca11);
-                            if (okB) stg_256_f64(p + 4, cb00, cb01, cb10, cb11);
+                            if (stA) stg_256_f64(p, ca00, ca01, ca10, ca11);
+                            if (stB) stg_256_f64(p + 4, cb00, cb01, cb10, cb11);
                         } else {
                             float* p = reinterpret_cast<float*>(args.ccc) + 4 * recA;
-                            if (okA && okB && !(recA & 1)) {
+                            if (stA && stB && !(recA & 1)) {
                                 stg_256_u32(p, __float_as_uint((float)ca00), __float_as_uint((float)ca01),
                                             __float_as_uint((float)ca10), __float_as_uint((float)ca11),
                                             __float_as_uint((float)cb00), __float_as_uint((float)cb01),
                                             __float_as_uint((float)cb10), __float_as_uint((float)cb11));
                             } else {
-                                if (okA)
+                                if (stA)
                                     stg_128_u32(p, __float_as_uint((float)ca00), __float_as_uint((float)ca01),
                                                 __float_as_uint((float)ca10), __float_as_uint((float)ca11));
-                                if (okB)
+                                if (stB)
                                     stg_128_u32(p + 4, __float_as_uint((float)cb00), __float_as_uint((float)cb01),
                                                 __float_as_uint((float)cb10), __float_as_uint((float)cb11));
                             }
