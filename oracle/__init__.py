@@ -70,6 +70,7 @@ def lib():
             getattr(L, name).argtypes = [p, i64, i64, p, ctypes.c_double, p, p]
         L.oracle_sparse_sums.argtypes = [p, i64, i64, p, p]
         L.oracle_sparse_pairs.argtypes = [p, i64, i64, p, p, ctypes.c_double, p, i64, p, p, p]
+        L.oracle_sparse_triples.argtypes = [p, i64, i64, p, p, ctypes.c_double, p, i64, p, p, p]
         _lib = L
     return _lib
 
@@ -183,6 +184,26 @@ def sparse_pairs(codes, idx, gamma: float = GAMMA):
         lib().oracle_sparse_pairs(_ptr(c), c.shape[0], c.shape[1], _ptr(S), _ptr(cnt), gamma,
                                   _ptr(idx), len(idx), _ptr(T), _ptr(C), _ptr(cij))
     return T, C, cij
+
+
+def sparse_triples(codes, idx, gamma: float = GAMMA):
+    """Sparse mode (reading A-17) for an explicit triple list: (T [m][8], CCC, c_ijk)."""
+    c = _codes_np(codes)
+    idx = np.ascontiguousarray(np.asarray(idx, dtype=np.int64).reshape(-1, 3))
+    S, cnt = sparse_sums(c)
+    m = idx.shape[0]
+    T = np.zeros((m, 8), np.int64)
+    C = np.zeros((m, 8), np.float64)
+    cc = np.zeros(m, np.int64)
+    if m:
+        lib().oracle_sparse_triples(_ptr(c), c.shape[0], c.shape[1], _ptr(S), _ptr(cnt), gamma,
+                                    _ptr(idx), m, _ptr(T), _ptr(C), _ptr(cc))
+    return T, C, cc
+
+
+def sparse_all_triples(codes, gamma: float = GAMMA):
+    """Every unique triple i<j<k, lexicographic: sparse (T, CCC, c_ijk)."""
+    return sparse_triples(codes, triple_list(_codes_np(codes).shape[0]), gamma)
 
 
 def sparse_all_pairs(codes, gamma: float = GAMMA):

@@ -263,3 +263,67 @@ void oracle_sparse_pairs(const uint8_t* codes, int64_t n_v, int64_t n_f, const i
                             ccc + 4 * r);
     }
 }
+
+/*
+ * ---- Sparse (missing-data) mode, 3-way: the same reading A-17 for triples,
+ * SPEC's "per-triple valid counts in the f_{i,j,k} divisor and per-vector valid counts
+ * for f_i":
+ *   T_ijk(a,b,c) = the Fig.2 enumeration over the fields where ALL THREE are present,
+ *   c_ijk = that number of fields,  f_ijk = T_ijk / (8 c_ijk)
+ *   CCC_ijk(a,b,c) = f_ijk(a,b,c) (1 - g f_i(a)) (1 - g f_j(b)) (1 - g f_k(c))   (Eq.4)
+ *   with f_i(a) = S_i(a) / (2 c_i) over vector i's present entries (0 if c_i = 0);
+ *   c_ijk = 0 -> T = 0 and CCC = 0.
+ */
+static void tally3_sparse_one(const uint8_t* vi, const uint8_t* vj, const uint8_t* vk, int64_t n_f,
+                              int64_t T[8], int64_t* c_ijk)
+{
+    for (int t = 0; t < 8; ++t) T[t] = 0;
+    *c_ijk = 0;
+    for (int64_t q = 0; q < n_f; ++q) {
+        if (elem_missing(vi[q]) || elem_missing(vj[q]) || elem_missing(vk[q])) continue;
+        *c_ijk += 1;
+        int ri[2] = {elem_r1(vi[q]), elem_r2(vi[q])};
+        int rj[2] = {elem_r1(vj[q]), elem_r2(vj[q])};
+        int rk[2] = {elem_r1(vk[q]), elem_r2(vk[q])};
+        for (int s = 0; s < 2; ++s)
+            for (int t = 0; t < 2; ++t)
+                for (int u = 0; u < 2; ++u)
+                    T[4 * ri[s] + 2 * rj[t] + rk[u]] += 1;
+    }
+}
+
+/* Sparse 3-way tallies, CCC and c_ijk for an explicit triple list idx[m][3]; S, cnt from
+ * oracle_sparse_sums.  ccc / cijk may be NULL. */
+void oracle_sparse_triples(const uint8_t* codes, int64_t n_v, int64_t n_f, const int64_t* S,
+                           const int64_t* cnt, double gamma, const int64_t* idx, int64_t m,
+                           int64_t* T, double* ccc, int64_t* cijk)
+{
+    (void)n_v;
+    #pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t r = 0; r < m; ++r) {
+        const int64_t ix[3] = {idx[3 * r], idx[3 * r + 1], idx[3 * r + 2]};
+        int64_t c;
+        tally3_sparse_one(codes + ix[0] * n_f, codes + ix[1] * n_f, codes + ix[2] * n_f, n_f,
+                          T + 8 * r, &c);
+        if (cijk) cijk[r] = c;
+        if (!ccc) continue;
+        for (int a = 0; a < 2; ++a)
+            for (int b = 0; b < 2; ++b)
+                for (int d = 0; d < 2; ++d) {
+                    const int cell = 4 * a + 2 * b + d;
+                    if (c == 0) {
+                        ccc[8 * r + cell] = 0.0;
+                        continue;
+                    }
+                    const int al[3] = {a, b, d};
+                    double f_ijk = (double)T[8 * r + cell] / (8.0 * (double)c);
+                    double v = f_ijk;
+                    for (int t = 0; t < 3; ++t) {
+                        const int64_t x = ix[t];
+                        double f = cnt[x] ? (double)S[2 * x + al[t]] / (2.0 * (double)cnt[x]) : 0.0;
+                        v *= (1.0 - gamma * f);
+                    }
+                    ccc[8 * r + cell] = v;
+                }
+    }
+}

@@ -358,3 +358,52 @@ def test_sparse_codes_generator():
     assert frac.max() < 0.35 and frac.min() >= 0.0 and frac.mean() > 0.05
     np.testing.assert_array_equal(synthgen.sparse_codes(8, 100, seed=4, row0=5).numpy(),
                                   synthgen.sparse_codes(13, 100, seed=4).numpy()[5:])
+
+
+# ------------------------------------------------------------- sparse 3-way (A-17 for triples)
+def test_sparse3_no_missing_equals_dense():
+    """With no missing entry the sparse 3-way tally / CCC equal the dense ones, c_ijk = n_f."""
+    c = synthgen.random_codes(9, 53, seed=21).numpy()
+    c[c == oracle.MISSING] = 1
+    Ts, Cs, cc = oracle.sparse_all_triples(c)
+    Td, Cd = oracle.all_triples(c)
+    np.testing.assert_array_equal(Ts, Td)
+    np.testing.assert_allclose(Cs, Cd, rtol=1e-15, atol=0)
+    assert np.all(cc == 53)
+
+
+def test_sparse3_column_deletion_and_marginals():
+    """Independent pins: T_ijk over the fields where all three are present is the DENSE
+    3-way tally of the three vectors restricted to those fields; sum T = 8 c_ijk; summing
+    out the k allele gives 2 x the sparse pair tally over the same fields; a vector with
+    every entry missing zeroes all its triples."""
+    c = synthgen.sparse_codes(8, 180, seed=22).numpy()
+    c[5, :] = oracle.MISSING
+    T, C, cc = oracle.sparse_all_triples(c)
+    for r, (i, j, k) in enumerate(oracle.triple_list(8)):
+        keep = (c[i] != oracle.MISSING) & (c[j] != oracle.MISSING) & (c[k] != oracle.MISSING)
+        assert cc[r] == keep.sum() and T[r].sum() == 8 * cc[r]
+        if 5 in (i, j, k):
+            assert cc[r] == 0 and not T[r].any() and not C[r].any()
+            continue
+        Td, _ = oracle.triples(c[[i, j, k]][:, keep], [[0, 1, 2]])
+        np.testing.assert_array_equal(T[r], Td[0])
+        T2, _ = oracle.pairs(c[[i, j]][:, keep], [[0, 1]])
+        np.testing.assert_array_equal(T[r].reshape(2, 2, 2).sum(2), 2 * T2[0].reshape(2, 2))
+
+
+def test_sparse3_ccc_exact_rational():
+    """3-way sparse CCC in fp64 against exact rationals (per-vector f over present entries,
+    per-triple divisor 8 c_ijk)."""
+    c = synthgen.sparse_codes(5, 37, seed=23).numpy()
+    T, C, cc = oracle.sparse_all_triples(c)
+    g = Fraction(2, 3)
+    S, cnt = oracle.sparse_sums(c)
+    for r, (i, j, k) in enumerate(oracle.triple_list(5)):
+        fs = [[Fraction(int(S[x, a]), 2 * int(cnt[x])) for a in range(2)] for x in (i, j, k)]
+        for a in range(2):
+            for b in range(2):
+                for d in range(2):
+                    exact = (Fraction(int(T[r, 4 * a + 2 * b + d]), 8 * int(cc[r])) * (1 - g * fs[0][a]) *
+                             (1 - g * fs[1][b]) * (1 - g * fs[2][d]))
+                    assert abs(C[r, 4 * a + 2 * b + d] - float(exact)) <= 4e-15 * float(exact) + 1e-300
