@@ -1,7 +1,7 @@
 """bench.py -- CCC comparisons/s of the B200 hot path.
 
 python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                [--workload c2|c4|c1|c2s|c2pop|c2fs] [--no-e2e] [--no-cpu]
+                [--workload c2|c4|c1|c2s|c4s|c2pop|c2fs] [--no-e2e] [--no-cpu]
 
 One step = one pass of the whole hot path over one synthetic batch resident in HBM:
   2-way (default, BASELINE configs[1] = C2: 20,000 vectors x 50,000 individuals):
@@ -48,6 +48,8 @@ WORKLOADS = {
     "c2fs": dict(way=2, n_v=20000, n_f=50000, fieldsplit=4,
                  label="2-way CCC, 20,000 x 50,000, field-axis split into 4 slices (SURVEY f3), "
                        "all slices simulated on one GPU"),
+    "c4s": dict(way=3, n_v=4096, n_f=16384, n_st=16, sparse=True,
+                label="3-way sparse-mode CCC (missing entries, SURVEY f1), 4,096 x 16,384, 16 stages"),
     "c4": dict(way=3, n_v=4096, n_f=16384, n_st=16,
                label="3-way CCC, 4,096 SNP vectors x 16,384 individuals, 16 stages (configs[3])"),
 }
@@ -158,6 +160,8 @@ def cpu_baseline(way, n_v, n_f, target_s=12.0, kind="random"):  # noqa: C901
         allidx = np.array([(a, b, c) for a in range(m_local) for b in range(a + 1, m_local)
                            for c in range(b + 1, m_local)])
         f = oracle.triples
+        if kind == "sparse":
+            f = lambda c, idx, S=None: oracle.sparse_triples(c, idx)   # noqa: E731
     S = oracle.allele_sums(sub)
     # calibrate, then run a sample sized for ~target_s seconds
     m = 64
@@ -395,12 +399,21 @@ def run_3way_single(args, wl):
     import synthgen
     from paper_1705_08213_b200 import ccc
     n_v, n_f, n_st = wl["n_v"], wl["n_f"], wl["n_st"]
+    sparse = wl.get("sparse", False)
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     flags = ccc.OUT_TALLY | ccc.OUT_CCC_F64
-    codes = synthgen.random_codes(n_v, n_f, seed=1, device=dev)
+    if sparse:
+        codes = synthgen.sparse_codes(n_v, n_f, seed=4, device=dev)
+    else:
+        codes = synthgen.random_codes(n_v, n_f, seed=1, device=dev)
     packed = torch.empty((n_v, ccc.ccc_packed_stride(n_f)), dtype=torch.uint8, device=dev)
-    ws = ccc.workspace(3, n_v, n_f, dev)
+    if sparse:
+        ws = torch.empty(ccc.lib().ccc_sparse3_workspace_bytes(n_v, n_f), dtype=torch.uint8, device=dev)
+        scratch = torch.empty(max(ccc.lib().ccc_3way_sparse_scratch_bytes(n_v, n_st, s) for s in range(n_st)),
+                              dtype=torch.uint8, device=dev)
+    else:
+        ws = ccc.workspace(3, n_v, n_f, dev)
     rmax = max(ccc.ccc_stage_range(n_v, n_st, s)[3] for s in range(n_st))
     T = torch.empty((rmax, 8), dtype=torch.int32, device=dev)
     C = torch.empty((rmax, 8), dtype=torch.float64, device=dev)
@@ -410,12 +423,18 @@ def run_3way_single(args, wl):
     def step(ev=None):
         ccc.ccc_pack(codes, packed)
         launches[0] += ccc.ccc_last_launch_count()
-        ccc.ccc_3way_prepare(packed, n_f, ccc.GAMMA, ws)
+        if sparse:
+            ccc.ccc_3way_sparse_prepare(packed, n_f, ccc.GAMMA, ws)
+        else:
+            ccc.ccc_3way_prepare(packed, n_f, ccc.GAMMA, ws)
         launches[0] += ccc.ccc_last_launch_count()
         for st in range(n_st):
             if ev:
                 ev[st][0].record(stream)
-            ccc.ccc_3way_stage(n_v, n_f, n_st, st, ws, flags, T, C)
+            if sparse:
+                ccc.ccc_3way_sparse_stage(n_v, n_f, n_st, st, ws, flags, T, C, None, scratch)
+            else:
+                ccc.ccc_3way_stage(n_v, n_f, n_st, st, ws, flags, T, C)
             launches[0] += ccc.ccc_last_launch_count()
             if ev:
                 ev[st][1].record(stream)
@@ -438,7 +457,8 @@ def run_3way_single(args, wl):
     k_ms = sum(a.elapsed_time(b) for st in kev for a, b in st) / (args.steps * n_st)
     return {"ms": ms, "kernel_ms": k_ms, "comparisons": comparisons(3, n_v, n_f),
             "launches": launches[0], "clocks": clk.summary(), "kernel": "tally3_kernel",
-            "out_bytes": comparisons(3, n_v, n_f) // n_f * 96, "stages": n_st}
+            "out_bytes": comparisons(3, n_v, n_f) // n_f * 96, "stages": n_st,
+            "forms_bytes": comparisons(3, n_v, n_f) // n_f * 7 * 4 * 2 if sparse else 0}
 
 
 # ------------------------------------------------------------------------ main
@@ -482,7 +502,7 @@ def main():
 
     if world > 1 or args.gpus > 1:
         if wl.get("sparse"):
-            raise SystemExit("--workload c2s is a single-GPU measurement")
+            raise SystemExit("the sparse workloads are single-GPU measurements")
         from paper_1705_08213_b200 import dist
         return dist.bench_main(args, wl, METRIC, UNIT)
 
@@ -501,7 +521,8 @@ def main():
         # sparse mode: 4 int8 MACs per comparison (n.n, n.v, v.n, v.v)
         ops = (8.0 if wl.get("sparse") else 2.0) * r["comparisons"]
     else:
-        ops = 2.0 * r["comparisons"] / wl["n_st"]
+        # sparse 3-way: 8 passes (trilinear forms) = 8 MACs per comparison
+        ops = (16.0 if wl.get("sparse") else 2.0) * r["comparisons"] / wl["n_st"]
     # int8 dense = 2 x bf16 dense (the guide's nominal ratio, 4.5 vs 2.25 PFLOP/s); the
     # burst figure applies: the timed region is ~0.1 s of back-to-back steps, not seconds.
     int8_peak = 2.0 * pk["bf16_tflops"]
@@ -538,11 +559,12 @@ def main():
         roof["frac"] = roof["achieved"] / roof["peak"]
     if wl["way"] == 3:
         roof["bound"] = "hbm"
-        roof["achieved"] = r["out_bytes"] / wl["n_st"] / k_s / 1e9
+        roof["achieved"] = (r["out_bytes"] + r.get("forms_bytes", 0)) / wl["n_st"] / k_s / 1e9
         roof["peak"] = pk["hbm_gbs"]
         roof["unit"] = "GB/s"
         roof["frac"] = roof["achieved"] / pk["hbm_gbs"]
-        roof["peak_source"] = f"hbm_gbs of MEASURED_PEAKS.json ({pk_kind}); FULL output 96 B/triple"
+        roof["peak_source"] = f"hbm_gbs of MEASURED_PEAKS.json ({pk_kind}); FULL output 96 B/triple" + (
+            " + 7 stored forms written and read back (56 B/triple)" if wl.get("sparse") else "")
         roof["tensor_TOPS"] = achieved
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,

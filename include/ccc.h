@@ -364,6 +364,30 @@ ccc_status ccc_2way_sparse(const uint8_t* packed_d, int64_t n_v, int64_t n_f, do
                            uint64_t* checksum_d, void* ws_d, size_t ws_bytes,
                            const ccc_compact* compact, void* stream);
 
+/* ---- Sparse (missing-data) mode, 3-way (reading A-17 for triples,
+ * SPEC S:303-304): T_ijk(a,b,c) over the fields where all three entries are present,
+ * c_ijk = that number, f_ijk = T/(8 c_ijk), per-vector f_i(a) = S_i(a)/(2 c_i) over the
+ * vector's present entries, CCC = f_ijk (1-g f_i(a))(1-g f_j(b))(1-g f_k(c)), 0 if
+ * c_ijk = 0.  With n = allele-1 count (0 where missing) and v = [present],
+ * rho(1) = n and rho(0) = 2v - n, so every cell is a signed sum of the 8 trilinear forms
+ * sum_q x_i x_j x_k (x in {n, v}); each form is one pass of the Hadamard pivot GEMM
+ * (tally3) over the N_s / V operands -- 8 int8 MACs per comparison.  Passes 0..6 store
+ * their form (uint32 per record) in the caller's scratch; pass 7 (v v v = c_ijk) reads
+ * them in its epilogue and writes the records.
+ * prepare: packed_d -> ws_d (>= ccc_sparse3_workspace_bytes): N_s, V [n_v][K_pad] int8,
+ *          s_i, c_i int32, w_i(a) double (sparse weights, gamma given here).
+ * stage:   records of stage `stage` of n_stages (ccc_stage_range), outputs as
+ *          ccc_3way_stage (a-major cells, lexicographic triples minus the stage's first
+ *          record); scratch_d >= ccc_3way_sparse_scratch_bytes(n_v, n_stages, stage). */
+size_t     ccc_sparse3_workspace_bytes(int64_t n_v, int64_t n_f);
+size_t     ccc_3way_sparse_scratch_bytes(int64_t n_v, int64_t n_stages, int64_t stage);
+ccc_status ccc_3way_sparse_prepare(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
+                                   void* ws_d, size_t ws_bytes, void* stream);
+ccc_status ccc_3way_sparse_stage(int64_t n_v, int64_t n_f, double gamma, int64_t n_stages, int64_t stage,
+                                 uint32_t out_flags, uint32_t* tallies_d, void* ccc_d, uint64_t* checksum_d,
+                                 void* ws_d, size_t ws_bytes, void* scratch_d, size_t scratch_bytes,
+                                 void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -101,15 +101,18 @@ __global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict_
 __global__ void __launch_bounds__(256) expand_sparse_kernel(
     const uint32_t* __restrict__ packed, int64_t n_v, int64_t n_v16, int64_t n_f,
     int64_t words_per_row, int64_t k_pad, double gamma, int8_t* __restrict__ X,
-    int32_t* __restrict__ s_out, int32_t* __restrict__ c_out, double* __restrict__ w_out) {
+    int32_t* __restrict__ s_out, int32_t* __restrict__ c_out, double* __restrict__ w_out,
+    int8_t* __restrict__ V) {
+    // V != NULL: the separate layout of the 3-way sparse mode -- n in row i of X, the
+    // presence bits in row i of V (n_v16 = n_v, no group interleaving)
     __shared__ int32_t red[2][8];
     const int64_t groups = k_pad / 16;
     for (int64_t i = blockIdx.x; i < n_v16; i += gridDim.x) {
         const bool real = i < n_v;
         const uint32_t* prow = packed + i * words_per_row;
         const int64_t xr = 32 * (i / 16) + (i % 16);
-        uint4* nrow = reinterpret_cast<uint4*>(X + xr * k_pad);
-        uint4* vrow = reinterpret_cast<uint4*>(X + (xr + 16) * k_pad);
+        uint4* nrow = reinterpret_cast<uint4*>(V ? X + i * k_pad : X + xr * k_pad);
+        uint4* vrow = reinterpret_cast<uint4*>(V ? V + i * k_pad : X + (xr + 16) * k_pad);
         int32_t sum = 0, cnt = 0;
         for (int64_t g = threadIdx.x; g < groups; g += blockDim.x) {
             const uint32_t p = (real && g < words_per_row) ? __ldg(prow + g) : 0u;
@@ -171,7 +174,19 @@ cudaError_t launch_expand_sparse(const uint8_t* packed, int64_t n_v, int64_t n_f
     int64_t blocks = n_v16 < (int64_t)num_sms * 8 ? n_v16 : (int64_t)num_sms * 8;
     if (blocks < 1) blocks = 1;
     expand_sparse_kernel<<<(int)blocks, 256, 0, stream>>>(
-        reinterpret_cast<const uint32_t*>(packed), n_v, n_v16, n_f, wpr, k_pad, gamma, X, s, c, w);
+        reinterpret_cast<const uint32_t*>(packed), n_v, n_v16, n_f, wpr, k_pad, gamma, X, s, c, w, nullptr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_expand_sparse3(const uint8_t* packed, int64_t n_v, int64_t n_f, double gamma, int8_t* Ns,
+                                  int8_t* V, int32_t* s, int32_t* c, double* w, int num_sms,
+                                  cudaStream_t stream) {
+    const int64_t wpr = (n_f + 63) / 64 * 4;
+    const int64_t k_pad = (n_f + 127) / 128 * 128;
+    int64_t blocks = n_v < (int64_t)num_sms * 8 ? n_v : (int64_t)num_sms * 8;
+    if (blocks < 1) blocks = 1;
+    expand_sparse_kernel<<<(int)blocks, 256, 0, stream>>>(
+        reinterpret_cast<const uint32_t*>(packed), n_v, n_v, n_f, wpr, k_pad, gamma, Ns, s, c, w, V);
     return cudaGetLastError();
 }
 

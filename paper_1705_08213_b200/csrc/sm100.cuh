@@ -406,6 +406,12 @@ __device__ __forceinline__ void stg_256_u32_if(bool ok, void* p, uint32_t a, uin
         "r"(a), "r"(b), "r"(c), "r"(d), "r"(e), "r"(f), "r"(g), "r"(h), "r"((uint32_t)ok)
         : "memory");
 }
+__device__ __forceinline__ void st_u32_if(bool ok, void* p, uint32_t a) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+        "@q st.global" CCC_ST_HINT ".u32 [%0], %1;\n\t}" ::"l"(p), "r"(a), "r"((uint32_t)ok)
+        : "memory");
+}
 __device__ __forceinline__ void stg_256_f64_if(bool ok, void* p, double a, double b, double c, double d) {
     asm volatile(
         "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"

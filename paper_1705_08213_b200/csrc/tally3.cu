@@ -189,7 +189,78 @@ __device__ __forceinline__ void emit3(const Tally3Args& a, uint64_t key, const u
     }
 }
 
-template <int kOrder, bool kExact, bool kCompact, bool kFull>
+// Sparse (missing-data) 3-way record, reading A-17 for triples (oracle_sparse_triples):
+// with n = allele-1 count (0 where missing) and v = [present], rho(1) = n, rho(0) = 2v - n,
+// so T(a,b,c) = sum_q rho_p(a) rho_m(b) rho_n(c) expands into the 8 trilinear forms
+// F[4 x_p + 2 x_m + x_n] = sum_q x_p x_m x_n (x = 0: n, 1: v); c_pmn = F[7] = #fields
+// where all three are present; CCC = T / (8 c_pmn) w_p(a) w_m(b) w_n(c) (0 if c_pmn = 0).
+// F[7] is this (final) pass's accumulator, F[0..6] were stored by the form passes.
+template <class O>
+__device__ __forceinline__ void sparse3_record(const Tally3Args& a, bool ok, uint32_t g3, int64_t rec,
+                                               const double (&wpm)[4], double wn0, double wn1, int64_t gp,
+                                               int64_t gm, int64_t gn, bool want_t, bool want_c64,
+                                               bool want_c32, bool want_ck, unsigned long long& ck_lo,
+                                               unsigned long long& ck_hi) {
+    uint32_t F[8];
+    const int64_t rc = ok ? rec : 0;
+#pragma unroll
+    for (int f = 0; f < 7; ++f) F[f] = ok ? __ldg(a.forms + (int64_t)f * a.form_stride + rc) : 0u;
+    F[7] = g3;
+    uint32_t t[8];
+#pragma unroll
+    for (int cell = 0; cell < 8; ++cell) {
+        const int al[3] = {(cell >> 2) & 1, (cell >> 1) & 1, cell & 1};
+        uint32_t acc = 0;
+#pragma unroll
+        for (int f = 0; f < 8; ++f) {
+            const int x[3] = {(f >> 2) & 1, (f >> 1) & 1, f & 1};
+            int coef = 1;
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                // allele 1 uses n only (+1); allele 0 = 2v - n: v -> +2, n -> -1
+                if (al[r] == 1) coef *= (x[r] == 0) ? 1 : 0;
+                else coef *= (x[r] == 1) ? 2 : -1;
+            }
+            if (coef) acc += (uint32_t)coef * F[f];
+        }
+        t[cell] = acc;
+    }
+    const uint32_t cpmn = F[7];
+    double cr[8];
+    const double inv = cpmn ? 1.0 / (8.0 * (double)cpmn) : 0.0;
+#pragma unroll
+    for (int ab = 0; ab < 4; ++ab) {
+        cr[2 * ab + 0] = (double)t[2 * ab + 0] * inv * wpm[ab] * wn0;
+        cr[2 * ab + 1] = (double)t[2 * ab + 1] * inv * wpm[ab] * wn1;
+    }
+    uint32_t tc[8];
+    double cc[8];
+    perm_cells<O::R0, O::R1, O::R2>(t, tc);
+    perm_cells<O::R0, O::R1, O::R2>(cr, cc);
+    if (want_t)
+        stg_256_u32_if(ok, a.tallies + 8 * rec, tc[0], tc[1], tc[2], tc[3], tc[4], tc[5], tc[6], tc[7]);
+    if (want_c64) {
+        double* q = reinterpret_cast<double*>(a.ccc) + 8 * rec;
+        stg_256_f64_if(ok, q, cc[0], cc[1], cc[2], cc[3]);
+        stg_256_f64_if(ok, q + 4, cc[4], cc[5], cc[6], cc[7]);
+    } else if (want_c32) {
+        float* q = reinterpret_cast<float*>(a.ccc) + 8 * rec;
+        stg_256_u32_if(ok, q, __float_as_uint((float)cc[0]), __float_as_uint((float)cc[1]),
+                       __float_as_uint((float)cc[2]), __float_as_uint((float)cc[3]),
+                       __float_as_uint((float)cc[4]), __float_as_uint((float)cc[5]),
+                       __float_as_uint((float)cc[6]), __float_as_uint((float)cc[7]));
+    }
+    if (want_ck && ok) {
+        const int64_t g[3] = {gp, gm, gn};
+        ck_fold3(ck_lo, ck_hi,
+                 (3ull << 60) | ((uint64_t)g[O::R0] << 40) | ((uint64_t)g[O::R1] << 20) | (uint64_t)g[O::R2],
+                 tc);
+    }
+}
+
+// kMode: 0 dense CCC; 1 sparse form pass (store the raw trilinear form G3 of this pass);
+// 2 sparse final pass (read the 7 stored forms, build the sparse tallies + CCC)
+template <int kOrder, bool kExact, bool kCompact, bool kFull, int kMode = 0>
 __global__ void __launch_bounds__(kThreads3, 1)
 tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const Tally3Args args) {
@@ -412,7 +483,7 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 // column terms of this unit: thread et <- column col0 + et
                 const int64_t nc = col0 + (et < (uint32_t)nval ? et : (uint32_t)(nval - 1));
                 const uint32_t sn = (uint32_t)__ldg(args.bn.s + nc);
-                const uint32_t gpn = gord<kOrder, 0, 2>(args.G, args.ldG, gp, args.bn.row0 + nc);
+                const uint32_t gpn = kMode ? 0u : gord<kOrder, 0, 2>(args.G, args.ldG, gp, args.bn.row0 + nc);
                 ColT3 v;
                 v.gpn2 = 2u * gpn;
                 v.cn = 4u * sn - 2u * gpn;
@@ -430,8 +501,10 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 ct[et] = v;
             }
             // general gamma: w_p(a) / (8 n_f); gamma = 2/3: integer U_p(a) = 3 n_f - S_p(a)
-            const double wp0 = kExact ? 0.0 : __ldg(args.bp.w + 2 * p) * inv8nf;
-            const double wp1 = kExact ? 0.0 : __ldg(args.bp.w + 2 * p + 1) * inv8nf;
+            // (sparse final pass: no 1/(8 n_f) here, the divisor 8 c_pmn is per record)
+            const double wscale = kMode == 2 ? 1.0 : inv8nf;
+            const double wp0 = kExact ? 0.0 : __ldg(args.bp.w + 2 * p) * wscale;
+            const double wp1 = kExact ? 0.0 : __ldg(args.bp.w + 2 * p + 1) * wscale;
             const uint64_t up0 = nf + s_p, up1 = 3u * nf - s_p;
             // my 2 rows m = row0(J) + rank*128 + quad*32 + half*16 + r*8 + lane/4
             int64_t rec_r[2], gm_r[2];
@@ -448,7 +521,7 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 const int64_t mc = m < args.m_hi ? m : args.m_hi - 1;
                 gm_r[r] = args.bm.row0 + mc;
                 s_m[r] = (uint32_t)__ldg(args.bm.s + mc);
-                const uint32_t gpm = ok ? gord<kOrder, 0, 1>(args.G, args.ldG, gp, gm_r[r]) : 0u;
+                const uint32_t gpm = (ok && !kMode) ? gord<kOrder, 0, 1>(args.G, args.ldG, gp, gm_r[r]) : 0u;
                 g_pm[r] = gpm;
                 gpm2[r] = 2u * gpm;
                 A_r[r] = 4u * s_p - 2u * gpm;
@@ -503,7 +576,8 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     nl = nl < gn_max ? nl : gn_max;
 #pragma unroll
                     for (int r = 0; r < 2; ++r) {
-                        if constexpr (kRowG) g[r][h] = (uint32_t)__ldg(grow[r] + nl);
+                        if constexpr (kMode != 0) g[r][h] = 0u;   // sparse passes: no G
+                        else if constexpr (kRowG) g[r][h] = (uint32_t)__ldg(grow[r] + nl);
                         else g[r][h] = (uint32_t)__ldg(args.G + (gcol0 + nl) * args.ldG + gm_r[r]);
                     }
                 }
@@ -548,6 +622,17 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         const bool ok = nl > lo_r[r] && nl < nval;
                         const ColT3& cn = h ? cB : cA;
                         const uint32_t g3 = va[r * 2 + h];
+                        if constexpr (kMode == 1) {
+                            // sparse form pass: the raw trilinear form of this pass
+                            const int64_t rec = rec_r[r] + nl;
+                            st_u32_if(ok, args.forms + (int64_t)args.form_self * args.form_stride + rec, g3);
+                            continue;
+                        }
+                        if constexpr (kMode == 2) {
+                            sparse3_record<O>(args, ok, g3, rec_r[r] + nl, wpm[r], cn.w0, cn.w1, gp, gm_r[r],
+                                              gcol0 + nl, want_t, want_c64, want_c32, want_ck, ck_lo, ck_hi);
+                            continue;
+                        }
                         const uint32_t gmn2 = 2u * gcur[r][h];
                         uint32_t t[8];   // role order: index 4 a_p + 2 a_m + a_n
                         t[7] = g3;
@@ -695,6 +780,8 @@ cudaError_t launch_tally3(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
             default: return go(tally3_kernel<5, E, Cp, Fu>);
         }
     };
+    if (a.mode == 1) return go(tally3_kernel<0, false, false, false, 1>);   // sparse passes:
+    if (a.mode == 2) return go(tally3_kernel<0, false, false, false, 2>);   // order 0 only
     using T = std::true_type;
     using F = std::false_type;
     // FULL with gamma = 2/3 (tallies + fp64 CCC, no checksum) gets a flag-free epilogue
