@@ -577,8 +577,12 @@ def main():
                              "per-vector rate U(0, 0.3) (P:1028-1043)") if wl.get("sparse") else
                             "type-1 uniform random 2-bit codes, seed 1 (P:657)",
                    "output": "FULL: uint32 tallies + fp64 CCC for every unique record",
-                   "l2": "inputs larger than L2 (codes %.2f GB, N %.2f GB)" % (
-                       wl["n_v"] * wl["n_f"] / 1e9, wl["n_v"] * wl["n_f"] / 1e9),
+                   "l2": ("inputs larger than L2 (codes %.2f GB, N %.2f GB)" % (
+                       wl["n_v"] * wl["n_f"] / 1e9, wl["n_v"] * wl["n_f"] / 1e9)) if wl["way"] == 2 else
+                         ("operands L2-resident by design (N %.2f GB, G %.2f GB); each stage writes "
+                          "%.0f GB of records, far larger than L2" % (
+                              wl["n_v"] * wl["n_f"] / 1e9, 4 * wl["n_v"] ** 2 / 1e9,
+                              comparisons(3, wl["n_v"], wl["n_f"]) / wl["n_f"] * 96 / wl["n_st"] / 1e9)),
                    "parallelism": "single GPU"},
         "roofline": roof,
         "gpu_launches": r["launches"],
