@@ -24,5 +24,17 @@ ex = [ccc.ccc_expand(ccc.ccc_pack(codes[lo:hi].contiguous().cuda()), n_f) for lo
 b = [ccc.block(*ex[i], bounds[i][0]) for i in range(3)]
 u = decomp.plan_3way(3, 1, bounds)[-1]
 ccc.ccc_3way_unit(b[u.pb], u.p_lo, u.p_hi, b[u.mb], u.m_lo, u.m_hi, b[u.nb], u.n_lo, u.n_hi, u.order, G, n_f, F)
+# sparse 2-way / 3-way, popcount baseline, field split (f1, f4, f3)
+sc = synthgen.sparse_codes(140, 210, seed=5)
+ccc.ccc_2way_sparse(ccc.ccc_pack(sc.cuda()), 210, out_flags=F)
+T3, C3, _ = ccc.three_way_sparse(sc[:90].contiguous().cuda(), out_flags=F, n_stages=2)
+To3, _, _ = oracle.sparse_all_triples(sc[:90])
+assert np.array_equal(T3.cpu().numpy().astype(np.int64) & 0xFFFFFFFF, To3)
+pc = ccc.ccc_pack(codes.cuda())
+Tp, _, _ = ccc.ccc_2way_popcount(pc, n_f, out_flags=F)
+from paper_1705_08213_b200 import fieldsplit
+Tf, _, _ = fieldsplit.run_simulated(codes.cuda(), 3, F, wave_tiles=1)
+Td, _, _ = ccc.two_way(codes.cuda(), out_flags=F)
+assert bool((Tp == Td).all()) and bool((Tf == Td).all())
 torch.cuda.synchronize()
 print("sanitize run ok")
