@@ -1,7 +1,7 @@
 """bench.py -- CCC comparisons/s of the B200 hot path.
 
 python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                [--workload c2|c4|c1|c2s|c4s|c2pop|c2fs] [--no-e2e] [--no-cpu]
+                [--workload c2|c4|c1|c2s|c4s|c2pop|c2fs|c4paper] [--no-e2e] [--no-cpu]
 
 One step = one pass of the whole hot path over one synthetic batch resident in HBM:
   2-way (default, BASELINE configs[1] = C2: 20,000 vectors x 50,000 individuals):
@@ -50,6 +50,9 @@ WORKLOADS = {
                        "all slices simulated on one GPU"),
     "c4s": dict(way=3, n_v=4096, n_f=16384, n_st=16, sparse=True,
                 label="3-way sparse-mode CCC (missing entries, SURVEY f1), 4,096 x 16,384, 16 stages"),
+    "c4paper": dict(way=3, n_v=4096, n_f=16384, n_st=16, paper=True,
+                    label="3-way CCC, 4,096 x 16,384, 16 stages, the paper's Table-1 route (3 masked pivot "
+                          "GEMMs + reconstruction) on the tensor pipe (SURVEY f4 baseline)"),
     "c4": dict(way=3, n_v=4096, n_f=16384, n_st=16,
                label="3-way CCC, 4,096 SNP vectors x 16,384 individuals, 16 stages (configs[3])"),
 }
@@ -400,6 +403,7 @@ def run_3way_single(args, wl):
     from paper_1705_08213_b200 import ccc
     n_v, n_f, n_st = wl["n_v"], wl["n_f"], wl["n_st"]
     sparse = wl.get("sparse", False)
+    paper = wl.get("paper", False)
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     flags = ccc.OUT_TALLY | ccc.OUT_CCC_F64
@@ -411,6 +415,10 @@ def run_3way_single(args, wl):
     if sparse:
         ws = torch.empty(ccc.lib().ccc_sparse3_workspace_bytes(n_v, n_f), dtype=torch.uint8, device=dev)
         scratch = torch.empty(max(ccc.lib().ccc_3way_sparse_scratch_bytes(n_v, n_st, s) for s in range(n_st)),
+                              dtype=torch.uint8, device=dev)
+    elif paper:
+        ws = torch.empty(ccc.lib().ccc_3way_paper_workspace_bytes(n_v, n_f), dtype=torch.uint8, device=dev)
+        scratch = torch.empty(max(ccc.lib().ccc_3way_paper_scratch_bytes(n_v, n_st, s) for s in range(n_st)),
                               dtype=torch.uint8, device=dev)
     else:
         ws = ccc.workspace(3, n_v, n_f, dev)
@@ -425,6 +433,8 @@ def run_3way_single(args, wl):
         launches[0] += ccc.ccc_last_launch_count()
         if sparse:
             ccc.ccc_3way_sparse_prepare(packed, n_f, ccc.GAMMA, ws)
+        elif paper:
+            ccc.ccc_3way_paper_prepare(packed, n_f, ccc.GAMMA, ws)
         else:
             ccc.ccc_3way_prepare(packed, n_f, ccc.GAMMA, ws)
         launches[0] += ccc.ccc_last_launch_count()
@@ -433,6 +443,8 @@ def run_3way_single(args, wl):
                 ev[st][0].record(stream)
             if sparse:
                 ccc.ccc_3way_sparse_stage(n_v, n_f, n_st, st, ws, flags, T, C, None, scratch)
+            elif paper:
+                ccc.ccc_3way_paper_stage(n_v, n_f, n_st, st, ws, flags, T, C, None, scratch)
             else:
                 ccc.ccc_3way_stage(n_v, n_f, n_st, st, ws, flags, T, C)
             launches[0] += ccc.ccc_last_launch_count()
@@ -458,7 +470,7 @@ def run_3way_single(args, wl):
     return {"ms": ms, "kernel_ms": k_ms, "comparisons": comparisons(3, n_v, n_f),
             "launches": launches[0], "clocks": clk.summary(), "kernel": "tally3_kernel",
             "out_bytes": comparisons(3, n_v, n_f) // n_f * 96, "stages": n_st,
-            "forms_bytes": comparisons(3, n_v, n_f) // n_f * 7 * 4 * 2 if sparse else 0}
+            "forms_bytes": comparisons(3, n_v, n_f) // n_f * (7 if sparse else 2) * 4 * 2 if (sparse or paper) else 0}
 
 
 # ------------------------------------------------------------------------ main
@@ -522,7 +534,7 @@ def main():
         ops = (8.0 if wl.get("sparse") else 2.0) * r["comparisons"]
     else:
         # sparse 3-way: 8 passes (trilinear forms) = 8 MACs per comparison
-        ops = (16.0 if wl.get("sparse") else 2.0) * r["comparisons"] / wl["n_st"]
+        ops = (16.0 if wl.get("sparse") else 6.0 if wl.get("paper") else 2.0) * r["comparisons"] / wl["n_st"]
     # int8 dense = 2 x bf16 dense (the guide's nominal ratio, 4.5 vs 2.25 PFLOP/s); the
     # burst figure applies: the timed region is ~0.1 s of back-to-back steps, not seconds.
     int8_peak = 2.0 * pk["bf16_tflops"]
@@ -564,7 +576,8 @@ def main():
         roof["unit"] = "GB/s"
         roof["frac"] = roof["achieved"] / pk["hbm_gbs"]
         roof["peak_source"] = f"hbm_gbs of MEASURED_PEAKS.json ({pk_kind}); FULL output 96 B/triple" + (
-            " + 7 stored forms written and read back (56 B/triple)" if wl.get("sparse") else "")
+            " + 7 stored forms written and read back (56 B/triple)" if wl.get("sparse") else
+            " + 2 stored masked forms written and read back (16 B/triple)" if wl.get("paper") else "")
         roof["tensor_TOPS"] = achieved
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,

@@ -388,6 +388,27 @@ ccc_status ccc_3way_sparse_stage(int64_t n_v, int64_t n_f, double gamma, int64_t
                                  void* ws_d, size_t ws_bytes, void* scratch_d, size_t scratch_bytes,
                                  void* stream);
 
+/* ---- The paper's 3-way route on the tensor pipe, as a comparison baseline (SURVEY §8(f)
+ * f4(ii); §3.2: Table 1 masks P:457-516, masked tallies P:518-525, the eight
+ * reconstruction equations P:527-560 under readings A-1..A-3), with the pivot on the
+ * first index: per class xi of the pivot's genotype ((0,0), heterozygote, (1,1)) one
+ * masked pivot GEMM F_xi = sum_{q in xi(i)} n_jq n_kq (the paper's three mGEMM3 per
+ * pivot), masked marginals Mx_xi(i,x) = sum_{q in xi(i)} n_xq (three 2-way GEMMs of the
+ * masks against N, in prepare) and the class counts; then
+ *   T(0,b,c) = 2 B_1(b,c) + B_2(b,c),  T(1,b,c) = 2 B_3(b,c) + B_2(b,c),
+ * B_xi(1,1) = F_xi, B_xi(1,0) = 2Mx_xi(i,j) - F_xi, B_xi(0,1) = 2Mx_xi(i,k) - F_xi,
+ * B_xi(0,0) = 4|xi(i)| - 2Mx_xi(i,j) - 2Mx_xi(i,k) + F_xi; CCC by Eq.4 (general gamma).
+ * Same records as ccc_3way_stage (bit-identical tallies).  ws_d >= ccc_3way_paper_
+ * workspace_bytes (N, s, w, 3 masks, counts, 3 n_v^2 int32 marginals); scratch_d >=
+ * ccc_3way_paper_scratch_bytes (2 stored forms per record).  Not the product path. */
+size_t     ccc_3way_paper_workspace_bytes(int64_t n_v, int64_t n_f);
+size_t     ccc_3way_paper_scratch_bytes(int64_t n_v, int64_t n_stages, int64_t stage);
+ccc_status ccc_3way_paper_prepare(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma, void* ws_d,
+                                  size_t ws_bytes, void* stream);
+ccc_status ccc_3way_paper_stage(int64_t n_v, int64_t n_f, double gamma, int64_t n_stages, int64_t stage,
+                                uint32_t out_flags, uint32_t* tallies_d, void* ccc_d, uint64_t* checksum_d,
+                                void* ws_d, size_t ws_bytes, void* scratch_d, size_t scratch_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

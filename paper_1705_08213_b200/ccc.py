@@ -135,6 +135,11 @@ _SIGS = {
     "ccc_3way_sparse_prepare": (_int, [_vp, _i64, _i64, _dbl, _vp, _sz, _vp]),
     "ccc_3way_sparse_stage": (_int, [_i64, _i64, _dbl, _i64, _i64, _u32, _vp, _vp, _vp, _vp, _sz, _vp, _sz,
                                      _vp]),
+    "ccc_3way_paper_workspace_bytes": (_sz, [_i64, _i64]),
+    "ccc_3way_paper_scratch_bytes": (_sz, [_i64, _i64, _i64]),
+    "ccc_3way_paper_prepare": (_int, [_vp, _i64, _i64, _dbl, _vp, _sz, _vp]),
+    "ccc_3way_paper_stage": (_int, [_i64, _i64, _dbl, _i64, _i64, _u32, _vp, _vp, _vp, _vp, _sz, _vp, _sz,
+                                    _vp]),
     "ccc_e2e_workspace_bytes": (_sz, [_i64, _i64, _u32]),
     "ccc_2way_host": (_int, [_vp, _i64, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _sz, _vp]),
 }
@@ -612,3 +617,26 @@ def three_way_sparse(codes: torch.Tensor, gamma: float = GAMMA, out_flags: int =
     T = torch.cat([o[0] for o in outs]) if out_flags & OUT_TALLY else None
     C = torch.cat([o[1] for o in outs]) if out_flags & (OUT_CCC_F64 | OUT_CCC_F32) else None
     return T, C, [o[2] for o in outs] if out_flags & OUT_CHECKSUM else None
+
+
+# ------------------------------------------------------------- f4(ii): the paper's 3-way route
+def ccc_3way_paper_prepare(packed: torch.Tensor, n_f: int, gamma: float = GAMMA, ws=None, stream=None):
+    n_v = packed.shape[0]
+    if ws is None:
+        ws = torch.empty(max(256, lib().ccc_3way_paper_workspace_bytes(n_v, n_f)), dtype=torch.uint8,
+                         device=packed.device)
+    _check(lib().ccc_3way_paper_prepare(_p(packed), n_v, n_f, gamma, _p(ws), ws.numel(), _stream(stream)))
+    return ws
+
+
+def ccc_3way_paper_stage(n_v: int, n_f: int, n_stages: int, stage: int, ws: torch.Tensor,
+                         out_flags: int = OUT_TALLY | OUT_CCC_F64, tallies=None, ccc=None, checksum=None,
+                         scratch=None, gamma: float = GAMMA, stream=None):
+    rc = ccc_stage_range(n_v, n_stages, stage)[3]
+    T, C, ck = _outputs(rc, 8, out_flags, ws.device, tallies, ccc, checksum)
+    nb = lib().ccc_3way_paper_scratch_bytes(n_v, n_stages, stage)
+    if scratch is None:
+        scratch = torch.empty(max(16, nb), dtype=torch.uint8, device=ws.device)
+    _check(lib().ccc_3way_paper_stage(n_v, n_f, gamma, n_stages, stage, out_flags, _p(T), _p(C), _p(ck),
+                                      _p(ws), ws.numel(), _p(scratch), scratch.numel(), _stream(stream)))
+    return T, C, ck

@@ -734,6 +734,133 @@ ccc_status ccc_3way_sparse_stage(int64_t n_v, int64_t n_f, double gamma, int64_t
     return CCC_OK;
 }
 
+// ---------------------------------------------------------------- f4(ii): paper's route
+namespace {
+struct PapLayout {
+    size_t N = 0, s = 0, w = 0, M = 0, cnt = 0, mx = 0, total = 0;
+};
+PapLayout pap_layout(int64_t n_v, int64_t n_f) {
+    PapLayout L;
+    size_t off = 0;
+    const size_t mat = al256((size_t)n_v * (size_t)kpad_of(n_f));
+    L.N = off;
+    off += mat;
+    L.s = off;
+    off += al256((size_t)n_v * 4);
+    L.w = off;
+    off += al256((size_t)n_v * 16);
+    L.M = off;                      // 3 class masks, contiguous [3][n_v][K_pad]
+    off += al256(3 * (size_t)n_v * (size_t)kpad_of(n_f));
+    L.cnt = off;                    // [3][n_v]
+    off += al256(3 * (size_t)n_v * 4);
+    L.mx = off;                     // [3][n_v][n_v] masked marginals
+    off += al256(3 * (size_t)n_v * (size_t)n_v * 4);
+    L.total = off + 256;
+    return L;
+}
+}  // namespace
+
+size_t ccc_3way_paper_workspace_bytes(int64_t n_v, int64_t n_f) {
+    if (n_v < 0 || n_f < 1) return 0;
+    return pap_layout(n_v, n_f).total;
+}
+
+size_t ccc_3way_paper_scratch_bytes(int64_t n_v, int64_t n_stages, int64_t stage) {
+    int64_t rng[4];
+    if (n_v < 3 || ccc_stage_range(n_v, n_stages, stage, rng) != CCC_OK) return 0;
+    return (size_t)2 * (size_t)rng[3] * sizeof(uint32_t);
+}
+
+ccc_status ccc_3way_paper_prepare(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma, void* ws_d,
+                                  size_t ws_bytes, void* stream) {
+    g_launches = 0;
+    CCC_CHECK(check_sizes(n_v, n_f));
+    if (n_v < 3) return CCC_OK;
+    if (!packed_d || !aligned(packed_d, 16))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "packed_d must be non-NULL and 16-B aligned");
+    const PapLayout L = pap_layout(n_v, n_f);
+    if (!ws_d || !aligned(ws_d, 256)) return fail(CCC_ERR_INVALID_ARGUMENT, "ws_d must be 256-B aligned");
+    if (ws_bytes < L.total) return fail(CCC_ERR_WORKSPACE, "workspace too small (see ccc_3way_paper_workspace_bytes)");
+    int sms;
+    CCC_CHECK(check_device(&sms));
+    uint8_t* ws = static_cast<uint8_t*>(ws_d);
+    cudaStream_t st = (cudaStream_t)stream;
+    int8_t* N = reinterpret_cast<int8_t*>(ws + L.N);
+    int32_t* s = reinterpret_cast<int32_t*>(ws + L.s);
+    double* w = reinterpret_cast<double*>(ws + L.w);
+    int8_t* M = reinterpret_cast<int8_t*>(ws + L.M);
+    CCC_CUDA(ccc::launch_expand(packed_d, n_v, n_f, gamma, N, s, w, sms, st), "expand launch");
+    CCC_CUDA(ccc::launch_expand_masks(packed_d, n_v, n_f, M, reinterpret_cast<int32_t*>(ws + L.cnt), sms, st),
+             "expand_masks launch");
+    g_launches = 2;
+    // masked marginals Mx_xi[p][x] = sum_{q: v_pq in xi} n_xq: the tally GEMM of the mask
+    // rows against N over the full square (no records, raw G out)
+    const size_t mat = (size_t)n_v * (size_t)kpad_of(n_f);
+    for (int x = 0; x < 3; ++x)
+        CCC_CHECK(block_impl(M + x * mat, s, w, n_v, 0, 0, n_v, N, s, w, n_v, 0, 0, n_f, gamma, 0, nullptr,
+                             nullptr, nullptr, reinterpret_cast<int32_t*>(ws + L.mx) + (size_t)x * n_v * n_v, n_v,
+                             nullptr, st, sms));
+    return CCC_OK;
+}
+
+ccc_status ccc_3way_paper_stage(int64_t n_v, int64_t n_f, double gamma, int64_t n_stages, int64_t stage,
+                                uint32_t out_flags, uint32_t* tallies_d, void* ccc_d, uint64_t* checksum_d,
+                                void* ws_d, size_t ws_bytes, void* scratch_d, size_t scratch_bytes, void* stream) {
+    (void)gamma;   // the weights were formed by ccc_3way_paper_prepare
+    g_launches = 0;
+    CCC_CHECK(check_sizes(n_v, n_f));
+    if (out_flags & ~15u) return fail(CCC_ERR_INVALID_ARGUMENT, "unknown out_flags bits");
+    int64_t rng[4];
+    CCC_CHECK(ccc_stage_range(n_v, n_stages, stage, rng));
+    if (n_v < 3 || rng[3] == 0) return CCC_OK;
+    CCC_CHECK(check_outputs(out_flags, tallies_d, ccc_d, checksum_d));
+    const PapLayout L = pap_layout(n_v, n_f);
+    if (!ws_d || !aligned(ws_d, 256)) return fail(CCC_ERR_INVALID_ARGUMENT, "ws_d must be 256-B aligned");
+    if (ws_bytes < L.total) return fail(CCC_ERR_WORKSPACE, "workspace too small (see ccc_3way_paper_workspace_bytes)");
+    if (!scratch_d || !aligned(scratch_d, 16) || scratch_bytes < (size_t)2 * (size_t)rng[3] * 4)
+        return fail(CCC_ERR_WORKSPACE, "scratch too small (see ccc_3way_paper_scratch_bytes)");
+    int sms;
+    CCC_CHECK(check_device(&sms));
+    uint8_t* ws = static_cast<uint8_t*>(ws_d);
+    const int64_t k_pad = kpad_of(n_f);
+    const size_t mat = (size_t)n_v * (size_t)k_pad;
+    const int8_t* N = reinterpret_cast<const int8_t*>(ws + L.N);
+    const int32_t* s = reinterpret_cast<const int32_t*>(ws + L.s);
+    const double* w = reinterpret_cast<const double*>(ws + L.w);
+    const int8_t* M = reinterpret_cast<const int8_t*>(ws + L.M);
+    const int32_t* mx = reinterpret_cast<const int32_t*>(ws + L.mx);
+    CUtensorMap tm;
+    CCC_CHECK(make_tmap(&tm, N, n_v, k_pad, 128));
+    for (int x = 0; x < 3; ++x) {   // the three masked pivot GEMMs (the paper's 3 mGEMM3)
+        ccc::Tally3Args a{};
+        a.bp = ccc::Blk3{M + x * mat, s, w, n_v, 0};   // pivot rows: the class-xi mask
+        a.bm = a.bn = ccc::Blk3{N, s, w, n_v, 0};
+        a.p_lo = rng[0];
+        a.p_hi = rng[1];
+        a.m_hi = a.n_hi = n_v;
+        a.same_pm = a.same_mn = 1;
+        a.ldG = n_v;
+        a.rec_base = rng[2];
+        a.k_pad = k_pad;
+        a.n_f = (int32_t)n_f;
+        a.k_blocks = (int32_t)(k_pad / ccc::kBK);
+        a.out_flags = (int32_t)out_flags;
+        a.tallies = tallies_d;
+        a.ccc = ccc_d;
+        a.checksum = reinterpret_cast<unsigned long long*>(checksum_d);
+        a.forms = static_cast<uint32_t*>(scratch_d);
+        a.form_stride = rng[3];
+        a.form_self = x;
+        a.mode = x < 2 ? 1 : 3;
+        for (int y = 0; y < 3; ++y) a.mx[y] = mx + (size_t)y * n_v * n_v;
+        a.mcnt = reinterpret_cast<const int32_t*>(ws + L.cnt);
+        int64_t units = 0;
+        CCC_CUDA(ccc::launch_tally3(tm, tm, a, sms, (cudaStream_t)stream, &units), "tally3 paper-route launch");
+        if (units) ++g_launches;
+    }
+    return CCC_OK;
+}
+
 int64_t ccc_3way_unit_records(const ccc_block* bp, int64_t p_lo, int64_t p_hi,
                               const ccc_block* bm, int64_t m_lo, int64_t m_hi,
                               const ccc_block* bn, int64_t n_lo, int64_t n_hi) {

@@ -197,6 +197,10 @@ struct Tally3Args {
     uint32_t* forms;
     int64_t form_stride;
     int32_t form_self, mode;
+    // f4(ii) paper route (mode 3): masked marginals Mx[xi][p * ldG + x] = sum_{q: v_pq in xi} n_xq
+    // and class counts cnt[xi][p] (xi = 0, 1, 2 for the paper's classes 1, 2, 3)
+    const int32_t* mx[3];
+    const int32_t* mcnt;
 };
 
 }  // namespace ccc

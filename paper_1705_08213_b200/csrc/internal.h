@@ -18,6 +18,8 @@ cudaError_t launch_expand_sparse(const uint8_t* packed, int64_t n_v, int64_t n_f
 cudaError_t launch_expand_sparse3(const uint8_t* packed, int64_t n_v, int64_t n_f, double gamma, int8_t* Ns,
                                   int8_t* V, int32_t* s, int32_t* c, double* w, int num_sms,
                                   cudaStream_t stream);
+cudaError_t launch_expand_masks(const uint8_t* packed, int64_t n_v, int64_t n_f, int8_t* M, int32_t* cnt,
+                                int num_sms, cudaStream_t stream);
 int tally2_b_box_rows();  // B rows per CTA per TMA box (256 single CTA, 128 CTA pair)
 int tally2_tile_rows();   // rows of a 2-way tile (256 CTA pair, 128 single CTA)
 int64_t fs_total_tiles(int64_t n_v);   // tiles of the diag 2-way schedule (f3 waves)

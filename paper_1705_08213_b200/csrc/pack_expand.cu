@@ -190,6 +190,64 @@ cudaError_t launch_expand_sparse3(const uint8_t* packed, int64_t n_v, int64_t n_
     return cudaGetLastError();
 }
 
+// f4(ii), the paper's 3-way route (Table 1, P:457-516 with reading A-3): one int8 mask row
+// per class xi of the pivot's genotype -- xi = 1: (0,0), xi = 2: heterozygote, xi = 3:
+// (1,1) -- over the true n_f fields (K padding and tail are 0), plus the class counts.
+__global__ void __launch_bounds__(256) expand_masks_kernel(const uint32_t* __restrict__ packed, int64_t n_v,
+                                                           int64_t n_f, int64_t words_per_row, int64_t k_pad,
+                                                           int8_t* __restrict__ M, int32_t* __restrict__ cnt) {
+    __shared__ int32_t red[3][8];
+    const int64_t groups = k_pad / 16;
+    const size_t mat = (size_t)n_v * (size_t)k_pad;
+    for (int64_t i = blockIdx.x; i < n_v; i += gridDim.x) {
+        const uint32_t* prow = packed + i * words_per_row;
+        int32_t c[3] = {0, 0, 0};
+        for (int64_t g = threadIdx.x; g < groups; g += blockDim.x) {
+            const uint32_t p = g < words_per_row ? __ldg(prow + g) : 0u;
+            const int64_t left = n_f - 16 * g;
+            const uint32_t inside = left <= 0 ? 0u : left >= 16 ? 0x55555555u
+                                                                : (uint32_t)((1ull << (2 * left)) - 1) & 0x55555555u;
+            const uint32_t lo = p & 0x55555555u, hi = (p >> 1) & 0x55555555u;
+            const uint32_t cls[3] = {~(lo | hi) & inside, (lo ^ hi) & inside, lo & hi & inside};
+#pragma unroll
+            for (int x = 0; x < 3; ++x) {
+                uint32_t o[4];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    uint32_t y = (cls[x] >> (8 * b)) & 0xFFu;
+                    y = (y | (y << 12)) & 0x000F000Fu;
+                    o[b] = (y | (y << 6)) & 0x03030303u;
+                }
+                c[x] += __popc(cls[x]);
+                __stcs(reinterpret_cast<uint4*>(M + x * mat + i * k_pad) + g, make_uint4(o[0], o[1], o[2], o[3]));
+            }
+        }
+#pragma unroll
+        for (int x = 0; x < 3; ++x)
+            for (int off = 16; off > 0; off >>= 1) c[x] += __shfl_xor_sync(0xffffffffu, c[x], off);
+        if ((threadIdx.x & 31) == 0)
+            for (int x = 0; x < 3; ++x) red[x][threadIdx.x >> 5] = c[x];
+        __syncthreads();
+        if (threadIdx.x < 3) {
+            int32_t v = 0;
+            for (int k = 0; k < (int)(blockDim.x >> 5); ++k) v += red[threadIdx.x][k];
+            cnt[threadIdx.x * n_v + i] = v;
+        }
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_expand_masks(const uint8_t* packed, int64_t n_v, int64_t n_f, int8_t* M, int32_t* cnt,
+                                int num_sms, cudaStream_t stream) {
+    const int64_t wpr = (n_f + 63) / 64 * 4;
+    const int64_t k_pad = (n_f + 127) / 128 * 128;
+    int64_t blocks = n_v < (int64_t)num_sms * 8 ? n_v : (int64_t)num_sms * 8;
+    if (blocks < 1) blocks = 1;
+    expand_masks_kernel<<<(int)blocks, 256, 0, stream>>>(reinterpret_cast<const uint32_t*>(packed), n_v, n_f,
+                                                         wpr, k_pad, M, cnt);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pack(const uint8_t* codes, int64_t n_v, int64_t n_f, uint8_t* packed,
                         int num_sms, cudaStream_t stream) {
     const int64_t wpr = (n_f + 63) / 64 * 4;

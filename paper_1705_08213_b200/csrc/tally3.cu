@@ -258,8 +258,77 @@ __device__ __forceinline__ void sparse3_record(const Tally3Args& a, bool ok, uin
     }
 }
 
+// f4(ii): the paper's 3-way route on the tensor pipe (§3.2, Table 1 P:457-516,
+// masked tallies P:518-525, reconstruction P:527-560 under readings A-1..A-3), pivot on
+// the first index: with the class masks of the pivot's genotype (xi = 1: (0,0),
+// 2: heterozygote, 3: (1,1)), F_xi = sum_{q in xi(p)} n_m n_n is one masked pivot GEMM
+// (passes 1, 2 stored, pass 3 here), and over q in xi(p)
+//   B_xi(1,1) = F_xi, B_xi(1,0) = 2 Mx_xi(p,m) - F_xi, B_xi(0,1) = 2 Mx_xi(p,n) - F_xi,
+//   B_xi(0,0) = 4 |xi(p)| - 2 Mx_xi(p,m) - 2 Mx_xi(p,n) + F_xi,
+// then T(0,b,c) = 2 B_1(b,c) + B_2(b,c), T(1,b,c) = 2 B_3(b,c) + B_2(b,c) (the pivot's
+// allele counts: rho(0) = 2 [(0,0)] + [het], rho(1) = 2 [(1,1)] + [het]).
+template <class O>
+__device__ __forceinline__ void paper3_record(const Tally3Args& a, bool ok, uint32_t g3, int64_t rec,
+                                              const double (&wpm)[4], double wn0, double wn1,
+                                              const uint32_t (&mxm)[3], const uint32_t (&cp)[3], int64_t gp,
+                                              int64_t gm, int64_t gn, bool want_t, bool want_c64,
+                                              bool want_c32, bool want_ck, unsigned long long& ck_lo,
+                                              unsigned long long& ck_hi) {
+    const int64_t rc = ok ? rec : 0;
+    uint32_t F[3], mxn[3];
+    F[0] = ok ? __ldg(a.forms + rc) : 0u;
+    F[1] = ok ? __ldg(a.forms + a.form_stride + rc) : 0u;
+    F[2] = g3;
+#pragma unroll
+    for (int x = 0; x < 3; ++x) mxn[x] = ok ? (uint32_t)__ldg(a.mx[x] + gp * a.ldG + gn) : 0u;
+    uint32_t B[3][4];   // [xi][2 b + c]
+#pragma unroll
+    for (int x = 0; x < 3; ++x) {
+        B[x][3] = F[x];
+        B[x][2] = 2u * mxm[x] - F[x];
+        B[x][1] = 2u * mxn[x] - F[x];
+        B[x][0] = 4u * cp[x] - 2u * mxm[x] - 2u * mxn[x] + F[x];
+    }
+    uint32_t t[8];
+#pragma unroll
+    for (int bc = 0; bc < 4; ++bc) {
+        t[bc] = 2u * B[0][bc] + B[1][bc];       // pivot allele 0
+        t[4 + bc] = 2u * B[2][bc] + B[1][bc];   // pivot allele 1
+    }
+    double cr[8];
+#pragma unroll
+    for (int ab = 0; ab < 4; ++ab) {
+        cr[2 * ab + 0] = (double)t[2 * ab + 0] * wpm[ab] * wn0;
+        cr[2 * ab + 1] = (double)t[2 * ab + 1] * wpm[ab] * wn1;
+    }
+    uint32_t tc[8];
+    double cc[8];
+    perm_cells<O::R0, O::R1, O::R2>(t, tc);
+    perm_cells<O::R0, O::R1, O::R2>(cr, cc);
+    if (want_t)
+        stg_256_u32_if(ok, a.tallies + 8 * rec, tc[0], tc[1], tc[2], tc[3], tc[4], tc[5], tc[6], tc[7]);
+    if (want_c64) {
+        double* q = reinterpret_cast<double*>(a.ccc) + 8 * rec;
+        stg_256_f64_if(ok, q, cc[0], cc[1], cc[2], cc[3]);
+        stg_256_f64_if(ok, q + 4, cc[4], cc[5], cc[6], cc[7]);
+    } else if (want_c32) {
+        float* q = reinterpret_cast<float*>(a.ccc) + 8 * rec;
+        stg_256_u32_if(ok, q, __float_as_uint((float)cc[0]), __float_as_uint((float)cc[1]),
+                       __float_as_uint((float)cc[2]), __float_as_uint((float)cc[3]),
+                       __float_as_uint((float)cc[4]), __float_as_uint((float)cc[5]),
+                       __float_as_uint((float)cc[6]), __float_as_uint((float)cc[7]));
+    }
+    if (want_ck && ok) {
+        const int64_t g[3] = {gp, gm, gn};
+        ck_fold3(ck_lo, ck_hi,
+                 (3ull << 60) | ((uint64_t)g[O::R0] << 40) | ((uint64_t)g[O::R1] << 20) | (uint64_t)g[O::R2],
+                 tc);
+    }
+}
+
 // kMode: 0 dense CCC; 1 sparse form pass (store the raw trilinear form G3 of this pass);
-// 2 sparse final pass (read the 7 stored forms, build the sparse tallies + CCC)
+// 2 sparse final pass (read the 7 stored forms, build the sparse tallies + CCC);
+// 3 paper-route final pass (f4 ii: read 2 stored masked forms + masked marginals)
 template <int kOrder, bool kExact, bool kCompact, bool kFull, int kMode = 0>
 __global__ void __launch_bounds__(kThreads3, 1)
 tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -514,6 +583,11 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             uint64_t upm[2][4];          // kFull: U_p(a_p) U_m(a_m) as integers
             const int32_t* grow[2];      // kRowG: &G[gm][gcol0]
             bool my_any = false;
+            uint32_t cp3[3] = {0u, 0u, 0u}, mxm3[2][3] = {{0u, 0u, 0u}, {0u, 0u, 0u}};   // kMode 3
+            if constexpr (kMode == 3) {
+#pragma unroll
+                for (int x = 0; x < 3; ++x) cp3[x] = (uint32_t)__ldg(args.mcnt + x * args.ldG + gp);
+            }
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
                 const int64_t m = sch.row0(J) + rank * 128 + quad * 32 + half * 16 + r * 8 + (lane >> 2);
@@ -559,6 +633,10 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 const int64_t lo = args.same_mn ? m - col0 : -1;
                 lo_r[r] = !ok ? kBN : lo < -1 ? -1 : lo > kBN ? kBN : (int32_t)lo;
                 grow[r] = args.G + gm_r[r] * args.ldG + gcol0;
+                if constexpr (kMode == 3) {
+#pragma unroll
+                    for (int x = 0; x < 3; ++x) mxm3[r][x] = (uint32_t)__ldg(args.mx[x] + gp * args.ldG + gm_r[r]);
+                }
                 my_any |= ok;
             }
 #ifdef CCC_D3_NOEPI
@@ -626,6 +704,12 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                             // sparse form pass: the raw trilinear form of this pass
                             const int64_t rec = rec_r[r] + nl;
                             st_u32_if(ok, args.forms + (int64_t)args.form_self * args.form_stride + rec, g3);
+                            continue;
+                        }
+                        if constexpr (kMode == 3) {
+                            paper3_record<O>(args, ok, g3, rec_r[r] + nl, wpm[r], cn.w0, cn.w1, mxm3[r], cp3, gp,
+                                             gm_r[r], gcol0 + nl, want_t, want_c64, want_c32, want_ck, ck_lo,
+                                             ck_hi);
                             continue;
                         }
                         if constexpr (kMode == 2) {
@@ -782,6 +866,7 @@ cudaError_t launch_tally3(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
     };
     if (a.mode == 1) return go(tally3_kernel<0, false, false, false, 1>);   // sparse passes:
     if (a.mode == 2) return go(tally3_kernel<0, false, false, false, 2>);   // order 0 only
+    if (a.mode == 3) return go(tally3_kernel<0, false, false, false, 3>);
     using T = std::true_type;
     using F = std::false_type;
     // FULL with gamma = 2/3 (tallies + fp64 CCC, no checksum) gets a flag-free epilogue
