@@ -4,14 +4,15 @@ cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_elapsed,lts__t_sector_hit_rate.pct,sm__cycles_elapsed.avg.per_second
 echo "== bench lines (no profiler)"
-for wl in c2 c4 c2s c2pop c2fs; do
+for wl in c2 c4 c2s c4s c4paper c2pop c2fs; do
   E=--no-e2e; C=--no-cpu; [ $wl = c2 ] && E= && C=
-  timeout 900 python bench.py --workload $wl --steps ${STEPS:-5} --warmup 3 $E $C > gpurun_out/bench_$wl.json 2> gpurun_out/bench_$wl.err
+  ST=${STEPS:-5}; [ $wl = c4s ] && ST=1; [ $wl = c4paper ] && ST=1; [ $wl = c4 ] && ST=2
+  timeout 900 python bench.py --workload $wl --steps $ST --warmup 3 $E $C > gpurun_out/bench_$wl.json 2> gpurun_out/bench_$wl.err
   tail -1 gpurun_out/bench_$wl.json | cut -c1-200
 done
 echo "== launch lists"
-for wl in c2 c4 c2pop c2fs c2s; do
-  S=2; [ $wl = c4 ] && S=1; [ $wl = c2pop ] && S=1
+for wl in c2 c4 c2pop c2fs c2s c4s c4paper; do
+  S=2; [ $wl = c4 ] && S=1; [ $wl = c2pop ] && S=1; [ $wl = c4s ] && S=1; [ $wl = c4paper ] && S=1
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_$wl.csv python bench.py --workload $wl --steps $S --warmup 1 --no-e2e --no-cpu > /dev/null 2> gpurun_out/launches_$wl.err
   tail -1 gpurun_out/launches_$wl.err

@@ -17,7 +17,7 @@ PROF = os.path.join(ROOT, "profiles")
 
 def short(name):
     for k in ("popc_tally2_kernel", "popc_stats_kernel", "fs_finish_kernel", "tally2_kernel",
-              "tally3_kernel", "pack_kernel", "expand_kernel"):
+              "tally3_kernel", "pack_kernel", "expand_masks_kernel", "expand_sparse_kernel", "expand_kernel"):
         if k in name:
             return k
     return name.split("(")[0][:60]
@@ -42,7 +42,7 @@ def launches(path):
         agg[k][0] += 1
         agg[k][1] += ns
     ours = {"tally2_kernel", "tally3_kernel", "pack_kernel", "expand_kernel", "popc_tally2_kernel",
-            "popc_stats_kernel", "fs_finish_kernel"}
+            "popc_stats_kernel", "fs_finish_kernel", "expand_masks_kernel", "expand_sparse_kernel"}
     tot = sum(v[1] for k, v in agg.items() if k in ours)   # the step = our kernels only
     res = {k: {"launches": c, "total_ms": t / 1e6, "mean_ms": t / 1e6 / c, "share_of_step": t / tot}
            for k, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]) if k in ours}
@@ -88,7 +88,7 @@ def main():
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     summary = {}
-    WLS = ("c2", "c4", "c2pop", "c2fs", "c2s")
+    WLS = ("c2", "c4", "c2pop", "c2fs", "c2s", "c4s", "c4paper")
     for wl in WLS:
         p = os.path.join(OUT, f"launches_{wl}.csv")
         if os.path.exists(p):
