@@ -65,12 +65,23 @@ __global__ void __launch_bounds__(256) fs_finish_kernel(const int32_t* __restric
         const uint32_t sj = col_ok ? (uint32_t)__ldg(s + j) : 0u;
         const double wj0 = 1.0 - gamma * ((two_nf - (double)sj) / two_nf);
         const double wj1 = 1.0 - gamma * ((double)sj / two_nf);
-        for (int32_t row = 0; row < tile_m; ++row) {
+        constexpr int kR = 4;   // rows in flight per thread (memory-level parallelism)
+        for (int32_t row0 = 0; row0 < tile_m; row0 += kR) {
+          uint32_t Gr[kR];
+#pragma unroll
+          for (int u = 0; u < kR; ++u) {
+            const int64_t i = (int64_t)bm * tile_m + row0 + u;
+            Gr[u] = 0;
+            if (i < n_v - 1 && col_ok && j > i)
+                for (int32_t f = 0; f < world; ++f)
+                    Gr[u] += (uint32_t)__ldg(tile + ((int64_t)f << 16) + (row0 + u) * kBN + col);
+          }
+#pragma unroll
+          for (int u = 0; u < kR; ++u) {
+            const int32_t row = row0 + u;
             const int64_t i = (int64_t)bm * tile_m + row;
-            if (i >= n_v - 1) break;                       // row-uniform
-            if (!col_ok || j <= i) continue;
-            uint32_t G = 0;
-            for (int32_t f = 0; f < world; ++f) G += (uint32_t)__ldg(tile + ((int64_t)f << 16) + row * kBN + col);
+            if (i >= n_v - 1 || !col_ok || j <= i) continue;
+            const uint32_t G = Gr[u];
             const uint32_t si = (uint32_t)__ldg(s + i);
             const uint32_t t11 = G, t10 = 2u * si - G, t01 = 2u * sj - G;
             const uint32_t t00 = four_nf - 2u * si - 2u * sj + G;
@@ -91,6 +102,7 @@ __global__ void __launch_bounds__(256) fs_finish_kernel(const int32_t* __restric
             if (want_ck)
                 fs_fold(ck_lo, ck_hi, (2ull << 60) | ((uint64_t)i << 40) | ((uint64_t)j << 20),
                         (uint64_t)t00 | ((uint64_t)t01 << 32), (uint64_t)t10 | ((uint64_t)t11 << 32));
+          }
         }
     }
     if (want_ck) {
