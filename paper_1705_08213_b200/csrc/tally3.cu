@@ -30,7 +30,19 @@
 namespace ccc {
 
 constexpr int kTileM3 = 256;         // pair tile rows (UMMA M = 256, cta_group::2)
-constexpr int kStages3 = 6;
+// Experimental (off): FULL-mode fp64 CCC records leave through shared memory and TMA
+// bulk stores (512-B row segments) instead of per-thread 256-bit global stores.  Measured
+// at C4: without the epilogue's global-store traffic the mainloop runs 64 instead of 96 us
+// per unit, but staging the records conflict-free (XOR-rotated 16-B chunks, 64-B row pad)
+// costs the epilogue 122-136 us per unit against 70 us with direct stores: 32.3 ms per
+// stage against 20.6 ms.  Kept for the next attempt (needs a cheaper staging layout).
+#ifndef CCC_TMA_STORE
+#define CCC_TMA_STORE 0
+#endif
+#ifndef CCC_STAGES3
+#define CCC_STAGES3 (CCC_TMA_STORE ? 4 : 6)
+#endif
+constexpr int kStages3 = CCC_STAGES3;
 constexpr int kABytes3 = 128 * kBK;  // 16 KB: this CTA's 128 rows of A
 constexpr int kBBytes3 = 128 * kBK;  // 16 KB: this CTA's 128 rows of B
 constexpr int kEpiWarps3 = 8;        // 2 per TMEM lane quadrant
@@ -48,7 +60,10 @@ struct ColT3 {
     double m0, m1;               // -2^52 w0, -2^52 w1 (kFull cell formula)
 };
 constexpr int kColOff3 = kPivOff3 + kStages3 * kPivBytes;
-constexpr int kBarOff3 = kColOff3 + 2 * kBN * (int)sizeof(ColT3);
+constexpr int kStgRow3 = 512 + 64;        // one staged row segment (8 records x 64 B) + bank pad
+constexpr int kStgBytes3 = 8 * kStgRow3;  // one staging buffer: 8 rows of CCC
+constexpr int kStgOff3 = kColOff3 + 2 * kBN * (int)sizeof(ColT3);
+constexpr int kBarOff3 = kStgOff3 + (CCC_TMA_STORE ? 8 * 2 * kStgBytes3 : 0);
 constexpr int kSmem3 = kBarOff3 + 512 + 1024;
 static_assert(kSmem3 <= 232448, "3-way shared memory");
 
@@ -531,6 +546,8 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         const uint32_t cpair = 2u * (lane & 3u);
         constexpr bool kRowG = O::pos(1) < O::pos(2);   // G_mn = G[gm][gn]: a row of G per m
         ColT3* coltab = reinterpret_cast<ColT3*>(smem + kColOff3);
+        uint8_t* stg = smem + kStgOff3 + (warp - 2) * 2 * kStgBytes3;   // 2 buffers (row halves r)
+        constexpr bool kBulk = kFull && CCC_TMA_STORE && kMode == 0;
         unsigned long long ck_lo = 0, ck_hi = 0;
         uint32_t acc = 0, acc_phase = 0;
         for (int64_t u = unit0;; u += units) {
@@ -692,6 +709,16 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 const ColT3 cA = ct[nA], cB = ct[nA + 1];
 #pragma unroll
                 for (int r = 0; r < 2; ++r) {
+                    // kBulk: this row's 8-record segment leaves by one 512-B bulk store if
+                    // all 8 records are valid; buffer r must be free of the bulk store
+                    // issued from it one column group ago
+                    const bool seg_ok = kBulk && (8 * c > lo_r[r]) && (8 * c + 8 <= nval);
+                    if constexpr (kBulk) {
+#ifndef CCC_D3_NOBULKWAIT
+                        if (lane < 8) bulk_wait_read<1>();
+#endif
+                        __syncwarp();
+                    }
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         // every record is computed; invalid ones (tile edges, j <= i) are
@@ -771,8 +798,28 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                                 }
                             } else if (want_c64) {
                                 double* q = reinterpret_cast<double*>(args.ccc) + 8 * rec;
-                                stg_256_f64_if(st_ok, q, cc[0], cc[1], cc[2], cc[3]);
-                                stg_256_f64_if(st_ok, q + 4, cc[4], cc[5], cc[6], cc[7]);
+                                if constexpr (kBulk) {
+                                    // stage record (row lane/4, column cpair + h); chunk
+                                    // k ^ (lane & 3) in step k: the 4 pairs of a row hit 4
+                                    // different bank groups, the 64-B row pad separates rows
+                                    uint8_t* rp = stg + r * kStgBytes3 + (lane >> 2) * kStgRow3 +
+                                                  (cpair + h) * 64;
+                                    const uint32_t q4 = lane & 3u;
+#pragma unroll
+                                    for (uint32_t k = 0; k < 4; ++k) {
+                                        const uint32_t kk = k ^ q4;
+                                        const double d0 = kk == 0 ? cc[0] : kk == 1 ? cc[2] : kk == 2 ? cc[4] : cc[6];
+                                        const double d1 = kk == 0 ? cc[1] : kk == 1 ? cc[3] : kk == 2 ? cc[5] : cc[7];
+                                        sts_v4_f64x2(rp + kk * 16, d0, d1);
+                                    }
+                                    if (!seg_ok) {
+                                        stg_256_f64_if(st_ok, q, cc[0], cc[1], cc[2], cc[3]);
+                                        stg_256_f64_if(st_ok, q + 4, cc[4], cc[5], cc[6], cc[7]);
+                                    }
+                                } else {
+                                    stg_256_f64_if(st_ok, q, cc[0], cc[1], cc[2], cc[3]);
+                                    stg_256_f64_if(st_ok, q + 4, cc[4], cc[5], cc[6], cc[7]);
+                                }
                             } else {
                                 float* q = reinterpret_cast<float*>(args.ccc) + 8 * rec;
                                 stg_256_u32_if(st_ok, q, __float_as_uint((float)cc[0]), __float_as_uint((float)cc[1]),
@@ -789,6 +836,24 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                                      tc);
                         }
                     }
+                    if constexpr (kBulk) {
+                        uint8_t* buf = stg + r * kStgBytes3;
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        const int64_t rb = (int64_t)__shfl_sync(0xffffffffu, (unsigned long long)rec_r[r],
+                                                                (lane & 7u) * 4u);
+                        const int32_t lo = __shfl_sync(0xffffffffu, lo_r[r], (lane & 7u) * 4u);
+                        if (lane < 8) {
+#ifdef CCC_D3_NOBULKISSUE
+                            if (false)
+#else
+                            if ((8 * c > lo) && (8 * c + 8 <= nval))
+#endif
+                                bulk_store(reinterpret_cast<double*>(args.ccc) + 8 * (rb + 8 * c),
+                                           buf + lane * kStgRow3, 512);
+                            bulk_commit();
+                        }
+                    }
                 }
             }
             tc_fence_before();
@@ -801,6 +866,7 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
         if (want_ck) ck_flush3(ck_lo, ck_hi, args.checksum);
+        if (lane < 8) bulk_wait<0>();   // bulk stores complete before the CTA exits
     }
 
     tc_fence_before();
