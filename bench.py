@@ -1,7 +1,7 @@
 """bench.py -- CCC comparisons/s of the B200 hot path.
 
 python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                [--workload c2|c4|c1|c2s|c4s|c2pop|c2fs|c4paper] [--no-e2e] [--no-cpu]
+                [--workload c2|c4|c1|c2s|c4s|c4f32|c4ck|c2pop|c2fs|c4paper] [--no-e2e] [--no-cpu]
 
 One step = one pass of the whole hot path over one synthetic batch resident in HBM:
   2-way (default, BASELINE configs[1] = C2: 20,000 vectors x 50,000 individuals):
@@ -53,6 +53,11 @@ WORKLOADS = {
     "c4paper": dict(way=3, n_v=4096, n_f=16384, n_st=16, paper=True,
                     label="3-way CCC, 4,096 x 16,384, 16 stages, the paper's Table-1 route (3 masked pivot "
                           "GEMMs + reconstruction) on the tensor pipe (SURVEY f4 baseline)"),
+    "c4f32": dict(way=3, n_v=4096, n_f=16384, n_st=16, flags="f32",
+                  label="3-way CCC, 4,096 x 16,384, 16 stages, FULL with fp32 CCC (64 B/triple; SURVEY 8(d))"),
+    "c4ck": dict(way=3, n_v=4096, n_f=16384, n_st=16, flags="ck",
+                 label="3-way CCC, 4,096 x 16,384, 16 stages, CHECKSUM mode (every record computed and "
+                       "folded, none stored; SURVEY 8(d) -- not a headline)"),
     "c4": dict(way=3, n_v=4096, n_f=16384, n_st=16,
                label="3-way CCC, 4,096 SNP vectors x 16,384 individuals, 16 stages (configs[3])"),
 }
@@ -406,7 +411,9 @@ def run_3way_single(args, wl):
     paper = wl.get("paper", False)
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
-    flags = ccc.OUT_TALLY | ccc.OUT_CCC_F64
+    flags = {"f32": ccc.OUT_TALLY | ccc.OUT_CCC_F32, "ck": ccc.OUT_CHECKSUM}.get(
+        wl.get("flags"), ccc.OUT_TALLY | ccc.OUT_CCC_F64)
+    rec_bytes = {"f32": 64, "ck": 0}.get(wl.get("flags"), 96)
     if sparse:
         codes = synthgen.sparse_codes(n_v, n_f, seed=4, device=dev)
     else:
@@ -423,8 +430,13 @@ def run_3way_single(args, wl):
     else:
         ws = ccc.workspace(3, n_v, n_f, dev)
     rmax = max(ccc.ccc_stage_range(n_v, n_st, s)[3] for s in range(n_st))
-    T = torch.empty((rmax, 8), dtype=torch.int32, device=dev)
-    C = torch.empty((rmax, 8), dtype=torch.float64, device=dev)
+    T = torch.empty((rmax, 8), dtype=torch.int32, device=dev) if flags & ccc.OUT_TALLY else None
+    C = None
+    if flags & ccc.OUT_CCC_F64:
+        C = torch.empty((rmax, 8), dtype=torch.float64, device=dev)
+    elif flags & ccc.OUT_CCC_F32:
+        C = torch.empty((rmax, 8), dtype=torch.float32, device=dev)
+    ck = torch.zeros(2, dtype=torch.int64, device=dev) if flags & ccc.OUT_CHECKSUM else None
     stream = torch.cuda.current_stream()
     launches = [0]
 
@@ -446,7 +458,7 @@ def run_3way_single(args, wl):
             elif paper:
                 ccc.ccc_3way_paper_stage(n_v, n_f, n_st, st, ws, flags, T, C, None, scratch)
             else:
-                ccc.ccc_3way_stage(n_v, n_f, n_st, st, ws, flags, T, C)
+                ccc.ccc_3way_stage(n_v, n_f, n_st, st, ws, flags, T, C, ck)
             launches[0] += ccc.ccc_last_launch_count()
             if ev:
                 ev[st][1].record(stream)
@@ -469,7 +481,7 @@ def run_3way_single(args, wl):
     k_ms = sum(a.elapsed_time(b) for st in kev for a, b in st) / (args.steps * n_st)
     return {"ms": ms, "kernel_ms": k_ms, "comparisons": comparisons(3, n_v, n_f),
             "launches": launches[0], "clocks": clk.summary(), "kernel": "tally3_kernel",
-            "out_bytes": comparisons(3, n_v, n_f) // n_f * 96, "stages": n_st,
+            "out_bytes": comparisons(3, n_v, n_f) // n_f * rec_bytes, "stages": n_st,
             "forms_bytes": comparisons(3, n_v, n_f) // n_f * (7 if sparse else 2) * 4 * 2 if (sparse or paper) else 0}
 
 
@@ -569,13 +581,16 @@ def main():
                 "peak_source": "148 SMs x 16 POPC/clk/SM x sampled SM clock (DESIGN.md §6)",
                 "tensor_path_equiv_frac_of_int8_peak": 2.0 * r["comparisons"] / k_s / 1e12 / int8_peak}
         roof["frac"] = roof["achieved"] / roof["peak"]
-    if wl["way"] == 3:
+    if wl["way"] == 3 and wl.get("flags") == "ck":
+        roof["peak_source"] += "; CHECKSUM mode: no record is stored, the tensor-pipe line is the roofline"
+    elif wl["way"] == 3:
         roof["bound"] = "hbm"
         roof["achieved"] = (r["out_bytes"] + r.get("forms_bytes", 0)) / wl["n_st"] / k_s / 1e9
         roof["peak"] = pk["hbm_gbs"]
         roof["unit"] = "GB/s"
         roof["frac"] = roof["achieved"] / pk["hbm_gbs"]
-        roof["peak_source"] = f"hbm_gbs of MEASURED_PEAKS.json ({pk_kind}); FULL output 96 B/triple" + (
+        rb = 64 if wl.get("flags") == "f32" else 96
+        roof["peak_source"] = f"hbm_gbs of MEASURED_PEAKS.json ({pk_kind}); FULL output {rb} B/triple" + (
             " + 7 stored forms written and read back (56 B/triple)" if wl.get("sparse") else
             " + 2 stored masked forms written and read back (16 B/triple)" if wl.get("paper") else "")
         roof["tensor_TOPS"] = achieved
@@ -589,7 +604,9 @@ def main():
                    "input": ("type-3 sparse HWE codes, seed 4, missing marker (1,0) with "
                              "per-vector rate U(0, 0.3) (P:1028-1043)") if wl.get("sparse") else
                             "type-1 uniform random 2-bit codes, seed 1 (P:657)",
-                   "output": "FULL: uint32 tallies + fp64 CCC for every unique record",
+                   "output": {"f32": "FULL: uint32 tallies + fp32 CCC for every unique record",
+                              "ck": "CHECKSUM: every record computed and folded into the 128-bit checksum, none stored"
+                              }.get(wl.get("flags"), "FULL: uint32 tallies + fp64 CCC for every unique record"),
                    "l2": ("inputs larger than L2 (codes %.2f GB, N %.2f GB)" % (
                        wl["n_v"] * wl["n_f"] / 1e9, wl["n_v"] * wl["n_f"] / 1e9)) if wl["way"] == 2 else
                          ("operands L2-resident by design (N %.2f GB, G %.2f GB); each stage writes "
