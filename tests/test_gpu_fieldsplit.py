@@ -111,3 +111,33 @@ def test_field_split_two_gpus_ipc():
     codes = synthgen.random_codes(n_v, n_f, seed=9, device="cuda")
     _, _, ck = ccc.two_way(codes, out_flags=CK)
     assert total == ccc.checksum_int(ck)
+
+
+def _worker_one_gpu(rank, world, port, n_v, n_f, q):
+    """Two processes on cuda:0: the real FieldSplit2Way (CUDA IPC slot buffers opened in
+    the other process, gloo for the collectives) -- the multi-process path without NVLink."""
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    codes = synthgen.random_codes(n_v, n_f, seed=9, device="cuda")
+    fs = fieldsplit.FieldSplit2Way(rank, world, n_v, n_f, wave_tiles=2, out_flags=TAL | CK)
+    T, _, ck = fs.run(codes[:, fs.f0:fs.f1].contiguous())
+    torch.cuda.synchronize()
+    rows = [ccc.ccc_pair_index(n_v, i, j) for i, j in ((0, 1), (5, n_v - 1), (n_v - 2, n_v - 1))]
+    q.put((rank, ccc.checksum_int(ck), T[rows].cpu().numpy()))
+    fs.close()
+    dist.destroy_process_group()
+
+
+def test_field_split_ipc_two_processes_one_gpu():
+    import torch.multiprocessing as mp
+    n_v, n_f, world = 700, 3000, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.spawn(_worker_one_gpu, args=(world, _free_port(), n_v, n_f, q), nprocs=world)
+    res = [q.get() for _ in range(world)]
+    total = sum(r[1] for r in res) % (1 << 128)
+    codes = synthgen.random_codes(n_v, n_f, seed=9)
+    To, _ = oracle.all_pairs(codes)
+    assert total == oracle.checksum(2, oracle.pair_list(n_v), To)
