@@ -58,6 +58,7 @@ struct ColT3 {
     uint32_t gpn2, cn, en, sn;   // 2 G_pn, 4 s_n - 2 G_pn, 2 G_pn - 4 s_n, s_n (mod 2^32)
     double w0, w1;               // n-side weights (exact: U_n(c) / (216 n_f^4))
     double m0, m1;               // -2^52 w0, -2^52 w1 (kFull cell formula)
+    float f0, f1;                // w0, w1 in fp32 (kF32 cell formula)
 };
 constexpr int kColOff3 = kPivOff3 + kStages3 * kPivBytes;
 constexpr int kStgRow3 = 512 + 64;        // one staged row segment (8 records x 64 B) + bank pad
@@ -344,7 +345,7 @@ __device__ __forceinline__ void paper3_record(const Tally3Args& a, bool ok, uint
 // kMode: 0 dense CCC; 1 sparse form pass (store the raw trilinear form G3 of this pass);
 // 2 sparse final pass (read the 7 stored forms, build the sparse tallies + CCC);
 // 3 paper-route final pass (f4 ii: read 2 stored masked forms + masked marginals)
-template <int kOrder, bool kExact, bool kCompact, bool kFull, int kMode = 0>
+template <int kOrder, bool kExact, bool kCompact, bool kFull, int kMode = 0, bool kF32 = false>
 __global__ void __launch_bounds__(kThreads3, 1)
 tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const Tally3Args args) {
@@ -535,9 +536,12 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         const uint32_t quad = warp & 3;
         const uint32_t half = (uint32_t)(warp - 2) >> 2;
         const uint32_t fl = (uint32_t)args.out_flags;
-        // kFull: out_flags == tallies + fp64 CCC (the FULL headline mode), no runtime tests
-        const bool want_t = kFull || (fl & 1u), want_c64 = kFull || (fl & 2u);
-        const bool want_c32 = !kFull && (fl & 4u), want_ck = !kFull && (fl & 8u);
+        // kFull: out_flags == tallies + fp64 CCC (the FULL headline mode), no runtime tests;
+        // kF32: tallies + fp32 CCC with gamma = 2/3, the cells formed in FP32 only
+        const bool want_t = kFull || kF32 || (fl & 1u);
+        const bool want_c64 = kFull || (!kF32 && (fl & 2u));
+        const bool want_c32 = kF32 || (!kFull && (fl & 4u));
+        const bool want_ck = !kFull && !kF32 && (fl & 8u);
         const bool want_c = want_c64 | want_c32;
         const uint32_t eight_nf = 8u * (uint32_t)args.n_f;
         const double inv8nf = 1.0 / (8.0 * (double)args.n_f);
@@ -580,6 +584,8 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     v.w1 = (double)(3u * nf - sn) * args.inv_d;
                     v.m0 = -4503599627370496.0 * v.w0;
                     v.m1 = -4503599627370496.0 * v.w1;
+                    v.f0 = (float)v.w0;
+                    v.f1 = (float)v.w1;
                 } else {
                     v.w0 = __ldg(args.bn.w + 2 * nc);
                     v.w1 = __ldg(args.bn.w + 2 * nc + 1);
@@ -598,6 +604,7 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             uint32_t gpm2[2], A_r[2], B_r[2], D_r[2], s_m[2], g_pm[2];
             double wpm[2][4];            // general: w_p(a_p) w_m(a_m) / (8 n_f); exact: U_p U_m
             uint64_t upm[2][4];          // kFull: U_p(a_p) U_m(a_m) as integers
+            float upmf[2][4];            // kF32: the same in fp32
             const int32_t* grow[2];      // kRowG: &G[gm][gcol0]
             bool my_any = false;
             uint32_t cp3[3] = {0u, 0u, 0u}, mxm3[2][3] = {{0u, 0u, 0u}, {0u, 0u, 0u}};   // kMode 3
@@ -620,7 +627,12 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 D_r[r] = eight_nf - 4u * s_p - 4u * s_m[r] + 2u * gpm;
                 if constexpr (kExact) {
                     const uint64_t um0 = nf + s_m[r], um1 = 3u * nf - s_m[r];
-                    if constexpr (kFull) {
+                    if constexpr (kF32) {
+                        upmf[r][0] = (float)(up0 * um0);
+                        upmf[r][1] = (float)(up0 * um1);
+                        upmf[r][2] = (float)(up1 * um0);
+                        upmf[r][3] = (float)(up1 * um1);
+                    } else if constexpr (kFull) {
                         upm[r][0] = up0 * um0;
                         upm[r][1] = up0 * um1;
                         upm[r][2] = up1 * um0;
@@ -771,7 +783,9 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                             double cr[8], cc[8];
 #pragma unroll
                             for (int ab = 0; ab < 4; ++ab) {
-                                if constexpr (kFull) {
+                                if constexpr (kF32) {
+                                    cr[2 * ab + 0] = cr[2 * ab + 1] = 0.0;   // formed in FP32 below
+                                } else if constexpr (kFull) {
                                     // P = T U_p U_m < 2^52 in integers; the double 2^52 + P is
                                     // P's bits under exponent 0x433, so CCC = P w_n =
                                     // fma(2^52 + P, w_n, -2^52 w_n): one rounding, one FP64 op
@@ -820,6 +834,24 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                                     stg_256_f64_if(st_ok, q, cc[0], cc[1], cc[2], cc[3]);
                                     stg_256_f64_if(st_ok, q + 4, cc[4], cc[5], cc[6], cc[7]);
                                 }
+                            } else if constexpr (kF32) {
+                                // fp32 only: T < 2^23 is exact as (2^23 + T) - 2^23, U_p U_m and
+                                // U_n / (216 n_f^4) rounded once each: error < 4 x 2^-24 << 1e-6
+                                float cf[8], cfo[8];
+#pragma unroll
+                                for (int ab = 0; ab < 4; ++ab) {
+#pragma unroll
+                                    for (int c1 = 0; c1 < 2; ++c1) {
+                                        const float tf = __int_as_float(0x4B000000 | (int)t[2 * ab + c1]) - 8388608.0f;
+                                        cf[2 * ab + c1] = tf * (upmf[r][ab] * (c1 ? cn.f1 : cn.f0));
+                                    }
+                                }
+                                perm_cells<O::R0, O::R1, O::R2>(cf, cfo);
+                                float* q = reinterpret_cast<float*>(args.ccc) + 8 * rec;
+                                stg_256_u32_if(st_ok, q, __float_as_uint(cfo[0]), __float_as_uint(cfo[1]),
+                                               __float_as_uint(cfo[2]), __float_as_uint(cfo[3]),
+                                               __float_as_uint(cfo[4]), __float_as_uint(cfo[5]),
+                                               __float_as_uint(cfo[6]), __float_as_uint(cfo[7]));
                             } else {
                                 float* q = reinterpret_cast<float*>(args.ccc) + 8 * rec;
                                 stg_256_u32_if(st_ok, q, __float_as_uint((float)cc[0]), __float_as_uint((float)cc[1]),
@@ -937,6 +969,18 @@ cudaError_t launch_tally3(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
     using F = std::false_type;
     // FULL with gamma = 2/3 (tallies + fp64 CCC, no checksum) gets a flag-free epilogue
     const bool full = !a.compact && a.out_flags == 3 && a.exact52;
+    // tallies + fp32 CCC, gamma = 2/3, T < 8 n_f < 2^23: the FP32-only cell path
+    const bool f32 = a.exact23 && !a.compact && a.out_flags == 5 && 8ll * a.n_f < (1ll << 23);
+    if (f32) {
+        switch (a.order) {
+            case 0: return go(tally3_kernel<0, true, false, false, 0, true>);
+            case 1: return go(tally3_kernel<1, true, false, false, 0, true>);
+            case 2: return go(tally3_kernel<2, true, false, false, 0, true>);
+            case 3: return go(tally3_kernel<3, true, false, false, 0, true>);
+            case 4: return go(tally3_kernel<4, true, false, false, 0, true>);
+            default: return go(tally3_kernel<5, true, false, false, 0, true>);
+        }
+    }
     if (a.exact23) {
         if (a.compact) return pick(T{}, T{}, F{});
         return full ? pick(T{}, F{}, T{}) : pick(T{}, F{}, F{});
