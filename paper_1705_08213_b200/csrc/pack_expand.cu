@@ -13,36 +13,51 @@
 
 namespace ccc {
 
-// One thread -> one 32-bit packed word (16 codes).
+// One CTA per vector row (grid-stride over rows, like expand); thread -> 32-bit packed
+// words of 16 codes each, two independent 16-B loads in flight per iteration.  (The
+// first version derived the row from a flat word index with a 64-bit division per word.)
+__device__ __forceinline__ uint32_t pack16(const uint4 c) {
+    const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
+    uint32_t out = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        uint32_t x = cw[b] & 0x03030303u;  // 4 codes, one per byte
+        // gather bits: byte k (2 bits) -> bits 2k..2k+1
+        x = (x | (x >> 6)) & 0x000F000Fu;
+        x = (x | (x >> 12)) & 0xFFu;
+        out |= x << (8 * b);
+    }
+    return out;
+}
+
 __global__ void __launch_bounds__(256) pack_kernel(const uint8_t* __restrict__ codes,
                                                    int64_t n_v, int64_t n_f, int64_t words_per_row,
                                                    uint32_t* __restrict__ packed) {
-    const int64_t total = n_v * words_per_row;
     const bool vec_ok = (n_f % 16) == 0 && (reinterpret_cast<uintptr_t>(codes) % 16) == 0;
-    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
-         w += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = w / words_per_row;
-        const int64_t q0 = (w - i * words_per_row) * 16;
-        const uint8_t* src = codes + i * n_f + q0;
-        uint32_t out = 0;
-        if (vec_ok && q0 + 16 <= n_f) {
-            const uint4 c = __ldcs(reinterpret_cast<const uint4*>(src));
-            const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                uint32_t x = cw[b] & 0x03030303u;  // 4 codes, one per byte
-                // gather bits: byte k (2 bits) -> bits 2k..2k+1
-                x = (x | (x >> 6)) & 0x000F000Fu;
-                x = (x | (x >> 12)) & 0xFFu;
-                out |= x << (8 * b);
-            }
-        } else {
-            for (int u = 0; u < 16; ++u) {
-                const int64_t q = q0 + u;
-                if (q < n_f) out |= (uint32_t)(src[u] & 3u) << (2 * u);
-            }
+    const int64_t full = vec_ok ? n_f / 16 : 0;          // words made of 16 in-range codes
+    for (int64_t i = blockIdx.x; i < n_v; i += gridDim.x) {
+        const uint8_t* row = codes + i * n_f;
+        uint32_t* prow = packed + i * words_per_row;
+        int64_t g = threadIdx.x;
+        for (; g + (int64_t)blockDim.x < full; g += 2 * (int64_t)blockDim.x) {
+            const uint4 c0 = __ldcs(reinterpret_cast<const uint4*>(row) + g);
+            const uint4 c1 = __ldcs(reinterpret_cast<const uint4*>(row) + g + blockDim.x);
+            prow[g] = pack16(c0);
+            prow[g + blockDim.x] = pack16(c1);
         }
-        packed[w] = out;
+        for (; g < words_per_row; g += blockDim.x) {
+            uint32_t out = 0;
+            if (g < full) {
+                out = pack16(__ldcs(reinterpret_cast<const uint4*>(row) + g));
+            } else {
+                const int64_t q0 = g * 16;
+                for (int u = 0; u < 16; ++u) {
+                    const int64_t q = q0 + u;
+                    if (q < n_f) out |= (uint32_t)(row[q] & 3u) << (2 * u);
+                }
+            }
+            prow[g] = out;
+        }
     }
 }
 
@@ -251,10 +266,7 @@ cudaError_t launch_expand_masks(const uint8_t* packed, int64_t n_v, int64_t n_f,
 cudaError_t launch_pack(const uint8_t* codes, int64_t n_v, int64_t n_f, uint8_t* packed,
                         int num_sms, cudaStream_t stream) {
     const int64_t wpr = (n_f + 63) / 64 * 4;
-    const int64_t total = n_v * wpr;
-    int64_t blocks = (total + 255) / 256;
-    const int64_t cap = (int64_t)num_sms * 8;
-    if (blocks > cap) blocks = cap;
+    int64_t blocks = n_v < (int64_t)num_sms * 8 ? n_v : (int64_t)num_sms * 8;
     if (blocks < 1) blocks = 1;
     pack_kernel<<<(int)blocks, 256, 0, stream>>>(codes, n_v, n_f, wpr,
                                                  reinterpret_cast<uint32_t*>(packed));
