@@ -470,3 +470,12 @@ def test_rings_world1_nccl():
     got = np.concatenate([np.array(t, dtype=np.int64).reshape(-1, 8) for _, _, t in res["pieces"]])
     np.testing.assert_array_equal(got, T3)
     assert len(res["pieces"]) > 1                     # the stage split was exercised
+
+
+def test_3way_epilogue_form_boundaries():
+    """The 3-way epilogue picks its cell formula by n_f: T U_p U_m < 2^52 (n_f <= 38,000:
+    one DFMA per cell) or not (two-multiply form), and 8 n_f < 2^23 for the FP32-only
+    fp32-CCC path.  Records on both sides of each boundary against the oracle."""
+    for n_v, n_f, flags in ((12, 38000, TAL | F64), (12, 38100, TAL | F64 | CK),
+                            (6, (1 << 20) - 8, TAL | F32), (6, (1 << 20) + 8, TAL | F32)):
+        _check_3way_full(_codes("random", n_v, n_f, seed=n_f), flags=flags)
