@@ -129,3 +129,50 @@ def test_workspace_sizes():
     assert b3 >= 4096 * 16384 + 4096 * 4096 * 4
     assert ccc.ccc_workspace_bytes(5, 10, 10) == 0
     assert ccc.ccc_e2e_workspace_bytes(1000, 100, ccc.OUT_TALLY | ccc.OUT_CCC_F64) > 0
+
+
+def test_header_compiles_as_c_and_links():
+    """include/ccc.h is plain C: a C translation unit that takes the address of every
+    declared function compiles with gcc and links against libccc.so."""
+    import os
+    import subprocess
+    import tempfile
+    syms = ccc.header_symbols()
+    src = "#include <stddef.h>\n#include <stdint.h>\n#include \"ccc.h\"\n" \
+          "void* table[] = {" + ", ".join(f"(void*)&{s}" for s in syms) + "};\n" \
+          "int main(void) { return table[0] == 0; }\n"
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    with tempfile.TemporaryDirectory() as d:
+        c = os.path.join(d, "t.c")
+        open(c, "w").write(src)
+        r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", inc, c, ccc.lib_path(),
+                            "-o", os.path.join(d, "t")], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+
+
+def test_validation_of_later_rows():
+    """f1 3-way sparse, f3 field split, f4 baselines: synchronous argument checks."""
+    lib = ccc.lib()
+    null = None
+    # field split: rank outside [0, world), ranges, empty waves launch nothing
+    assert lib.ccc_2way_fs_export(ctypes.c_void_p(256), ctypes.c_void_p(256), 100, 64, ctypes.c_void_p(256),
+                                  2, 2, 0, 1, null) == ccc.ERR_INVALID_ARGUMENT
+    assert lib.ccc_2way_fs_export(ctypes.c_void_p(256), ctypes.c_void_p(256), 100, 64, ctypes.c_void_p(256),
+                                  0, 2, 3, 1, null) == ccc.ERR_INVALID_ARGUMENT
+    assert lib.ccc_2way_fs_export(null, null, 100, 64, null, 0, 2, 4, 4, null) == ccc.OK
+    assert lib.ccc_2way_fs_finish(null, null, 100, 64, 2 / 3, 0, 2, 0, 0, 0, null, null, null, null) == ccc.OK
+    assert lib.ccc_2way_fs_finish(ctypes.c_void_p(256), ctypes.c_void_p(256), 100, 64, 2 / 3, 0, 2, 0, 3,
+                                  ccc.OUT_TALLY, null, null, null, null) == ccc.ERR_INVALID_ARGUMENT
+    # popcount baseline: NULL packed
+    assert lib.ccc_2way_popcount(null, 10, 10, 2 / 3, 0, null, null, null, ctypes.c_void_p(256), 1 << 20,
+                                 null) == ccc.ERR_INVALID_ARGUMENT
+    # sparse 3-way / paper route: small workspace, small scratch
+    assert lib.ccc_3way_sparse_prepare(ctypes.c_void_p(256), 10, 10, 2 / 3, ctypes.c_void_p(256), 16,
+                                       null) == ccc.ERR_WORKSPACE
+    wsb = lib.ccc_sparse3_workspace_bytes(10, 10)
+    assert lib.ccc_3way_sparse_stage(10, 10, 2 / 3, 1, 0, ccc.OUT_TALLY, ctypes.c_void_p(256), null, null,
+                                     ctypes.c_void_p(256), wsb, ctypes.c_void_p(256), 4, null) == ccc.ERR_WORKSPACE
+    assert lib.ccc_3way_sparse_scratch_bytes(10, 1, 0) == 7 * 120 * 4
+    assert lib.ccc_3way_paper_scratch_bytes(10, 1, 0) == 2 * 120 * 4
+    assert lib.ccc_3way_paper_workspace_bytes(10, 10) > 3 * 10 * 10 * 4
+    assert lib.ccc_3way_paper_prepare(null, 2, 10, 2 / 3, null, 0, null) == ccc.OK   # n_v < 3: nothing
