@@ -479,3 +479,75 @@ def test_3way_epilogue_form_boundaries():
     for n_v, n_f, flags in ((12, 38000, TAL | F64), (12, 38100, TAL | F64 | CK),
                             (6, (1 << 20) - 8, TAL | F32), (6, (1 << 20) + 8, TAL | F32)):
         _check_3way_full(_codes("random", n_v, n_f, seed=n_f), flags=flags)
+
+
+def test_2way_C3_block_full_size():
+    """configs[2] (160,000 x 100,000, block-circulant over 8 GPUs): rank 0's ring-step-1
+    unit -- the full 20,000 x 20,000 off-diagonal block pair at n_f = 100,000, in the
+    launch configuration of the multi-GPU bench (blocks aligned to 256) -- sampled pairs
+    against the brute force, sum T = 4 n_f on every record."""
+    from paper_1705_08213_b200 import decomp
+    n_v, n_f, P = 160000, 100000, 8
+    bounds = decomp.block_bounds(n_v, P, align=256)
+    u = [x for x in decomp.plan_2way(P, 0, bounds) if not x.diag][0]
+    (a0, a1), (b0, b1) = bounds[u.a], bounds[u.b]
+    exp = []
+    for lo, hi in ((a0, a1), (b0, b1)):
+        c = synthgen.random_codes(hi - lo, n_f, seed=1, device="cuda", row0=lo)
+        exp.append(ccc.ccc_expand(ccc.ccc_pack(c), n_f))
+        del c
+    m = decomp.unit2_records(u, bounds)
+    T = torch.empty((m, 4), dtype=torch.int32, device="cuda")
+    C = torch.empty((m, 4), dtype=torch.float64, device="cuda")
+    ccc.ccc_2way_block(*exp[0], a0, u.a_lo, u.a_hi, *exp[1], b0, False, n_f, TAL | F64, T, C)
+    torch.cuda.synchronize()
+    assert bool((T.sum(1, dtype=torch.int64) == 4 * n_f).all())
+    rng = np.random.default_rng(8)
+    nb = b1 - b0
+    loc = [(int(i), int(j)) for i, j in zip(rng.integers(u.a_lo, u.a_hi, 700), rng.integers(0, nb, 700))]
+    loc += [(u.a_lo, 0), (u.a_hi - 1, nb - 1), (u.a_lo, nb - 1), (u.a_hi - 1, 0)]
+    rows = torch.tensor([(i - u.a_lo) * nb + j for i, j in loc], device="cuda")
+    glob = sorted({a0 + i for i, _ in loc} | {b0 + j for _, j in loc})
+    pos = {g: t for t, g in enumerate(glob)}
+    sub = torch.cat([synthgen.random_codes(1, n_f, seed=1, row0=g) for g in glob])
+    To, Co = oracle.pairs(sub, np.array([(pos[a0 + i], pos[b0 + j]) for i, j in loc], dtype=np.int64))
+    np.testing.assert_array_equal(_t(T[rows]), To)
+    _ccc_close(C[rows].cpu().numpy(), Co)
+
+
+def test_3way_C5_unit_full_size():
+    """configs[4] (16,384 x 32,768, tetrahedral over 8 GPUs): a {A<B<C} part of rank 1's
+    plan at full size (blocks of 2,048 vectors, n_f = 32,768, the pairwise G of all 16,384
+    vectors by the 2-way kernel), first 4 pivots: sampled triples against the brute force
+    and sum T = 8 n_f on every record."""
+    from paper_1705_08213_b200 import decomp
+    n_v, n_f, P = 16384, 32768, 8
+    bounds = decomp.block_bounds(n_v, P, align=256)
+    codes = synthgen.random_codes(n_v, n_f, seed=1, device="cuda")
+    N, s, w = ccc.ccc_expand(ccc.ccc_pack(codes), n_f)
+    del codes
+    G = torch.zeros((n_v, n_v), dtype=torch.int32, device="cuda")
+    ccc.ccc_2way_block(N, s, w, 0, 0, n_v, N, s, w, 0, True, n_f, 0, g=G, ldg=n_v)
+    blk = lambda b: ccc.block(N[bounds[b][0]:bounds[b][1]], s[bounds[b][0]:bounds[b][1]],
+                              w[bounds[b][0]:bounds[b][1]], bounds[b][0])
+    u = [x for x in decomp.plan_3way(P, 1, bounds) if x.order == ("m", "p", "n")][0]
+    p_hi = u.p_lo + 4
+    T, C, _ = ccc.ccc_3way_unit(blk(u.pb), u.p_lo, p_hi, blk(u.mb), u.m_lo, u.m_hi, blk(u.nb), u.n_lo,
+                                u.n_hi, u.order, G, n_f, TAL | F64)
+    torch.cuda.synchronize()
+    nm, nn = u.m_hi - u.m_lo, u.n_hi - u.n_lo
+    assert T.shape[0] == 4 * nm * nn
+    assert bool((T.sum(1, dtype=torch.int64) == 8 * n_f).all())
+    rng = np.random.default_rng(9)
+    loc = [(int(p), int(m), int(k)) for p, m, k in
+           zip(rng.integers(0, 4, 500), rng.integers(0, nm, 500), rng.integers(0, nn, 500))]
+    loc += [(0, 0, 0), (3, nm - 1, nn - 1)]
+    rows = torch.tensor([(p * nm + m) * nn + k for p, m, k in loc], device="cuda")
+    p0, m0, n0 = bounds[u.pb][0] + u.p_lo, bounds[u.mb][0] + u.m_lo, bounds[u.nb][0] + u.n_lo
+    trip = [(m0 + m, p0 + p, n0 + k) for p, m, k in loc]          # canonical (i < j < k)
+    glob = sorted({g for t in trip for g in t})
+    pos = {g: t for t, g in enumerate(glob)}
+    sub = torch.cat([synthgen.random_codes(1, n_f, seed=1, row0=g) for g in glob])
+    To, Co = oracle.triples(sub, np.array([[pos[x] for x in t] for t in trip], dtype=np.int64))
+    np.testing.assert_array_equal(_t(T[rows]), To)
+    _ccc_close(C[rows].cpu().numpy(), Co)
