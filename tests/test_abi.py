@@ -176,3 +176,32 @@ def test_validation_of_later_rows():
     assert lib.ccc_3way_paper_scratch_bytes(10, 1, 0) == 2 * 120 * 4
     assert lib.ccc_3way_paper_workspace_bytes(10, 10) > 3 * 10 * 10 * 4
     assert lib.ccc_3way_paper_prepare(null, 2, 10, 2 / 3, null, 0, null) == ccc.OK   # n_v < 3: nothing
+
+
+def test_product_path_fails_loudly_without_the_library():
+    """No CPU fallback: with the library missing, the binding raises instead of computing
+    anything (checked in a fresh interpreter so this process's loaded library is untouched)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_1705_08213_b200 import ccc\n"
+            "try:\n    ccc.lib()\nexcept ImportError as e:\n    print('raised', e)\n"
+            "else:\n    print('loaded')\n") % root
+    env = dict(os.environ, CCC_LIB="/nonexistent/libccc.so")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+    assert r.stdout.startswith("raised") and "no CPU fallback" in r.stdout, r.stdout + r.stderr
+
+
+def test_product_package_does_not_import_the_oracle():
+    """The product (paper_1705_08213_b200/) never imports oracle/ or baselines/ (DESIGN.md §3)."""
+    import os
+    import re
+    pkg = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1705_08213_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+(oracle|baselines)\b", txt, re.M), f
+                assert "ccc_oracle" not in txt and "liboracle" not in txt, f
