@@ -70,10 +70,20 @@ static_assert(kSmem3 <= 232448, "3-way shared memory");
 
 // Units: (m-tile, n-tile) in TriSched order (triangular when m and n share a block),
 // pivots innermost.
+#ifndef CCC_PIVOT_OUTER
+#define CCC_PIVOT_OUTER 0
+#endif
 struct PivotSched {
     TriSched tiles;
     int64_t p_lo, p_hi, m_lo, m_hi, n_lo, n_hi, tt, base, cnt;
     int32_t same_pm, same_mn, J, K;
+    // pivot-outer order (one block, p < m < n): for each pivot, the upper-triangle tiles
+    // (J <= K) from the first row tile holding an m > p -- concurrent units then share the
+    // pivot and write into one contiguous stretch of the stage's records
+    int32_t pout, nt;
+    int64_t pc;
+    __host__ __device__ static int64_t tri(int64_t r) { return r > 0 ? r * (r + 1) / 2 : 0; }
+    __host__ __device__ int64_t pcount(int64_t p) const { return tri(nt - (p + 1) / kTileM3); }
 
     __host__ __device__ int64_t pivots(int32_t Jt, int32_t Kt) const {
         int64_t m_max = tiles.a_lo + (int64_t)Jt * kTileM3 + kTileM3 - 1;
@@ -104,11 +114,33 @@ struct PivotSched {
         base = 0;
         cnt = 0;
         J = K = 0;
+        pout = CCC_PIVOT_OUTER && same_pm && same_mn;
+        if (pout) {
+            nt = (int32_t)((n_hi + kTileM3 - 1) / kTileM3);
+            pc = p_lo;
+            if (p_lo >= p_hi) tt = -1;
+            else cnt = pcount(p_lo);
+            return;
+        }
         if (tiles.get(0, J, K)) cnt = pivots(J, K);
         else tt = -1;
     }
     __host__ __device__ bool get(int64_t u, int32_t& Jo, int32_t& Ko, int64_t& po) {
         if (tt < 0) return false;
+        if (pout) {
+            while (u >= base + cnt) {
+                base += cnt;
+                if (++pc >= p_hi) { tt = -1; return false; }
+                cnt = pcount(pc);
+            }
+            int64_t l = u - base;
+            int32_t j = (int32_t)((pc + 1) / kTileM3);
+            while (l >= nt - j) { l -= nt - j; ++j; }
+            Jo = j;
+            Ko = j + (int32_t)l;
+            po = pc;
+            return true;
+        }
         while (u >= base + cnt) {
             base += cnt;
             ++tt;
@@ -911,6 +943,11 @@ int64_t tally3_units(const Tally3Args& a) {
     PivotSched sch;
     sch.init(a);
     if (sch.tt < 0) return 0;
+    if (sch.pout) {
+        int64_t units = 0;
+        for (int64_t p = a.p_lo; p < a.p_hi; ++p) units += sch.pcount(p);
+        return units;
+    }
     TriSched t = sch.tiles;
     t.P = t.Q = 0;
     t.base = 0;
