@@ -477,6 +477,14 @@ def bench_main_3way(args, wl, metric, unit):
                           "output": "FULL, staged", "l2": "outputs larger than L2"},
                "gpu_launches": args.steps * (1 + ring.launches), "checksum": f"{ck:032x}",
                "clocks": clk.summary()}
+        from bench import peaks
+        pk, pk_kind = peaks()
+        # FULL records: 96 B per triple over all ranks; per-GPU HBM write rate vs the peak
+        gbs = comps / n_f * 96 / P / (ms_step / 1e3) / 1e9
+        out["roofline"] = {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                           "frac": gbs / pk["hbm_gbs"], "traffic": None, "kernel": "tally3_kernel",
+                           "peak_source": f"hbm_gbs of MEASURED_PEAKS.json ({pk_kind}); per GPU, "
+                                          "whole step (96 B/triple)"}
         print(json.dumps(out))
     dist.barrier()
     dist.destroy_process_group()
