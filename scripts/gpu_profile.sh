@@ -4,9 +4,9 @@ cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_elapsed,lts__t_sector_hit_rate.pct,sm__cycles_elapsed.avg.per_second
 echo "== bench lines (no profiler)"
-for wl in c2 c4 c2s c4s c4paper c2pop c2fs; do
+for wl in c2 c4 c4f32 c4ck c2s c4s c4paper c2pop c2fs; do
   E=--no-e2e; C=--no-cpu; [ $wl = c2 ] && E= && C=
-  ST=${STEPS:-5}; [ $wl = c4s ] && ST=1; [ $wl = c4paper ] && ST=1; [ $wl = c4 ] && ST=2
+  ST=${STEPS:-5}; [ $wl = c4s ] && ST=1; [ $wl = c4paper ] && ST=1; [ $wl = c4 ] && ST=2; [ $wl = c4f32 ] && ST=2; [ $wl = c4ck ] && ST=2
   timeout 900 python bench.py --workload $wl --steps $ST --warmup 3 $E $C > gpurun_out/bench_$wl.json 2> gpurun_out/bench_$wl.err
   tail -1 gpurun_out/bench_$wl.json | cut -c1-200
 done
