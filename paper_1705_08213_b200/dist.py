@@ -327,6 +327,9 @@ def bench_main(args, wl, metric, unit):
         ring.ck.zero_()
         ring.run(packed, timed=timed)
 
+    # the timed steps write exactly what the single-GPU line writes (tallies + fp64 CCC);
+    # the cross-rank checksum comes from one extra, untimed verification step below
+    be.out_flags = ccc.OUT_TALLY | ccc.OUT_CCC_F64
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -350,6 +353,10 @@ def bench_main(args, wl, metric, unit):
     dist.barrier()
     tmax = torch.tensor([ms], dtype=torch.float64, device="cuda")
     dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    be.out_flags = flags                       # verification step: + the 128-bit checksum
+    step()
+    torch.cuda.synchronize()
+    be.out_flags = ccc.OUT_TALLY | ccc.OUT_CCC_F64
     ck = checksum_total(ring.ck)
     comps = n_f * (n_v * (n_v - 1) // 2)
     ms_step = float(tmax.item()) / args.steps
@@ -448,6 +455,7 @@ def bench_main_3way(args, wl, metric, unit):
         ring.ck.zero_()
         ring.run(packed)
 
+    be.out_flags = ccc.OUT_TALLY | ccc.OUT_CCC_F64   # as the single-GPU line; checksum below
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -463,6 +471,9 @@ def bench_main_3way(args, wl, metric, unit):
         torch.cuda.synchronize()
     tmax = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device="cuda")
     dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    be.out_flags = flags                                # untimed verification step
+    step()
+    torch.cuda.synchronize()
     ck = checksum_total(ring.ck)
     comps = n_f * (n_v * (n_v - 1) * (n_v - 2) // 6)
     ms_step = float(tmax.item()) / args.steps
