@@ -37,8 +37,9 @@ __device__ __forceinline__ void fs_fold(unsigned long long& lo, unsigned long lo
 }  // namespace
 
 // One CTA per owned tile at a time (tiles visited in increasing schedule order per CTA,
-// so the TriSched cursor only walks forward); thread = column, loop over the tile rows.
-__global__ void __launch_bounds__(256) fs_finish_kernel(const int32_t* __restrict__ slots,
+// so the TriSched cursor only walks forward); 128 threads, thread = 2 adjacent columns
+// (int2 slot loads; the two records' tallies leave as one 256-bit store), 4 rows in flight.
+__global__ void __launch_bounds__(128) fs_finish_kernel(const int32_t* __restrict__ slots,
                                                         const int32_t* __restrict__ s, int64_t n_v,
                                                         int64_t n_f, double gamma, int32_t owner,
                                                         int32_t world, int64_t t_lo, int64_t t_end,
@@ -52,7 +53,7 @@ __global__ void __launch_bounds__(256) fs_finish_kernel(const int32_t* __restric
     const bool want_t = flags & 1u, want_c64 = flags & 2u, want_c32 = flags & 4u, want_ck = flags & 8u;
     const double two_nf = 2.0 * (double)n_f, inv4nf = 1.0 / (4.0 * (double)n_f);
     const uint32_t four_nf = 4u * (uint32_t)n_f;
-    const int col = threadIdx.x;
+    const int col = 2 * threadIdx.x;
     unsigned long long ck_lo = 0, ck_hi = 0;
     for (int64_t k = blockIdx.x; k < owned; k += gridDim.x) {
         const int64_t t = first + k * world;
@@ -60,49 +61,82 @@ __global__ void __launch_bounds__(256) fs_finish_kernel(const int32_t* __restric
         if (!sch.get(t, bm, bn)) break;
         const int64_t q = (t - t_lo) / world;
         const int32_t* tile = slots + ((q * world) << 16);
-        const int64_t j = (int64_t)bn * kBN + col;
-        const bool col_ok = j < n_v;
-        const uint32_t sj = col_ok ? (uint32_t)__ldg(s + j) : 0u;
-        const double wj0 = 1.0 - gamma * ((two_nf - (double)sj) / two_nf);
-        const double wj1 = 1.0 - gamma * ((double)sj / two_nf);
+        int64_t j[2];
+        bool col_ok[2];
+        uint32_t sj[2];
+        double wj0[2], wj1[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            j[h] = (int64_t)bn * kBN + col + h;
+            col_ok[h] = j[h] < n_v;
+            sj[h] = col_ok[h] ? (uint32_t)__ldg(s + j[h]) : 0u;
+            wj0[h] = 1.0 - gamma * ((two_nf - (double)sj[h]) / two_nf);
+            wj1[h] = 1.0 - gamma * ((double)sj[h] / two_nf);
+        }
         constexpr int kR = 4;   // rows in flight per thread (memory-level parallelism)
         for (int32_t row0 = 0; row0 < tile_m; row0 += kR) {
-          uint32_t Gr[kR];
+            int2 Gr[kR];
 #pragma unroll
-          for (int u = 0; u < kR; ++u) {
-            const int64_t i = (int64_t)bm * tile_m + row0 + u;
-            Gr[u] = 0;
-            if (i < n_v - 1 && col_ok && j > i)
-                for (int32_t f = 0; f < world; ++f)
-                    Gr[u] += (uint32_t)__ldg(tile + ((int64_t)f << 16) + (row0 + u) * kBN + col);
-          }
+            for (int u = 0; u < kR; ++u) {
+                const int64_t i = (int64_t)bm * tile_m + row0 + u;
+                Gr[u] = make_int2(0, 0);
+                if (i < n_v - 1 && col_ok[0] && j[1] > i)
+                    for (int32_t f = 0; f < world; ++f) {
+                        const int2 v = __ldg(reinterpret_cast<const int2*>(tile + ((int64_t)f << 16) +
+                                                                           (row0 + u) * kBN + col));
+                        Gr[u].x += v.x;
+                        Gr[u].y += v.y;
+                    }
+            }
 #pragma unroll
-          for (int u = 0; u < kR; ++u) {
-            const int32_t row = row0 + u;
-            const int64_t i = (int64_t)bm * tile_m + row;
-            if (i >= n_v - 1 || !col_ok || j <= i) continue;
-            const uint32_t G = Gr[u];
-            const uint32_t si = (uint32_t)__ldg(s + i);
-            const uint32_t t11 = G, t10 = 2u * si - G, t01 = 2u * sj - G;
-            const uint32_t t00 = four_nf - 2u * si - 2u * sj + G;
-            const int64_t rec = i * (2 * n_v - i - 1) / 2 + (j - i - 1);
-            if (want_t) stg_128_u32(tallies + 4 * rec, t00, t01, t10, t11);
-            if (want_c64 || want_c32) {
+            for (int u = 0; u < kR; ++u) {
+                const int64_t i = (int64_t)bm * tile_m + row0 + u;
+                if (i >= n_v - 1) continue;
+                const uint32_t si = (uint32_t)__ldg(s + i);
                 const double wi0 = (1.0 - gamma * ((two_nf - (double)si) / two_nf)) * inv4nf;
                 const double wi1 = (1.0 - gamma * ((double)si / two_nf)) * inv4nf;
-                const double c00 = (double)t00 * wi0 * wj0, c01 = (double)t01 * wi0 * wj1;
-                const double c10 = (double)t10 * wi1 * wj0, c11 = (double)t11 * wi1 * wj1;
-                if (want_c64)
-                    stg_256_f64(reinterpret_cast<double*>(ccc) + 4 * rec, c00, c01, c10, c11);
-                else
-                    stg_128_u32(reinterpret_cast<float*>(ccc) + 4 * rec, __float_as_uint((float)c00),
-                                __float_as_uint((float)c01), __float_as_uint((float)c10),
-                                __float_as_uint((float)c11));
+                uint32_t tt[2][4];
+                double cc[2][4];
+                bool ok[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    ok[h] = col_ok[h] && j[h] > i;
+                    const uint32_t G = (uint32_t)(h ? Gr[u].y : Gr[u].x);
+                    tt[h][3] = G;
+                    tt[h][2] = 2u * si - G;
+                    tt[h][1] = 2u * sj[h] - G;
+                    tt[h][0] = four_nf - 2u * si - 2u * sj[h] + G;
+                    cc[h][0] = (double)tt[h][0] * wi0 * wj0[h];
+                    cc[h][1] = (double)tt[h][1] * wi0 * wj1[h];
+                    cc[h][2] = (double)tt[h][2] * wi1 * wj0[h];
+                    cc[h][3] = (double)tt[h][3] * wi1 * wj1[h];
+                }
+                const int64_t rec = i * (2 * n_v - i - 1) / 2 + (j[0] - i - 1);   // record of column col
+                if (want_t) {
+                    if (ok[0] && ok[1] && !(rec & 1))
+                        stg_256_u32(tallies + 4 * rec, tt[0][0], tt[0][1], tt[0][2], tt[0][3], tt[1][0],
+                                    tt[1][1], tt[1][2], tt[1][3]);
+                    else
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+                            if (ok[h]) stg_128_u32(tallies + 4 * (rec + h), tt[h][0], tt[h][1], tt[h][2], tt[h][3]);
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (!ok[h]) continue;
+                    if (want_c64)
+                        stg_256_f64(reinterpret_cast<double*>(ccc) + 4 * (rec + h), cc[h][0], cc[h][1], cc[h][2],
+                                    cc[h][3]);
+                    else if (want_c32)
+                        stg_128_u32(reinterpret_cast<float*>(ccc) + 4 * (rec + h), __float_as_uint((float)cc[h][0]),
+                                    __float_as_uint((float)cc[h][1]), __float_as_uint((float)cc[h][2]),
+                                    __float_as_uint((float)cc[h][3]));
+                    if (want_ck)
+                        fs_fold(ck_lo, ck_hi, (2ull << 60) | ((uint64_t)i << 40) | ((uint64_t)j[h] << 20),
+                                (uint64_t)tt[h][0] | ((uint64_t)tt[h][1] << 32),
+                                (uint64_t)tt[h][2] | ((uint64_t)tt[h][3] << 32));
+                }
             }
-            if (want_ck)
-                fs_fold(ck_lo, ck_hi, (2ull << 60) | ((uint64_t)i << 40) | ((uint64_t)j << 20),
-                        (uint64_t)t00 | ((uint64_t)t01 << 32), (uint64_t)t10 | ((uint64_t)t11 << 32));
-          }
         }
     }
     if (want_ck) {
@@ -135,7 +169,7 @@ cudaError_t launch_fs_finish(const int32_t* slots, const int32_t* s, int64_t n_v
     if (t_end <= t_lo) return cudaSuccess;
     const int64_t owned = (t_end - t_lo + world - 1) / world;
     const int64_t grid = owned < 8 * (int64_t)num_sms ? owned : 8 * (int64_t)num_sms;
-    fs_finish_kernel<<<(unsigned)grid, 256, 0, stream>>>(slots, s, n_v, n_f, gamma, owner, world, t_lo,
+    fs_finish_kernel<<<(unsigned)grid, 128, 0, stream>>>(slots, s, n_v, n_f, gamma, owner, world, t_lo,
                                                          t_end, tally2_tile_rows(), flags, tallies, ccc,
                                                          checksum);
     return cudaGetLastError();
