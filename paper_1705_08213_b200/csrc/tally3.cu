@@ -14,12 +14,16 @@
 // The paper instead runs three masked mGEMM3 per pivot (Table 1); this
 // needs one int8 MAC per unique 3-way comparison.
 //
-// A work unit is (row tile J of 128 m's, column tile K of 256 n's, pivot p); units are
-// ordered tile-outer / pivot-inner so the ~148 concurrent CTAs share the same N_M, N_N
-// panels in L2 and differ only in their 128-byte pivot rows.
+// A work unit is (row tile J of 256 m's on a CTA pair -- 128 per CTA --, column tile K of
+// 256 n's, pivot p); units are ordered tile-outer / pivot-inner so the 74 concurrent CTA
+// pairs share the same N_M, N_N panels and G_mn tile in L2 and differ only in their
+// 128-byte pivot rows.
 // Warp roles: 0 TMA producer (A, B tiles + pivot chunk), 1 TMEM alloc + MMA issuer,
-// 2..9 epilogue (2 per TMEM lane quadrant), 10..11 transform (A <- A o n_p in shared
+// 2..9 epilogue (2 per TMEM lane quadrant), 10..13 transform (A <- A o n_p in shared
 // memory, in place, then fence.proxy.async so the tensor core sees it).
+// Template modes beyond the dense CCC epilogue (kMode): 1 = store this pass's raw form
+// G3 (sparse 3-way form passes, paper-route masked passes), 2 = sparse final pass,
+// 3 = paper-route final pass; kFull / kF32 = flag-free FULL epilogues (gamma = 2/3).
 #include "sm100.cuh"
 #include "common.cuh"
 #include "internal.h"
