@@ -588,6 +588,7 @@ def main():
     if wl["way"] == 3 and wl.get("flags") == "ck":
         roof["peak_source"] += "; CHECKSUM mode: no record is stored, the tensor-pipe line is the roofline"
     elif wl["way"] == 3:
+        roof.pop("note", None)
         roof["bound"] = "hbm"
         roof["achieved"] = (r["out_bytes"] + r.get("forms_bytes", 0)) / wl["n_st"] / k_s / 1e9
         roof["peak"] = pk["hbm_gbs"]
