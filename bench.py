@@ -190,6 +190,27 @@ def cpu_baseline(way, n_v, n_f, target_s=12.0, kind="random"):  # noqa: C901
                       f"workload, brute-force Fig.1/Fig.2 enumeration, {dt:.1f} s"}
 
 
+def int8_library_ceiling(n=8192, reps=10):
+    """cuBLASLt's int8 GEMM (torch._int_mm, int32 accumulate) on n^3 in the same
+    job -- a library reference point for the tensor-pipe line, not a peak."""
+    import torch
+    a = torch.randint(-3, 4, (n, n), dtype=torch.int8, device="cuda")
+    b = torch.randint(-3, 4, (n, n), dtype=torch.int8, device="cuda").t()
+    for _ in range(3):
+        torch._int_mm(a, b)
+    torch.cuda.synchronize()
+    best = 1e30
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch._int_mm(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    return {"torch_int_mm_TOPS": 2.0 * n ** 3 / (best / 1e3) / 1e12, "shape": f"{n}^3 int8 -> int32",
+            "ms": best}
+
+
 def cpu_optimized(n_v, n_f, target_s=8.0):
     """the paper's "optimized CPU version" -- bit-packed
     AND + popcount on the host cores (baselines/cpu_popcount.c), on the first rows of the
@@ -567,6 +588,13 @@ def main():
     hbm_write = r["out_bytes"] / (ms_step / 1e3) / 1e9
     roof["out_write_GBps"] = hbm_write
     roof["out_write_frac_of_hbm"] = hbm_write / pk["hbm_gbs"]
+    if wl["way"] == 2 and not wl.get("popcount") and args.workload in ("c2", "c2s"):
+        try:
+            lib_ceil = int8_library_ceiling()
+            roof["int8_library_ceiling"] = lib_ceil
+            roof["frac_of_library_ceiling"] = achieved / lib_ceil["torch_int_mm_TOPS"]
+        except Exception as e:   # noqa: BLE001 -- a reference point only
+            roof["int8_library_ceiling"] = {"error": str(e)[:200]}
     if wl.get("fieldsplit"):
         # the export GEMMs of all slices (tensor) + the owners' reduce/epilogue (HBM)
         pairs = r["comparisons"] / wl["n_f"]
