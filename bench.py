@@ -1,7 +1,7 @@
 """bench.py -- CCC comparisons/s of the B200 hot path.
 
 python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                [--workload c2|c4|c1|c2s|c4s|c4f32|c4ck|c2pop|c2fs|c4paper] [--no-e2e] [--no-cpu]
+                [--workload c2|c2hwe|c4|c1|c2s|c4s|c4f32|c4ck|c2pop|c2fs|c4paper] [--no-e2e] [--no-cpu]
 
 One step = one pass of the whole hot path over one synthetic batch resident in HBM:
   2-way (default, BASELINE configs[1] = C2: 20,000 vectors x 50,000 individuals):
@@ -42,6 +42,9 @@ WORKLOADS = {
                label="2-way CCC, 20,000 SNP vectors x 50,000 individuals (configs[1])"),
     "c2s": dict(way=2, n_v=20000, n_f=50000, sparse=True,
                 label="2-way sparse-mode CCC (missing entries, SURVEY f1), 20,000 x 50,000"),
+    "c2hwe": dict(way=2, n_v=20000, n_f=50000, kind="hwe",
+                  label="2-way CCC, 20,000 x 50,000, Hardy-Weinberg SNP-like input (type 1b, seed 2): "
+                        "the data-independence check of SURVEY 8(d) / P:719-724"),
     "c2pop": dict(way=2, n_v=20000, n_f=50000, popcount=True,
                   label="2-way CCC, 20,000 x 50,000, the paper's popcount tally on CUDA cores "
                         "(SURVEY f4 baseline)"),
@@ -253,6 +256,8 @@ def run_2way_single(args, wl):
     flags = ccc.OUT_TALLY | ccc.OUT_CCC_F64
     if sparse:
         codes = synthgen.sparse_codes(n_v, n_f, seed=4, device=dev)    # resident in HBM
+    elif wl.get("kind") == "hwe":
+        codes = synthgen.hwe_codes(n_v, n_f, seed=2, device=dev)       # resident in HBM
     else:
         codes = synthgen.random_codes(n_v, n_f, seed=1, device=dev)    # resident in HBM
     packed = torch.empty((n_v, ccc.ccc_packed_stride(n_f)), dtype=torch.uint8, device=dev)
@@ -529,7 +534,7 @@ def main():
         vals = []
         for _ in range(args.warmup + args.steps):
             vals.append(cpu_baseline(wl["way"], wl["n_v"], wl["n_f"], target_s=4.0,
-                                     kind="sparse" if wl.get("sparse") else "random"))
+                                     kind="sparse" if wl.get("sparse") else wl.get("kind", "random")))
         vals = vals[args.warmup:]
         v = sorted(x["value"] for x in vals)[len(vals) // 2]
         cb = dict(vals[0])
@@ -636,7 +641,9 @@ def main():
         "config": {"workload": wl["label"], "n_v": wl["n_v"], "n_f": wl["n_f"],
                    "input": ("type-3 sparse HWE codes, seed 4, missing marker (1,0) with "
                              "per-vector rate U(0, 0.3) (P:1028-1043)") if wl.get("sparse") else
-                            "type-1 uniform random 2-bit codes, seed 1 (P:657)",
+                            ("type-1b Hardy-Weinberg codes, p_i ~ U(0.05, 0.5), seed 2"
+                             if wl.get("kind") == "hwe" else
+                             "type-1 uniform random 2-bit codes, seed 1 (P:657)"),
                    "output": {"f32": "FULL: uint32 tallies + fp32 CCC for every unique record",
                               "ck": "CHECKSUM: every record computed and folded into the 128-bit checksum, none stored"
                               }.get(wl.get("flags"), "FULL: uint32 tallies + fp64 CCC for every unique record"),
@@ -655,7 +662,7 @@ def main():
         out["e2e"] = r["e2e"]
     if args.cpu:
         out["cpu_baseline"] = cpu_baseline(wl["way"], wl["n_v"], wl["n_f"],
-                                           kind="sparse" if wl.get("sparse") else "random")
+                                           kind="sparse" if wl.get("sparse") else wl.get("kind", "random"))
         if wl["way"] == 2 and not wl.get("sparse"):
             out["cpu_optimized"] = cpu_optimized(wl["n_v"], wl["n_f"])
     print(json.dumps(out))
