@@ -89,6 +89,7 @@ class ClockSampler:
         self.index = index
         self.period = period_s
         self.sm = []
+        self.power = []
         self.bits = 0
         self.max_mhz = None
         self._stop = threading.Event()
@@ -106,6 +107,7 @@ class ClockSampler:
                     try:
                         self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
                         self.bits |= int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))
+                        self.power.append(pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0)   # W
                     except Exception:  # noqa: BLE001 - sampling is best effort
                         pass
                     time.sleep(self.period)
@@ -127,8 +129,13 @@ class ClockSampler:
         if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": 0}
         sm = sorted(self.sm)
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.max_mhz, "reasons": reasons,
-                "samples": len(sm), "sm_mhz_min": sm[0]}
+        out = {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.max_mhz, "reasons": reasons,
+               "samples": len(sm), "sm_mhz_min": sm[0]}
+        if self.power:
+            pw = sorted(self.power)
+            out["power_w_median"] = pw[len(pw) // 2]
+            out["power_w_max"] = pw[-1]
+        return out
 
 
 # ------------------------------------------------------------------------ helpers
