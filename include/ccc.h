@@ -317,6 +317,18 @@ ccc_status ccc_2way_host(const uint8_t* codes_h, int64_t n_v, int64_t n_f, doubl
                          uint64_t* checksum_h, void* dev_ws_d, size_t dev_ws_bytes,
                          void* stream);
 
+/* 3-way end to end with stage streaming to host (SURVEY §8(f) f2 "stage streaming"; stages
+ * P:621-626): H2D of codes_h (uint8 [n_v][n_f]), pack, ccc_3way_prepare, then the n_stages
+ * stages of ccc_3way_stage computed into two device stage buffers in turn while a copy
+ * stream drains the previous stage's records to tallies_h / ccc_h (host memory of the full
+ * C(n_v,3) records, lexicographic -- pinned for overlap); checksum_h gets the whole result's
+ * checksum.  dev_ws_d >= ccc_3way_host_workspace_bytes(n_v, n_f, n_stages, out_flags).
+ * Returns after the last copy (synchronises `stream` and the internal copy stream). */
+size_t     ccc_3way_host_workspace_bytes(int64_t n_v, int64_t n_f, int64_t n_stages, uint32_t out_flags);
+ccc_status ccc_3way_host(const uint8_t* codes_h, int64_t n_v, int64_t n_f, double gamma, uint32_t out_flags,
+                         int64_t n_stages, uint32_t* tallies_h, void* ccc_h, uint64_t* checksum_h,
+                         void* dev_ws_d, size_t dev_ws_bytes, void* stream);
+
 /* Number of kernels the last successful call on this thread enqueued (for the
  * bench's gpu_launches count). */
 int64_t ccc_last_launch_count(void);

@@ -140,6 +140,8 @@ _SIGS = {
     "ccc_3way_paper_prepare": (_int, [_vp, _i64, _i64, _dbl, _vp, _sz, _vp]),
     "ccc_3way_paper_stage": (_int, [_i64, _i64, _dbl, _i64, _i64, _u32, _vp, _vp, _vp, _vp, _sz, _vp, _sz,
                                     _vp]),
+    "ccc_3way_host_workspace_bytes": (_sz, [_i64, _i64, _i64, _u32]),
+    "ccc_3way_host": (_int, [_vp, _i64, _i64, _dbl, _u32, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
     "ccc_e2e_workspace_bytes": (_sz, [_i64, _i64, _u32]),
     "ccc_2way_host": (_int, [_vp, _i64, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _sz, _vp]),
 }
@@ -640,3 +642,31 @@ def ccc_3way_paper_stage(n_v: int, n_f: int, n_stages: int, stage: int, ws: torc
     _check(lib().ccc_3way_paper_stage(n_v, n_f, gamma, n_stages, stage, out_flags, _p(T), _p(C), _p(ck),
                                       _p(ws), ws.numel(), _p(scratch), scratch.numel(), _stream(stream)))
     return T, C, ck
+
+
+# ------------------------------------------------------------- f2: 3-way stage streaming to host
+def ccc_3way_host(codes_h: torch.Tensor, gamma: float = GAMMA, out_flags: int = OUT_TALLY | OUT_CCC_F64,
+                  n_stages: int = 1, tallies_h=None, ccc_h=None, checksum_h=None, ws=None, stream=None):
+    """Host codes in, every 3-way record streamed stage by stage into host buffers (pinned
+    for overlap); allocates the host outputs (pinned) when not given."""
+    if codes_h.dtype != torch.uint8 or codes_h.device.type != "cpu" or not codes_h.is_contiguous():
+        raise ValueError("codes_h must be a contiguous uint8 CPU tensor")
+    n_v, n_f = codes_h.shape
+    m = ccc_num_unique(3, n_v)
+    if out_flags & OUT_TALLY and tallies_h is None:
+        tallies_h = torch.empty((m, 8), dtype=torch.int32, pin_memory=True)
+    if out_flags & OUT_CCC_F64 and ccc_h is None:
+        ccc_h = torch.empty((m, 8), dtype=torch.float64, pin_memory=True)
+    if out_flags & OUT_CCC_F32 and ccc_h is None:
+        ccc_h = torch.empty((m, 8), dtype=torch.float32, pin_memory=True)
+    if out_flags & OUT_CHECKSUM and checksum_h is None:
+        checksum_h = torch.zeros(2, dtype=torch.int64)
+    if ws is None:
+        ws = torch.empty(lib().ccc_3way_host_workspace_bytes(n_v, n_f, n_stages, out_flags), dtype=torch.uint8,
+                         device="cuda")
+    _check(lib().ccc_3way_host(codes_h.data_ptr(), n_v, n_f, gamma, out_flags, n_stages,
+                               tallies_h.data_ptr() if tallies_h is not None else None,
+                               ccc_h.data_ptr() if ccc_h is not None else None,
+                               checksum_h.data_ptr() if checksum_h is not None else None,
+                               _p(ws), ws.numel(), _stream(stream)))
+    return tallies_h, ccc_h, checksum_h

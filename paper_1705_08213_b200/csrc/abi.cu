@@ -1109,6 +1109,135 @@ ccc_status ccc_2way_host(const uint8_t* codes_h, int64_t n_v, int64_t n_f, doubl
     return rc;
 }
 
+// ------------------------------------------------------- f2: 3-way stage streaming to host
+namespace {
+struct H3Layout {
+    size_t codes = 0, packed = 0, ws = 0, ck = 0, st_t[2] = {0, 0}, st_c[2] = {0, 0}, total = 0;
+    int64_t stage_cap = 0;
+};
+H3Layout h3_layout(int64_t n_v, int64_t n_f, int64_t n_stages, uint32_t flags) {
+    H3Layout L;
+    size_t off = 0;
+    L.codes = off;
+    off += al256((size_t)n_v * n_f);
+    L.packed = off;
+    off += al256((size_t)n_v * pstride_of(n_f));
+    L.ws = off;
+    off += al256(ws_layout(3, n_v, n_f).total);
+    L.ck = off;
+    off += 256;
+    int64_t cap = 0, rng[4];
+    for (int64_t st = 0; st < n_stages; ++st)
+        if (ccc_stage_range(n_v, n_stages, st, rng) == CCC_OK) cap = std::max<int64_t>(cap, rng[3]);
+    L.stage_cap = cap;
+    const size_t cb = (flags & CCC_OUT_CCC_F64) ? 64 : (flags & CCC_OUT_CCC_F32) ? 32 : 0;
+    for (int b = 0; b < 2; ++b) {
+        L.st_t[b] = off;
+        if (flags & CCC_OUT_TALLY) off += al256((size_t)cap * 32);
+        L.st_c[b] = off;
+        off += al256((size_t)cap * cb);
+    }
+    L.total = off + 256;
+    return L;
+}
+}  // namespace
+
+size_t ccc_3way_host_workspace_bytes(int64_t n_v, int64_t n_f, int64_t n_stages, uint32_t out_flags) {
+    if (n_v < 3 || n_f < 1 || n_stages < 1) return 256;
+    return h3_layout(n_v, n_f, n_stages, out_flags).total;
+}
+
+ccc_status ccc_3way_host(const uint8_t* codes_h, int64_t n_v, int64_t n_f, double gamma, uint32_t out_flags,
+                         int64_t n_stages, uint32_t* tallies_h, void* ccc_h, uint64_t* checksum_h,
+                         void* dev_ws_d, size_t dev_ws_bytes, void* stream) {
+    g_launches = 0;
+    CCC_CHECK(check_sizes(n_v, n_f));
+    if (out_flags & ~15u) return fail(CCC_ERR_INVALID_ARGUMENT, "unknown out_flags bits");
+    if (n_stages < 1) return fail(CCC_ERR_INVALID_ARGUMENT, "n_stages must be >= 1");
+    if (n_v < 3) return CCC_OK;
+    CCC_CHECK(check_outputs(out_flags, tallies_h, ccc_h, checksum_h));
+    if (!codes_h) return fail(CCC_ERR_INVALID_ARGUMENT, "codes_h must not be NULL");
+    const H3Layout L = h3_layout(n_v, n_f, n_stages, out_flags);
+    if (!dev_ws_d || !aligned(dev_ws_d, 256))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "dev_ws_d must be 256-B aligned");
+    if (dev_ws_bytes < L.total) return fail(CCC_ERR_WORKSPACE, "device workspace too small");
+    int sms;
+    CCC_CHECK(check_device(&sms));
+    uint8_t* base = static_cast<uint8_t*>(dev_ws_d);
+    uint8_t* ws = base + L.ws;
+    const size_t ws_bytes = ws_layout(3, n_v, n_f).total;
+    uint64_t* ck = reinterpret_cast<uint64_t*>(base + L.ck);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t cbytes = (out_flags & CCC_OUT_CCC_F64) ? 8 : 4;
+    const bool want_c = out_flags & (CCC_OUT_CCC_F64 | CCC_OUT_CCC_F32);
+    CCC_CUDA(cudaMemcpyAsync(base + L.codes, codes_h, (size_t)n_v * n_f, cudaMemcpyHostToDevice, st), "H2D codes");
+    CCC_CUDA(ccc::launch_pack(base + L.codes, n_v, n_f, base + L.packed, sms, st), "pack launch");
+    CCC_CHECK(ccc_3way_prepare(base + L.packed, n_v, n_f, gamma, ws, ws_bytes, stream));
+    int64_t launches = 1 + g_launches;
+    if (out_flags & CCC_OUT_CHECKSUM) CCC_CUDA(cudaMemsetAsync(ck, 0, 16, st), "memset");
+    cudaStream_t cs = nullptr;
+    cudaEvent_t done[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
+    ccc_status rc = CCC_OK;
+    auto cleanup = [&]() {
+        for (int b = 0; b < 2; ++b) {
+            if (done[b]) cudaEventDestroy(done[b]);
+            if (copied[b]) cudaEventDestroy(copied[b]);
+        }
+        if (cs) cudaStreamDestroy(cs);
+    };
+    cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+        e = cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) {
+        cleanup();
+        return cuda_fail(e, "stream/event create");
+    }
+    // stage s computes into buffer s % 2 while the copy stream drains stage s - 1 to host
+    for (int64_t sg = 0; sg < n_stages && rc == CCC_OK; ++sg) {
+        int64_t rng[4];
+        rc = ccc_stage_range(n_v, n_stages, sg, rng);
+        if (rc != CCC_OK || rng[3] == 0) continue;
+        const int b = (int)(sg & 1);
+        if (sg >= 2 && (e = cudaStreamWaitEvent(st, copied[b], 0)) != cudaSuccess) {
+            rc = cuda_fail(e, "wait");
+            break;
+        }
+        uint32_t* bt = reinterpret_cast<uint32_t*>(base + L.st_t[b]);
+        void* bc = base + L.st_c[b];
+        rc = ccc_3way_stage(n_v, n_f, gamma, n_stages, sg, out_flags, (out_flags & CCC_OUT_TALLY) ? bt : nullptr,
+                            want_c ? bc : nullptr, (out_flags & CCC_OUT_CHECKSUM) ? ck : nullptr, ws, ws_bytes,
+                            nullptr, stream);
+        if (rc != CCC_OK) break;
+        launches += g_launches;
+        if ((e = cudaEventRecord(done[b], st)) != cudaSuccess || (e = cudaStreamWaitEvent(cs, done[b], 0)) != cudaSuccess) {
+            rc = cuda_fail(e, "event");
+            break;
+        }
+        const int64_t rec0 = rng[2], nrec = rng[3];
+        if (out_flags & CCC_OUT_TALLY)
+            e = cudaMemcpyAsync(tallies_h + 8 * rec0, bt, (size_t)nrec * 32, cudaMemcpyDeviceToHost, cs);
+        if (e == cudaSuccess && want_c)
+            e = cudaMemcpyAsync(static_cast<uint8_t*>(ccc_h) + (size_t)rec0 * 8 * cbytes, bc, (size_t)nrec * 8 * cbytes,
+                                cudaMemcpyDeviceToHost, cs);
+        if (e == cudaSuccess) e = cudaEventRecord(copied[b], cs);
+        if (e != cudaSuccess) {
+            rc = cuda_fail(e, "D2H stage");
+            break;
+        }
+    }
+    if (rc == CCC_OK && (out_flags & CCC_OUT_CHECKSUM)) {
+        e = cudaMemcpyAsync(checksum_h, ck, 16, cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) rc = cuda_fail(e, "D2H checksum");
+    }
+    if ((e = cudaStreamSynchronize(cs)) != cudaSuccess && rc == CCC_OK) rc = cuda_fail(e, "sync copy stream");
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess && rc == CCC_OK) rc = cuda_fail(e, "sync stream");
+    cleanup();
+    if (rc == CCC_OK) g_launches = launches;
+    return rc;
+}
+
 // ------------------------------------------------------------------ sparse mode (f1)
 int64_t ccc_sparse_rows(int64_t n_v) { return n_v < 0 ? -1 : 2 * ((n_v + 15) / 16 * 16); }
 
