@@ -57,20 +57,6 @@ __device__ __forceinline__ void ck_flush(unsigned long long lo, unsigned long lo
     }
 }
 
-// mbarrier waits: CCC_WAIT_SLEEP=1 uses try_wait with a suspend-time hint (the waiting warp
-// sleeps in the barrier unit instead of re-issuing try_wait)
-#ifndef CCC_WAIT_SLEEP
-#define CCC_WAIT_SLEEP 0
-#endif
-#if CCC_WAIT_SLEEP
-#define T2_WAIT mbar_wait_sleep
-#else
-#define T2_WAIT mbar_wait
-#endif
-
-#ifndef CCC_EPI_PACE_NS
-#define CCC_EPI_PACE_NS 0   // > 0: minimum ns per 8-column group of the epilogue
-#endif
 #ifndef CCC_EPI_WARPS
 #define CCC_EPI_WARPS 4
 #endif
@@ -167,7 +153,7 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 const bool rev = args.k_alternate && (((t - unit0) / units) & 1);
                 for (int32_t kk = 0; kk < args.k_blocks; ++kk) {
                     const int32_t kb = rev ? args.k_blocks - 1 - kk : kk;
-                    T2_WAIT(&empty[stage], phase ^ 1);
+                    mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sa = smA + stage * C::kABytes;
                     uint8_t* sb = smB + stage * C::kBBytes;
                     if constexpr (kPair == 2) {
@@ -198,12 +184,12 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 if ((args.t_hi > 0 && t >= args.t_hi) || !sch.get(t, bm, bn)) break;
                 unsigned long long* tr = args.trace ? args.trace + 8 * t : nullptr;
                 if (tr) tr[0] = globaltimer();
-                T2_WAIT(&tempty[acc], acc_phase ^ 1);
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 if (tr) tr[1] = globaltimer();
                 const uint32_t d = tmem_base + acc * kBN;
                 for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
-                    T2_WAIT(&full[stage], phase);
+                    mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t sa = a0 + stage * C::kABytes, sb = b0 + stage * C::kBBytes;
 #pragma unroll
@@ -246,7 +232,7 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         for (int64_t t = unit0;; t += units) {
             int32_t bm, bn;
             if ((args.t_hi > 0 && t >= args.t_hi) || !sch.get(t, bm, bn)) break;
-            T2_WAIT(&tfull[acc], acc_phase);
+            mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int64_t xrow = args.a_lo + (int64_t)bm * C::kTileM + rank * 128 + quad * 32;
             const int64_t i_w = xrow >> 1;                    // first vector of my group
@@ -343,7 +329,7 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             if ((args.t_hi > 0 && t >= args.t_hi) || !sch.get(t, bm, bn)) break;
             unsigned long long* tr = (args.trace && warp == 2 && rank == 0) ? args.trace + 8 * t : nullptr;
             if (tr && lane == 0) tr[3] = globaltimer();
-            T2_WAIT(&tfull[acc], acc_phase);
+            mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             if (tr && lane == 0) tr[4] = globaltimer();
             // my 4 rows: r = quad*32 + h*16 + e*8 + lane/4, h, e in {0,1}
@@ -373,22 +359,7 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             const bool any_row = __any_sync(0xffffffffu, my_any);
             const int32_t warp_jlo = __shfl_sync(0xffffffffu, jlo_r[0], 0);
             const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + acc * kBN;
-#if CCC_EPI_PACE_NS > 0
-            // pacing: spread this tile's record stores over ~the mainloop time of the next
-            // tile instead of one burst (the burst slows the concurrent mainloop)
-            const unsigned long long pace_t0 = globaltimer();
-#endif
             for (int c = c_begin; c < c_end; ++c) {
-#if CCC_EPI_PACE_NS > 0
-                {
-                    const unsigned long long due = pace_t0 + (unsigned long long)(c - c_begin) * CCC_EPI_PACE_NS;
-                    unsigned long long now = globaltimer();
-                    while (now < due) {
-                        __nanosleep((unsigned)(due - now));
-                        now = globaltimer();
-                    }
-                }
-#endif
                 const int32_t j0 = bn * kBN + c * 8;
                 if (!any_row || j0 >= nB || j0 + 8 <= warp_jlo) continue;  // warp-uniform
                 uint32_t va[4], vb[4];

@@ -34,17 +34,8 @@
 namespace ccc {
 
 constexpr int kTileM3 = 256;         // pair tile rows (UMMA M = 256, cta_group::2)
-// Experimental (off): FULL-mode fp64 CCC records leave through shared memory and TMA
-// bulk stores (512-B row segments) instead of per-thread 256-bit global stores.  Measured
-// at C4: without the epilogue's global-store traffic the mainloop runs 64 instead of 96 us
-// per unit, but staging the records conflict-free (XOR-rotated 16-B chunks, 64-B row pad)
-// costs the epilogue 122-136 us per unit against 70 us with direct stores: 32.3 ms per
-// stage against 20.6 ms.  Kept for the next attempt (needs a cheaper staging layout).
-#ifndef CCC_TMA_STORE
-#define CCC_TMA_STORE 0
-#endif
 #ifndef CCC_STAGES3
-#define CCC_STAGES3 (CCC_TMA_STORE ? 4 : 6)
+#define CCC_STAGES3 6
 #endif
 constexpr int kStages3 = CCC_STAGES3;
 constexpr int kABytes3 = 128 * kBK;  // 16 KB: this CTA's 128 rows of A
@@ -65,29 +56,16 @@ struct ColT3 {
     float f0, f1;                // w0, w1 in fp32 (kF32 cell formula)
 };
 constexpr int kColOff3 = kPivOff3 + kStages3 * kPivBytes;
-constexpr int kStgRow3 = 512 + 64;        // one staged row segment (8 records x 64 B) + bank pad
-constexpr int kStgBytes3 = 8 * kStgRow3;  // one staging buffer: 8 rows of CCC
-constexpr int kStgOff3 = kColOff3 + 2 * kBN * (int)sizeof(ColT3);
-constexpr int kBarOff3 = kStgOff3 + (CCC_TMA_STORE ? 8 * 2 * kStgBytes3 : 0);
+constexpr int kBarOff3 = kColOff3 + 2 * kBN * (int)sizeof(ColT3);
 constexpr int kSmem3 = kBarOff3 + 512 + 1024;
 static_assert(kSmem3 <= 232448, "3-way shared memory");
 
 // Units: (m-tile, n-tile) in TriSched order (triangular when m and n share a block),
 // pivots innermost.
-#ifndef CCC_PIVOT_OUTER
-#define CCC_PIVOT_OUTER 0
-#endif
 struct PivotSched {
     TriSched tiles;
     int64_t p_lo, p_hi, m_lo, m_hi, n_lo, n_hi, tt, base, cnt;
     int32_t same_pm, same_mn, J, K;
-    // pivot-outer order (one block, p < m < n): for each pivot, the upper-triangle tiles
-    // (J <= K) from the first row tile holding an m > p -- concurrent units then share the
-    // pivot and write into one contiguous stretch of the stage's records
-    int32_t pout, nt;
-    int64_t pc;
-    __host__ __device__ static int64_t tri(int64_t r) { return r > 0 ? r * (r + 1) / 2 : 0; }
-    __host__ __device__ int64_t pcount(int64_t p) const { return tri(nt - (p + 1) / kTileM3); }
 
     __host__ __device__ int64_t pivots(int32_t Jt, int32_t Kt) const {
         int64_t m_max = tiles.a_lo + (int64_t)Jt * kTileM3 + kTileM3 - 1;
@@ -118,33 +96,11 @@ struct PivotSched {
         base = 0;
         cnt = 0;
         J = K = 0;
-        pout = CCC_PIVOT_OUTER && same_pm && same_mn;
-        if (pout) {
-            nt = (int32_t)((n_hi + kTileM3 - 1) / kTileM3);
-            pc = p_lo;
-            if (p_lo >= p_hi) tt = -1;
-            else cnt = pcount(p_lo);
-            return;
-        }
         if (tiles.get(0, J, K)) cnt = pivots(J, K);
         else tt = -1;
     }
     __host__ __device__ bool get(int64_t u, int32_t& Jo, int32_t& Ko, int64_t& po) {
         if (tt < 0) return false;
-        if (pout) {
-            while (u >= base + cnt) {
-                base += cnt;
-                if (++pc >= p_hi) { tt = -1; return false; }
-                cnt = pcount(pc);
-            }
-            int64_t l = u - base;
-            int32_t j = (int32_t)((pc + 1) / kTileM3);
-            while (l >= nt - j) { l -= nt - j; ++j; }
-            Jo = j;
-            Ko = j + (int32_t)l;
-            po = pc;
-            return true;
-        }
         while (u >= base + cnt) {
             base += cnt;
             ++tt;
@@ -586,8 +542,6 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         const uint32_t cpair = 2u * (lane & 3u);
         constexpr bool kRowG = O::pos(1) < O::pos(2);   // G_mn = G[gm][gn]: a row of G per m
         ColT3* coltab = reinterpret_cast<ColT3*>(smem + kColOff3);
-        uint8_t* stg = smem + kStgOff3 + (warp - 2) * 2 * kStgBytes3;   // 2 buffers (row halves r)
-        constexpr bool kBulk = kFull && CCC_TMA_STORE && kMode == 0;
         unsigned long long ck_lo = 0, ck_hi = 0;
         uint32_t acc = 0, acc_phase = 0;
         for (int64_t u = unit0;; u += units) {
@@ -727,10 +681,6 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             };
             uint32_t gnext[2][2] = {{0u, 0u}, {0u, 0u}};
             if (c_end > 0) load_gmn(0, gnext);
-#ifdef CCC_G2AHEAD
-            uint32_t gnext2[2][2] = {{0u, 0u}, {0u, 0u}};
-            if (c_end > 1) load_gmn(1, gnext2);
-#endif
             named_bar_sync(1, 32 * kEpiWarps3);   // column table of this unit is complete
             mbar_wait_sleep(&tfull[acc], acc_phase);
             tc_fence_after();
@@ -742,31 +692,14 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 tmem_ld_wait_keep(vnext);
                 const uint32_t va[4] = {vnext[0], vnext[1], vnext[2], vnext[3]};
                 const uint32_t gcur[2][2] = {{gnext[0][0], gnext[0][1]}, {gnext[1][0], gnext[1][1]}};
-#ifdef CCC_G2AHEAD
-                if (c + 1 < c_end) tmem_ld_16x256(taddr + (c + 1) * 8, vnext);
-#pragma unroll
-                for (int x = 0; x < 4; ++x) gnext[x >> 1][x & 1] = gnext2[x >> 1][x & 1];
-                if (c + 2 < c_end) load_gmn(c + 2, gnext2);
-#else
                 if (c + 1 < c_end) {
                     tmem_ld_16x256(taddr + (c + 1) * 8, vnext);
                     load_gmn(c + 1, gnext);
                 }
-#endif
                 const int32_t nA = c * 8 + (int32_t)cpair;    // local column of h = 0
                 const ColT3 cA = ct[nA], cB = ct[nA + 1];
 #pragma unroll
                 for (int r = 0; r < 2; ++r) {
-                    // kBulk: this row's 8-record segment leaves by one 512-B bulk store if
-                    // all 8 records are valid; buffer r must be free of the bulk store
-                    // issued from it one column group ago
-                    const bool seg_ok = kBulk && (8 * c > lo_r[r]) && (8 * c + 8 <= nval);
-                    if constexpr (kBulk) {
-#ifndef CCC_D3_NOBULKWAIT
-                        if (lane < 8) bulk_wait_read<1>();
-#endif
-                        __syncwarp();
-                    }
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         // every record is computed; invalid ones (tile edges, j <= i) are
@@ -848,28 +781,8 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                                 }
                             } else if (want_c64) {
                                 double* q = reinterpret_cast<double*>(args.ccc) + 8 * rec;
-                                if constexpr (kBulk) {
-                                    // stage record (row lane/4, column cpair + h); chunk
-                                    // k ^ (lane & 3) in step k: the 4 pairs of a row hit 4
-                                    // different bank groups, the 64-B row pad separates rows
-                                    uint8_t* rp = stg + r * kStgBytes3 + (lane >> 2) * kStgRow3 +
-                                                  (cpair + h) * 64;
-                                    const uint32_t q4 = lane & 3u;
-#pragma unroll
-                                    for (uint32_t k = 0; k < 4; ++k) {
-                                        const uint32_t kk = k ^ q4;
-                                        const double d0 = kk == 0 ? cc[0] : kk == 1 ? cc[2] : kk == 2 ? cc[4] : cc[6];
-                                        const double d1 = kk == 0 ? cc[1] : kk == 1 ? cc[3] : kk == 2 ? cc[5] : cc[7];
-                                        sts_v4_f64x2(rp + kk * 16, d0, d1);
-                                    }
-                                    if (!seg_ok) {
-                                        stg_256_f64_if(st_ok, q, cc[0], cc[1], cc[2], cc[3]);
-                                        stg_256_f64_if(st_ok, q + 4, cc[4], cc[5], cc[6], cc[7]);
-                                    }
-                                } else {
-                                    stg_256_f64_if(st_ok, q, cc[0], cc[1], cc[2], cc[3]);
-                                    stg_256_f64_if(st_ok, q + 4, cc[4], cc[5], cc[6], cc[7]);
-                                }
+                                stg_256_f64_if(st_ok, q, cc[0], cc[1], cc[2], cc[3]);
+                                stg_256_f64_if(st_ok, q + 4, cc[4], cc[5], cc[6], cc[7]);
                             } else if constexpr (kF32) {
                                 // fp32 only: T < 2^23 is exact as (2^23 + T) - 2^23, U_p U_m and
                                 // U_n / (216 n_f^4) rounded once each: error < 4 x 2^-24 << 1e-6
@@ -904,24 +817,6 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                                      tc);
                         }
                     }
-                    if constexpr (kBulk) {
-                        uint8_t* buf = stg + r * kStgBytes3;
-                        fence_proxy_async_smem();
-                        __syncwarp();
-                        const int64_t rb = (int64_t)__shfl_sync(0xffffffffu, (unsigned long long)rec_r[r],
-                                                                (lane & 7u) * 4u);
-                        const int32_t lo = __shfl_sync(0xffffffffu, lo_r[r], (lane & 7u) * 4u);
-                        if (lane < 8) {
-#ifdef CCC_D3_NOBULKISSUE
-                            if (false)
-#else
-                            if ((8 * c > lo) && (8 * c + 8 <= nval))
-#endif
-                                bulk_store(reinterpret_cast<double*>(args.ccc) + 8 * (rb + 8 * c),
-                                           buf + lane * kStgRow3, 512);
-                            bulk_commit();
-                        }
-                    }
                 }
             }
             tc_fence_before();
@@ -934,7 +829,6 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
         if (want_ck) ck_flush3(ck_lo, ck_hi, args.checksum);
-        if (lane < 8) bulk_wait<0>();   // bulk stores complete before the CTA exits
     }
 
     tc_fence_before();
@@ -947,11 +841,6 @@ int64_t tally3_units(const Tally3Args& a) {
     PivotSched sch;
     sch.init(a);
     if (sch.tt < 0) return 0;
-    if (sch.pout) {
-        int64_t units = 0;
-        for (int64_t p = a.p_lo; p < a.p_hi; ++p) units += sch.pcount(p);
-        return units;
-    }
     TriSched t = sch.tiles;
     t.P = t.Q = 0;
     t.base = 0;
