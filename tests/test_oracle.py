@@ -407,3 +407,23 @@ def test_sparse3_ccc_exact_rational():
                     exact = (Fraction(int(T[r, 4 * a + 2 * b + d]), 8 * int(cc[r])) * (1 - g * fs[0][a]) *
                              (1 - g * fs[1][b]) * (1 - g * fs[2][d]))
                     assert abs(C[r, 4 * a + 2 * b + d] - float(exact)) <= 4e-15 * float(exact) + 1e-300
+
+
+@pytest.mark.parametrize("row", read_golden("sparse_hand_values.txt"))
+def test_sparse_hand_values(row):
+    """Sparse mode worked by hand (tests/golden/sparse_hand_values.txt, reading A-17)."""
+    name, inputs, expected, _ = row
+    a = _args(inputs)
+    vs = [_vec(a[k]) for k in ("vi", "vj", "vk") if k in a]
+    codes = np.array(vs, np.uint8)
+    parts = dict(p.split("=") for p in (x.strip() for x in expected.split(";")))
+    T_want = [int(x) for x in parts["T"].split(",")]
+    C_want = [Fraction(x) for x in parts["C"].split(",")]
+    if name == "sparse_pair":
+        T, C, c = oracle.sparse_pairs(codes, [[0, 1]])
+    else:
+        T, C, c = oracle.sparse_triples(codes, [[0, 1, 2]])
+    assert list(T[0]) == T_want and int(c[0]) == int(parts["c"])
+    for got, want in zip(C[0], C_want):
+        assert abs(got - float(want)) <= 1e-15 * float(want) + (0.0 if want else 0.0)
+        assert (got == 0) == (want == 0)
