@@ -105,3 +105,23 @@ def test_sparse3_large_stage_sampled():
         _ccc_close(C[rows].cpu().numpy(), Co)
         sums = T.to(torch.int64).sum(1)
         assert bool((sums % 8 == 0).all())
+
+
+def test_sparse_hand_values_through_the_kernels():
+    """The hand-worked sparse examples (tests/golden/sparse_hand_values.txt) through the
+    CUDA path: tallies exact, CCC equal to the exact fractions within 1e-12."""
+    from fractions import Fraction
+    from conftest import read_golden
+    for name, inputs, expected, _ in read_golden("sparse_hand_values.txt"):
+        vs = [[int(c) for c in part.split("=")[1].split(",")] for part in inputs.split(";")]
+        codes = torch.tensor(vs, dtype=torch.uint8)
+        parts = dict(p.strip().split("=") for p in expected.split(";"))
+        T_want = [int(x) for x in parts["T"].split(",")]
+        C_want = [float(Fraction(x)) for x in parts["C"].split(",")]
+        if name == "sparse_pair":
+            T, C, _ = ccc.ccc_2way_sparse(ccc.ccc_pack(codes.cuda()), codes.shape[1], out_flags=TAL | F64)
+        else:
+            T, C, _ = ccc.three_way_sparse(codes.cuda(), out_flags=TAL | F64)
+        torch.cuda.synchronize()
+        assert list(_t(T)[0]) == T_want
+        _ccc_close(C.cpu().numpy()[0], np.array(C_want))
