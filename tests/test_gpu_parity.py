@@ -564,3 +564,42 @@ def test_3way_host_stage_streaming(n_stages):
     np.testing.assert_array_equal(T.numpy().astype(np.int64) & 0xFFFFFFFF, To)
     _ccc_close(C.numpy(), Co)
     assert ccc.checksum_int(ck) == oracle.checksum(3, oracle.triple_list(n_v), To)
+
+
+def _golden_vec(spec):
+    out = []
+    for part in spec.split(","):
+        if "*" in part:
+            c, n = part.split("*")
+            out += [int(c)] * int(n)
+        else:
+            out.append(int(part))
+    return out
+
+
+def test_golden_hand_values_through_the_kernels():
+    """SPEC's hand values and our n_f = 1 figure-style examples (tests/golden/) through the
+    CUDA path: tallies exact, CCC equal to the exact fractions (independent of the oracle)."""
+    from fractions import Fraction
+    from conftest import read_golden
+    for name, inputs, expected, _ in read_golden("spec_hand_values.txt"):
+        if name not in ("pair_tally", "ccc2", "ccc3", "reconstruct3"):
+            continue
+        a = dict(kv.strip().split("=") for kv in inputs.split(";"))
+        vs = [_golden_vec(a[k]) for k in ("vi", "vj", "vk") if k in a]
+        codes = torch.tensor(vs, dtype=torch.uint8).cuda()
+        want = [Fraction(x) for x in expected.split("=")[1].split(",")]
+        if name in ("pair_tally", "ccc2"):
+            T, C, _ = ccc.two_way(codes, out_flags=TAL | F64)
+        else:
+            T, C, _ = ccc.three_way(codes, out_flags=TAL | F64)
+        torch.cuda.synchronize()
+        if name in ("pair_tally", "reconstruct3"):
+            assert list(_t(T)[0]) == [int(x) for x in want], name
+        else:
+            _ccc_close(C.cpu().numpy()[0], np.array([float(x) for x in want]))
+    for way, cs, expected, _ in read_golden("fig_examples_nf1.txt"):
+        codes = torch.tensor([[int(c)] for c in cs.split()], dtype=torch.uint8).cuda()
+        T = (ccc.two_way if way == "2" else ccc.three_way)(codes, out_flags=TAL)[0]
+        torch.cuda.synchronize()
+        assert list(_t(T)[0]) == [int(x) for x in expected.split(",")]
