@@ -20,6 +20,10 @@
 #include "common.cuh"
 #include "internal.h"
 
+#ifndef CCC_FS_MINB
+#define CCC_FS_MINB 5   // CTAs per SM the register budget is fitted to
+#endif
+
 namespace ccc {
 
 namespace {
@@ -38,19 +42,28 @@ __device__ __forceinline__ void fs_fold(unsigned long long& lo, unsigned long lo
 
 // One CTA per owned tile at a time (tiles visited in increasing schedule order per CTA,
 // so the TriSched cursor only walks forward); 128 threads, thread = 2 adjacent columns
-// (int2 slot loads; the two records' tallies leave as one 256-bit store), 4 rows in flight.
-__global__ void __launch_bounds__(128) fs_finish_kernel(const int32_t* __restrict__ slots,
+// (int2 slot loads; the two records' tallies leave as one 256-bit store).  The row terms
+// (s_i, w_i(0) / 4n_f, w_i(1) / 4n_f) are computed once per tile into shared memory, so
+// a thread carries only its column terms and kR x W partial loads in flight; W is the
+// world size as a template constant (0 = runtime loop) so every load is issued before the
+// first sum.  Register use stays low enough for 8+ CTAs per SM (the kernel is HBM-bound
+// and needs the bytes in flight).
+template <int W, bool CK>
+__global__ void __launch_bounds__(128, CCC_FS_MINB) fs_finish_kernel(const int32_t* __restrict__ slots,
                                                         const int32_t* __restrict__ s, int64_t n_v,
                                                         int64_t n_f, double gamma, int32_t owner,
-                                                        int32_t world, int64_t t_lo, int64_t t_end,
+                                                        int32_t world_rt, int64_t t_lo, int64_t t_end,
                                                         int32_t tile_m, uint32_t flags,
                                                         uint32_t* __restrict__ tallies, void* ccc,
                                                         unsigned long long* checksum) {
+    __shared__ double row_w0[256], row_w1[256];
+    __shared__ uint32_t row_s[256];
+    const int32_t world = W > 0 ? W : world_rt;
     TriSched sch;
     sch.init(0, n_v, n_v, 1, tile_m, 2048, 2048);   // the schedule of ccc_2way_block(diag)
     const int64_t first = t_lo + ((owner - t_lo % world) % world + world) % world;
     const int64_t owned = first < t_end ? (t_end - first + world - 1) / world : 0;
-    const bool want_t = flags & 1u, want_c64 = flags & 2u, want_c32 = flags & 4u, want_ck = flags & 8u;
+    const bool want_t = flags & 1u, want_c64 = flags & 2u, want_c32 = flags & 4u;
     const double two_nf = 2.0 * (double)n_f, inv4nf = 1.0 / (4.0 * (double)n_f);
     const uint32_t four_nf = 4u * (uint32_t)n_f;
     const int col = 2 * threadIdx.x;
@@ -61,85 +74,114 @@ __global__ void __launch_bounds__(128) fs_finish_kernel(const int32_t* __restric
         if (!sch.get(t, bm, bn)) break;
         const int64_t q = (t - t_lo) / world;
         const int32_t* tile = slots + ((q * world) << 16);
-        int64_t j[2];
-        bool col_ok[2];
-        uint32_t sj[2];
-        double wj0[2], wj1[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            j[h] = (int64_t)bn * kBN + col + h;
-            col_ok[h] = j[h] < n_v;
-            sj[h] = col_ok[h] ? (uint32_t)__ldg(s + j[h]) : 0u;
-            wj0[h] = 1.0 - gamma * ((two_nf - (double)sj[h]) / two_nf);
-            wj1[h] = 1.0 - gamma * ((double)sj[h] / two_nf);
+        __syncthreads();   // the previous tile's row terms are no longer read
+        for (int r = threadIdx.x; r < tile_m; r += blockDim.x) {
+            const int64_t i = (int64_t)bm * tile_m + r;
+            const uint32_t si = i < n_v ? (uint32_t)__ldg(s + i) : 0u;
+            row_s[r] = si;
+            row_w0[r] = (1.0 - gamma * ((two_nf - (double)si) / two_nf)) * inv4nf;
+            row_w1[r] = (1.0 - gamma * ((double)si / two_nf)) * inv4nf;
         }
-        constexpr int kR = 4;   // rows in flight per thread (memory-level parallelism)
-        for (int32_t row0 = 0; row0 < tile_m; row0 += kR) {
+        __syncthreads();
+        const int64_t j0 = (int64_t)bn * kBN + col;
+        const bool ok0 = j0 < n_v, ok1 = j0 + 1 < n_v;
+        const uint32_t sj0 = ok0 ? (uint32_t)__ldg(s + j0) : 0u;
+        const uint32_t sj1 = ok1 ? (uint32_t)__ldg(s + j0 + 1) : 0u;
+        const double wj00 = 1.0 - gamma * ((two_nf - (double)sj0) / two_nf);
+        const double wj01 = 1.0 - gamma * ((double)sj0 / two_nf);
+        const double wj10 = 1.0 - gamma * ((two_nf - (double)sj1) / two_nf);
+        const double wj11 = 1.0 - gamma * ((double)sj1 / two_nf);
+        const int64_t i0 = (int64_t)bm * tile_m;
+        // rows of this tile holding a record of column j0 + 1: i < j0 + 1 and i < n_v - 1
+        int64_t r_end = (j0 + 1 < n_v ? j0 + 1 : n_v - 1) - i0;
+        if (!ok0) r_end = 0;
+        r_end = r_end < 0 ? 0 : (r_end > tile_m ? tile_m : r_end);
+        constexpr int kR = W == 1 ? 8 : 4;   // rows in flight per thread
+        for (int32_t row0 = 0; row0 < (int32_t)r_end; row0 += kR) {
             int2 Gr[kR];
 #pragma unroll
-            for (int u = 0; u < kR; ++u) {
-                const int64_t i = (int64_t)bm * tile_m + row0 + u;
-                Gr[u] = make_int2(0, 0);
-                if (i < n_v - 1 && col_ok[0] && j[1] > i)
-                    for (int32_t f = 0; f < world; ++f) {
-                        const int2 v = __ldg(reinterpret_cast<const int2*>(tile + ((int64_t)f << 16) +
-                                                                           (row0 + u) * kBN + col));
-                        Gr[u].x += v.x;
-                        Gr[u].y += v.y;
+            for (int u = 0; u < kR; ++u) Gr[u] = make_int2(0, 0);
+            if constexpr (W > 0) {
+                int2 v[kR][W];
+#pragma unroll
+                for (int u = 0; u < kR; ++u)
+#pragma unroll
+                    for (int f = 0; f < W; ++f)
+                        v[u][f] = row0 + u < r_end
+                                      ? __ldg(reinterpret_cast<const int2*>(tile + ((int64_t)f << 16) +
+                                                                            (row0 + u) * kBN + col))
+                                      : make_int2(0, 0);
+#pragma unroll
+                for (int u = 0; u < kR; ++u)
+#pragma unroll
+                    for (int f = 0; f < W; ++f) {
+                        Gr[u].x += v[u][f].x;
+                        Gr[u].y += v[u][f].y;
                     }
+            } else {
+                for (int32_t f = 0; f < world; ++f)
+#pragma unroll
+                    for (int u = 0; u < kR; ++u)
+                        if (row0 + u < r_end) {
+                            const int2 v = __ldg(reinterpret_cast<const int2*>(tile + ((int64_t)f << 16) +
+                                                                               (row0 + u) * kBN + col));
+                            Gr[u].x += v.x;
+                            Gr[u].y += v.y;
+                        }
             }
 #pragma unroll
             for (int u = 0; u < kR; ++u) {
-                const int64_t i = (int64_t)bm * tile_m + row0 + u;
-                if (i >= n_v - 1) continue;
-                const uint32_t si = (uint32_t)__ldg(s + i);
-                const double wi0 = (1.0 - gamma * ((two_nf - (double)si) / two_nf)) * inv4nf;
-                const double wi1 = (1.0 - gamma * ((double)si / two_nf)) * inv4nf;
-                uint32_t tt[2][4];
-                double cc[2][4];
-                bool ok[2];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    ok[h] = col_ok[h] && j[h] > i;
-                    const uint32_t G = (uint32_t)(h ? Gr[u].y : Gr[u].x);
-                    tt[h][3] = G;
-                    tt[h][2] = 2u * si - G;
-                    tt[h][1] = 2u * sj[h] - G;
-                    tt[h][0] = four_nf - 2u * si - 2u * sj[h] + G;
-                    cc[h][0] = (double)tt[h][0] * wi0 * wj0[h];
-                    cc[h][1] = (double)tt[h][1] * wi0 * wj1[h];
-                    cc[h][2] = (double)tt[h][2] * wi1 * wj0[h];
-                    cc[h][3] = (double)tt[h][3] * wi1 * wj1[h];
-                }
-                const int64_t rec = i * (2 * n_v - i - 1) / 2 + (j[0] - i - 1);   // record of column col
+                const int32_t r = row0 + u;
+                if (r >= r_end) break;
+                const int64_t i = i0 + r;
+                const uint32_t si = row_s[r];
+                const double wi0 = row_w0[r], wi1 = row_w1[r];
+                const bool okA = j0 > i, okB = ok1;   // column j0 + 1 > i holds for every r < r_end
+                const uint32_t GA = (uint32_t)Gr[u].x, GB = (uint32_t)Gr[u].y;
+                const uint32_t a3 = GA, a2 = 2u * si - GA, a1 = 2u * sj0 - GA, a0 = four_nf - 2u * si - 2u * sj0 + GA;
+                const uint32_t b3 = GB, b2 = 2u * si - GB, b1 = 2u * sj1 - GB, b0 = four_nf - 2u * si - 2u * sj1 + GB;
+                const int64_t rec = i * (2 * n_v - i - 1) / 2 + (j0 - i - 1);   // record of column j0
                 if (want_t) {
-                    if (ok[0] && ok[1] && !(rec & 1))
-                        stg_256_u32(tallies + 4 * rec, tt[0][0], tt[0][1], tt[0][2], tt[0][3], tt[1][0],
-                                    tt[1][1], tt[1][2], tt[1][3]);
-                    else
-#pragma unroll
-                        for (int h = 0; h < 2; ++h)
-                            if (ok[h]) stg_128_u32(tallies + 4 * (rec + h), tt[h][0], tt[h][1], tt[h][2], tt[h][3]);
+                    if (okA && okB && !(rec & 1))
+                        stg_256_u32(tallies + 4 * rec, a0, a1, a2, a3, b0, b1, b2, b3);
+                    else {
+                        if (okA) stg_128_u32(tallies + 4 * rec, a0, a1, a2, a3);
+                        if (okB) stg_128_u32(tallies + 4 * (rec + 1), b0, b1, b2, b3);
+                    }
                 }
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    if (!ok[h]) continue;
-                    if (want_c64)
-                        stg_256_f64(reinterpret_cast<double*>(ccc) + 4 * (rec + h), cc[h][0], cc[h][1], cc[h][2],
-                                    cc[h][3]);
-                    else if (want_c32)
-                        stg_128_u32(reinterpret_cast<float*>(ccc) + 4 * (rec + h), __float_as_uint((float)cc[h][0]),
-                                    __float_as_uint((float)cc[h][1]), __float_as_uint((float)cc[h][2]),
-                                    __float_as_uint((float)cc[h][3]));
-                    if (want_ck)
-                        fs_fold(ck_lo, ck_hi, (2ull << 60) | ((uint64_t)i << 40) | ((uint64_t)j[h] << 20),
-                                (uint64_t)tt[h][0] | ((uint64_t)tt[h][1] << 32),
-                                (uint64_t)tt[h][2] | ((uint64_t)tt[h][3] << 32));
+                if (want_c64) {
+                    double* c = reinterpret_cast<double*>(ccc) + 4 * rec;
+                    if (okA)
+                        stg_256_f64(c, (double)a0 * wi0 * wj00, (double)a1 * wi0 * wj01, (double)a2 * wi1 * wj00,
+                                    (double)a3 * wi1 * wj01);
+                    if (okB)
+                        stg_256_f64(c + 4, (double)b0 * wi0 * wj10, (double)b1 * wi0 * wj11,
+                                    (double)b2 * wi1 * wj10, (double)b3 * wi1 * wj11);
+                } else if (want_c32) {
+                    float* c = reinterpret_cast<float*>(ccc) + 4 * rec;
+                    if (okA)
+                        stg_128_u32(c, __float_as_uint((float)((double)a0 * wi0 * wj00)),
+                                    __float_as_uint((float)((double)a1 * wi0 * wj01)),
+                                    __float_as_uint((float)((double)a2 * wi1 * wj00)),
+                                    __float_as_uint((float)((double)a3 * wi1 * wj01)));
+                    if (okB)
+                        stg_128_u32(c + 4, __float_as_uint((float)((double)b0 * wi0 * wj10)),
+                                    __float_as_uint((float)((double)b1 * wi0 * wj11)),
+                                    __float_as_uint((float)((double)b2 * wi1 * wj10)),
+                                    __float_as_uint((float)((double)b3 * wi1 * wj11)));
+                }
+                if constexpr (CK) {
+                    if (okA)
+                        fs_fold(ck_lo, ck_hi, (2ull << 60) | ((uint64_t)i << 40) | ((uint64_t)j0 << 20),
+                                (uint64_t)a0 | ((uint64_t)a1 << 32), (uint64_t)a2 | ((uint64_t)a3 << 32));
+                    if (okB)
+                        fs_fold(ck_lo, ck_hi, (2ull << 60) | ((uint64_t)i << 40) | ((uint64_t)(j0 + 1) << 20),
+                                (uint64_t)b0 | ((uint64_t)b1 << 32), (uint64_t)b2 | ((uint64_t)b3 << 32));
                 }
             }
         }
     }
-    if (want_ck) {
+    if constexpr (CK) {
         for (int o = 16; o > 0; o >>= 1) {
             const unsigned long long olo = __shfl_xor_sync(0xffffffffu, ck_lo, o);
             const unsigned long long ohi = __shfl_xor_sync(0xffffffffu, ck_hi, o);
@@ -168,10 +210,30 @@ cudaError_t launch_fs_finish(const int32_t* slots, const int32_t* s, int64_t n_v
     const int64_t t_end = (t_hi > 0 && t_hi < all) ? t_hi : all;
     if (t_end <= t_lo) return cudaSuccess;
     const int64_t owned = (t_end - t_lo + world - 1) / world;
-    const int64_t grid = owned < 8 * (int64_t)num_sms ? owned : 8 * (int64_t)num_sms;
-    fs_finish_kernel<<<(unsigned)grid, 128, 0, stream>>>(slots, s, n_v, n_f, gamma, owner, world, t_lo,
-                                                         t_end, tally2_tile_rows(), flags, tallies, ccc,
-                                                         checksum);
+    const bool ck = flags & 8u;
+    auto go = [&](auto kern) {
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0) != cudaSuccess || per_sm < 1)
+            per_sm = 4;
+        const int64_t cap = (int64_t)per_sm * num_sms;
+        const int64_t grid = owned < cap ? owned : cap;
+        kern<<<(unsigned)grid, 128, 0, stream>>>(slots, s, n_v, n_f, gamma, owner, world, t_lo, t_end,
+                                                 tally2_tile_rows(), flags, tallies, ccc, checksum);
+    };
+#define CCC_FS_CASE(w)                                                   \
+    case w:                                                              \
+        ck ? go(fs_finish_kernel<w, true>) : go(fs_finish_kernel<w, false>); \
+        break;
+    switch (world) {
+        CCC_FS_CASE(1)
+        CCC_FS_CASE(2)
+        CCC_FS_CASE(3)
+        CCC_FS_CASE(4)
+        CCC_FS_CASE(8)
+        default:
+            ck ? go(fs_finish_kernel<0, true>) : go(fs_finish_kernel<0, false>);
+    }
+#undef CCC_FS_CASE
     return cudaGetLastError();
 }
 
