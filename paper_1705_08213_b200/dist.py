@@ -131,6 +131,34 @@ class CudaBackend:
         return self.ccc.ccc_last_launch_count()
 
 
+class _StagedRecv:
+    """Completion of a host-staged receive: wait, then copy into the device buffer."""
+
+    def __init__(self, reqs, host, dst):
+        self.reqs, self.host, self.dst = reqs, host, dst
+
+    def wait(self):
+        for q in self.reqs:
+            q.wait()
+        self.dst.copy_(self.host)
+
+
+def ring_shift(cur: torch.Tensor, nxt: torch.Tensor, r: int, P: int, group=None):
+    """Post send(cur -> r-1) and recv(nxt <- r+1); returns the requests to wait on.
+
+    NCCL moves the device buffers directly (NVLink).  gloo cannot move CUDA tensors point to
+    point, so under a gloo group the packed block is staged through host memory -- the
+    transport that lets several ranks share one GPU in the tests; the kernels are the same."""
+    if cur.is_cuda and dist.get_backend(group) == "gloo":
+        host = torch.empty(nxt.shape, dtype=nxt.dtype)
+        ops = [dist.P2POp(dist.isend, cur.contiguous().cpu(), (r - 1) % P, group),
+               dist.P2POp(dist.irecv, host, (r + 1) % P, group)]
+        return [_StagedRecv(dist.batch_isend_irecv(ops), host, nxt)]
+    ops = [dist.P2POp(dist.isend, cur.contiguous(), (r - 1) % P, group),
+           dist.P2POp(dist.irecv, nxt, (r + 1) % P, group)]
+    return dist.batch_isend_irecv(ops)
+
+
 class Ring2Way:
     """Per-rank state of the block-circulant 2-way computation (buffers are reused
     across calls so a bench step does no allocation)."""
@@ -166,9 +194,7 @@ class Ring2Way:
             if d < self.steps:
                 nb = (r + d + 1) % P
                 nxt = self.recv[d % 2][: self._rows(nb)]
-                ops = [dist.P2POp(dist.isend, cur.contiguous(), (r - 1) % P, self.group),
-                       dist.P2POp(dist.irecv, nxt, (r + 1) % P, self.group)]
-                reqs = dist.batch_isend_irecv(ops)
+                reqs = ring_shift(cur, nxt, r, P, self.group)
             held = (r + d) % P
             if d == 0:
                 held_exp = own
@@ -245,9 +271,7 @@ class Ring3Way:
             if d < P - 1:
                 nb = (r + d + 1) % P
                 nxt = self.recv[d % 2][: self.bounds[nb][1] - self.bounds[nb][0]]
-                ops = [dist.P2POp(dist.isend, cur.contiguous(), (r - 1) % P, self.group),
-                       dist.P2POp(dist.irecv, nxt, (r + 1) % P, self.group)]
-                reqs = dist.batch_isend_irecv(ops)
+                reqs = ring_shift(cur, nxt, r, P, self.group)
             if d == 0:   # own-block unit overlaps the gather
                 self.launches += self._run_units(lambda u: u.pb == u.mb == u.nb, sink)
             for q in reqs:
@@ -279,6 +303,8 @@ class Ring3Way:
 def checksum_total(ck_local: torch.Tensor, group=None) -> int:
     """Sum of the ranks' 128-bit checksums mod 2^128 (host-side, exact)."""
     world = dist.get_world_size(group)
+    if ck_local.is_cuda and dist.get_backend(group) == "gloo":
+        ck_local = ck_local.cpu()
     buf = [torch.zeros_like(ck_local) for _ in range(world)]
     dist.all_gather(buf, ck_local, group=group)
     tot = 0

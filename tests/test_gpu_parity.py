@@ -362,6 +362,56 @@ def test_ring_nccl_two_gpus():
     assert cks[0] == cks[1] == oracle.checksum(2, oracle.pair_list(n_v), To)
 
 
+def _gloo_ring_worker(rank, world, port, n_v2, n_v3, n_f, q):
+    import os
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1705_08213_b200 import decomp, dist as cdist
+    be = cdist.CudaBackend(n_f, ccc.GAMMA, TAL | CK)
+    res = {"rank": rank}
+    bounds = decomp.block_bounds(n_v2, world)
+    lo, hi = bounds[rank]
+    r2 = cdist.Ring2Way(be, bounds, rank, world)
+    r2.run(be.pack(synthgen.random_codes(hi - lo, n_f, seed=5, row0=lo, device="cuda")))
+    res["ck2"] = cdist.checksum_total(r2.ck)
+    bounds = decomp.block_bounds(n_v3, world)
+    lo, hi = bounds[rank]
+    r3 = cdist.Ring3Way(be, bounds, rank, world, max_records=3000)
+    r3.run(be.pack(synthgen.random_codes(hi - lo, n_f, seed=6, row0=lo, device="cuda")))
+    res["ck3"] = cdist.checksum_total(r3.ck)
+    dist.destroy_process_group()
+    q.put(res)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_rings_multi_rank_one_gpu(world):
+    """Ring2Way / Ring3Way with the CUDA backend at world 2 and 3: every rank a process on
+    cuda:0 (gloo, packed blocks staged through host memory -- the only multi-rank form a
+    one-GPU box can run); the ranks' checksums add up to the oracle's over all pairs and
+    all triples."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    n_v2, n_v3, n_f = 700, 130, 333
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_gloo_ring_worker, args=(r, world, port, n_v2, n_v3, n_f, q))
+          for r in range(world)]
+    [p.start() for p in ps]
+    res = [q.get(timeout=300) for _ in range(world)]
+    [p.join(timeout=60) for p in ps]
+    T2, _ = oracle.all_pairs(synthgen.random_codes(n_v2, n_f, seed=5))
+    T3, _ = oracle.all_triples(synthgen.random_codes(n_v3, n_f, seed=6))
+    ck2 = oracle.checksum(2, oracle.pair_list(n_v2), T2)
+    ck3 = oracle.checksum(3, oracle.triple_list(n_v3), T3)
+    for r in res:
+        assert r["ck2"] == ck2 and r["ck3"] == ck3, r["rank"]
+
+
 @pytest.mark.parametrize("P,gamma", [(1, oracle.GAMMA), (2, oracle.GAMMA), (3, oracle.GAMMA),
                                      (4, oracle.GAMMA), (3, 0.25)])
 def test_tetrahedral_units_on_one_gpu(P, gamma):
