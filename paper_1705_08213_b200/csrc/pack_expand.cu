@@ -13,9 +13,6 @@
 
 namespace ccc {
 
-// One CTA per vector row (grid-stride over rows, like expand); thread -> 32-bit packed
-// words of 16 codes each, two independent 16-B loads in flight per iteration.  (The
-// first version derived the row from a flat word index with a 64-bit division per word.)
 __device__ __forceinline__ uint32_t pack16(const uint4 c) {
     const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
     uint32_t out = 0;
@@ -30,79 +27,96 @@ __device__ __forceinline__ uint32_t pack16(const uint4 c) {
     return out;
 }
 
+// Warp per vector row (8 rows per CTA in flight, grid-stride over rows).  A warp pass
+// covers 128 packed words: lane l handles words base + 32 u + l (u = 0..3), so each of the
+// four 16-B code loads and each 4-B word store of the pass is one contiguous warp access,
+// with four loads in flight per lane.  A warp per row keeps the ragged end of a row to a
+// fraction of one warp pass (a CTA per row left up to 255 threads idle on the last pass).
+__device__ __forceinline__ uint32_t pack_word_scalar(const uint8_t* row, int64_t n_f, int64_t g) {
+    uint32_t out = 0;
+    const int64_t q0 = g * 16;
+    for (int u = 0; u < 16; ++u) {
+        const int64_t q = q0 + u;
+        if (q < n_f) out |= (uint32_t)(row[q] & 3u) << (2 * u);
+    }
+    return out;
+}
+
 __global__ void __launch_bounds__(256) pack_kernel(const uint8_t* __restrict__ codes,
                                                    int64_t n_v, int64_t n_f, int64_t words_per_row,
                                                    uint32_t* __restrict__ packed) {
     const bool vec_ok = (n_f % 16) == 0 && (reinterpret_cast<uintptr_t>(codes) % 16) == 0;
     const int64_t full = vec_ok ? n_f / 16 : 0;          // words made of 16 in-range codes
-    for (int64_t i = blockIdx.x; i < n_v; i += gridDim.x) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); i < n_v; i += (int64_t)gridDim.x * 8) {
         const uint8_t* row = codes + i * n_f;
         uint32_t* prow = packed + i * words_per_row;
-        int64_t g = threadIdx.x;
-        for (; g + (int64_t)blockDim.x < full; g += 2 * (int64_t)blockDim.x) {
-            const uint4 c0 = __ldcs(reinterpret_cast<const uint4*>(row) + g);
-            const uint4 c1 = __ldcs(reinterpret_cast<const uint4*>(row) + g + blockDim.x);
-            prow[g] = pack16(c0);
-            prow[g + blockDim.x] = pack16(c1);
+        const uint4* crow = reinterpret_cast<const uint4*>(row);
+        int64_t base = 0;
+        for (; base + 128 <= full; base += 128) {
+            uint4 c[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) c[u] = __ldcs(crow + base + 32 * u + lane);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) prow[base + 32 * u + lane] = pack16(c[u]);
         }
-        for (; g < words_per_row; g += blockDim.x) {
-            uint32_t out = 0;
-            if (g < full) {
-                out = pack16(__ldcs(reinterpret_cast<const uint4*>(row) + g));
-            } else {
-                const int64_t q0 = g * 16;
-                for (int u = 0; u < 16; ++u) {
-                    const int64_t q = q0 + u;
-                    if (q < n_f) out |= (uint32_t)(row[q] & 3u) << (2 * u);
-                }
-            }
-            prow[g] = out;
-        }
+        for (int64_t g = base + lane; g < words_per_row; g += 32)
+            prow[g] = g < full ? pack16(__ldcs(crow + g)) : pack_word_scalar(row, n_f, g);
     }
 }
 
-// One CTA per vector row.  Each thread expands 16 codes (one packed word) per step.
+// Warp per vector row (8 rows per CTA): a warp pass covers 128 packed words, lane l words
+// base + 32 u + l -> four coalesced 4-B loads in flight, four coalesced 16-B streaming
+// stores of int8 counts; the row sum is a warp reduction (no CTA barrier between rows).
+__device__ __forceinline__ uint4 expand_word(uint32_t p) {
+    // n = r1 + r2 per 2-bit code: (p & 0x5555...) + ((p >> 1) & 0x5555...)
+    const uint32_t cnt = (p & 0x55555555u) + ((p >> 1) & 0x55555555u);
+    uint32_t o[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        uint32_t x = (cnt >> (8 * b)) & 0xFFu;  // 4 counts, 2 bits each
+        x = (x | (x << 12)) & 0x000F000Fu;
+        x = (x | (x << 6)) & 0x03030303u;
+        o[b] = x;
+    }
+    return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
 __global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict__ packed,
                                                      int64_t n_v, int64_t n_f,
                                                      int64_t words_per_row, int64_t k_pad,
                                                      double gamma, int8_t* __restrict__ N,
                                                      int32_t* __restrict__ s_out,
                                                      double* __restrict__ w_out) {
-    __shared__ int32_t red[8];
-    const int64_t groups = k_pad / 16;
-    for (int64_t i = blockIdx.x; i < n_v; i += gridDim.x) {
+    const int64_t groups = k_pad / 16;   // output words (16 counts each), a multiple of 8
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); i < n_v; i += (int64_t)gridDim.x * 8) {
         const uint32_t* prow = packed + i * words_per_row;
         uint4* nrow = reinterpret_cast<uint4*>(N + i * k_pad);
         int32_t sum = 0;
-        for (int64_t g = threadIdx.x; g < groups; g += blockDim.x) {
-            const uint32_t p = g < words_per_row ? __ldg(prow + g) : 0u;
-            // n = r1 + r2 per 2-bit code: (p & 0x5555...) + ((p >> 1) & 0x5555...)
-            const uint32_t cnt = (p & 0x55555555u) + ((p >> 1) & 0x55555555u);
-            uint32_t o[4];
+        for (int64_t base = 0; base < groups; base += 128) {
+            uint32_t p[4];
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                uint32_t x = (cnt >> (8 * b)) & 0xFFu;  // 4 counts, 2 bits each
-                x = (x | (x << 12)) & 0x000F000Fu;
-                x = (x | (x << 6)) & 0x03030303u;
-                o[b] = x;
+            for (int u = 0; u < 4; ++u) {
+                const int64_t g = base + 32 * u + lane;
+                p[u] = g < words_per_row ? __ldg(prow + g) : 0u;
             }
-            sum += __popc(p);  // sum of r1 + r2 over the 16 codes
-            __stcs(nrow + g, make_uint4(o[0], o[1], o[2], o[3]));
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t g = base + 32 * u + lane;
+                sum += __popc(p[u]);   // sum of r1 + r2 over the 16 codes
+                if (g < groups) __stcs(nrow + g, expand_word(p[u]));
+            }
         }
         for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int32_t s = 0;
-            for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += red[k];
-            s_out[i] = s;
+        if (lane == 0) {
+            s_out[i] = sum;
             const double two_nf = 2.0 * (double)n_f;
-            const double f1 = (double)s / two_nf;                       // Eq.1, a = 1
-            const double f0 = (double)(2 * n_f - (int64_t)s) / two_nf;  // Eq.1, a = 0
+            const double f1 = (double)sum / two_nf;                       // Eq.1, a = 1
+            const double f0 = (double)(2 * n_f - (int64_t)sum) / two_nf;  // Eq.1, a = 0
             w_out[2 * i + 0] = 1.0 - gamma * f0;
             w_out[2 * i + 1] = 1.0 - gamma * f1;
         }
-        __syncthreads();
     }
 }
 
@@ -266,7 +280,8 @@ cudaError_t launch_expand_masks(const uint8_t* packed, int64_t n_v, int64_t n_f,
 cudaError_t launch_pack(const uint8_t* codes, int64_t n_v, int64_t n_f, uint8_t* packed,
                         int num_sms, cudaStream_t stream) {
     const int64_t wpr = (n_f + 63) / 64 * 4;
-    int64_t blocks = n_v < (int64_t)num_sms * 8 ? n_v : (int64_t)num_sms * 8;
+    const int64_t rows_blocks = (n_v + 7) / 8;   // a warp per row, 8 per CTA
+    int64_t blocks = rows_blocks < (int64_t)num_sms * 8 ? rows_blocks : (int64_t)num_sms * 8;
     if (blocks < 1) blocks = 1;
     pack_kernel<<<(int)blocks, 256, 0, stream>>>(codes, n_v, n_f, wpr,
                                                  reinterpret_cast<uint32_t*>(packed));
@@ -277,7 +292,8 @@ cudaError_t launch_expand(const uint8_t* packed, int64_t n_v, int64_t n_f, doubl
                           int8_t* N, int32_t* s, double* w, int num_sms, cudaStream_t stream) {
     const int64_t wpr = (n_f + 63) / 64 * 4;
     const int64_t k_pad = (n_f + 127) / 128 * 128;
-    int64_t blocks = n_v < (int64_t)num_sms * 8 ? n_v : (int64_t)num_sms * 8;
+    const int64_t rows_blocks = (n_v + 7) / 8;   // a warp per row, 8 per CTA
+    int64_t blocks = rows_blocks < (int64_t)num_sms * 8 ? rows_blocks : (int64_t)num_sms * 8;
     if (blocks < 1) blocks = 1;
     expand_kernel<<<(int)blocks, 256, 0, stream>>>(reinterpret_cast<const uint32_t*>(packed),
                                                    n_v, n_f, wpr, k_pad, gamma, N, s, w);
