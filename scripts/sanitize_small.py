@@ -36,5 +36,11 @@ from paper_1705_08213_b200 import fieldsplit
 Tf, _, _ = fieldsplit.run_simulated(codes.cuda(), 3, F, wave_tiles=1)
 Td, _, _ = ccc.two_way(codes.cuda(), out_flags=F)
 assert bool((Tp == Td).all()) and bool((Tf == Td).all())
+Tf5, _, _ = fieldsplit.run_simulated(codes.cuda(), 5, F)          # generic-world finish
+assert bool((Tf5 == Td).all())
+c16 = synthgen.random_codes(130, 4096 + 256, seed=6)              # vector pack path
+T16, _, _ = ccc.two_way(c16.cuda(), out_flags=ccc.OUT_TALLY)
+To16, _ = oracle.all_pairs(c16)
+assert np.array_equal(T16.cpu().numpy().astype(np.int64) & 0xFFFFFFFF, To16)
 torch.cuda.synchronize()
 print("sanitize run ok")
