@@ -45,23 +45,33 @@ __device__ __forceinline__ uint32_t pack_word_scalar(const uint8_t* row, int64_t
 __global__ void __launch_bounds__(256) pack_kernel(const uint8_t* __restrict__ codes,
                                                    int64_t n_v, int64_t n_f, int64_t words_per_row,
                                                    uint32_t* __restrict__ packed) {
-    const bool vec_ok = (n_f % 16) == 0 && (reinterpret_cast<uintptr_t>(codes) % 16) == 0;
-    const int64_t full = vec_ok ? n_f / 16 : 0;          // words made of 16 in-range codes
+    // rows are 16-B aligned when n_f % 16 == 0 (uint4 loads), 4-B aligned when n_f % 4 == 0
+    // (four u32 loads per word, e.g. the field slices of f3); otherwise bytes
+    const uintptr_t base_addr = reinterpret_cast<uintptr_t>(codes);
+    const bool vec16 = (n_f % 16) == 0 && (base_addr % 16) == 0;
+    const bool vec4 = !vec16 && (n_f % 4) == 0 && (base_addr % 4) == 0;
+    const int64_t full = (vec16 || vec4) ? n_f / 16 : 0;   // words made of 16 in-range codes
     const int lane = threadIdx.x & 31;
     for (int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); i < n_v; i += (int64_t)gridDim.x * 8) {
         const uint8_t* row = codes + i * n_f;
         uint32_t* prow = packed + i * words_per_row;
         const uint4* crow = reinterpret_cast<const uint4*>(row);
+        const uint32_t* crow4 = reinterpret_cast<const uint32_t*>(row);
+        auto load16 = [&](int64_t g) -> uint4 {
+            if (vec16) return __ldcs(crow + g);
+            return make_uint4(__ldcs(crow4 + 4 * g), __ldcs(crow4 + 4 * g + 1), __ldcs(crow4 + 4 * g + 2),
+                              __ldcs(crow4 + 4 * g + 3));
+        };
         int64_t base = 0;
         for (; base + 128 <= full; base += 128) {
             uint4 c[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) c[u] = __ldcs(crow + base + 32 * u + lane);
+            for (int u = 0; u < 4; ++u) c[u] = load16(base + 32 * u + lane);
 #pragma unroll
             for (int u = 0; u < 4; ++u) prow[base + 32 * u + lane] = pack16(c[u]);
         }
         for (int64_t g = base + lane; g < words_per_row; g += 32)
-            prow[g] = g < full ? pack16(__ldcs(crow + g)) : pack_word_scalar(row, n_f, g);
+            prow[g] = g < full ? pack16(load16(g)) : pack_word_scalar(row, n_f, g);
     }
 }
 

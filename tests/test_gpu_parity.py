@@ -43,7 +43,7 @@ def _codes(kind, n_v, n_f, seed=None):
 
 
 # ------------------------------------------------------------------- pack / expand
-@pytest.mark.parametrize("n_v,n_f", [(1, 1), (3, 63), (5, 64), (7, 65), (9, 1000), (33, 4111)])
+@pytest.mark.parametrize("n_v,n_f", [(1, 1), (3, 63), (5, 64), (7, 65), (9, 1000), (33, 4111), (11, 4100), (6, 12500)])
 def test_pack_expand(n_v, n_f):
     codes = _codes("random", n_v, n_f, seed=n_f)
     packed = ccc.ccc_pack(codes.cuda())
