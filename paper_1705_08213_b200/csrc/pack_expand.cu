@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict_
 }
 
 // Sparse (missing-data) mode, §7 item 1, reading A-17: the code
-// (1,0) marks a missing entry.  One CTA per vector i writes two operand rows of the
+// (1,0) marks a missing entry.  One warp per vector i writes two operand rows of the
 // group-interleaved matrix X (groups of 16 vectors: 16 rows n, then 16 rows v):
 //   X[32 (i/16) + i%16]      = n_{iq} = rho_{i,q}(1) on present entries, 0 if missing
 //   X[32 (i/16) + 16 + i%16] = v_{iq} = [entry present], 0 on the K padding
@@ -144,63 +144,64 @@ __global__ void __launch_bounds__(256) expand_sparse_kernel(
     int8_t* __restrict__ V) {
     // V != NULL: the separate layout of the 3-way sparse mode -- n in row i of X, the
     // presence bits in row i of V (n_v16 = n_v, no group interleaving)
-    __shared__ int32_t red[2][8];
+    // a warp per vector (8 per CTA), warp passes of 128 packed words as in expand_kernel
     const int64_t groups = k_pad / 16;
-    for (int64_t i = blockIdx.x; i < n_v16; i += gridDim.x) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); i < n_v16; i += (int64_t)gridDim.x * 8) {
         const bool real = i < n_v;
         const uint32_t* prow = packed + i * words_per_row;
         const int64_t xr = 32 * (i / 16) + (i % 16);
         uint4* nrow = reinterpret_cast<uint4*>(V ? X + i * k_pad : X + xr * k_pad);
         uint4* vrow = reinterpret_cast<uint4*>(V ? V + i * k_pad : X + (xr + 16) * k_pad);
         int32_t sum = 0, cnt = 0;
-        for (int64_t g = threadIdx.x; g < groups; g += blockDim.x) {
-            const uint32_t p = (real && g < words_per_row) ? __ldg(prow + g) : 0u;
-            const int64_t left = n_f - 16 * g;       // codes of this group inside n_f
-            const uint32_t inside = !real || left <= 0 ? 0u
-                                    : left >= 16 ? 0x55555555u
-                                                 : (uint32_t)((1ull << (2 * left)) - 1) & 0x55555555u;
-            const uint32_t lo = p & 0x55555555u, hi = (p >> 1) & 0x55555555u;   // r2, r1
-            const uint32_t present = (~hi | lo) & inside;       // not (r1, r2) = (1, 0)
-            const uint32_t n = lo + (hi & lo);                   // r1 + r2 if present, else 0
-            uint32_t on[4], ov[4];
+        for (int64_t base = 0; base < groups; base += 128) {
+            uint32_t pw[4];
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                uint32_t x = (n >> (8 * b)) & 0xFFu;
-                x = (x | (x << 12)) & 0x000F000Fu;
-                on[b] = (x | (x << 6)) & 0x03030303u;
-                uint32_t y = (present >> (8 * b)) & 0xFFu;
-                y = (y | (y << 12)) & 0x000F000Fu;
-                ov[b] = (y | (y << 6)) & 0x03030303u;
+            for (int u = 0; u < 4; ++u) {
+                const int64_t g = base + 32 * u + lane;
+                pw[u] = (real && g < words_per_row) ? __ldg(prow + g) : 0u;
             }
-            sum += __popc(lo) + __popc(hi & lo);
-            cnt += __popc(present);
-            __stcs(nrow + g, make_uint4(on[0], on[1], on[2], on[3]));
-            __stcs(vrow + g, make_uint4(ov[0], ov[1], ov[2], ov[3]));
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t g = base + 32 * u + lane;
+                if (g >= groups) continue;
+                const uint32_t p = pw[u];
+                const int64_t left = n_f - 16 * g;       // codes of this group inside n_f
+                const uint32_t inside = !real || left <= 0 ? 0u
+                                        : left >= 16 ? 0x55555555u
+                                                     : (uint32_t)((1ull << (2 * left)) - 1) & 0x55555555u;
+                const uint32_t lo = p & 0x55555555u, hi = (p >> 1) & 0x55555555u;   // r2, r1
+                const uint32_t present = (~hi | lo) & inside;       // not (r1, r2) = (1, 0)
+                const uint32_t n = lo + (hi & lo);                   // r1 + r2 if present, else 0
+                uint32_t on[4], ov[4];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    uint32_t x = (n >> (8 * b)) & 0xFFu;
+                    x = (x | (x << 12)) & 0x000F000Fu;
+                    on[b] = (x | (x << 6)) & 0x03030303u;
+                    uint32_t y = (present >> (8 * b)) & 0xFFu;
+                    y = (y | (y << 12)) & 0x000F000Fu;
+                    ov[b] = (y | (y << 6)) & 0x03030303u;
+                }
+                sum += __popc(lo) + __popc(hi & lo);
+                cnt += __popc(present);
+                __stcs(nrow + g, make_uint4(on[0], on[1], on[2], on[3]));
+                __stcs(vrow + g, make_uint4(ov[0], ov[1], ov[2], ov[3]));
+            }
         }
         for (int off = 16; off > 0; off >>= 1) {
             sum += __shfl_xor_sync(0xffffffffu, sum, off);
             cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
         }
-        if ((threadIdx.x & 31) == 0) {
-            red[0][threadIdx.x >> 5] = sum;
-            red[1][threadIdx.x >> 5] = cnt;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0 && real) {
-            int32_t sv = 0, cv = 0;
-            for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
-                sv += red[0][k];
-                cv += red[1][k];
-            }
-            s_out[i] = sv;
-            c_out[i] = cv;
-            const double two_c = 2.0 * (double)cv;
-            const double f1 = cv ? (double)sv / two_c : 0.0;                 // S_i(1) / (2 c_i)
-            const double f0 = cv ? (double)(2 * cv - sv) / two_c : 0.0;      // S_i(0) / (2 c_i)
+        if (lane == 0 && real) {
+            s_out[i] = sum;
+            c_out[i] = cnt;
+            const double two_c = 2.0 * (double)cnt;
+            const double f1 = cnt ? (double)sum / two_c : 0.0;                 // S_i(1) / (2 c_i)
+            const double f0 = cnt ? (double)(2 * cnt - sum) / two_c : 0.0;     // S_i(0) / (2 c_i)
             w_out[2 * i + 0] = 1.0 - gamma * f0;
             w_out[2 * i + 1] = 1.0 - gamma * f1;
         }
-        __syncthreads();
     }
 }
 
@@ -210,7 +211,8 @@ cudaError_t launch_expand_sparse(const uint8_t* packed, int64_t n_v, int64_t n_f
     const int64_t wpr = (n_f + 63) / 64 * 4;
     const int64_t k_pad = (n_f + 127) / 128 * 128;
     const int64_t n_v16 = (n_v + 15) / 16 * 16;
-    int64_t blocks = n_v16 < (int64_t)num_sms * 8 ? n_v16 : (int64_t)num_sms * 8;
+    const int64_t rows_blocks = (n_v16 + 7) / 8;   // a warp per row, 8 per CTA
+    int64_t blocks = rows_blocks < (int64_t)num_sms * 8 ? rows_blocks : (int64_t)num_sms * 8;
     if (blocks < 1) blocks = 1;
     expand_sparse_kernel<<<(int)blocks, 256, 0, stream>>>(
         reinterpret_cast<const uint32_t*>(packed), n_v, n_v16, n_f, wpr, k_pad, gamma, X, s, c, w, nullptr);
@@ -222,7 +224,8 @@ cudaError_t launch_expand_sparse3(const uint8_t* packed, int64_t n_v, int64_t n_
                                   cudaStream_t stream) {
     const int64_t wpr = (n_f + 63) / 64 * 4;
     const int64_t k_pad = (n_f + 127) / 128 * 128;
-    int64_t blocks = n_v < (int64_t)num_sms * 8 ? n_v : (int64_t)num_sms * 8;
+    const int64_t rows_blocks = (n_v + 7) / 8;   // a warp per row, 8 per CTA
+    int64_t blocks = rows_blocks < (int64_t)num_sms * 8 ? rows_blocks : (int64_t)num_sms * 8;
     if (blocks < 1) blocks = 1;
     expand_sparse_kernel<<<(int)blocks, 256, 0, stream>>>(
         reinterpret_cast<const uint32_t*>(packed), n_v, n_v, n_f, wpr, k_pad, gamma, Ns, s, c, w, V);
