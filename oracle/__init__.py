@@ -48,7 +48,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c99",
-                               "-o", tmp, _SRC])
+                               "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -71,6 +71,12 @@ def lib():
         L.oracle_sparse_sums.argtypes = [p, i64, i64, p, p]
         L.oracle_sparse_pairs.argtypes = [p, i64, i64, p, p, ctypes.c_double, p, i64, p, p, p]
         L.oracle_sparse_triples.argtypes = [p, i64, i64, p, p, ctypes.c_double, p, i64, p, p, p]
+        L.oracle_planted_sums.argtypes = [p, p, i64, i64, p]
+        for name in ("oracle_planted_pairs", "oracle_planted_triples"):
+            getattr(L, name).argtypes = [p, p, i64, i64, ctypes.c_double, i64, i64, p, p]
+        for name in ("oracle_planted_check2", "oracle_planted_check3"):
+            getattr(L, name).argtypes = [p, p, i64, i64, ctypes.c_double, i64, i64, p, p,
+                                         ctypes.c_int, ctypes.c_double, p, p]
         _lib = L
     return _lib
 
@@ -367,6 +373,82 @@ def planted_tally2(L, H, n_f, i, j):
                     rb = nj if b == 1 else 2 - nj
                     T[2 * a + b] += w * ra * rb
     return T
+
+
+def _lh(L, H):
+    return (np.ascontiguousarray(L, dtype=np.int64), np.ascontiguousarray(H, dtype=np.int64))
+
+
+def planted_sums(L, H, n_f):
+    """Eq.1 numerators S [n_v][2] of the planted vectors, by the piecewise closed form of
+    ccc_oracle.c (rho constant between the breakpoints 0, L_i, L_i + H_i, n_f)."""
+    L, H = _lh(L, H)
+    S = np.zeros((len(L), 2), dtype=np.int64)
+    lib().oracle_planted_sums(_ptr(L), _ptr(H), len(L), n_f, _ptr(S))
+    return S
+
+
+def planted_pairs(L, H, n_f, rec0=0, nrec=None, gamma: float = GAMMA):
+    """Closed-form records [rec0, rec0+nrec) of the lexicographic pair order:
+    (T int64 [nrec][4], CCC fp64 [nrec][4])."""
+    L, H = _lh(L, H)
+    n_v = len(L)
+    if nrec is None:
+        nrec = n_v * (n_v - 1) // 2 - rec0
+    T = np.zeros((nrec, 4), np.int64)
+    C = np.zeros((nrec, 4), np.float64)
+    if nrec:
+        lib().oracle_planted_pairs(_ptr(L), _ptr(H), n_v, n_f, gamma, rec0, nrec, _ptr(T), _ptr(C))
+    return T, C
+
+
+def planted_triples(L, H, n_f, rec0=0, nrec=None, gamma: float = GAMMA):
+    """Closed-form records [rec0, rec0+nrec) of the lexicographic triple order."""
+    L, H = _lh(L, H)
+    n_v = len(L)
+    if nrec is None:
+        nrec = n_v * (n_v - 1) * (n_v - 2) // 6 - rec0
+    T = np.zeros((nrec, 8), np.int64)
+    C = np.zeros((nrec, 8), np.float64)
+    if nrec:
+        lib().oracle_planted_triples(_ptr(L), _ptr(H), n_v, n_f, gamma, rec0, nrec, _ptr(T), _ptr(C))
+    return T, C
+
+
+def _host_ptr(a):
+    """(pointer, element size) of a contiguous host array (numpy or torch CPU tensor)."""
+    if a is None:
+        return None, 0
+    if hasattr(a, "data_ptr"):
+        if a.is_cuda or not a.is_contiguous():
+            raise ValueError("records must be contiguous host memory")
+        return ctypes.c_void_p(a.data_ptr()), a.element_size()
+    a = np.ascontiguousarray(a)
+    return _ptr(a), a.itemsize
+
+
+def planted_check(way: int, L, H, n_f, rec0, nrec, T=None, C=None, rtol=1e-12,
+                  gamma: float = GAMMA):
+    """Compare caller-held records [rec0, rec0+nrec) (tallies uint32/int32 [nrec][cells],
+    CCC fp64 or fp32 [nrec][cells], host memory) with the planted closed form, record by
+    record in C.  Returns dict(bad_tallies, bad_ccc, first_bad, max_rel)."""
+    L, H = _lh(L, H)
+    cells = 4 if way == 2 else 8
+    for a in (T, C):
+        if a is not None and tuple(a.shape) != (nrec, cells):
+            raise ValueError(f"records must be [{nrec}][{cells}]")
+    pt, st = _host_ptr(T)
+    if T is not None and st != 4:
+        raise ValueError("tallies must be 32-bit")
+    pc, sc = _host_ptr(C)
+    res = np.zeros(3, np.int64)
+    mrel = ctypes.c_double(0.0)
+    fn = lib().oracle_planted_check2 if way == 2 else lib().oracle_planted_check3
+    fn(_ptr(L), _ptr(H), len(L), n_f, gamma, rec0, nrec, pt, pc, sc, rtol, _ptr(res),
+       ctypes.byref(mrel))
+    keep = (T, C)   # noqa: F841 -- alive across the call
+    return {"bad_tallies": int(res[0]), "bad_ccc": int(res[1]), "first_bad": int(res[2]),
+            "max_rel": mrel.value}
 
 
 def planted_tally3(L, H, n_f, i, j, k):

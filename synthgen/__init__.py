@@ -151,7 +151,8 @@ def planted_lengths(n_v: int, n_f: int, seed: int = 3):
     return L, H
 
 
-def planted_codes(n_v: int, n_f: int, seed: int = 3, device="cpu", permute: bool = True):
+def planted_codes(n_v: int, n_f: int, seed: int = 3, device="cpu", permute: bool = True,
+                  chunk_rows: int = 256):
     """Type-2 planted data (§5: "randomized placement of entries
     specifically chosen so that the correctness of every result value can be verified
     analytically").
@@ -159,23 +160,26 @@ def planted_codes(n_v: int, n_f: int, seed: int = 3, device="cpu", permute: bool
     Before the column permutation, vector i holds code 3 = (1,1) on [0, L_i), the
     heterozygous codes 1 = (0,1) / 2 = (1,0) alternating (by field parity) on
     [L_i, L_i + H_i), and code 0 = (0,0) after. One seeded column permutation shared
-    by all vectors is then applied. Returns (codes uint8 [n_v][n_f], L, H, perm).
+    by all vectors is then applied. Generated chunk by chunk of rows on `device` (full
+    sizes stay within memory). Returns (codes uint8 [n_v][n_f], L, H, perm).
     """
     L, H = planted_lengths(n_v, n_f, seed)
-    q = torch.arange(n_f, dtype=torch.int64)
-    Lt = torch.tensor(L, dtype=torch.int64)[:, None]
-    Ht = torch.tensor(H, dtype=torch.int64)[:, None]
-    het = torch.where((q % 2) == 0, 1, 2)[None, :].expand(n_v, n_f)
-    codes = torch.zeros((n_v, n_f), dtype=torch.int64)
-    codes = torch.where(q[None, :] < Lt, torch.full_like(codes, 3), codes)
-    mid = (q[None, :] >= Lt) & (q[None, :] < Lt + Ht)
-    codes = torch.where(mid, het, codes)
     perm = torch.arange(n_f)
     if permute:
         g = torch.Generator().manual_seed(seed)
         perm = torch.randperm(n_f, generator=g)
-        codes = codes[:, perm]
-    return codes.to(torch.uint8).to(device), L, H, perm
+    out = torch.empty((n_v, n_f), dtype=torch.uint8, device=device)
+    # column c of the output holds pre-permutation field perm[c]
+    qp = perm.to(device=device, dtype=torch.int64)[None, :]
+    het = torch.where((qp % 2) == 0, 1, 2).to(torch.uint8)
+    Lt = torch.tensor(L, dtype=torch.int64, device=device)[:, None]
+    Et = Lt + torch.tensor(H, dtype=torch.int64, device=device)[:, None]
+    for r0 in range(0, n_v, chunk_rows):
+        r1 = min(n_v, r0 + chunk_rows)
+        lo, hi = Lt[r0:r1], Et[r0:r1]
+        c = torch.where(qp < hi, het, torch.zeros((), dtype=torch.uint8, device=device))
+        out[r0:r1] = torch.where(qp < lo, torch.full((), 3, dtype=torch.uint8, device=device), c)
+    return out, L, H, perm
 
 
 def make_codes(kind: str, n_v: int, n_f: int, seed: int | None = None, device="cpu",

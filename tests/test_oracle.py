@@ -247,6 +247,89 @@ def test_planted_closed_form():
         assert list(T3[r]) == oracle.planted_tally3(L, H, 97, i, j, k)
 
 
+def _planted_by_hand(L, H, n_f, seed):
+    """Planted codes built here from (L, H) without synthgen: (1,1) on [0, L), the two
+    heterozygote codes alternating on [L, L+H), (0,0) after, then a shared column shuffle."""
+    rng = np.random.default_rng(seed)
+    codes = np.zeros((len(L), n_f), np.uint8)
+    for i, (l, h) in enumerate(zip(L, H)):
+        codes[i, :l] = 3
+        codes[i, l:l + h] = rng.choice([1, 2], size=h)
+    return codes[:, rng.permutation(n_f)]
+
+
+@pytest.mark.parametrize("n_v,n_f,seed", [(40, 7, 1), (33, 64, 2), (25, 301, 3), (12, 1, 4)])
+def test_planted_closed_form_c_vs_brute_force(n_v, n_f, seed):
+    """The C closed form of the planted design (oracle_planted_*) equals the
+    Fig.1 / Fig.2 brute force record for record -- tallies and fp64 CCC bit-identical --
+    including the edge intervals L = 0, H = 0, L + H = n_f."""
+    rng = np.random.default_rng(seed)
+    L = rng.integers(0, n_f + 1, n_v)
+    H = np.array([rng.integers(0, n_f - l + 1) for l in L])
+    L[:4] = [0, n_f, 0, n_f // 2]
+    H[:4] = [0, 0, n_f, n_f - n_f // 2]
+    codes = _planted_by_hand(L, H, n_f, seed)
+    T, C = oracle.all_pairs(codes)
+    Tp, Cp = oracle.planted_pairs(L, H, n_f)
+    np.testing.assert_array_equal(Tp, T)
+    np.testing.assert_array_equal(Cp, C)
+    T3, C3 = oracle.all_triples(codes[:20])
+    Tp3, Cp3 = oracle.planted_triples(L[:20], H[:20], n_f)
+    np.testing.assert_array_equal(Tp3, T3)
+    np.testing.assert_array_equal(Cp3, C3)
+    np.testing.assert_array_equal(oracle.planted_sums(L, H, n_f), oracle.allele_sums(codes))
+    for g in (0.0, 0.5):
+        np.testing.assert_array_equal(oracle.planted_pairs(L, H, n_f, gamma=g)[1],
+                                      oracle.all_pairs(codes, g)[1])
+
+
+def test_planted_closed_form_c_vs_python_intervals():
+    """...and the Python interval form (planted_tally2/3) on synthgen's planted data."""
+    n_v, n_f = 30, 1001
+    L, H = synthgen.planted_lengths(n_v, n_f, 3)
+    Tp, _ = oracle.planted_pairs(L, H, n_f)
+    for r, (i, j) in enumerate(oracle.pair_list(n_v)):
+        assert list(Tp[r]) == oracle.planted_tally2(L, H, n_f, i, j)
+    Tp3, _ = oracle.planted_triples(L, H, n_f, 50, 400)
+    for r, (i, j, k) in enumerate(oracle.triple_list(n_v)[50:450]):
+        assert list(Tp3[r]) == oracle.planted_tally3(L, H, n_f, i, j, k)
+
+
+@pytest.mark.parametrize("way", [2, 3])
+def test_planted_checker_catches_errors(way):
+    """The full-size checker (oracle_planted_check2/3) passes the closed-form records at
+    rtol = 0 (the hoisted 3-way evaluation is bit-identical), on any sub-range, and flags a
+    tally off by one, a CCC cell off by 1e-11 relative, a nonzero CCC where the tally is 0,
+    a NaN, fp32 beyond 1e-6 and records shifted by one position."""
+    n_v, n_f = 45, 333
+    L, H = synthgen.planted_lengths(n_v, n_f, 3)
+    T, C = (oracle.planted_pairs if way == 2 else oracle.planted_triples)(L, H, n_f)
+    T = T.astype(np.uint32)
+    m = len(T)
+    chk = lambda rec0, t, c, **kw: oracle.planted_check(way, L, H, n_f, rec0, len(t if t is not None else c), t, c, **kw)  # noqa: E731
+    assert chk(0, T, C, rtol=0) == {"bad_tallies": 0, "bad_ccc": 0, "first_bad": -1, "max_rel": 0.0}
+    assert chk(m // 3, T[m // 3: m // 2], C[m // 3: m // 2], rtol=0)["first_bad"] == -1
+    assert chk(0, T, C.astype(np.float32), rtol=1e-6)["bad_ccc"] == 0
+    assert chk(0, T, C.astype(np.float32), rtol=1e-9)["bad_ccc"] > 0
+    bad = T.copy()
+    bad[m // 2, 1] += 1
+    r = chk(0, bad, C)
+    assert (r["bad_tallies"], r["bad_ccc"], r["first_bad"]) == (1, 0, m // 2)
+    for r0, val in ((7, None), (m - 1, np.nan)):
+        Cb = C.copy()
+        nzc = np.flatnonzero(Cb[r0])[0]
+        Cb[r0, nzc] = Cb[r0, nzc] * (1 + 1e-11) if val is None else val
+        r = chk(0, T, Cb)
+        assert (r["bad_tallies"], r["bad_ccc"], r["first_bad"]) == (0, 1, r0)
+    zr, zc = np.argwhere(T == 0)[0]
+    Cb = C.copy()
+    Cb[zr, zc] = 1e-300
+    assert chk(0, T, Cb)["bad_ccc"] == 1
+    r = chk(1, T[:-1], C[:-1])
+    assert r["bad_tallies"] > m // 2 and r["first_bad"] == 0
+    assert chk(0, T, None)["bad_ccc"] == 0 and chk(0, None, C)["bad_tallies"] == 0
+
+
 def test_padding_independence():
     """Results are over exactly n_f fields (A-9): appending fields changes sums by the
     appended contribution only; n_f=65 all-(0,0) gives 260 (not 4*128)."""
