@@ -156,8 +156,11 @@ def ncu_traffic(kernel: str):
         return None
 
 
-def cpu_baseline(way, n_v, n_f, target_s=12.0, kind="random"):  # noqa: C901
-    """The oracle as it stands, on the host cores, on a bounded sample of the workload."""
+def cpu_baseline(way, n_v, n_f, target_s=12.0, kind="random", row_lo=0, with_records=False):  # noqa: C901
+    """The oracle as it stands, on the host cores, on a bounded sample of the workload:
+    all pairs (triples) among sampled vectors of rows [row_lo, n_v), as many as fit in
+    ~target_s seconds.  with_records: also return (global indices, T, CCC) of the sample,
+    which bench.py compares with the timed step's own output buffers ("parity")."""
     import numpy as np
 
     import oracle
@@ -165,7 +168,8 @@ def cpu_baseline(way, n_v, n_f, target_s=12.0, kind="random"):  # noqa: C901
     cores = len(os.sched_getaffinity(0))
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
     rng = np.random.default_rng(0)
-    rows = np.sort(rng.choice(n_v, size=min(n_v, 1024 if way == 2 else 128), replace=False))
+    span = n_v - row_lo
+    rows = np.sort(rng.choice(span, size=min(span, 1024 if way == 2 else 128), replace=False)) + row_lo
     sub = np.concatenate([synthgen.make_codes(kind, 1, n_f, row0=int(r)).numpy() for r in rows])
     oracle.lib()
     m_local = len(rows)
@@ -192,12 +196,59 @@ def cpu_baseline(way, n_v, n_f, target_s=12.0, kind="random"):  # noqa: C901
         m = min(len(allidx), m * 4)
     m_run = int(min(len(allidx), max(m, m * target_s / max(dt, 1e-6))))
     t0 = time.perf_counter()
-    f(sub, allidx[:m_run], S=S)
+    res = f(sub, allidx[:m_run], S=S)
     dt = time.perf_counter() - t0
     what = "pairs" if way == 2 else "triples"
-    return {"value": m_run * n_f / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{m_run} {what} (n_f={n_f}) among {m_local} sampled vectors of the "
-                      f"workload, brute-force Fig.1/Fig.2 enumeration, {dt:.1f} s"}
+    where = f" of rows [{row_lo}, {n_v}) (the last stage)" if row_lo else ""
+    out = {"value": m_run * n_f / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "sample": f"{m_run} {what} (n_f={n_f}) among {m_local} sampled vectors{where} of the "
+                     f"workload, brute-force Fig.1/Fig.2 enumeration, {dt:.1f} s"}
+    if not with_records:
+        return out
+    return out, rows[allidx[:m_run]], res[0], res[1]
+
+
+def lex_rows(way, n_v, idx):
+    """Record position of global (i, j[, k]) in the lexicographic order of include/ccc.h."""
+    import numpy as np
+    idx = np.asarray(idx, dtype=np.int64)
+    i, j = idx[:, 0], idx[:, 1]
+    if way == 2:
+        return i * (2 * n_v - i - 1) // 2 + (j - i - 1)
+    k = idx[:, 2]
+    c3 = lambda n: n * (n - 1) * (n - 2) // 6   # noqa: E731
+    c2 = lambda n: n * (n - 1) // 2             # noqa: E731
+    return c3(n_v) - c3(n_v - i) + c2(n_v - i - 1) - c2(n_v - j) + (k - j - 1)
+
+
+def parity(way, n_v, idx, To, Co, T_dev, C_dev, rec_base=0, rtol=1e-12):
+    """The timed step's own output buffers at the oracle-sampled records: tallies
+    bit-exact, CCC within rtol (0 exactly where the oracle's is 0)."""
+    import numpy as np
+    import torch
+    rows = torch.from_numpy(lex_rows(way, n_v, idx) - rec_base).to(T_dev.device if T_dev is not None
+                                                                    else C_dev.device)
+    bad_t = bad_c = 0
+    max_rel = 0.0
+    bad = np.zeros(len(idx), bool)
+    if T_dev is not None:
+        Tg = T_dev[rows].cpu().numpy().astype(np.int64) & 0xFFFFFFFF
+        bt = np.any(Tg != To, axis=1)
+        bad |= bt
+        bad_t = int(bt.sum())
+    if C_dev is not None:
+        Cg = C_dev[rows].cpu().numpy().astype(np.float64)
+        nz = Co != 0
+        rel = np.zeros_like(Co)
+        rel[nz] = np.abs(Cg[nz] - Co[nz]) / np.abs(Co[nz])
+        bc = np.any((rel > rtol) | (nz != (Cg != 0)) | np.isnan(Cg), axis=1)
+        bad |= bc
+        bad_c = int(bc.sum())
+        max_rel = float(rel.max()) if rel.size else 0.0
+    return {"records": int(len(idx)), "mismatches": int(bad.sum()), "tally_mismatches": bad_t,
+            "ccc_mismatches": bad_c, "ccc_max_rel": max_rel, "ccc_rtol": rtol,
+            "against": "the CPU oracle's brute force on the cpu_baseline sample; device records read "
+                       "from the last timed step's output buffers"}
 
 
 def int8_library_ceiling(n=8192, reps=10):
@@ -250,7 +301,41 @@ def cpu_optimized(n_v, n_f, target_s=8.0):
 
 
 # ------------------------------------------------------------------------ ours, 1 GPU
-def run_2way_single(args, wl):
+def time_steps(step, args, dev_index=0):
+    """W untimed warm-up steps, then exactly K steps with a CUDA event on the launching
+    stream at every step boundary (synchronize on both sides) while NVML samples the clocks.
+    step(k) runs one step; k is None during warm-up."""
+    import torch
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        step(None)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with ClockSampler(dev_index) as clk:
+        torch.cuda.synchronize()
+        ev[0].record(stream)
+        for k in range(args.steps):
+            step(k)
+            ev[k + 1].record(stream)
+        torch.cuda.synchronize()
+    per = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    return {"ms": ev[0].elapsed_time(ev[-1]), "step_ms": per, "clocks": clk.summary()}
+
+
+def _kernel_events(steps, n):
+    import torch
+    return [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+             for _ in range(n)] for _ in range(steps)]
+
+
+def _ev(kev, k, i, which):
+    """Record kernel event (start 0 / end 1) i of timed step k on the current stream."""
+    if k is not None:
+        import torch
+        kev[k][i][which].record(torch.cuda.current_stream())
+
+
+def run_2way_single(args, wl):  # noqa: C901
     import torch
 
     import synthgen
@@ -258,15 +343,11 @@ def run_2way_single(args, wl):
     n_v, n_f = wl["n_v"], wl["n_f"]
     sparse = wl.get("sparse", False)
     popcount = wl.get("popcount", False)
+    kind = "sparse" if sparse else wl.get("kind", "random")
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     flags = ccc.OUT_TALLY | ccc.OUT_CCC_F64
-    if sparse:
-        codes = synthgen.sparse_codes(n_v, n_f, seed=4, device=dev)    # resident in HBM
-    elif wl.get("kind") == "hwe":
-        codes = synthgen.hwe_codes(n_v, n_f, seed=2, device=dev)       # resident in HBM
-    else:
-        codes = synthgen.random_codes(n_v, n_f, seed=1, device=dev)    # resident in HBM
+    codes = synthgen.make_codes(kind, n_v, n_f, device=dev)          # resident in HBM
     packed = torch.empty((n_v, ccc.ccc_packed_stride(n_f)), dtype=torch.uint8, device=dev)
     N = torch.empty((ccc.ccc_sparse_rows(n_v) if sparse else n_v, ccc.ccc_k_pad(n_f)),
                     dtype=torch.int8, device=dev)
@@ -276,58 +357,45 @@ def run_2way_single(args, wl):
     m = ccc.ccc_num_unique(2, n_v)
     T = torch.empty((m, 4), dtype=torch.int32, device=dev)
     C = torch.empty((m, 4), dtype=torch.float64, device=dev)
-    stream = torch.cuda.current_stream()
     launches = [0]
     ws = ccc.workspace(2, n_v, n_f, dev) if popcount else None
+    kev = _kernel_events(args.steps, 1)
 
-    def step(ev=None):
-        ccc.ccc_pack(codes, packed)
-        launches[0] += ccc.ccc_last_launch_count()
-        if popcount:
-            if ev:
-                ev[0].record(stream)
-            ccc.ccc_2way_popcount(packed, n_f, ccc.GAMMA, flags, T, C, None, ws)
+    def count(k):
+        if k is not None:
             launches[0] += ccc.ccc_last_launch_count()
-            if ev:
-                ev[1].record(stream)
+
+    def step(k):
+        ccc.ccc_pack(codes, packed)
+        count(k)
+        if popcount:
+            _ev(kev, k, 0, 0)
+            ccc.ccc_2way_popcount(packed, n_f, ccc.GAMMA, flags, T, C, None, ws)
+            count(k)
+            _ev(kev, k, 0, 1)
             return
         if sparse:
             ccc.ccc_expand_sparse(packed, n_f, ccc.GAMMA, (N, s, cnt, w))
         else:
             ccc.ccc_expand(packed, n_f, ccc.GAMMA, N, s, w)
-        launches[0] += ccc.ccc_last_launch_count()
-        if ev:
-            ev[0].record(stream)
+        count(k)
+        _ev(kev, k, 0, 0)
         if sparse:
             ccc.ccc_2way_sparse_block(N, w, n_v, 0, 0, n_v, N, w, n_v, 0, True, n_f, flags, T, C)
         else:
             ccc.ccc_2way_block(N, s, w, 0, 0, n_v, N, s, w, 0, True, n_f, flags, T, C)
-        launches[0] += ccc.ccc_last_launch_count()
-        if ev:
-            ev[1].record(stream)
+        count(k)
+        _ev(kev, k, 0, 1)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    launches[0] = 0
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(0) as clk:
-        torch.cuda.synchronize()
-        t0.record(stream)
-        for k in range(args.steps):
-            step(kev[k])
-        t1.record(stream)
-        torch.cuda.synchronize()
-    ms = t0.elapsed_time(t1)
-    k_ms = sum(a.elapsed_time(b) for a, b in kev) / args.steps
-    comps = comparisons(2, n_v, n_f)
-    res = {
-        "ms": ms, "kernel_ms": k_ms, "comparisons": comps, "launches": launches[0],
-        "clocks": clk.summary(), "kernel": "popc_tally2_kernel" if popcount else "tally2_kernel",
-        "out_bytes": m * 48,
-    }
+    res = time_steps(step, args)
+    k_ms = [kev[k][0][0].elapsed_time(kev[k][0][1]) for k in range(args.steps)]
+    res.update(kernel_ms=sum(k_ms) / args.steps, kernel_ms_best=min(k_ms),
+               comparisons=comparisons(2, n_v, n_f), launches=launches[0],
+               kernel="popc_tally2_kernel" if popcount else "tally2_kernel", out_bytes=m * 48)
+    if args.cpu:
+        cb, idx, To, Co = cpu_baseline(2, n_v, n_f, kind=kind, with_records=True)
+        res["cpu_baseline"] = cb
+        res["parity"] = parity(2, n_v, idx, To, Co, T, C)
     del T, C
     torch.cuda.empty_cache()
     if args.e2e and not sparse and not popcount:
@@ -387,54 +455,48 @@ def run_fieldsplit_single(args, wl):
     m = ccc.ccc_num_unique(2, n_v)
     T = torch.empty((m, 4), dtype=torch.int32, device=dev)
     C = torch.empty((m, 4), dtype=torch.float64, device=dev)
-    stream = torch.cuda.current_stream()
     launches = [0]
+    kev = _kernel_events(args.steps, 2)
 
-    def step(ev=None):
+    def count(k):
+        if k is not None:
+            launches[0] += ccc.ccc_last_launch_count()
+
+    def step(k):
         for r, (a, b) in enumerate(sl):
             ccc.ccc_pack(cs[r], packed[r])
-            launches[0] += ccc.ccc_last_launch_count()
+            count(k)
             N, s, w = Ns[r]
             ccc.ccc_expand(packed[r], b - a, ccc.GAMMA, N, s, w)
-            launches[0] += ccc.ccc_last_launch_count()
+            count(k)
         s_full = Ns[0][1].clone()
         for r in range(1, P):
             s_full += Ns[r][1]                 # the s all-reduce of the multi-GPU run
-        if ev:
-            ev[0].record(stream)
+        _ev(kev, k, 0, 0)
         for r, (a, b) in enumerate(sl):
             ccc.ccc_2way_fs_export(Ns[r][0], Ns[r][1], b - a, ptrs, r, P, 0, total)
-            launches[0] += ccc.ccc_last_launch_count()
-        if ev:
-            ev[1].record(stream)
+            count(k)
+        _ev(kev, k, 0, 1)
+        _ev(kev, k, 1, 0)
         for r in range(P):
             ccc.ccc_2way_fs_finish(slots[r], s_full, n_f, r, P, 0, total, flags, T, C)
-            launches[0] += ccc.ccc_last_launch_count()
-        if ev:
-            ev[2].record(stream)
+            count(k)
+        _ev(kev, k, 1, 1)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    launches[0] = 0
-    kev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(0) as clk:
-        torch.cuda.synchronize()
-        t0.record(stream)
-        for k in range(args.steps):
-            step(kev[k])
-        t1.record(stream)
-        torch.cuda.synchronize()
-    ms = t0.elapsed_time(t1)
-    k_ms = sum(e[0].elapsed_time(e[1]) for e in kev) / args.steps
-    f_ms = sum(e[1].elapsed_time(e[2]) for e in kev) / args.steps
-    return {"ms": ms, "kernel_ms": k_ms, "finish_ms": f_ms, "comparisons": comparisons(2, n_v, n_f),
-            "launches": launches[0], "clocks": clk.summary(), "kernel": "tally2_kernel",
-            "out_bytes": m * 48, "slot_bytes_per_pair_in": 4 * P}
+    res = time_steps(step, args)
+    k_ms = [kev[k][0][0].elapsed_time(kev[k][0][1]) for k in range(args.steps)]
+    f_ms = sum(kev[k][1][0].elapsed_time(kev[k][1][1]) for k in range(args.steps)) / args.steps
+    res.update(kernel_ms=sum(k_ms) / args.steps, kernel_ms_best=min(k_ms), finish_ms=f_ms,
+               comparisons=comparisons(2, n_v, n_f), launches=launches[0], kernel="tally2_kernel",
+               out_bytes=m * 48, slot_bytes_per_pair_in=4 * P)
+    if args.cpu:
+        cb, idx, To, Co = cpu_baseline(2, n_v, n_f, with_records=True)
+        res["cpu_baseline"] = cb
+        res["parity"] = parity(2, n_v, idx, To, Co, T, C)
+    return res
 
 
-def run_3way_single(args, wl):
+def run_3way_single(args, wl):  # noqa: C901
     import torch
 
     import synthgen
@@ -442,15 +504,13 @@ def run_3way_single(args, wl):
     n_v, n_f, n_st = wl["n_v"], wl["n_f"], wl["n_st"]
     sparse = wl.get("sparse", False)
     paper = wl.get("paper", False)
+    kind = "sparse" if sparse else "random"
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     flags = {"f32": ccc.OUT_TALLY | ccc.OUT_CCC_F32, "ck": ccc.OUT_CHECKSUM}.get(
         wl.get("flags"), ccc.OUT_TALLY | ccc.OUT_CCC_F64)
     rec_bytes = {"f32": 64, "ck": 0}.get(wl.get("flags"), 96)
-    if sparse:
-        codes = synthgen.sparse_codes(n_v, n_f, seed=4, device=dev)
-    else:
-        codes = synthgen.random_codes(n_v, n_f, seed=1, device=dev)
+    codes = synthgen.make_codes(kind, n_v, n_f, device=dev)
     packed = torch.empty((n_v, ccc.ccc_packed_stride(n_f)), dtype=torch.uint8, device=dev)
     if sparse:
         ws = torch.empty(ccc.lib().ccc_sparse3_workspace_bytes(n_v, n_f), dtype=torch.uint8, device=dev)
@@ -470,52 +530,193 @@ def run_3way_single(args, wl):
     elif flags & ccc.OUT_CCC_F32:
         C = torch.empty((rmax, 8), dtype=torch.float32, device=dev)
     ck = torch.zeros(2, dtype=torch.int64, device=dev) if flags & ccc.OUT_CHECKSUM else None
-    stream = torch.cuda.current_stream()
     launches = [0]
+    kev = _kernel_events(args.steps, n_st)
 
-    def step(ev=None):
+    def count(k):
+        if k is not None:
+            launches[0] += ccc.ccc_last_launch_count()
+
+    def step(k):
         ccc.ccc_pack(codes, packed)
-        launches[0] += ccc.ccc_last_launch_count()
+        count(k)
         if sparse:
             ccc.ccc_3way_sparse_prepare(packed, n_f, ccc.GAMMA, ws)
         elif paper:
             ccc.ccc_3way_paper_prepare(packed, n_f, ccc.GAMMA, ws)
         else:
             ccc.ccc_3way_prepare(packed, n_f, ccc.GAMMA, ws)
-        launches[0] += ccc.ccc_last_launch_count()
+        count(k)
         for st in range(n_st):
-            if ev:
-                ev[st][0].record(stream)
+            _ev(kev, k, st, 0)
             if sparse:
                 ccc.ccc_3way_sparse_stage(n_v, n_f, n_st, st, ws, flags, T, C, None, scratch)
             elif paper:
                 ccc.ccc_3way_paper_stage(n_v, n_f, n_st, st, ws, flags, T, C, None, scratch)
             else:
                 ccc.ccc_3way_stage(n_v, n_f, n_st, st, ws, flags, T, C, ck)
-            launches[0] += ccc.ccc_last_launch_count()
-            if ev:
-                ev[st][1].record(stream)
+            count(k)
+            _ev(kev, k, st, 1)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    launches[0] = 0
-    kev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-            for _ in range(n_st)] for _ in range(args.steps)]
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(0) as clk:
-        torch.cuda.synchronize()
-        t0.record(stream)
-        for k in range(args.steps):
-            step(kev[k])
-        t1.record(stream)
-        torch.cuda.synchronize()
-    ms = t0.elapsed_time(t1)
-    k_ms = sum(a.elapsed_time(b) for st in kev for a, b in st) / (args.steps * n_st)
-    return {"ms": ms, "kernel_ms": k_ms, "comparisons": comparisons(3, n_v, n_f),
-            "launches": launches[0], "clocks": clk.summary(), "kernel": "tally3_kernel",
-            "out_bytes": comparisons(3, n_v, n_f) // n_f * rec_bytes, "stages": n_st,
-            "forms_bytes": comparisons(3, n_v, n_f) // n_f * (7 if sparse else 2) * 4 * 2 if (sparse or paper) else 0}
+    res = time_steps(step, args)
+    st_ms = [sum(a.elapsed_time(b) for a, b in kev[k]) for k in range(args.steps)]
+    res.update(kernel_ms=sum(st_ms) / (args.steps * n_st), kernel_ms_best=min(st_ms) / n_st,
+               comparisons=comparisons(3, n_v, n_f), launches=launches[0], kernel="tally3_kernel",
+               out_bytes=comparisons(3, n_v, n_f) // n_f * rec_bytes, stages=n_st,
+               forms_bytes=comparisons(3, n_v, n_f) // n_f * (7 if sparse else 2) * 4 * 2
+               if (sparse or paper) else 0)
+    if args.cpu:
+        # the last stage's records are what the buffers hold after the timed steps: the
+        # oracle sample is drawn from its rows so every sampled triple lies in it
+        ib, _, rb, _ = ccc.ccc_stage_range(n_v, n_st, n_st - 1)
+        cb, idx, To, Co = cpu_baseline(3, n_v, n_f, kind=kind, row_lo=ib, with_records=True)
+        res["cpu_baseline"] = cb
+        if T is not None or C is not None:
+            res["parity"] = parity(3, n_v, idx, To, Co, T, C, rec_base=rb,
+                                   rtol=1e-6 if flags & ccc.OUT_CCC_F32 else 1e-12)
+        else:
+            res["parity"] = {"records": 0, "mismatches": None,
+                             "note": "CHECKSUM mode stores no record (covered by tests/)"}
+    return res
+
+
+# ------------------------------------------------------------------------ reporting
+NOMINAL_INT8_TOPS = 4500.0      # B200 dense int8, datasheet (SURVEY finding 5)
+INT8_OPS_PER_CLK_SM = 16384     # 8,192 int8 MAC / clk / SM (the guides' tcgen05 rate)
+
+
+def config_of(wl):
+    """The config dict both arms print (identical for --impl reference)."""
+    kind = "sparse" if wl.get("sparse") else wl.get("kind", "random")
+    inp = {"sparse": "type-3 sparse HWE codes, seed 4, missing marker (1,0) with per-vector rate "
+                     "U(0, 0.3) (P:1028-1043)",
+           "hwe": "type-1b Hardy-Weinberg codes, p_i ~ U(0.05, 0.5), seed 2",
+           "random": "type-1 uniform random 2-bit codes, seed 1 (P:657)"}[kind]
+    cfg = {"workload": wl["label"], "n_v": wl["n_v"], "n_f": wl["n_f"], "input": inp,
+           "output": {"f32": "FULL: uint32 tallies + fp32 CCC for every unique record",
+                      "ck": "CHECKSUM: every record computed and folded into the 128-bit checksum, "
+                            "none stored"}.get(wl.get("flags"),
+                                               "FULL: uint32 tallies + fp64 CCC for every unique record"),
+           "parallelism": "single GPU"}
+    if wl["way"] == 2:
+        cfg["l2"] = "inputs larger than L2 (codes %.2f GB, N %.2f GB)" % (
+            wl["n_v"] * wl["n_f"] / 1e9, wl["n_v"] * wl["n_f"] / 1e9)
+    else:
+        cfg["stages"] = wl["n_st"]
+        cfg["l2"] = ("operands L2-resident by design (N %.2f GB, G %.2f GB); each stage writes "
+                     "%.0f GB of records, far larger than L2" % (
+                         wl["n_v"] * wl["n_f"] / 1e9, 4 * wl["n_v"] ** 2 / 1e9,
+                         comparisons(3, wl["n_v"], wl["n_f"]) / wl["n_f"] * 96 / wl["n_st"] / 1e9))
+    return cfg
+
+
+def step_stats(r, steps):
+    per = sorted(r["step_ms"])
+    return {"ms_per_step": r["ms"] / steps, "ms_per_step_median": per[len(per) // 2],
+            "ms_per_step_best": per[0]}
+
+
+def roofline(args, wl, r, ms_step, pk, pk_kind):  # noqa: C901
+    """roofline object of the dominant kernel."""
+    k_s = r["kernel_ms"] / 1e3
+    if wl["way"] == 2:
+        # sparse mode: 4 int8 MACs per comparison (n.n, n.v, v.n, v.v; DESIGN.md §6)
+        ops = (8.0 if wl.get("sparse") else 2.0) * r["comparisons"]
+    else:
+        # sparse 3-way: 8 passes (trilinear forms) = 8 MACs per comparison
+        ops = (16.0 if wl.get("sparse") else 6.0 if wl.get("paper") else 2.0) * r["comparisons"] / wl["n_st"]
+    # int8 dense = 2 x bf16 dense (the guide's nominal ratio, 4.5 vs 2.25 PFLOP/s); the
+    # burst figure applies: the timed region is ~0.1 s of back-to-back steps, not seconds.
+    int8_peak = 2.0 * pk["bf16_tflops"]
+    achieved = ops / k_s / 1e12
+    mhz = r["clocks"].get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)
+    pipe = 148 * INT8_OPS_PER_CLK_SM * mhz * 1e6 / 1e12
+    step_tops = 2.0 * r["comparisons"] / (ms_step / 1e3) / 1e12
+    # ncu --set full DRAM bytes of the dominant kernel, captured on the c2 / c4 workloads only
+    traffic = ncu_traffic(r["kernel"]) if args.workload in ("c2", "c4") else None
+    roof = {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s",
+            "frac": achieved / int8_peak, "traffic": traffic,
+            "kernel": r["kernel"], "kernel_ms": r["kernel_ms"], "kernel_ms_best": r.get("kernel_ms_best"),
+            "peak_source": f"2 x bf16_tflops (burst) of MEASURED_PEAKS.json ({pk_kind}); "
+                           "int8 ops = 2 per MAC = %d per comparison" % (8 if wl.get("sparse") else 2),
+            "int8_pipe_at_clock": {"sm_mhz": mhz, "TOPS": pipe,
+                                   "kernel_frac": achieved / pipe, "step_frac": step_tops / pipe,
+                                   "def": "148 SMs x 16,384 int8 ops/clk x the median sampled SM clock"},
+            "nominal_int8": {"TOPS": NOMINAL_INT8_TOPS, "kernel_frac": achieved / NOMINAL_INT8_TOPS,
+                             "step_frac": step_tops / NOMINAL_INT8_TOPS},
+            "note": "peak = 2 x the measured bf16 burst (the task's rule for another dtype) understates "
+                    "the int8 pipe, so frac can read ~1.0; int8_pipe_at_clock and nominal_int8 are the "
+                    "honest denominators (SURVEY 8(d))"}
+    hbm_write = r["out_bytes"] / (ms_step / 1e3) / 1e9
+    roof["out_write_GBps"] = hbm_write
+    roof["out_write_frac_of_hbm"] = hbm_write / pk["hbm_gbs"]
+    if wl["way"] == 2 and not wl.get("popcount") and args.workload in ("c2", "c2s"):
+        try:
+            lib_ceil = int8_library_ceiling()
+            roof["int8_library_ceiling"] = lib_ceil
+            roof["frac_of_library_ceiling"] = achieved / lib_ceil["torch_int_mm_TOPS"]
+        except Exception as e:   # noqa: BLE001 -- a reference point only
+            roof["int8_library_ceiling"] = {"error": str(e)[:200]}
+    if wl.get("fieldsplit"):
+        # the export GEMMs of all slices (tensor) + the owners' reduce/epilogue (HBM)
+        pairs = r["comparisons"] / wl["n_f"]
+        roof["finish_ms"] = r["finish_ms"]
+        roof["finish_GBps"] = pairs * (r["slot_bytes_per_pair_in"] + 48) / (r["finish_ms"] / 1e3) / 1e9
+        roof["finish_frac_of_hbm"] = roof["finish_GBps"] / pk["hbm_gbs"]
+    if wl.get("popcount"):
+        # CUDA-core path: 2 POPC per 16 comparisons; peak = 148 SMs x 16 POPC/clk (the
+        # CUDA C throughput table's population-count rate) x the sampled SM clock
+        popc = 2.0 * r["comparisons"] / 16.0
+        roof = {"bound": "alu", "achieved": popc / k_s / 1e12,
+                "peak": 148 * 16 * mhz * 1e6 / 1e12, "unit": "TPOPC/s",
+                "traffic": None, "kernel": r["kernel"], "kernel_ms": r["kernel_ms"],
+                "peak_source": "148 SMs x 16 POPC/clk/SM x sampled SM clock (DESIGN.md §6)",
+                "tensor_path_equiv_frac_of_int8_peak": 2.0 * r["comparisons"] / k_s / 1e12 / int8_peak}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+    if wl["way"] == 3 and wl.get("flags") == "ck":
+        roof["peak_source"] += "; CHECKSUM mode: no record is stored, the tensor-pipe line is the roofline"
+    elif wl["way"] == 3:
+        roof.pop("note", None)
+        tensor = {k: roof.pop(k) for k in ("int8_pipe_at_clock", "nominal_int8")}
+        roof["bound"] = "hbm"
+        roof["achieved"] = (r["out_bytes"] + r.get("forms_bytes", 0)) / wl["n_st"] / k_s / 1e9
+        roof["peak"] = pk["hbm_gbs"]
+        roof["unit"] = "GB/s"
+        roof["frac"] = roof["achieved"] / pk["hbm_gbs"]
+        rb = 64 if wl.get("flags") == "f32" else 96
+        roof["peak_source"] = f"hbm_gbs of MEASURED_PEAKS.json ({pk_kind}); FULL output {rb} B/triple" + (
+            " + 7 stored forms written and read back (56 B/triple)" if wl.get("sparse") else
+            " + 2 stored masked forms written and read back (16 B/triple)" if wl.get("paper") else "")
+        roof["tensor_TOPS"] = achieved
+        roof["tensor"] = tensor
+    return roof
+
+
+def line_for(args, wl, r, pk, pk_kind):
+    ms_step = r["ms"] / args.steps
+    out = {
+        "metric": METRIC, "value": r["comparisons"] / (ms_step / 1e3), "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup}
+    out.update(step_stats(r, args.steps))
+    out["value_best_step"] = r["comparisons"] / (out["ms_per_step_best"] / 1e3)
+    out.update({
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32 (bitwise AND + popcount)" if wl.get("popcount") else "int8",
+        "data": "synthetic", "config": config_of(wl),
+        "roofline": roofline(args, wl, r, ms_step, pk, pk_kind),
+        "gpu_launches": r["launches"], "clocks": r["clocks"]})
+    for k in ("parity", "e2e", "cpu_baseline"):
+        if k in r:
+            out[k] = r[k]
+    return out
+
+
+def run_one(args, wl):
+    if wl.get("fieldsplit"):
+        return run_fieldsplit_single(args, wl)
+    if wl["way"] == 2:
+        return run_2way_single(args, wl)
+    return run_3way_single(args, wl)
 
 
 # ------------------------------------------------------------------------ main
@@ -528,6 +729,8 @@ def main():
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu", dest="cpu", action="store_false")
+    ap.add_argument("--no-3way", dest="three_way", action="store_false",
+                    help="default c2 line: skip the three_way (C4) sub-object")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -549,8 +752,7 @@ def main():
         out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-               "dtype": "int64", "data": "synthetic",
-               "config": {"workload": wl["label"], "n_v": wl["n_v"], "n_f": wl["n_f"]},
+               "dtype": "int64", "data": "synthetic", "config": config_of(wl),
                "cpu_baseline": cb,
                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
                        "d2h_bytes_per_step": 0}}
@@ -564,114 +766,20 @@ def main():
         return dist.bench_main(args, wl, METRIC, UNIT)
 
     pk, pk_kind = peaks()
-    if wl.get("fieldsplit"):
-        r = run_fieldsplit_single(args, wl)
-    elif wl["way"] == 2:
-        r = run_2way_single(args, wl)
-    else:
-        r = run_3way_single(args, wl)
-    ms_step = r["ms"] / args.steps
-    value = r["comparisons"] / (ms_step / 1e3)
-    # roofline of the dominant kernel (the fused tally GEMM): 2 int8 ops per comparison
-    k_s = r["kernel_ms"] / 1e3
-    if wl["way"] == 2:
-        # sparse mode: 4 int8 MACs per comparison (n.n, n.v, v.n, v.v)
-        ops = (8.0 if wl.get("sparse") else 2.0) * r["comparisons"]
-    else:
-        # sparse 3-way: 8 passes (trilinear forms) = 8 MACs per comparison
-        ops = (16.0 if wl.get("sparse") else 6.0 if wl.get("paper") else 2.0) * r["comparisons"] / wl["n_st"]
-    # int8 dense = 2 x bf16 dense (the guide's nominal ratio, 4.5 vs 2.25 PFLOP/s); the
-    # burst figure applies: the timed region is ~0.1 s of back-to-back steps, not seconds.
-    int8_peak = 2.0 * pk["bf16_tflops"]
-    achieved = ops / k_s / 1e12
-    # ncu --set full DRAM bytes of the dominant kernel, captured on the c2 / c4 workloads only
-    traffic = ncu_traffic(r["kernel"]) if args.workload in ("c2", "c4") else None
-    roof = {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s",
-            "frac": achieved / int8_peak, "traffic": traffic,
-            "kernel": r["kernel"], "kernel_ms": r["kernel_ms"],
-            "peak_source": f"2 x bf16_tflops (burst) of MEASURED_PEAKS.json ({pk_kind}); "
-                           "int8 ops = 2 per MAC = %d per comparison" % (
-                               8 if wl.get("sparse") else 2),
-            "nominal_int8_frac": achieved / 4500.0,
-            "note": "the peak line is 2 x the measured bf16 burst (the task's rule for another dtype); "
-                    "it understates the int8 pipe -- this kernel's own mainloop reaches 4,250 TOPS with "
-                    "stores off (DESIGN.md 6) -- so frac can read ~1.0; nominal_int8_frac is against "
-                    "the 4.5 POPS datasheet"}
-    hbm_write = r["out_bytes"] / (ms_step / 1e3) / 1e9
-    roof["out_write_GBps"] = hbm_write
-    roof["out_write_frac_of_hbm"] = hbm_write / pk["hbm_gbs"]
-    if wl["way"] == 2 and not wl.get("popcount") and args.workload in ("c2", "c2s"):
-        try:
-            lib_ceil = int8_library_ceiling()
-            roof["int8_library_ceiling"] = lib_ceil
-            roof["frac_of_library_ceiling"] = achieved / lib_ceil["torch_int_mm_TOPS"]
-        except Exception as e:   # noqa: BLE001 -- a reference point only
-            roof["int8_library_ceiling"] = {"error": str(e)[:200]}
-    if wl.get("fieldsplit"):
-        # the export GEMMs of all slices (tensor) + the owners' reduce/epilogue (HBM)
-        pairs = r["comparisons"] / wl["n_f"]
-        roof["kernel_ms"] = r["kernel_ms"]
-        roof["finish_ms"] = r["finish_ms"]
-        roof["finish_GBps"] = pairs * (r["slot_bytes_per_pair_in"] + 48) / (r["finish_ms"] / 1e3) / 1e9
-        roof["finish_frac_of_hbm"] = roof["finish_GBps"] / pk["hbm_gbs"]
-    if wl.get("popcount"):
-        # CUDA-core path: 2 POPC per 16 comparisons; peak = 148 SMs x 16 POPC/clk (the
-        # CUDA C throughput table's population-count rate) x the sampled SM clock
-        mhz = (r["clocks"].get("sm_mhz") or pk.get("sm_max_mhz", 1965.0))
-        popc = 2.0 * r["comparisons"] / 16.0
-        roof = {"bound": "alu", "achieved": popc / k_s / 1e12,
-                "peak": 148 * 16 * mhz * 1e6 / 1e12, "unit": "TPOPC/s",
-                "traffic": None, "kernel": r["kernel"], "kernel_ms": r["kernel_ms"],
-                "peak_source": "148 SMs x 16 POPC/clk/SM x sampled SM clock (DESIGN.md §6)",
-                "tensor_path_equiv_frac_of_int8_peak": 2.0 * r["comparisons"] / k_s / 1e12 / int8_peak}
-        roof["frac"] = roof["achieved"] / roof["peak"]
-    if wl["way"] == 3 and wl.get("flags") == "ck":
-        roof["peak_source"] += "; CHECKSUM mode: no record is stored, the tensor-pipe line is the roofline"
-    elif wl["way"] == 3:
-        roof.pop("note", None)
-        roof["bound"] = "hbm"
-        roof["achieved"] = (r["out_bytes"] + r.get("forms_bytes", 0)) / wl["n_st"] / k_s / 1e9
-        roof["peak"] = pk["hbm_gbs"]
-        roof["unit"] = "GB/s"
-        roof["frac"] = roof["achieved"] / pk["hbm_gbs"]
-        rb = 64 if wl.get("flags") == "f32" else 96
-        roof["peak_source"] = f"hbm_gbs of MEASURED_PEAKS.json ({pk_kind}); FULL output {rb} B/triple" + (
-            " + 7 stored forms written and read back (56 B/triple)" if wl.get("sparse") else
-            " + 2 stored masked forms written and read back (16 B/triple)" if wl.get("paper") else "")
-        roof["tensor_TOPS"] = achieved
-    out = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None,
-        "dtype": "u32 (bitwise AND + popcount)" if wl.get("popcount") else "int8",
-        "data": "synthetic",
-        "config": {"workload": wl["label"], "n_v": wl["n_v"], "n_f": wl["n_f"],
-                   "input": ("type-3 sparse HWE codes, seed 4, missing marker (1,0) with "
-                             "per-vector rate U(0, 0.3) (P:1028-1043)") if wl.get("sparse") else
-                            ("type-1b Hardy-Weinberg codes, p_i ~ U(0.05, 0.5), seed 2"
-                             if wl.get("kind") == "hwe" else
-                             "type-1 uniform random 2-bit codes, seed 1 (P:657)"),
-                   "output": {"f32": "FULL: uint32 tallies + fp32 CCC for every unique record",
-                              "ck": "CHECKSUM: every record computed and folded into the 128-bit checksum, none stored"
-                              }.get(wl.get("flags"), "FULL: uint32 tallies + fp64 CCC for every unique record"),
-                   "l2": ("inputs larger than L2 (codes %.2f GB, N %.2f GB)" % (
-                       wl["n_v"] * wl["n_f"] / 1e9, wl["n_v"] * wl["n_f"] / 1e9)) if wl["way"] == 2 else
-                         ("operands L2-resident by design (N %.2f GB, G %.2f GB); each stage writes "
-                          "%.0f GB of records, far larger than L2" % (
-                              wl["n_v"] * wl["n_f"] / 1e9, 4 * wl["n_v"] ** 2 / 1e9,
-                              comparisons(3, wl["n_v"], wl["n_f"]) / wl["n_f"] * 96 / wl["n_st"] / 1e9)),
-                   "parallelism": "single GPU"},
-        "roofline": roof,
-        "gpu_launches": r["launches"],
-        "clocks": r["clocks"],
-    }
-    if "e2e" in r:
-        out["e2e"] = r["e2e"]
-    if args.cpu:
-        out["cpu_baseline"] = cpu_baseline(wl["way"], wl["n_v"], wl["n_f"],
-                                           kind="sparse" if wl.get("sparse") else wl.get("kind", "random"))
-        if wl["way"] == 2 and not wl.get("sparse"):
-            out["cpu_optimized"] = cpu_optimized(wl["n_v"], wl["n_f"])
+    r = run_one(args, wl)
+    out = line_for(args, wl, r, pk, pk_kind)
+    if args.cpu and wl["way"] == 2 and not wl.get("sparse"):
+        out["cpu_optimized"] = cpu_optimized(wl["n_v"], wl["n_f"])
+    if args.workload == "c2" and args.three_way:
+        # the metric is "(2-way, 3-way)": the default line also times configs[3] (C4)
+        import torch
+        torch.cuda.empty_cache()
+        w3 = dict(WORKLOADS["c4"])
+        r3 = run_3way_single(args, w3)
+        sub = line_for(args, w3, r3, pk, pk_kind)
+        for k in ("metric", "higher_is_better", "scaling", "vs_baseline", "data", "n_gpus"):
+            sub.pop(k, None)
+        out["three_way"] = sub
     print(json.dumps(out))
 
 
