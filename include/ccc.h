@@ -285,7 +285,8 @@ int64_t ccc_3way_unit_records(const ccc_block* bp, int64_t p_lo, int64_t p_hi,
  * bm == bn implies n > m (blocks are identified by row0).  `order` (0..5) says which role
  * sits in each slot of the sorted triple (i<j<k): roles p=0, m=1, n=2, orders
  * 0:(p,m,n) 1:(p,n,m) 2:(m,p,n) 3:(m,n,p) 4:(n,p,m) 5:(n,m,p); records hold the canonical
- * (Eq.5-ordered) cells.  G_d: the pairwise G = N N^T by GLOBAL index, G[min*ldG + max]
+ * (Eq.5-ordered) cells.  When bp == bm the order must place p before m, when bm == bn m
+ * before n (both: order 0 only), else CCC_ERR_INVALID_ARGUMENT.  G_d: the pairwise G = N N^T by GLOBAL index, G[min*ldG + max]
  * (upper triangle, e.g. from ccc_2way_block with g_d).  Record layouts:
  *   bp==bm==bn : in-block lexicographic triple order, starting at the first pivot p_lo;
  *   bp==bm     : record = (in-block pair index of (p,m) - that of (p_lo,p_lo+1)) * |N| + n-n_lo;

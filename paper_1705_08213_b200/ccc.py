@@ -198,15 +198,72 @@ def _stream(stream):
     return ctypes.c_void_p(stream)
 
 
-def _dev(t, dtype, name):
+def _req(t, dtype, shape, name, cuda=True, optional=True):
+    """Validate a tensor crossing the ABI: device (CUDA or host), dtype, contiguity and the
+    exact shape the C call will address (None in `shape` = any extent).  The C side only
+    sees a raw pointer, so this is the one place a wrong buffer can be caught before a
+    kernel or a D2H copy runs past its end."""
     if t is None:
-        return
-    if not t.is_cuda:
+        if optional:
+            return
+        raise ValueError(f"{name} is required")
+    if not isinstance(t, torch.Tensor):
+        raise ValueError(f"{name} must be a torch tensor")
+    if cuda and not t.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor")
+    if not cuda and t.is_cuda:
+        raise ValueError(f"{name} must be a host (CPU) tensor")
     if t.dtype != dtype:
         raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
+    if shape is not None:
+        if t.dim() != len(shape) or any(e is not None and t.shape[d] != e for d, e in enumerate(shape)):
+            raise ValueError(f"{name} must have shape {tuple('*' if e is None else e for e in shape)}, "
+                             f"got {tuple(t.shape)}")
+
+
+def _dev(t, dtype, name, shape=None):
+    _req(t, dtype, shape, name, cuda=True)
+
+
+def _bytes(t, need, name, cuda=True):
+    """A uint8 scratch/workspace buffer of at least `need` bytes."""
+    _req(t, torch.uint8, None, name, cuda=cuda, optional=False)
+    if t.numel() < need:
+        raise ValueError(f"{name} holds {t.numel()} bytes, needs {need}")
+
+
+def _check_outs(n_rec, width, out_flags, tallies, ccc, checksum, cuda=True, require=True):
+    """Caller-supplied record buffers must be [>= n_rec][width] of the flag's dtype (a reused
+    larger buffer is fine: the records land in its first n_rec rows)."""
+    cdt = (torch.float32 if out_flags & OUT_CCC_F32 and not out_flags & OUT_CCC_F64
+           else torch.float64)
+    for t, dt, name in ((tallies, torch.int32, "tallies"), (ccc, cdt, "ccc")):
+        _req(t, dt, (None, width), name, cuda)
+        if t is not None and t.shape[0] < n_rec:
+            raise ValueError(f"{name} has {t.shape[0]} rows, the call writes {n_rec}")
+    _req(checksum, torch.int64, (2,), "checksum", cuda)
+    if not require:        # the caller allocates what is missing
+        return
+    for flag, t, name in ((OUT_TALLY, tallies, "tallies"), (OUT_CCC_F64 | OUT_CCC_F32, ccc, "ccc"),
+                          (OUT_CHECKSUM, checksum, "checksum")):
+        if out_flags & flag and t is None and n_rec:
+            raise ValueError(f"out_flags asks for {name} but no buffer was given")
+
+
+def _packed(packed, n_f, name="packed"):
+    _dev(packed, torch.uint8, name, (None, ccc_packed_stride(n_f)))
+    return packed.shape[0]
+
+
+def _expanded(N, s, w, n_f, name):
+    """(N int8 [rows][K_pad], s int32 [rows], w f64 [rows][2]) of one block."""
+    rows = N.shape[0] if isinstance(N, torch.Tensor) else 0
+    _dev(N, torch.int8, f"N_{name}", (rows, ccc_k_pad(n_f)))
+    _dev(s, torch.int32, f"s_{name}", (rows,))
+    _dev(w, torch.float64, f"w_{name}", (rows, 2))
+    return rows
 
 
 # ----------------------------------------------------------------------- host helpers
@@ -259,19 +316,18 @@ def workspace(num_way: int, n_v: int, n_f: int, device=None) -> torch.Tensor:
 
 # ----------------------------------------------------------------------- device path
 def ccc_pack(codes: torch.Tensor, packed: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-    _dev(codes, torch.uint8, "codes")
+    _dev(codes, torch.uint8, "codes", (None, None))
     n_v, n_f = codes.shape
     if packed is None:
         packed = torch.empty((n_v, ccc_packed_stride(n_f)), dtype=torch.uint8, device=codes.device)
-    _dev(packed, torch.uint8, "packed")
+    _dev(packed, torch.uint8, "packed", (n_v, ccc_packed_stride(n_f)))
     _check(lib().ccc_pack(_p(codes), n_v, n_f, _p(packed), _stream(stream)))
     return packed
 
 
 def ccc_expand(packed: torch.Tensor, n_f: int, gamma: float = GAMMA, N=None, s=None, w=None,
                stream=None):
-    _dev(packed, torch.uint8, "packed")
-    n_v = packed.shape[0]
+    n_v = _packed(packed, n_f)
     dev = packed.device
     if N is None:
         N = torch.empty((n_v, ccc_k_pad(n_f)), dtype=torch.int8, device=dev)
@@ -279,13 +335,16 @@ def ccc_expand(packed: torch.Tensor, n_f: int, gamma: float = GAMMA, N=None, s=N
         s = torch.empty(n_v, dtype=torch.int32, device=dev)
     if w is None:
         w = torch.empty((n_v, 2), dtype=torch.float64, device=dev)
-    _dev(N, torch.int8, "N"), _dev(s, torch.int32, "s"), _dev(w, torch.float64, "w")
+    _dev(N, torch.int8, "N", (n_v, ccc_k_pad(n_f)))
+    _dev(s, torch.int32, "s", (n_v,))
+    _dev(w, torch.float64, "w", (n_v, 2))
     _check(lib().ccc_expand(_p(packed), n_v, n_f, gamma, _p(N), _p(s), _p(w), _stream(stream)))
     return N, s, w
 
 
 def _outputs(n_rec: int, width: int, out_flags: int, device, tallies=None, ccc=None,
              checksum=None):
+    _check_outs(n_rec, width, out_flags, tallies, ccc, checksum, require=False)
     if out_flags & OUT_TALLY and tallies is None:
         tallies = torch.empty((n_rec, width), dtype=torch.int32, device=device)
     if out_flags & OUT_CCC_F64 and ccc is None:
@@ -310,12 +369,12 @@ def ccc_2way(packed: torch.Tensor, n_f: int, gamma: float = GAMMA,
              ws=None, stream=None, compact: Compact | None = None):
     """Tallies (uint32 bit patterns in an int32 tensor) [C(n_v,2)][4], CCC, checksum[2]
     (with `compact`: the compacted buffers of that object instead)."""
-    _dev(packed, torch.uint8, "packed")
-    n_v = packed.shape[0]
+    n_v = _packed(packed, n_f)
     cp, tallies, ccc, checksum = _outs(ccc_num_unique(2, n_v), 4, out_flags, packed.device,
                                        tallies, ccc, checksum, compact)
     if ws is None:
         ws = workspace(2, n_v, n_f, packed.device)
+    _bytes(ws, ccc_workspace_bytes(2, n_v, n_f), "ws")
     _check(lib().ccc_2way(_p(packed), n_v, n_f, gamma, out_flags, _p(tallies), _p(ccc),
                           _p(checksum), _p(ws), ws.numel(), cp, _stream(stream)))
     return tallies, ccc, checksum
@@ -326,11 +385,12 @@ def ccc_2way_popcount(packed: torch.Tensor, n_f: int, gamma: float = GAMMA,
                       ws=None, stream=None):
     """The paper's popcount tally (mGEMM2 idea) on CUDA cores: a comparison
     baseline with the outputs of ccc_2way."""
-    n_v = packed.shape[0]
+    n_v = _packed(packed, n_f)
     dev = packed.device
     T, C, ck = _outputs(ccc_num_unique(2, n_v), 4, out_flags, dev, tallies, ccc, checksum)
     if ws is None:
         ws = workspace(2, n_v, n_f, dev)
+    _bytes(ws, ccc_workspace_bytes(2, n_v, n_f), "ws")
     _check(lib().ccc_2way_popcount(_p(packed), n_v, n_f, gamma, out_flags, _p(T), _p(C),
                                    _p(ck), _p(ws), ws.numel(), _stream(stream)))
     return T, C, ck
@@ -349,7 +409,12 @@ def ccc_2way_fs_export(N, s, n_f_slice: int, slot_ptrs: torch.Tensor, rank: int,
                        t_lo: int, t_hi: int, stream=None):
     """GEMM of this field slice; partial tiles go to the owners' slots (slot_ptrs: int64
     device tensor of `world` device addresses)."""
-    _dev(N, torch.int8, "N")
+    n_v = N.shape[0] if isinstance(N, torch.Tensor) else 0
+    _dev(N, torch.int8, "N", (n_v, ccc_k_pad(n_f_slice)))
+    _dev(s, torch.int32, "s", (n_v,))
+    _dev(slot_ptrs, torch.int64, "slot_ptrs", (world,))
+    if not 0 <= rank < world:
+        raise ValueError("rank must be in [0, world)")
     _check(lib().ccc_2way_fs_export(_p(N), _p(s), N.shape[0], n_f_slice, _p(slot_ptrs), rank, world,
                                     t_lo, t_hi, _stream(stream)))
 
@@ -358,7 +423,11 @@ def ccc_2way_fs_finish(slots: torch.Tensor, s, n_f: int, rank: int, world: int, 
                        out_flags: int, tallies=None, ccc=None, checksum=None, gamma: float = GAMMA,
                        stream=None):
     """Reduce this owner's partial tiles and write their records (ccc_2way layout)."""
+    _dev(s, torch.int32, "s", (None,))
     n_v = s.shape[0]
+    _req(slots, torch.int32, None, "slots", optional=False)
+    if slots.numel() * 4 < ccc_2way_fs_slot_bytes(world, t_lo, t_hi):
+        raise ValueError("slots smaller than ccc_2way_fs_slot_bytes(world, t_lo, t_hi)")
     T, C, ck = _outputs(ccc_num_unique(2, n_v), 4, out_flags, s.device, tallies, ccc, checksum)
     _check(lib().ccc_2way_fs_finish(_p(slots), _p(s), n_v, n_f, gamma, rank, world, t_lo, t_hi,
                                     out_flags, _p(T), _p(C), _p(ck), _stream(stream)))
@@ -401,11 +470,17 @@ def ccc_2way_block(N_a, s_a, w_a, a_row0, a_lo, a_hi, N_b, s_b, w_b, b_row0, dia
     """gamma: the value the w arrays were expanded with (selects the kernel's arithmetic).
     Output buffers are the caller's (dense layout) or those of `compact`."""
     cp = None
+    n_a = _expanded(N_a, s_a, w_a, n_f, "a")
+    n_b = _expanded(N_b, s_b, w_b, n_f, "b")
+    if not 0 <= a_lo <= a_hi <= n_a:
+        raise ValueError("row range [a_lo, a_hi) must lie inside block a")
+    n_rec = (sum(n_a - 1 - i for i in range(a_lo, a_hi)) if diag else (a_hi - a_lo) * n_b)
     if compact is not None:
         cp, tallies, ccc = ctypes.byref(compact._c), compact.tallies, compact.ccc
-    n_a, n_b = N_a.shape[0], N_b.shape[0]
-    for t, n in ((N_a, "N_a"), (N_b, "N_b")):
-        _dev(t, torch.int8, n)
+        _req(checksum, torch.int64, (2,), "checksum")
+    else:
+        _check_outs(n_rec, 4, out_flags, tallies, ccc, checksum)
+    _req(g, torch.int32, None, "g")
     _check(lib().ccc_2way_block(_p(N_a), _p(s_a), _p(w_a), n_a, a_row0, a_lo, a_hi, _p(N_b),
                                 _p(s_b), _p(w_b), n_b, b_row0, int(bool(diag)), n_f, gamma, out_flags,
                                 _p(tallies), _p(ccc), _p(checksum), _p(g), ldg, cp,
@@ -414,10 +489,10 @@ def ccc_2way_block(N_a, s_a, w_a, a_row0, a_lo, a_hi, N_b, s_b, w_b, b_row0, dia
 
 
 def ccc_3way_prepare(packed, n_f, gamma=GAMMA, ws=None, stream=None):
-    _dev(packed, torch.uint8, "packed")
-    n_v = packed.shape[0]
+    n_v = _packed(packed, n_f)
     if ws is None:
         ws = workspace(3, n_v, n_f, packed.device)
+    _bytes(ws, ccc_workspace_bytes(3, n_v, n_f), "ws")
     _check(lib().ccc_3way_prepare(_p(packed), n_v, n_f, gamma, _p(ws), ws.numel(),
                                   _stream(stream)))
     return ws
@@ -428,6 +503,7 @@ def ccc_3way_stage(n_v, n_f, n_stages, stage, ws, out_flags=OUT_TALLY | OUT_CCC_
                    compact: Compact | None = None):
     """gamma: the value given to ccc_3way_prepare for this workspace."""
     _, _, _, rec_count = ccc_stage_range(n_v, n_stages, stage)
+    _bytes(ws, ccc_workspace_bytes(3, n_v, n_f), "ws")
     cp, tallies, ccc, checksum = _outs(rec_count, 8, out_flags, ws.device, tallies, ccc,
                                        checksum, compact)
     _check(lib().ccc_3way_stage(n_v, n_f, gamma, n_stages, stage, out_flags, _p(tallies), _p(ccc),
@@ -438,13 +514,13 @@ def ccc_3way_stage(n_v, n_f, n_stages, stage, ws, out_flags=OUT_TALLY | OUT_CCC_
 def ccc_3way(packed, n_f, gamma=GAMMA, out_flags=OUT_TALLY | OUT_CCC_F64, n_stages=1, stage=0,
              tallies=None, ccc=None, checksum=None, ws=None, stream=None,
              compact: Compact | None = None):
-    _dev(packed, torch.uint8, "packed")
-    n_v = packed.shape[0]
+    n_v = _packed(packed, n_f)
     _, _, _, rec_count = ccc_stage_range(n_v, n_stages, stage)
     cp, tallies, ccc, checksum = _outs(rec_count, 8, out_flags, packed.device, tallies, ccc,
                                        checksum, compact)
     if ws is None:
         ws = workspace(3, n_v, n_f, packed.device)
+    _bytes(ws, ccc_workspace_bytes(3, n_v, n_f), "ws")
     _check(lib().ccc_3way(_p(packed), n_v, n_f, gamma, out_flags, n_stages, stage, _p(tallies),
                           _p(ccc), _p(checksum), _p(ws), ws.numel(), cp, _stream(stream)))
     return tallies, ccc, checksum
@@ -456,7 +532,10 @@ ORDERS = {("p", "m", "n"): 0, ("p", "n", "m"): 1, ("m", "p", "n"): 2, ("m", "n",
 
 def block(N, s, w, row0: int) -> CccBlock:
     """ccc_block descriptor of an expanded block (keep the tensors alive)."""
-    _dev(N, torch.int8, "N"), _dev(s, torch.int32, "s"), _dev(w, torch.float64, "w")
+    rows = N.shape[0] if isinstance(N, torch.Tensor) else 0
+    _dev(N, torch.int8, "N", (rows, None))
+    _dev(s, torch.int32, "s", (rows,))
+    _dev(w, torch.float64, "w", (rows, 2))
     return CccBlock(N.data_ptr(), s.data_ptr(), w.data_ptr(), N.shape[0], row0)
 
 
@@ -475,6 +554,9 @@ def ccc_3way_unit(bp, p_lo, p_hi, bm, m_lo, m_hi, bn, n_lo, n_hi, order, G, n_f,
     n_rec = ccc_3way_unit_records(bp, p_lo, p_hi, bm, m_lo, m_hi, bn, n_lo, n_hi)
     if n_rec < 0:
         raise ValueError("invalid unit ranges")
+    _dev(G, torch.int32, "G", (None, None))
+    if G.shape[0] != G.shape[1]:
+        raise ValueError("G must be the square [n_v][n_v] pairwise G")
     cp, tallies, ccc, checksum = _outs(n_rec, 8, out_flags, G.device, tallies, ccc, checksum,
                                        compact)
     _check(lib().ccc_3way_unit(ctypes.byref(bp), p_lo, p_hi, ctypes.byref(bm), m_lo, m_hi,
@@ -504,6 +586,8 @@ def ccc_2way_host(codes_h: torch.Tensor, gamma: float = GAMMA,
     if dev_ws is None:
         dev_ws = torch.empty(ccc_e2e_workspace_bytes(n_v, n_f, out_flags), dtype=torch.uint8,
                              device="cuda")
+    _check_outs(m, 4, out_flags, tallies_h, ccc_h, checksum_h, cuda=False)
+    _bytes(dev_ws, ccc_e2e_workspace_bytes(n_v, n_f, out_flags), "dev_ws")
     _check(lib().ccc_2way_host(_p(codes_h), n_v, n_f, gamma, out_flags, _p(tallies_h), _p(ccc_h),
                                _p(checksum_h), _p(dev_ws), dev_ws.numel(), _stream(stream)))
     return tallies_h, ccc_h, checksum_h
@@ -525,8 +609,7 @@ def ccc_expand_sparse(packed: torch.Tensor, n_f: int, gamma: float = GAMMA, out=
                       stream=None):
     """packed -> (X int8 [ccc_sparse_rows(n_v)][K_pad], s, c int32 [n_v], w f64 [n_v][2])
     (written into `out` = (X, s, c, w) if given)."""
-    _dev(packed, torch.uint8, "packed")
-    n_v = packed.shape[0]
+    n_v = _packed(packed, n_f)
     dev = packed.device
     if out is None:
         X = torch.empty((ccc_sparse_rows(n_v), ccc_k_pad(n_f)), dtype=torch.int8, device=dev)
@@ -535,8 +618,10 @@ def ccc_expand_sparse(packed: torch.Tensor, n_f: int, gamma: float = GAMMA, out=
         w = torch.empty((n_v, 2), dtype=torch.float64, device=dev)
     else:
         X, s, c, w = out
-    _dev(X, torch.int8, "X"), _dev(s, torch.int32, "s"), _dev(c, torch.int32, "c")
-    _dev(w, torch.float64, "w")
+    _dev(X, torch.int8, "X", (ccc_sparse_rows(n_v), ccc_k_pad(n_f)))
+    _dev(s, torch.int32, "s", (n_v,))
+    _dev(c, torch.int32, "c", (n_v,))
+    _dev(w, torch.float64, "w", (n_v, 2))
     _check(lib().ccc_expand_sparse(_p(packed), n_v, n_f, gamma, _p(X), _p(s), _p(c), _p(w),
                                    _stream(stream)))
     return X, s, c, w
@@ -546,9 +631,17 @@ def ccc_2way_sparse_block(X_a, w_a, n_a, a_row0, a_lo, a_hi, X_b, w_b, n_b, b_ro
                           out_flags, tallies=None, ccc=None, checksum=None, stream=None,
                           compact: Compact | None = None):
     cp = None
+    for X, w, n, nm in ((X_a, w_a, n_a, "a"), (X_b, w_b, n_b, "b")):
+        _dev(X, torch.int8, f"X_{nm}", (ccc_sparse_rows(n), ccc_k_pad(n_f)))
+        _dev(w, torch.float64, f"w_{nm}", (n, 2))
+    if not 0 <= a_lo <= a_hi <= n_a:
+        raise ValueError("row range [a_lo, a_hi) must lie inside block a")
+    n_rec = (sum(n_a - 1 - i for i in range(a_lo, a_hi)) if diag else (a_hi - a_lo) * n_b)
     if compact is not None:
         cp, tallies, ccc = ctypes.byref(compact._c), compact.tallies, compact.ccc
-    _dev(X_a, torch.int8, "X_a"), _dev(X_b, torch.int8, "X_b")
+        _req(checksum, torch.int64, (2,), "checksum")
+    else:
+        _check_outs(n_rec, 4, out_flags, tallies, ccc, checksum)
     _check(lib().ccc_2way_sparse_block(_p(X_a), _p(w_a), n_a, a_row0, a_lo, a_hi, _p(X_b),
                                        _p(w_b), n_b, b_row0, int(bool(diag)), n_f, out_flags,
                                        _p(tallies), _p(ccc), _p(checksum), cp, _stream(stream)))
@@ -559,13 +652,13 @@ def ccc_2way_sparse(packed: torch.Tensor, n_f: int, gamma: float = GAMMA,
                     out_flags: int = OUT_TALLY | OUT_CCC_F64, tallies=None, ccc=None,
                     checksum=None, ws=None, stream=None, compact: Compact | None = None):
     """Sparse-mode 2-way (code 2 = (1,0) marks a missing entry): records as ccc_2way."""
-    _dev(packed, torch.uint8, "packed")
-    n_v = packed.shape[0]
+    n_v = _packed(packed, n_f)
     cp, tallies, ccc, checksum = _outs(ccc_num_unique(2, n_v), 4, out_flags, packed.device,
                                        tallies, ccc, checksum, compact)
     if ws is None:
         ws = torch.empty(max(lib().ccc_sparse_workspace_bytes(n_v, n_f), 256), dtype=torch.uint8,
                          device=packed.device)
+    _bytes(ws, lib().ccc_sparse_workspace_bytes(n_v, n_f), "ws")
     _check(lib().ccc_2way_sparse(_p(packed), n_v, n_f, gamma, out_flags, _p(tallies), _p(ccc),
                                  _p(checksum), _p(ws), ws.numel(), cp, _stream(stream)))
     return tallies, ccc, checksum
@@ -587,10 +680,11 @@ def three_way(codes: torch.Tensor, gamma: float = GAMMA, out_flags: int = OUT_TA
 # ------------------------------------------------------------- f1: sparse 3-way
 def ccc_3way_sparse_prepare(packed: torch.Tensor, n_f: int, gamma: float = GAMMA, ws=None, stream=None):
     """Expand for the sparse 3-way mode: the workspace (N_s, V, s, c, w)."""
-    n_v = packed.shape[0]
+    n_v = _packed(packed, n_f)
     if ws is None:
         ws = torch.empty(max(256, lib().ccc_sparse3_workspace_bytes(n_v, n_f)), dtype=torch.uint8,
                          device=packed.device)
+    _bytes(ws, lib().ccc_sparse3_workspace_bytes(n_v, n_f), "ws")
     _check(lib().ccc_3way_sparse_prepare(_p(packed), n_v, n_f, gamma, _p(ws), ws.numel(), _stream(stream)))
     return ws
 
@@ -604,6 +698,8 @@ def ccc_3way_sparse_stage(n_v: int, n_f: int, n_stages: int, stage: int, ws: tor
     nb = lib().ccc_3way_sparse_scratch_bytes(n_v, n_stages, stage)
     if scratch is None:
         scratch = torch.empty(max(16, nb), dtype=torch.uint8, device=ws.device)
+    _bytes(ws, lib().ccc_sparse3_workspace_bytes(n_v, n_f), "ws")
+    _bytes(scratch, nb, "scratch")
     _check(lib().ccc_3way_sparse_stage(n_v, n_f, gamma, n_stages, stage, out_flags, _p(T), _p(C), _p(ck),
                                        _p(ws), ws.numel(), _p(scratch), scratch.numel(), _stream(stream)))
     return T, C, ck
@@ -623,10 +719,11 @@ def three_way_sparse(codes: torch.Tensor, gamma: float = GAMMA, out_flags: int =
 
 # ------------------------------------------------------------- f4(ii): the paper's 3-way route
 def ccc_3way_paper_prepare(packed: torch.Tensor, n_f: int, gamma: float = GAMMA, ws=None, stream=None):
-    n_v = packed.shape[0]
+    n_v = _packed(packed, n_f)
     if ws is None:
         ws = torch.empty(max(256, lib().ccc_3way_paper_workspace_bytes(n_v, n_f)), dtype=torch.uint8,
                          device=packed.device)
+    _bytes(ws, lib().ccc_3way_paper_workspace_bytes(n_v, n_f), "ws")
     _check(lib().ccc_3way_paper_prepare(_p(packed), n_v, n_f, gamma, _p(ws), ws.numel(), _stream(stream)))
     return ws
 
@@ -639,6 +736,8 @@ def ccc_3way_paper_stage(n_v: int, n_f: int, n_stages: int, stage: int, ws: torc
     nb = lib().ccc_3way_paper_scratch_bytes(n_v, n_stages, stage)
     if scratch is None:
         scratch = torch.empty(max(16, nb), dtype=torch.uint8, device=ws.device)
+    _bytes(ws, lib().ccc_3way_paper_workspace_bytes(n_v, n_f), "ws")
+    _bytes(scratch, nb, "scratch")
     _check(lib().ccc_3way_paper_stage(n_v, n_f, gamma, n_stages, stage, out_flags, _p(T), _p(C), _p(ck),
                                       _p(ws), ws.numel(), _p(scratch), scratch.numel(), _stream(stream)))
     return T, C, ck
@@ -664,6 +763,8 @@ def ccc_3way_host(codes_h: torch.Tensor, gamma: float = GAMMA, out_flags: int = 
     if ws is None:
         ws = torch.empty(lib().ccc_3way_host_workspace_bytes(n_v, n_f, n_stages, out_flags), dtype=torch.uint8,
                          device="cuda")
+    _check_outs(m, 8, out_flags, tallies_h, ccc_h, checksum_h, cuda=False)
+    _bytes(ws, lib().ccc_3way_host_workspace_bytes(n_v, n_f, n_stages, out_flags), "ws")
     _check(lib().ccc_3way_host(codes_h.data_ptr(), n_v, n_f, gamma, out_flags, n_stages,
                                tallies_h.data_ptr() if tallies_h is not None else None,
                                ccc_h.data_ptr() if ccc_h is not None else None,

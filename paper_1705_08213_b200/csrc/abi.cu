@@ -905,6 +905,17 @@ ccc_status ccc_3way_unit(const ccc_block* bp, int64_t p_lo, int64_t p_hi, const 
         return fail(CCC_ERR_INVALID_ARGUMENT, "same row/column block needs whole ranges");
     if (spm && !smn && !(m_lo == 0 && m_hi == bm->rows))
         return fail(CCC_ERR_INVALID_ARGUMENT, "same pivot/row block needs the whole row range");
+    {
+        // slot position of each role under `order` (include/ccc.h: 0 pmn, 1 pnm, 2 mpn,
+        // 3 mnp, 4 npm, 5 nmp).  A shared block enumerates p < m (m < n) only, so the
+        // order must place those roles in that order or the keys are not canonical.
+        static const int pos_p[6] = {0, 0, 1, 2, 1, 2}, pos_m[6] = {1, 2, 0, 0, 2, 1},
+                         pos_n[6] = {2, 1, 2, 1, 0, 0};
+        if (spm && pos_p[order] > pos_m[order])
+            return fail(CCC_ERR_INVALID_ARGUMENT, "pivot and row block shared: order must put p before m");
+        if (smn && pos_m[order] > pos_n[order])
+            return fail(CCC_ERR_INVALID_ARGUMENT, "row and column block shared: order must put m before n");
+    }
     const int64_t recs = ccc_3way_unit_records(bp, p_lo, p_hi, bm, m_lo, m_hi, bn, n_lo, n_hi);
     if (recs == 0) return CCC_OK;
     CCC_CHECK(check_outputs(out_flags, tallies_d, ccc_d, checksum_d));

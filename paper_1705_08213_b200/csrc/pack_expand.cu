@@ -110,6 +110,10 @@ __global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict_
             for (int u = 0; u < 4; ++u) {
                 const int64_t g = base + 32 * u + lane;
                 p[u] = g < words_per_row ? __ldg(prow + g) : 0u;
+                // codes past n_f in the last word are not elements (whatever the caller's
+                // padding holds): mask them like expand_sparse_kernel does
+                const int64_t left = n_f - 16 * g;
+                if (left < 16) p[u] &= left <= 0 ? 0u : (uint32_t)((1ull << (2 * left)) - 1);
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {

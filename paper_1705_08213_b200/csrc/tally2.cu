@@ -566,13 +566,20 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
 }
 
 // ------------------------------------------------------------------------- host side
+// Diagnostic knobs (1-CTA variant, super-tile shape, K direction, per-tile trace) exist
+// only in builds with -DCCC_DIAG (scripts/); the product library ignores the environment,
+// so the field-split export and finish kernels always share one tile schedule.
 static int pair_mode() {
+#ifdef CCC_DIAG
     static int mode = -1;
     if (mode < 0) {
         const char* e = getenv("CCC_TALLY2_CTA");
         mode = (e && e[0] == '1') ? 1 : 2;
     }
     return mode;
+#else
+    return 2;
+#endif
 }
 
 int tally2_tile_rows() { return pair_mode() == 2 ? 256 : 128; }
@@ -583,6 +590,7 @@ cudaError_t launch_tally2(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
     const int pm = pair_mode();
     TriSched sch;
     Tally2Args a2 = a;
+#ifdef CCC_DIAG
     {
         const char* e = getenv("CCC_SUPER");   // "rows,cols" in elements
         if (e) sscanf(e, "%d,%d", &a2.sup_rows, &a2.sup_cols);
@@ -591,6 +599,7 @@ cudaError_t launch_tally2(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
         const char* tre = getenv("CCC_TRACE_PTR");   // diagnostics: device pointer (decimal)
         a2.trace = tre ? reinterpret_cast<unsigned long long*>(strtoull(tre, nullptr, 10)) : nullptr;
     }
+#endif
     sch.init(a.a_lo, a.nA, a.nB, a.diag, (pm == 2 || a.sparse) ? Cfg2<2>::kTileM : Cfg2<1>::kTileM,
              a2.sup_rows, a2.sup_cols);
     const int64_t all_tiles = sch.total();

@@ -854,10 +854,12 @@ int64_t tally3_units(const Tally3Args& a) {
 cudaError_t launch_tally3(const CUtensorMap& tmA, const CUtensorMap& tmB, const Tally3Args& a0,
                           int num_sms, cudaStream_t stream, int64_t* n_units_out) {
     Tally3Args a = a0;
+#ifdef CCC_DIAG
     {
         const char* tre = getenv("CCC_TRACE_PTR");   // diagnostics: device pointer (decimal)
         a.trace = tre ? reinterpret_cast<unsigned long long*>(strtoull(tre, nullptr, 10)) : nullptr;
     }
+#endif
     const int64_t units = tally3_units(a);
     if (n_units_out) *n_units_out = units;
     if (units == 0) return cudaSuccess;

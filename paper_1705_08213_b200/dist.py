@@ -100,14 +100,18 @@ class CudaBackend:
                                                u.n_lo, u.n_hi, u.order), ring.bounds)
 
     def unit(self, ring, u, p_lo, p_hi, ck):
+        """One piece of a tetrahedral unit into a reused record buffer: the views it returns
+        (and hands to Ring3Way's sink) are valid only until the next piece is launched on
+        the current stream -- a sink that keeps records must copy them on this stream."""
         f = self.out_flags
         n_rec = self.unit_records(ring, u, p_lo, p_hi)
-        if not hasattr(self, "_buf3") or self._buf3[0] < n_rec:
+        buf = getattr(self, "_buf3", None)
+        if buf is None or buf[0] < n_rec or buf[1] != f:
             T = torch.empty((n_rec, 8), dtype=torch.int32, device=self.device) if f & 1 else None
             C = (torch.empty((n_rec, 8), dtype=torch.float64, device=self.device) if f & 2 else
                  torch.empty((n_rec, 8), dtype=torch.float32, device=self.device) if f & 4 else None)
-            self._buf3 = (n_rec, T, C)
-        _, T, C = self._buf3
+            self._buf3 = (n_rec, f, T, C)
+        _, _, T, C = self._buf3
         T = T[:n_rec] if T is not None else None
         C = C[:n_rec] if C is not None else None
         self.ccc.ccc_3way_unit(self._blk(ring, u.pb), p_lo, p_hi, self._blk(ring, u.mb), u.m_lo,
@@ -258,7 +262,8 @@ class Ring3Way:
 
     def run(self, packed_own, sink=None):
         """One pass; sink(unit, p_lo, p_hi, outputs) receives each piece's records (on the
-        device; the default drops them after the checksum fold)."""
+        device, in a buffer the next piece overwrites: copy on the current stream to keep
+        them; the default drops them after the checksum fold)."""
         be, r, P = self.be, self.rank, self.P
         lo, hi = self.bounds[r]
         be.expand_into(packed_own, self.full, lo, hi)

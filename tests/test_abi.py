@@ -205,3 +205,36 @@ def test_product_package_does_not_import_the_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(import|from)\s+(oracle|baselines)\b", txt, re.M), f
                 assert "ccc_oracle" not in txt and "liboracle" not in txt, f
+
+
+def test_binding_rejects_bad_buffers_before_the_abi():
+    """every wrapper checks device, dtype, contiguity and shape of its inputs and
+    of caller-supplied outputs before a pointer reaches the C ABI (no CUDA needed: the
+    checks raise first)."""
+    import torch
+
+    from paper_1705_08213_b200 import ccc
+    cpu = torch.zeros((4, ccc.ccc_packed_stride(100)), dtype=torch.uint8)
+    with pytest.raises(ValueError, match="CUDA"):
+        ccc.ccc_expand(cpu, 100)
+    with pytest.raises(ValueError, match="CUDA"):
+        ccc.ccc_2way_popcount(cpu, 100)
+    with pytest.raises(ValueError, match="CUDA"):
+        ccc.ccc_3way_sparse_prepare(cpu, 100)
+    with pytest.raises(ValueError, match="shape"):
+        ccc._req(torch.zeros((4, 7), dtype=torch.uint8), torch.uint8, (None, ccc.ccc_packed_stride(100)),  # noqa: SLF001
+                 "packed", cuda=False)
+    with pytest.raises(ValueError, match="rows"):
+        ccc._check_outs(10, 4, ccc.OUT_TALLY, torch.zeros((9, 4), dtype=torch.int32), None, None,  # noqa: SLF001
+                        cuda=False)
+    with pytest.raises(ValueError, match="float64"):
+        ccc._check_outs(10, 4, ccc.OUT_CCC_F64, None, torch.zeros((10, 4), dtype=torch.float32), None,  # noqa: SLF001
+                        cuda=False)
+    with pytest.raises(ValueError, match="no buffer"):
+        ccc._check_outs(10, 8, ccc.OUT_TALLY, None, None, None, cuda=False)   # noqa: SLF001
+    with pytest.raises(ValueError, match="CUDA"):
+        ccc._check_outs(1, 4, 0, None, None, torch.zeros(2, dtype=torch.int64), cuda=True)   # noqa: SLF001
+    codes = torch.zeros((3, 100), dtype=torch.uint8)
+    with pytest.raises(ValueError, match="tallies"):
+        ccc.ccc_2way_host(codes, out_flags=ccc.OUT_TALLY, tallies_h=torch.zeros((2, 4), dtype=torch.int32),
+                          dev_ws=torch.zeros(1, dtype=torch.uint8))

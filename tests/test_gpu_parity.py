@@ -653,3 +653,46 @@ def test_golden_hand_values_through_the_kernels():
         T = (ccc.two_way if way == "2" else ccc.three_way)(codes, out_flags=TAL)[0]
         torch.cuda.synchronize()
         assert list(_t(T)[0]) == [int(x) for x in expected.split(",")]
+
+
+def test_expand_ignores_garbage_tail():
+    """codes past n_f in the last packed word are not elements -- expand masks
+    them, so caller-made packed rows with non-zero padding give the same N, s, w."""
+    for n_f in (100, 65, 1):
+        codes = _codes("random", 9, n_f, seed=n_f)
+        packed = ccc.ccc_pack(codes.cuda())
+        dirty = packed.clone()
+        q = torch.arange(dirty.shape[1] * 4)
+        byte_has_tail = torch.zeros(dirty.shape[1], dtype=torch.bool)
+        byte_has_tail[(q[q >= n_f] // 4).unique()] = True
+        for b in torch.nonzero(byte_has_tail).flatten().tolist():
+            keep = 0
+            for e in range(4):
+                if 4 * b + e < n_f:
+                    keep |= 3 << (2 * e)
+            dirty[:, b] = (dirty[:, b] & keep) | (0xFF & ~keep)
+        assert not torch.equal(dirty, packed)
+        N0, s0, w0 = ccc.ccc_expand(packed, n_f)
+        N1, s1, w1 = ccc.ccc_expand(dirty, n_f)
+        assert torch.equal(N0, N1) and torch.equal(s0, s1) and torch.equal(w0, w1)
+        np.testing.assert_array_equal(s1.cpu().numpy(), oracle.allele_sums(codes)[:, 1])
+
+
+def test_3way_unit_rejects_noncanonical_orders():
+    """with a shared pivot/row block the order must put p before m (with a shared
+    row/column block m before n); other orders are INVALID_ARGUMENT, not silent garbage."""
+    n_v, n_f = 64, 200
+    N, s, w = ccc.ccc_expand(ccc.ccc_pack(_codes("random", n_v, n_f, seed=3).cuda()), n_f)
+    G = torch.zeros((n_v, n_v), dtype=torch.int32, device="cuda")
+    ccc.ccc_2way_block(N, s, w, 0, 0, n_v, N, s, w, 0, True, n_f, 0, g=G, ldg=n_v)
+    A = ccc.block(N[:32], s[:32], w[:32], 0)
+    B = ccc.block(N[32:], s[32:], w[32:], 32)
+    for order in range(6):
+        ok_pm = order in (0, 1, 4)           # p before m
+        ok_mn = order in (0, 2, 3)           # m before n
+        for (bp, bm, bn, ok) in ((A, A, B, ok_pm), (B, A, A, ok_mn), (A, A, A, order == 0)):
+            if ok:
+                ccc.ccc_3way_unit(bp, 0, 2, bm, 0, 32, bn, 0, 32, order, G, n_f, TAL)
+            else:
+                with pytest.raises(ValueError, match="order must put"):
+                    ccc.ccc_3way_unit(bp, 0, 2, bm, 0, 32, bn, 0, 32, order, G, n_f, TAL)
