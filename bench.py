@@ -1,7 +1,8 @@
 """bench.py -- CCC comparisons/s of the B200 hot path.
 
 python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                [--workload c2|c2hwe|c4|c1|c2s|c4s|c4f32|c4ck|c2pop|c2fs|c4paper] [--no-e2e] [--no-cpu]
+                [--workload c2|c2hwe|c4|c1|c2s|c4s|c4f32|c4ck|c2pop|c2fs|c4paper|c3|c5]
+                [--no-e2e] [--no-cpu] [--no-3way]
 
 One step = one pass of the whole hot path over one synthetic batch resident in HBM:
   2-way (default, BASELINE configs[1] = C2: 20,000 vectors x 50,000 individuals):
@@ -15,9 +16,14 @@ One step = one pass of the whole hot path over one synthetic batch resident in H
   field split (--workload c2fs: C2 split into 4 field slices, all slices
       on one GPU): per slice ccc_pack -> ccc_expand -> ccc_2way_fs_export (tally GEMM whose
       epilogue stores partial tiles into the owners' slots), then per owner ccc_2way_fs_finish
+The default line also carries "three_way": configs[3] (C4) timed the same way.
 At N > 1 (torchrun), the 2-way path runs the block-circulant decomposition with the
 packed vector blocks passed round a ring over NCCL send/recv; per-GPU load is kept at
-C2's (weak scaling: n_v = 20,000 * sqrt(N)).
+C2's (weak scaling: n_v = 20,000 * sqrt(N)); --workload c4 the tetrahedral 3-way.
+--workload c3 / c5: the BASELINE multi-GPU configs (160,000 x 100,000 2-way, 16,384 x
+32,768 3-way), strong-scaled, at any N including 1 (records in phases / pieces).
+Every decomposed run ends with an untimed checksum step compared with a single-GPU
+CHECKSUM-mode run of the whole problem ("decomposition_check").
 value = unique comparisons (pairs x n_f) of all ranks / max-over-ranks device time.
 """
 from __future__ import annotations
@@ -63,6 +69,12 @@ WORKLOADS = {
                        "folded, none stored; SURVEY 8(d) -- not a headline)"),
     "c4": dict(way=3, n_v=4096, n_f=16384, n_st=16,
                label="3-way CCC, 4,096 SNP vectors x 16,384 individuals, 16 stages (configs[3])"),
+    # the BASELINE multi-GPU configs, strong-scaled (the whole problem at every N; at N = 1
+    # the records -- 614 GB / 70 TB -- are written in phases / pieces into one reused buffer)
+    "c3": dict(way=2, n_v=160000, n_f=100000, strong=True,
+               label="2-way CCC, 160,000 SNP vectors x 100,000 individuals, block-circulant (configs[2])"),
+    "c5": dict(way=3, n_v=16384, n_f=32768, strong=True,
+               label="3-way CCC, 16,384 SNP vectors x 32,768 individuals, tetrahedral (configs[4])"),
 }
 
 
@@ -585,8 +597,10 @@ NOMINAL_INT8_TOPS = 4500.0      # B200 dense int8, datasheet (SURVEY finding 5)
 INT8_OPS_PER_CLK_SM = 16384     # 8,192 int8 MAC / clk / SM (the guides' tcgen05 rate)
 
 
-def config_of(wl):
-    """The config dict both arms print (identical for --impl reference)."""
+def config_of(wl, P=1):
+    """The config dict both arms print (--impl reference prints the same one)."""
+    if P > 1 or wl.get("strong"):
+        return dist_config(wl, P)
     kind = "sparse" if wl.get("sparse") else wl.get("kind", "random")
     inp = {"sparse": "type-3 sparse HWE codes, seed 4, missing marker (1,0) with per-vector rate "
                      "U(0, 0.3) (P:1028-1043)",
@@ -608,6 +622,31 @@ def config_of(wl):
                          wl["n_v"] * wl["n_f"] / 1e9, 4 * wl["n_v"] ** 2 / 1e9,
                          comparisons(3, wl["n_v"], wl["n_f"]) / wl["n_f"] * 96 / wl["n_st"] / 1e9))
     return cfg
+
+
+def dist_config(wl, P):
+    """Config of the decomposed runs (dist.bench_main): weak-scaled c2 / c4 at N > 1, or the
+    strong-scaled BASELINE multi-GPU configs c3 / c5 at any N."""
+    from paper_1705_08213_b200.dist import weak_scaled_nv, weak_scaled_nv3
+    way, n_f, strong = wl["way"], wl["n_f"], wl.get("strong", False)
+    if strong:
+        n_v = wl["n_v"]
+        what = f"{wl['label']} on {P} GPU(s)"
+    else:
+        n_v = weak_scaled_nv(wl["n_v"], P) if way == 2 else weak_scaled_nv3(wl["n_v"], P)
+        what = ((f"2-way CCC block-circulant, {n_v} SNP vectors x {n_f} individuals over {P} GPUs "
+                 "(per-GPU load = configs[1])") if way == 2 else
+                (f"3-way CCC tetrahedral, {n_v} SNP vectors x {n_f} individuals over {P} GPUs "
+                 "(per-GPU load = configs[3])"))
+    return {"workload": what, "n_v": n_v, "n_f": n_f,
+            "input": "type-1 uniform random 2-bit codes, seed 1 (P:657)",
+            "parallelism": f"block-circulant dp{P}" if way == 2 else f"tetrahedral dp{P}",
+            "ring": ("packed 2-bit blocks, NCCL send/recv, overlapped" if way == 2 else
+                     "ring all-gather with retention of packed blocks, NCCL send/recv"),
+            "output": "FULL: uint32 tallies + fp64 CCC for every unique record; phases / pieces "
+                      "into one reused buffer per rank when the records exceed HBM (P:1060-1069, "
+                      "P:621-626)",
+            "l2": "inputs larger than L2" if way == 2 else "operands L2-resident, records far larger than L2"}
 
 
 def step_stats(r, steps):
@@ -741,9 +780,11 @@ def main():
             return
         # The reference arm is the CPU oracle (no runnable reference implementation
         # exists for this paper): a bounded sample of the same workload per step.
+        P = max(world, args.gpus)
+        cfg = config_of(wl, P)
         vals = []
         for _ in range(args.warmup + args.steps):
-            vals.append(cpu_baseline(wl["way"], wl["n_v"], wl["n_f"], target_s=4.0,
+            vals.append(cpu_baseline(wl["way"], cfg["n_v"], wl["n_f"], target_s=4.0,
                                      kind="sparse" if wl.get("sparse") else wl.get("kind", "random")))
         vals = vals[args.warmup:]
         v = sorted(x["value"] for x in vals)[len(vals) // 2]
@@ -751,15 +792,16 @@ def main():
         cb["value"] = v
         out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-               "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-               "dtype": "int64", "data": "synthetic", "config": config_of(wl),
+               "higher_is_better": True, "vs_baseline": None,
+               "dtype": "int64", "data": "synthetic", "config": cfg,
+               "scaling": "strong" if wl.get("strong") else "weak",
                "cpu_baseline": cb,
                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
                        "d2h_bytes_per_step": 0}}
         print(json.dumps(out))
         return
 
-    if world > 1 or args.gpus > 1:
+    if world > 1 or args.gpus > 1 or wl.get("strong"):
         if wl.get("sparse"):
             raise SystemExit("the sparse workloads are single-GPU measurements")
         from paper_1705_08213_b200 import dist

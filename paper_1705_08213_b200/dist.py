@@ -99,6 +99,14 @@ class CudaBackend:
         return decomp.unit3_count(decomp.Unit3(u.pb, p_lo, p_hi, u.mb, u.m_lo, u.m_hi, u.nb,
                                                u.n_lo, u.n_hi, u.order), ring.bounds)
 
+    def reserve_unit_records(self, n_rec):
+        f = self.out_flags
+        self._buf3 = None
+        T = torch.empty((n_rec, 8), dtype=torch.int32, device=self.device) if f & 1 else None
+        C = (torch.empty((n_rec, 8), dtype=torch.float64, device=self.device) if f & 2 else
+             torch.empty((n_rec, 8), dtype=torch.float32, device=self.device) if f & 4 else None)
+        self._buf3 = (n_rec, f, T, C)
+
     def unit(self, ring, u, p_lo, p_hi, ck):
         """One piece of a tetrahedral unit into a reused record buffer: the views it returns
         (and hands to Ring3Way's sink) are valid only until the next piece is launched on
@@ -106,10 +114,11 @@ class CudaBackend:
         f = self.out_flags
         n_rec = self.unit_records(ring, u, p_lo, p_hi)
         buf = getattr(self, "_buf3", None)
-        if buf is None or buf[0] < n_rec or buf[1] != f:
+        if buf is None or buf[0] < n_rec or (buf[1] & 7) != (f & 7):
             T = torch.empty((n_rec, 8), dtype=torch.int32, device=self.device) if f & 1 else None
             C = (torch.empty((n_rec, 8), dtype=torch.float64, device=self.device) if f & 2 else
                  torch.empty((n_rec, 8), dtype=torch.float32, device=self.device) if f & 4 else None)
+            self._buf3 = None
             self._buf3 = (n_rec, f, T, C)
         _, _, T, C = self._buf3
         T = T[:n_rec] if T is not None else None
@@ -163,11 +172,44 @@ def ring_shift(cur: torch.Tensor, nxt: torch.Tensor, r: int, P: int, group=None)
     return dist.batch_isend_irecv(ops)
 
 
+def row_bands(u, bounds, max_records):
+    """Cut a 2-way unit into row bands of at most max_records records each -- the paper's
+    2-way "phases" (§7 item 3: compute a subset of the blocks per run so the
+    results fit in memory).  A band never splits a row; a single row above the bound is a
+    band of its own.  None = the whole unit."""
+    if max_records is None:
+        return [(u.a_lo, u.a_hi)]
+    n_b = bounds[u.b][1] - bounds[u.b][0]
+    out, lo, acc = [], u.a_lo, 0
+    for i in range(u.a_lo, u.a_hi):
+        r = (n_b - 1 - i) if u.diag else n_b
+        if acc and acc + r > max_records:
+            out.append((lo, i))
+            lo, acc = i, 0
+        acc += r
+    if u.a_hi > lo:
+        out.append((lo, u.a_hi))
+    return out
+
+
+def band_records(u, bounds, lo, hi) -> int:
+    n_b = bounds[u.b][1] - bounds[u.b][0]
+    if u.diag:
+        return sum(n_b - 1 - i for i in range(lo, hi))
+    return (hi - lo) * n_b
+
+
 class Ring2Way:
     """Per-rank state of the block-circulant 2-way computation (buffers are reused
-    across calls so a bench step does no allocation)."""
+    across calls so a bench step does no allocation).
 
-    def __init__(self, backend, bounds, rank: int, world: int, group=None):
+    max_records = None: every unit keeps its own record buffers (`run` returns them).
+    max_records = M: every unit is cut into row-band phases of <= M records (row_bands)
+    and all phases write into ONE reused buffer; `sink(unit, a_lo, a_hi, (T, C))` sees each
+    phase's records before the next phase overwrites them (copy on the current stream to
+    keep them).  This is how configs[2] (614 GB of records at P = 1) runs in FULL mode."""
+
+    def __init__(self, backend, bounds, rank: int, world: int, group=None, max_records=None):
         self.be = backend
         self.bounds = bounds
         self.rank = rank
@@ -179,17 +221,29 @@ class Ring2Way:
         self.max_rows = max(rows)
         self.recv = [backend.packed_empty(self.max_rows) for _ in range(2 if self.steps else 0)]
         self.other = backend.expanded_empty(self.max_rows) if self.steps else None
-        self.out = [backend.outputs(decomp.unit2_records(u, bounds)) for u in self.units]
+        self.own = backend.expanded_empty(rows[rank])
+        self.max_records = max_records
+        self.phases = [row_bands(u, bounds, max_records) for u in self.units]
+        if max_records is None:
+            self.out = [backend.outputs(decomp.unit2_records(u, bounds)) for u in self.units]
+        else:
+            big = max(band_records(u, bounds, lo, hi) for u, ph in zip(self.units, self.phases)
+                      for lo, hi in ph)
+            self.buf = backend.outputs(big)
+            self.out = None
         self.ck = backend.checksum_zero()
         self.launches = 0
 
     def _rows(self, b):
         return self.bounds[b][1] - self.bounds[b][0]
 
-    def run(self, packed_own, timed=False):
+    def n_phases(self) -> int:
+        return sum(len(ph) for ph in self.phases)
+
+    def run(self, packed_own, timed=False, sink=None):
         """One pass over this rank's units.  packed_own: the rank's packed block."""
         be, r, P = self.be, self.rank, self.P
-        own = be.expand(packed_own)
+        own = be.expand(packed_own, self.own)
         self.launches = 1
         cur = packed_own
         for d in range(self.steps + 1):
@@ -212,11 +266,19 @@ class Ring2Way:
                 B = own if u.b == r else held_exp
                 if d == 0:
                     A = B = own
-                self.launches += be.block(A, self.bounds[u.a][0], u.a_lo, u.a_hi, B,
-                                          self.bounds[u.b][0], u.diag, self.out[ui], self.ck,
-                                          timed=timed)
                 assert u.a == r or u.b == r
                 assert held in (u.a, u.b)
+                for lo, hi in self.phases[ui]:
+                    if self.out is not None:
+                        out = self.out[ui]
+                    else:
+                        n = band_records(u, self.bounds, lo, hi)
+                        out = tuple(x[:n] if x is not None else None for x in self.buf)
+                    self.launches += be.block(A, self.bounds[u.a][0], lo, hi, B,
+                                              self.bounds[u.b][0], u.diag, out, self.ck,
+                                              timed=timed)
+                    if sink is not None:
+                        sink(u, lo, hi, out)
             for q in reqs:
                 q.wait()
             if nxt is not None:
@@ -248,6 +310,11 @@ class Ring3Way:
         self.max_records = max_records
         self.ck = backend.checksum_zero()
         self.launches = 0
+        if hasattr(backend, "reserve_unit_records"):
+            # one record buffer sized for the largest piece up front (no regrowth mid-run)
+            backend.reserve_unit_records(max((backend.unit_records(self, u, lo, hi)
+                                              for u in self.units for lo, hi in self._pieces(u)),
+                                             default=0))
 
     def _pieces(self, u):
         """Split a unit into pivot sub-ranges of <= max_records records."""
@@ -306,7 +373,11 @@ class Ring3Way:
 
 
 def checksum_total(ck_local: torch.Tensor, group=None) -> int:
-    """Sum of the ranks' 128-bit checksums mod 2^128 (host-side, exact)."""
+    """Sum of the ranks' 128-bit checksums mod 2^128 (host-side, exact); a world of one
+    without a process group returns the local value."""
+    if not dist.is_available() or not dist.is_initialized():
+        lo, hi = (int(x) & ((1 << 64) - 1) for x in ck_local.cpu().tolist())
+        return (hi << 64) | lo
     world = dist.get_world_size(group)
     if ck_local.is_cuda and dist.get_backend(group) == "gloo":
         ck_local = ck_local.cpu()
@@ -327,130 +398,6 @@ def weak_scaled_nv(n_v1: int, P: int, align: int = 256) -> int:
     return max(q, int(round(n_v1 * math.sqrt(P) / q)) * q)
 
 
-# ----------------------------------------------------------------------------- bench
-def bench_main(args, wl, metric, unit):
-    """bench.py at N > 1 (torchrun, NCCL): weak-scaled block-circulant 2-way."""
-    import json
-    import time
-
-    import synthgen
-    from . import ccc
-
-    if wl["way"] == 3:
-        return bench_main_3way(args, wl, metric, unit)
-    dist.init_process_group("nccl")
-    rank, P = dist.get_rank(), dist.get_world_size()
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    n_f = wl["n_f"]
-    n_v = weak_scaled_nv(wl["n_v"], P)
-    bounds = decomp.block_bounds(n_v, P, align=256)
-    lo, hi = bounds[rank]
-    flags = ccc.OUT_TALLY | ccc.OUT_CCC_F64 | ccc.OUT_CHECKSUM
-    be = CudaBackend(n_f, ccc.GAMMA, flags)
-    ring = Ring2Way(be, bounds, rank, P)
-    codes = synthgen.random_codes(hi - lo, n_f, seed=1, device="cuda", row0=lo)
-    packed = be.packed_empty(hi - lo)
-    stream = torch.cuda.current_stream()
-
-    def step(timed=False):
-        be.pack(codes, packed)
-        ring.ck.zero_()
-        ring.run(packed, timed=timed)
-
-    # the timed steps write exactly what the single-GPU line writes (tallies + fp64 CCC);
-    # the cross-rank checksum comes from one extra, untimed verification step below
-    be.out_flags = ccc.OUT_TALLY | ccc.OUT_CCC_F64
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    dist.barrier()
-    be.kernel_events.clear()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    from bench import ClockSampler
-    clk = ClockSampler(local)
-    torch.cuda.synchronize()
-    dist.barrier()
-    with clk:
-        t0.record(stream)
-        launches = 0
-        for _ in range(args.steps):
-            step(timed=True)
-            launches += 1 + ring.launches
-        t1.record(stream)
-        torch.cuda.synchronize()
-    ms = t0.elapsed_time(t1)
-    kms = sum(a.elapsed_time(b) for a, b in be.kernel_events)
-    dist.barrier()
-    tmax = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    be.out_flags = flags                       # verification step: + the 128-bit checksum
-    step()
-    torch.cuda.synchronize()
-    be.out_flags = ccc.OUT_TALLY | ccc.OUT_CCC_F64
-    ck = checksum_total(ring.ck)
-    comps = n_f * (n_v * (n_v - 1) // 2)
-    ms_step = float(tmax.item()) / args.steps
-
-    # e2e: the same step through the public API with host buffers: H2D of this rank's
-    # genotype codes from pinned memory, D2H of every record it computes
-    e2e = None
-    if args.e2e:
-        codes_h = codes.cpu().pin_memory()
-        outs_h = [tuple(x.cpu().pin_memory() if x is not None else None for x in o) for o in ring.out]
-        d2h = sum(x.numel() * x.element_size() for o in ring.out for x in o if x is not None)
-        e_steps = max(1, min(args.steps, 3))
-
-        def e2e_step():
-            codes.copy_(codes_h, non_blocking=True)
-            step()
-            for o, oh in zip(ring.out, outs_h):
-                for x, xh in zip(o, oh):
-                    if x is not None:
-                        xh.copy_(x, non_blocking=True)
-            torch.cuda.synchronize()
-
-        e2e_step()
-        dist.barrier()
-        t = time.perf_counter()
-        for _ in range(e_steps):
-            e2e_step()
-        dt = torch.tensor([(time.perf_counter() - t) / e_steps], dtype=torch.float64, device="cuda")
-        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-        e2e = {"value": comps / float(dt.item()), "unit": unit,
-               "h2d_bytes_per_step": (hi - lo) * n_f, "d2h_bytes_per_step": d2h,
-               "steps": e_steps, "ms_per_step": float(dt.item()) * 1e3,
-               "api": "dist.Ring2Way over the libccc binding, pinned host codes in / records out "
-                      "(per-rank bytes)"}
-    if rank == 0:
-        from bench import peaks
-        pk, pk_kind = peaks()
-        my_comps = n_f * sum(decomp.unit2_records(u, bounds) for u in ring.units)
-        ach = 2.0 * my_comps * args.steps / (kms / 1e3) / 1e12
-        peak = 2.0 * pk["bf16_tflops"]
-        out = {
-            "metric": metric, "value": comps / (ms_step / 1e3), "unit": unit, "n_gpus": P,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
-            "data": "synthetic",
-            "config": {"workload": f"2-way CCC block-circulant, {n_v} SNP vectors x {n_f} "
-                                   f"individuals over {P} GPUs (per-GPU load = configs[1])",
-                       "n_v": n_v, "n_f": n_f, "parallelism": f"block-circulant dp{P}",
-                       "ring": "packed 2-bit blocks, NCCL send/recv, overlapped",
-                       "l2": "inputs larger than L2"},
-            "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                         "frac": ach / peak, "traffic": None, "kernel": "tally2_kernel",
-                         "peak_source": f"2 x bf16_tflops of MEASURED_PEAKS.json ({pk_kind})"},
-            "gpu_launches": launches, "checksum": f"{ck:032x}",
-            "clocks": clk.summary(),
-        }
-        if e2e:
-            out["e2e"] = e2e
-        print(json.dumps(out))
-    dist.barrier()
-    dist.destroy_process_group()
-
-
 def weak_scaled_nv3(n_v1: int, P: int, align: int = 256) -> int:
     """n_v at P GPUs with the same per-GPU triple count as n_v1 on one GPU."""
     if P == 1:
@@ -459,74 +406,233 @@ def weak_scaled_nv3(n_v1: int, P: int, align: int = 256) -> int:
     return max(q, int(round(n_v1 * P ** (1.0 / 3.0) / q)) * q)
 
 
-def bench_main_3way(args, wl, metric, unit):
-    """bench.py --workload c4 at N > 1: tetrahedral 3-way, weak-scaled from C4."""
+# ----------------------------------------------------------------------------- bench
+class _World:
+    """One process per GPU: torch.distributed over NCCL when launched by torchrun
+    (WORLD_SIZE > 1), a world of one without a process group otherwise."""
+
+    def __init__(self):
+        self.P = int(os.environ.get("WORLD_SIZE", "1"))
+        if self.P > 1:
+            dist.init_process_group("nccl")
+            self.rank, self.P = dist.get_rank(), dist.get_world_size()
+        else:
+            self.rank = 0
+        self.local = int(os.environ.get("LOCAL_RANK", self.rank))
+        torch.cuda.set_device(self.local)
+
+    def barrier(self):
+        if self.P > 1:
+            dist.barrier()
+
+    def max(self, v: float) -> float:
+        if self.P == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.P > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+
+
+def record_budget(bytes_per_record: int, reserve_bytes: int) -> int:
+    """Records that fit in the free HBM after `reserve_bytes` more are set aside."""
+    free, _ = torch.cuda.mem_get_info()
+    return max(1, int((free - reserve_bytes - (6 << 30)) // bytes_per_record))
+
+
+def _timed(W, step, args):
+    """W warm-ups, barrier + synchronize, exactly K steps between CUDA events on the
+    launching stream (NVML clocks sampled meanwhile), max over ranks."""
+    from bench import ClockSampler
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    W.barrier()
+    stream = torch.cuda.current_stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    clk = ClockSampler(W.local)
+    torch.cuda.synchronize()
+    W.barrier()
+    with clk:
+        ev[0].record(stream)
+        for k in range(args.steps):
+            step(True)
+            ev[k + 1].record(stream)
+        torch.cuda.synchronize()
+    per = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    ms = W.max(ev[0].elapsed_time(ev[-1]))
+    per_max = [W.max(x) for x in per]
+    return ms, per_max, clk.summary()
+
+
+def bench_main(args, wl, metric, unit):  # noqa: C901
+    """bench.py through the decompositions: N > 1 (torchrun, NCCL) or the strong-scaled
+    BASELINE configs (c3, c5) at any N.  2-way: block-circulant ring with row-band phases
+    when the records exceed HBM; 3-way: tetrahedral units cut into pivot pieces.  After
+    the timed steps, one untimed step with the 128-bit checksum is summed over the ranks
+    and compared with a single-GPU CHECKSUM-mode run of the whole problem on rank 0 (the
+    paper's bit-for-bit check across decompositions)."""
     import json
 
     import synthgen
     from . import ccc
 
-    dist.init_process_group("nccl")
-    rank, P = dist.get_rank(), dist.get_world_size()
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
+    W = _World()
+    rank, P = W.rank, W.P
+    strong = wl.get("strong", False)
+    way = wl["way"]
     n_f = wl["n_f"]
-    n_v = weak_scaled_nv3(wl["n_v"], P)
+    if way == 2:
+        n_v = wl["n_v"] if strong else weak_scaled_nv(wl["n_v"], P)
+    else:
+        n_v = wl["n_v"] if strong else weak_scaled_nv3(wl["n_v"], P)
     bounds = decomp.block_bounds(n_v, P, align=256)
     lo, hi = bounds[rank]
-    flags = ccc.OUT_TALLY | ccc.OUT_CCC_F64 | ccc.OUT_CHECKSUM
-    be = CudaBackend(n_f, ccc.GAMMA, flags)
-    max_rec = int(os.environ.get("CCC_3WAY_STAGE_RECORDS", 700_000_000))   # ~67 GB / stage
-    ring = Ring3Way(be, bounds, rank, P, max_records=max_rec)
+    full = ccc.OUT_TALLY | ccc.OUT_CCC_F64
+    be = CudaBackend(n_f, ccc.GAMMA, full)
     codes = synthgen.random_codes(hi - lo, n_f, seed=1, device="cuda", row0=lo)
     packed = be.packed_empty(hi - lo)
+    k_pad, stride = ccc.ccc_k_pad(n_f), ccc.ccc_packed_stride(n_f)
+    rec_bytes = 48 if way == 2 else 96
+    if way == 2:
+        units = decomp.plan_2way(P, rank, bounds)
+        my_rec = sum(decomp.unit2_records(u, bounds) for u in units)
+        max_rows = max(b - a for a, b in bounds)
+        fixed = 2 * max_rows * k_pad + 2 * max_rows * stride          # own + other N, recv
+        budget = record_budget(rec_bytes, fixed)
+        max_rec = None if my_rec <= budget else budget
+        ring = Ring2Way(be, bounds, rank, P, max_records=max_rec)
+        phases = ring.n_phases()
+    else:
+        my_rec = decomp.total_triples(P, bounds) // P
+        fixed = n_v * k_pad + 4 * n_v * n_v + 2 * max(b - a for a, b in bounds) * stride
+        max_rec = min(record_budget(rec_bytes, fixed), 1 << 40)
+        ring = Ring3Way(be, bounds, rank, P, max_records=max_rec)
+        phases = sum(len(ring._pieces(u)) for u in ring.units)
+    launches = [0]
 
-    def step():
+    def step(timed):
         be.pack(codes, packed)
         ring.ck.zero_()
-        ring.run(packed)
+        if way == 2:
+            ring.run(packed, timed=timed)
+        else:
+            ring.run(packed)
+        if timed:
+            launches[0] += 1 + ring.launches
 
-    be.out_flags = ccc.OUT_TALLY | ccc.OUT_CCC_F64   # as the single-GPU line; checksum below
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    dist.barrier()
-    from bench import ClockSampler
-    clk = ClockSampler(local)
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with clk:
-        t0.record()
-        for _ in range(args.steps):
-            step()
-        t1.record()
-        torch.cuda.synchronize()
-    tmax = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device="cuda")
-    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    be.out_flags = flags                                # untimed verification step
-    step()
+    ms, per, clk = _timed(W, step, args)
+    kms = sum(a.elapsed_time(b) for a, b in be.kernel_events) if way == 2 else None
+    if kms is not None:
+        kms = W.max(kms)
+    # verification: + the checksum, summed over ranks
+    be.out_flags = full | ccc.OUT_CHECKSUM
+    step(False)
     torch.cuda.synchronize()
     ck = checksum_total(ring.ck)
-    comps = n_f * (n_v * (n_v - 1) * (n_v - 2) // 6)
-    ms_step = float(tmax.item()) / args.steps
+    be.out_flags = full
+    comps = n_f * (n_v * (n_v - 1) // 2 if way == 2 else n_v * (n_v - 1) * (n_v - 2) // 6)
+    ms_step = ms / args.steps
+    e2e = None
+    if args.e2e and way == 2 and ring.out is not None:
+        # the same step through the public API with host buffers: H2D of this rank's genotype
+        # codes from pinned memory, D2H of every record it computes, max over ranks
+        import time
+        codes_h = codes.cpu().pin_memory()
+        outs_h = [tuple(x.cpu().pin_memory() if x is not None else None for x in o) for o in ring.out]
+        d2h = sum(x.numel() * x.element_size() for o in ring.out for x in o if x is not None)
+        e_steps = max(1, min(args.steps, 3))
+
+        def e2e_step():
+            codes.copy_(codes_h, non_blocking=True)
+            step(False)
+            for o, oh in zip(ring.out, outs_h):
+                for x, xh in zip(o, oh):
+                    if x is not None:
+                        xh.copy_(x, non_blocking=True)
+            torch.cuda.synchronize()
+
+        e2e_step()
+        W.barrier()
+        t = time.perf_counter()
+        for _ in range(e_steps):
+            e2e_step()
+        dt = W.max((time.perf_counter() - t) / e_steps)
+        e2e = {"value": comps / dt, "unit": unit, "h2d_bytes_per_step": (hi - lo) * n_f,
+               "d2h_bytes_per_step": d2h, "steps": e_steps, "ms_per_step": dt * 1e3,
+               "api": "dist.Ring2Way over the libccc binding, pinned host codes in / records out "
+                      "(per-rank bytes)"}
+        del outs_h, codes_h
+    # the single-GPU CHECKSUM-mode reference run of the whole problem (rank 0, untimed)
+    ring_phases = phases
+    del ring
+    torch.cuda.empty_cache()
+    ref = None
     if rank == 0:
+        all_codes = codes if P == 1 else synthgen.random_codes(n_v, n_f, seed=1, device="cuda")
+        pk_all = ccc.ccc_pack(all_codes)
+        del all_codes
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        if way == 2:
+            _, _, ck1 = ccc.ccc_2way(pk_all, n_f, out_flags=ccc.OUT_CHECKSUM)
+        else:
+            _, _, ck1 = ccc.ccc_3way(pk_all, n_f, out_flags=ccc.OUT_CHECKSUM)
+        t1.record()
+        torch.cuda.synchronize()
+        ref = {"single_gpu_checksum": f"{ccc.checksum_int(ck1):032x}",
+               "match": ccc.checksum_int(ck1) == ck,
+               "ms": t0.elapsed_time(t1),
+               "how": ("ccc_2way" if way == 2 else "ccc_3way (1 stage)") + " of all %d vectors on "
+                      "rank 0's GPU in CHECKSUM mode vs the sum of the ranks' checksums of the "
+                      "decomposed run (P:651-656)" % n_v}
+    if rank == 0:
+        from bench import INT8_OPS_PER_CLK_SM, NOMINAL_INT8_TOPS, peaks
+        pk, pk_kind = peaks()
+        per_s = sorted(per)
+        mhz = clk.get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)
+        pipe = 148 * INT8_OPS_PER_CLK_SM * mhz * 1e6 / 1e12
+        from bench import config_of
+        cfg = config_of(wl, P)
         out = {"metric": metric, "value": comps / (ms_step / 1e3), "unit": unit, "n_gpus": P,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-               "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-               "dtype": "int8", "data": "synthetic",
-               "config": {"workload": f"3-way CCC tetrahedral, {n_v} SNP vectors x {n_f} "
-                                      f"individuals over {P} GPUs (per-GPU load = configs[3])",
-                          "n_v": n_v, "n_f": n_f, "parallelism": f"tetrahedral dp{P}",
-                          "output": "FULL, staged", "l2": "outputs larger than L2"},
-               "gpu_launches": args.steps * (1 + ring.launches), "checksum": f"{ck:032x}",
-               "clocks": clk.summary()}
-        from bench import peaks
-        pk, pk_kind = peaks()
-        # FULL records: 96 B per triple over all ranks; per-GPU HBM write rate vs the peak
-        gbs = comps / n_f * 96 / P / (ms_step / 1e3) / 1e9
-        out["roofline"] = {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                           "frac": gbs / pk["hbm_gbs"], "traffic": None, "kernel": "tally3_kernel",
-                           "peak_source": f"hbm_gbs of MEASURED_PEAKS.json ({pk_kind}); per GPU, "
-                                          "whole step (96 B/triple)"}
+               "ms_per_step_median": per_s[len(per_s) // 2], "ms_per_step_best": per_s[0],
+               "higher_is_better": True, "scaling": "strong" if strong else "weak",
+               "vs_baseline": None, "dtype": "int8", "data": "synthetic", "config": cfg,
+               "gpu_launches": launches[0], "checksum": f"{ck:032x}",
+               "decomposition_check": ref, "clocks": clk,
+               "phases_per_rank": ring_phases if max_rec is not None else 1}
+        step_tops = 2.0 * comps / P / (ms_step / 1e3) / 1e12
+        if way == 2:
+            ach = 2.0 * n_f * my_rec * args.steps / (kms / 1e3) / 1e12
+            peak = 2.0 * pk["bf16_tflops"]
+            out["roofline"] = {
+                "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                "traffic": None, "kernel": "tally2_kernel",
+                "peak_source": f"2 x bf16_tflops of MEASURED_PEAKS.json ({pk_kind}); per GPU (rank 0)",
+                "int8_pipe_at_clock": {"sm_mhz": mhz, "TOPS": pipe, "kernel_frac": ach / pipe,
+                                       "step_frac": step_tops / pipe},
+                "nominal_int8": {"TOPS": NOMINAL_INT8_TOPS, "kernel_frac": ach / NOMINAL_INT8_TOPS,
+                                 "step_frac": step_tops / NOMINAL_INT8_TOPS}}
+        else:
+            gbs = comps / n_f * rec_bytes / P / (ms_step / 1e3) / 1e9
+            out["roofline"] = {
+                "bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": gbs / pk["hbm_gbs"], "traffic": None, "kernel": "tally3_kernel",
+                "peak_source": f"hbm_gbs of MEASURED_PEAKS.json ({pk_kind}); per GPU, whole step "
+                               "(96 B/triple)",
+                "tensor": {"int8_pipe_at_clock": {"sm_mhz": mhz, "TOPS": pipe, "step_frac": step_tops / pipe},
+                           "nominal_int8": {"TOPS": NOMINAL_INT8_TOPS,
+                                            "step_frac": step_tops / NOMINAL_INT8_TOPS}}}
+        out["e2e"] = e2e
+        if e2e is None:
+            out["e2e_note"] = ("not measured on this workload: one step's records (%.0f GB) are "
+                               "written in phases and exceed host memory; e2e is measured on the "
+                               "configs[1] line" % (comps / n_f * rec_bytes / 1e9))
         print(json.dumps(out))
-    dist.barrier()
-    dist.destroy_process_group()
+    W.close()

@@ -88,6 +88,83 @@ def _worker(rank, world, port, n_v, n_f, q):
         dist.destroy_process_group()
 
 
+def _worker_phases(rank, world, port, n_v, n_f, max_rec, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1705_08213_b200.dist import Ring2Way, checksum_total
+        bounds = decomp.block_bounds(n_v, world)
+        lo, hi = bounds[rank]
+        codes = synthgen.random_codes(hi - lo, n_f, seed=7, row0=lo)
+        ring = Ring2Way(OracleBackend(n_f), bounds, rank, world, max_records=max_rec)
+        got = []
+
+        def sink(u, a_lo, a_hi, out):   # copy: the next phase overwrites the buffer
+            sub = decomp.Unit2(u.a, u.b, a_lo, a_hi, u.diag, u.step)
+            got.append((list(decomp.unit2_pairs(sub, bounds)), out[0].numpy().copy(),
+                        out[1].numpy().copy()))
+
+        assert ring.run(codes, sink=sink) is None
+        q.put((rank, checksum_total(ring.ck), got, ring.n_phases(), ring.buf[0].shape[0]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,max_rec", [(1, 17), (2, 25), (3, 40), (4, 9)])
+def test_ring_2way_phases_gloo(world, max_rec):
+    """2-way phases: every unit cut into row bands of <= max_records records
+    written into ONE reused buffer; the sink sees each band before it is overwritten.  All
+    ranks' bands together cover every pair exactly once with the oracle's records."""
+    n_v, n_f = 26, 31
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_phases, args=(r, world, port, n_v, n_f, max_rec, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    codes = synthgen.random_codes(n_v, n_f, seed=7)
+    To, Co = oracle.all_pairs(codes)
+    index = {tuple(p): r for r, p in enumerate(oracle.pair_list(n_v))}
+    seen = set()
+    for rank, ck, got, nph, cap in res:
+        assert ck == oracle.checksum(2, oracle.pair_list(n_v), To)
+        assert nph == len(got) > 1
+        for pairs, T, C in got:
+            rows = {i for i, _ in pairs}
+            assert len(pairs) <= max(max_rec, max(sum(1 for p in pairs if p[0] == i) for i in rows))
+            assert len(pairs) <= cap
+            for k, pr in enumerate(pairs):
+                assert pr not in seen
+                seen.add(pr)
+                np.testing.assert_array_equal(T[k], To[index[pr]])
+                np.testing.assert_allclose(C[k], Co[index[pr]], rtol=1e-15)
+    assert len(seen) == n_v * (n_v - 1) // 2
+
+
+def test_row_bands():
+    """Row bands never split a row, respect the bound unless one row exceeds it, and cover
+    the unit's rows in order (pure host logic)."""
+    from paper_1705_08213_b200.dist import band_records, row_bands
+    bounds = decomp.block_bounds(1000, 4)
+    for P, r in ((1, 0), (4, 0), (4, 3)):
+        bounds = decomp.block_bounds(1000, P)
+        for u in decomp.plan_2way(P, r, bounds):
+            for m in (1, 50, 997, 10 ** 6):
+                bands = row_bands(u, bounds, m)
+                assert bands[0][0] == u.a_lo and bands[-1][1] == u.a_hi
+                assert all(b[1] == c[0] for b, c in zip(bands, bands[1:]))
+                assert sum(band_records(u, bounds, a, b) for a, b in bands) == decomp.unit2_records(u, bounds)
+                for a, b in bands:
+                    assert band_records(u, bounds, a, b) <= m or b - a == 1
+            assert row_bands(u, bounds, None) == [(u.a_lo, u.a_hi)]
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
