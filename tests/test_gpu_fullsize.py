@@ -38,6 +38,7 @@ def check_records(way, L, H, n_f, rec0, T, C, chunk=1 << 25):
     chunk's copy overlaps the current chunk's check) and compare every record with the
     oracle's planted closed form.  Returns the summed oracle.planted_check result."""
     n, cells = T.shape
+    chunk = max(1, min(chunk, n))
     bufs = [(torch.empty((chunk, cells), dtype=torch.int32, pin_memory=True),
              torch.empty((chunk, cells), dtype=torch.float64, pin_memory=True)) for _ in range(2)]
     stream = torch.cuda.Stream()
@@ -128,3 +129,49 @@ def test_C4_planted_every_record_all_stages():
         assert r["max_rel"] <= 1e-12
         total += rc
     assert total == ccc.ccc_num_unique(3, n_v)
+
+
+def test_ring2way_phases_planted_every_record():
+    """2-way phases as the c3 bench runs them: Ring2Way at world 1 with a
+    record bound that cuts the diagonal block into many row bands written into one reused
+    buffer; every band's records checked against the planted closed form before the next
+    band overwrites them."""
+    from paper_1705_08213_b200 import decomp
+    from paper_1705_08213_b200.dist import CudaBackend, Ring2Way
+    n_v, n_f = 12000, 30000
+    codes, L, H, _ = synthgen.planted_codes(n_v, n_f, seed=3, device="cuda")
+    be = CudaBackend(n_f, oracle.GAMMA, TAL | F64)
+    ring = Ring2Way(be, decomp.block_bounds(n_v, 1, align=256), 0, 1, max_records=7_000_000)
+    assert ring.n_phases() >= 10
+    seen = []
+
+    def sink(u, lo, hi, out):
+        rec0 = lo * (2 * n_v - lo - 1) // 2          # first pair (lo, lo+1) of the band
+        r = check_records(2, L, H, n_f, rec0, out[0], out[1])
+        assert (r["bad_tallies"], r["bad_ccc"]) == (0, 0), (lo, hi, r)
+        seen.append(r["records"])
+
+    ring.run(ccc.ccc_pack(codes), sink=sink)
+    assert len(seen) == ring.n_phases() and sum(seen) == n_v * (n_v - 1) // 2
+
+
+def test_ring3way_pieces_planted_every_record():
+    """3-way pieces as the c5 bench runs them: Ring3Way at world 1 cuts the
+    {A,A,A} unit into pivot pieces of bounded record count in one reused buffer; every
+    piece checked against the planted closed form."""
+    from paper_1705_08213_b200 import decomp
+    from paper_1705_08213_b200.dist import CudaBackend, Ring3Way
+    n_v, n_f = 2048, 8192
+    codes, L, H, _ = synthgen.planted_codes(n_v, n_f, seed=3, device="cuda")
+    be = CudaBackend(n_f, oracle.GAMMA, TAL | F64)
+    ring = Ring3Way(be, decomp.block_bounds(n_v, 1, align=256), 0, 1, max_records=100_000_000)
+    seen = []
+
+    def sink(u, p_lo, p_hi, out):
+        rec0 = sum((n_v - 1 - i) * (n_v - 2 - i) // 2 for i in range(p_lo))   # triples before p_lo
+        r = check_records(3, L, H, n_f, rec0, out[0], out[1])
+        assert (r["bad_tallies"], r["bad_ccc"]) == (0, 0), (p_lo, p_hi, r)
+        seen.append(r["records"])
+
+    ring.run(ccc.ccc_pack(codes), sink=sink)
+    assert len(seen) >= 10 and sum(seen) == n_v * (n_v - 1) * (n_v - 2) // 6
