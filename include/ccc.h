@@ -206,6 +206,31 @@ ccc_status ccc_2way_fs_finish(const int32_t* slots_d, const int32_t* s_d, int64_
                               double gamma, int rank, int world, int64_t t_lo, int64_t t_hi,
                               uint32_t out_flags, uint32_t* tallies_d, void* ccc_d, uint64_t* checksum_d,
                               void* stream);
+/* The same fused reduce-scatter for ONE block of the block-circulant decomposition -- the
+ * composition of the field split with the vector-block ring, i.e. the paper's 2-D
+ * n_pv x n_pf grid: the ranks of one field group each hold the same
+ * two vector blocks A, B over their own field slice and split the tiles of the block's
+ * schedule among themselves (owner(t) = t mod world).  Geometry exactly as
+ * ccc_2way_block: rows [a_lo, a_hi) of block A (n_a rows, global row 0 = a_row0) against
+ * the n_b rows of block B (b_row0); diag != 0: A and B are one block (same pointers,
+ * n_a == n_b) and only local pairs i < j.  Tiles: ccc_2way_fs_block_tiles (-1 on invalid
+ * geometry); slot sizing and the wave protocol as above.  Export: N_a / N_b int8
+ * [rows][ccc_k_pad(n_f_slice)] (128-B aligned) and the slice's s_a / s_b (read only by the
+ * per-row setup).  Finish: s_a / s_b = the FULL allele sums of the two blocks (s_a == s_b
+ * when diag), n_f = the full field count; records land in ccc_2way_block's layout for
+ * that geometry (own tiles only), checksum keys use the global indices.  Errors as
+ * ccc_2way_fs_export / ccc_2way_fs_finish. */
+int64_t    ccc_2way_fs_block_tiles(int64_t n_a, int64_t a_lo, int64_t a_hi, int64_t n_b, int diag);
+ccc_status ccc_2way_fs_block_export(const int8_t* N_a, const int32_t* s_a, int64_t n_a, int64_t a_lo,
+                                    int64_t a_hi, const int8_t* N_b, const int32_t* s_b, int64_t n_b,
+                                    int diag, int64_t n_f_slice, int32_t* const* slots_d, int rank,
+                                    int world, int64_t t_lo, int64_t t_hi, void* stream);
+ccc_status ccc_2way_fs_block_finish(const int32_t* slots_d, const int32_t* s_a, int64_t n_a,
+                                    int64_t a_row0, int64_t a_lo, int64_t a_hi, const int32_t* s_b,
+                                    int64_t n_b, int64_t b_row0, int diag, int64_t n_f, double gamma,
+                                    int rank, int world, int64_t t_lo, int64_t t_hi,
+                                    uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
+                                    uint64_t* checksum_d, void* stream);
 /* Peer-shareable device buffers for the slots (one process per GPU): cudaMalloc'd here
  * (a CUDA IPC handle must name a whole allocation; these are the only buffers the
  * library allocates, and only on request), exported as a CCC_IPC_HANDLE_BYTES handle,

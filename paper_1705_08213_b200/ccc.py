@@ -109,6 +109,11 @@ _SIGS = {
     "ccc_2way_fs_export": (_int, [_vp, _vp, _i64, _i64, _vp, _int, _int, _i64, _i64, _vp]),
     "ccc_2way_fs_finish": (_int, [_vp, _vp, _i64, _i64, _dbl, _int, _int, _i64, _i64, _u32, _vp, _vp,
                                   _vp, _vp]),
+    "ccc_2way_fs_block_tiles": (_i64, [_i64, _i64, _i64, _i64, _int]),
+    "ccc_2way_fs_block_export": (_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _int, _i64, _vp, _int,
+                                        _int, _i64, _i64, _vp]),
+    "ccc_2way_fs_block_finish": (_int, [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _int, _i64,
+                                        _dbl, _int, _int, _i64, _i64, _u32, _vp, _vp, _vp, _vp]),
     "ccc_ipc_malloc": (_int, [_sz, _vp]),
     "ccc_ipc_free": (_int, [_vp]),
     "ccc_ipc_get_handle": (_int, [_vp, _vp]),
@@ -431,6 +436,67 @@ def ccc_2way_fs_finish(slots: torch.Tensor, s, n_f: int, rank: int, world: int, 
     T, C, ck = _outputs(ccc_num_unique(2, n_v), 4, out_flags, s.device, tallies, ccc, checksum)
     _check(lib().ccc_2way_fs_finish(_p(slots), _p(s), n_v, n_f, gamma, rank, world, t_lo, t_hi,
                                     out_flags, _p(T), _p(C), _p(ck), _stream(stream)))
+    return T, C, ck
+
+
+def ccc_2way_fs_block_tiles(n_a: int, a_lo: int, a_hi: int, n_b: int, diag: bool) -> int:
+    n = lib().ccc_2way_fs_block_tiles(n_a, a_lo, a_hi, n_b, int(bool(diag)))
+    if n < 0:
+        raise ValueError("invalid block geometry")
+    return n
+
+
+def block_records(n_a: int, a_lo: int, a_hi: int, n_b: int, diag: bool) -> int:
+    """Records of ccc_2way_block's layout for this geometry (host arithmetic on indices)."""
+    return sum(n_a - 1 - i for i in range(a_lo, a_hi)) if diag else (a_hi - a_lo) * n_b
+
+
+def ccc_2way_fs_block_export(N_a, s_a, a_lo: int, a_hi: int, N_b, s_b, diag: bool, n_f_slice: int,
+                             slot_ptrs: torch.Tensor, rank: int, world: int, t_lo: int, t_hi: int,
+                             stream=None):
+    """Export GEMM of one block of the vector decomposition on this field slice (2-D grid):
+    partial tiles go to the owners' slots (slot_ptrs: int64 device tensor of `world`
+    device addresses)."""
+    n_a = N_a.shape[0] if isinstance(N_a, torch.Tensor) else 0
+    n_b = N_b.shape[0] if isinstance(N_b, torch.Tensor) else 0
+    _dev(N_a, torch.int8, "N_a", (n_a, ccc_k_pad(n_f_slice)))
+    _dev(N_b, torch.int8, "N_b", (n_b, ccc_k_pad(n_f_slice)))
+    _dev(s_a, torch.int32, "s_a", (n_a,))
+    _dev(s_b, torch.int32, "s_b", (n_b,))
+    _dev(slot_ptrs, torch.int64, "slot_ptrs", (world,))
+    if not 0 <= rank < world:
+        raise ValueError("rank must be in [0, world)")
+    if diag and (N_a.data_ptr() != N_b.data_ptr() or s_a.data_ptr() != s_b.data_ptr()):
+        raise ValueError("a diag block passes the same N / s for A and B")
+    _check(lib().ccc_2way_fs_block_export(_p(N_a), _p(s_a), n_a, a_lo, a_hi, _p(N_b), _p(s_b), n_b,
+                                          int(bool(diag)), n_f_slice, _p(slot_ptrs), rank, world, t_lo,
+                                          t_hi, _stream(stream)))
+
+
+def ccc_2way_fs_block_finish(slots, s_a, a_row0: int, a_lo: int, a_hi: int, s_b, b_row0: int, diag: bool,
+                             n_f: int, rank: int, world: int, t_lo: int, t_hi: int, out_flags: int,
+                             tallies=None, ccc=None, checksum=None, gamma: float = GAMMA, stream=None,
+                             slot_ptr: int | None = None):
+    """Reduce this owner's partial tiles of one block and write their records (the
+    ccc_2way_block layout of the geometry).  s_a / s_b: the blocks' full allele sums.
+    slots: this owner's int32 slot tensor, or slot_ptr (an IPC buffer's device address)."""
+    _dev(s_a, torch.int32, "s_a", (None,))
+    _dev(s_b, torch.int32, "s_b", (None,))
+    n_a, n_b = s_a.shape[0], s_b.shape[0]
+    if not 0 <= a_lo <= a_hi <= n_a:
+        raise ValueError("row range [a_lo, a_hi) must lie inside block a")
+    if slot_ptr is None:
+        _req(slots, torch.int32, None, "slots", optional=False)
+        if slots.numel() * 4 < ccc_2way_fs_slot_bytes(world, t_lo, t_hi):
+            raise ValueError("slots smaller than ccc_2way_fs_slot_bytes(world, t_lo, t_hi)")
+        sp = _p(slots)
+    else:
+        sp = ctypes.c_void_p(slot_ptr)
+    n_rec = block_records(n_a, a_lo, a_hi, n_b, diag)
+    T, C, ck = _outputs(n_rec, 4, out_flags, s_a.device, tallies, ccc, checksum)
+    _check(lib().ccc_2way_fs_block_finish(sp, _p(s_a), n_a, a_row0, a_lo, a_hi, _p(s_b), n_b, b_row0,
+                                          int(bool(diag)), n_f, gamma, rank, world, t_lo, t_hi, out_flags,
+                                          _p(T), _p(C), _p(ck), _stream(stream)))
     return T, C, ck
 
 

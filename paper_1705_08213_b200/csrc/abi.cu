@@ -434,39 +434,55 @@ ccc_status ccc_2way_popcount(const uint8_t* packed_d, int64_t n_v, int64_t n_f, 
 }
 
 // ---------------------------------------------------------------- f3: field split
-int64_t ccc_2way_fs_tiles(int64_t n_v) { return n_v < 2 ? 0 : ccc::fs_total_tiles(n_v); }
-
-size_t ccc_2way_fs_slot_bytes(int world, int64_t t_lo, int64_t t_hi) {
-    if (world < 1 || t_hi <= t_lo) return 0;
-    const int64_t owned = (t_hi - t_lo + world - 1) / world;
-    return (size_t)owned * (size_t)world * 65536u * sizeof(int32_t);
+namespace {
+ccc_status fs_geom(int64_t n_a, int64_t a_row0, int64_t a_lo, int64_t a_hi, int64_t n_b, int64_t b_row0,
+                   int diag, ccc::FsGeom* g) {
+    if (n_a < 0 || n_b < 0 || !(0 <= a_lo && a_lo <= a_hi && a_hi <= n_a))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "need 0 <= a_lo <= a_hi <= n_a and n_b >= 0");
+    if (diag && n_a != n_b) return fail(CCC_ERR_INVALID_ARGUMENT, "diag block needs n_a == n_b");
+    if (a_row0 < 0 || b_row0 < 0 || a_row0 + n_a > CCC_MAX_NV || b_row0 + n_b > CCC_MAX_NV)
+        return fail(CCC_ERR_INVALID_ARGUMENT, "global row indices out of range");
+    *g = ccc::FsGeom{};
+    g->a_lo = a_lo;
+    g->nA = a_hi - a_lo;
+    g->nB = n_b;
+    g->a_row0 = a_row0;
+    g->b_row0 = b_row0;
+    g->diag = diag ? 1 : 0;
+    return CCC_OK;
 }
 
-ccc_status ccc_2way_fs_export(const int8_t* N_d, const int32_t* s_d, int64_t n_v, int64_t n_f_slice,
-                              int32_t* const* slots_d, int rank, int world, int64_t t_lo, int64_t t_hi,
-                              void* stream) {
+ccc_status fs_export_impl(const int8_t* N_a, const int32_t* s_a, int64_t n_a, const int8_t* N_b,
+                          const int32_t* s_b, const ccc::FsGeom& g, int64_t n_f_slice, int32_t* const* slots_d,
+                          int rank, int world, int64_t t_lo, int64_t t_hi, void* stream) {
     g_launches = 0;
-    CCC_CHECK(check_sizes(n_v, n_f_slice));
+    CCC_CHECK(check_sizes(n_a, n_f_slice));
+    CCC_CHECK(check_sizes(g.nB, n_f_slice));
     if (world < 1 || rank < 0 || rank >= world) return fail(CCC_ERR_INVALID_ARGUMENT, "need 0 <= rank < world");
     if (t_lo < 0 || t_hi < t_lo) return fail(CCC_ERR_INVALID_ARGUMENT, "need 0 <= t_lo <= t_hi");
-    if (n_v < 2 || t_hi == t_lo) return CCC_OK;
-    if (!N_d || !aligned(N_d, 128) || !s_d || !slots_d)
-        return fail(CCC_ERR_INVALID_ARGUMENT, "N_d (128-B aligned), s_d and slots_d must be non-NULL");
+    if (g.nA == 0 || g.nB == 0 || t_hi == t_lo) return CCC_OK;
+    if (g.diag && N_a != N_b) return fail(CCC_ERR_INVALID_ARGUMENT, "diag block needs A == B");
+    if (!N_a || !N_b || !aligned(N_a, 128) || !aligned(N_b, 128) || !s_a || !s_b || !slots_d)
+        return fail(CCC_ERR_INVALID_ARGUMENT, "N (128-B aligned), s and slots_d must be non-NULL");
     int sms;
     CCC_CHECK(check_device(&sms));
     const int64_t k_pad = kpad_of(n_f_slice);
     CUtensorMap tmA, tmB;
-    CCC_CHECK(make_tmap(&tmA, N_d, n_v, k_pad, ccc::kBM));
-    CCC_CHECK(make_tmap(&tmB, N_d, n_v, k_pad, (uint32_t)ccc::tally2_b_box_rows()));
+    CCC_CHECK(make_tmap(&tmA, N_a, n_a, k_pad, ccc::kBM));
+    CCC_CHECK(make_tmap(&tmB, N_b, g.nB, k_pad, (uint32_t)ccc::tally2_b_box_rows()));
     ccc::Tally2Args a{};
-    a.a_lo = 0;
-    a.nA = a.nB = n_v;
-    a.diag = 1;
+    a.a_lo = g.a_lo;
+    a.nA = g.nA;
+    a.nB = g.nB;
+    a.a_row0 = g.a_row0;
+    a.b_row0 = g.b_row0;
+    a.diag = g.diag;
     a.n_f = (int32_t)n_f_slice;
     a.k_blocks = (int32_t)(k_pad / ccc::kBK);
     a.out_flags = 0;
     a.exact23 = 1;          // the per-row setup then reads s only (no w)
-    a.s_a = a.s_b = s_d;
+    a.s_a = s_a;
+    a.s_b = s_b;
     a.sup_rows = a.sup_cols = 2048;   // the schedule ccc_2way_fs_finish walks
     a.t_lo = t_lo;
     a.t_hi = t_hi;
@@ -479,26 +495,87 @@ ccc_status ccc_2way_fs_export(const int8_t* N_d, const int32_t* s_d, int64_t n_v
     return CCC_OK;
 }
 
-ccc_status ccc_2way_fs_finish(const int32_t* slots_d, const int32_t* s_d, int64_t n_v, int64_t n_f,
-                              double gamma, int rank, int world, int64_t t_lo, int64_t t_hi,
-                              uint32_t out_flags, uint32_t* tallies_d, void* ccc_d, uint64_t* checksum_d,
-                              void* stream) {
+ccc_status fs_finish_impl(const int32_t* slots_d, const int32_t* s_a, const int32_t* s_b, const ccc::FsGeom& g,
+                          int64_t n_f, double gamma, int rank, int world, int64_t t_lo, int64_t t_hi,
+                          uint32_t out_flags, uint32_t* tallies_d, void* ccc_d, uint64_t* checksum_d,
+                          void* stream) {
     g_launches = 0;
-    CCC_CHECK(check_sizes(n_v, n_f));
+    CCC_CHECK(check_sizes(g.nB, n_f));
     if (out_flags & ~15u) return fail(CCC_ERR_INVALID_ARGUMENT, "unknown out_flags bits");
     if (world < 1 || rank < 0 || rank >= world) return fail(CCC_ERR_INVALID_ARGUMENT, "need 0 <= rank < world");
     if (t_lo < 0 || t_hi < t_lo) return fail(CCC_ERR_INVALID_ARGUMENT, "need 0 <= t_lo <= t_hi");
-    if (n_v < 2 || t_hi == t_lo) return CCC_OK;
+    if (g.nA == 0 || g.nB == 0 || t_hi == t_lo) return CCC_OK;
     CCC_CHECK(check_outputs(out_flags, tallies_d, ccc_d, checksum_d));
-    if (!slots_d || !s_d) return fail(CCC_ERR_INVALID_ARGUMENT, "slots_d and s_d must be non-NULL");
+    if (!slots_d || !s_a || !s_b) return fail(CCC_ERR_INVALID_ARGUMENT, "slots_d and s must be non-NULL");
     int sms;
     CCC_CHECK(check_device(&sms));
-    CCC_CUDA(ccc::launch_fs_finish(slots_d, s_d, n_v, n_f, gamma, rank, world, t_lo, t_hi, out_flags,
+    CCC_CUDA(ccc::launch_fs_finish(slots_d, s_a, s_b, g, n_f, gamma, rank, world, t_lo, t_hi, out_flags,
                                    tallies_d, ccc_d, reinterpret_cast<unsigned long long*>(checksum_d),
                                    sms, (cudaStream_t)stream),
              "fs finish launch");
     ++g_launches;
     return CCC_OK;
+}
+}  // namespace
+
+int64_t ccc_2way_fs_tiles(int64_t n_v) { return n_v < 2 ? 0 : ccc::fs_total_tiles(n_v); }
+
+int64_t ccc_2way_fs_block_tiles(int64_t n_a, int64_t a_lo, int64_t a_hi, int64_t n_b, int diag) {
+    ccc::FsGeom g;
+    if (fs_geom(n_a, 0, a_lo, a_hi, n_b, 0, diag, &g) != CCC_OK) return -1;
+    if (g.nA == 0 || g.nB == 0) return 0;
+    return ccc::fs_block_tiles(g);
+}
+
+size_t ccc_2way_fs_slot_bytes(int world, int64_t t_lo, int64_t t_hi) {
+    if (world < 1 || t_hi <= t_lo) return 0;
+    const int64_t owned = (t_hi - t_lo + world - 1) / world;
+    return (size_t)owned * (size_t)world * 65536u * sizeof(int32_t);
+}
+
+ccc_status ccc_2way_fs_export(const int8_t* N_d, const int32_t* s_d, int64_t n_v, int64_t n_f_slice,
+                              int32_t* const* slots_d, int rank, int world, int64_t t_lo, int64_t t_hi,
+                              void* stream) {
+    g_launches = 0;
+    ccc::FsGeom g;
+    CCC_CHECK(fs_geom(n_v, 0, 0, n_v, n_v, 0, 1, &g));
+    if (n_v < 2) return CCC_OK;
+    return fs_export_impl(N_d, s_d, n_v, N_d, s_d, g, n_f_slice, slots_d, rank, world, t_lo, t_hi, stream);
+}
+
+ccc_status ccc_2way_fs_finish(const int32_t* slots_d, const int32_t* s_d, int64_t n_v, int64_t n_f,
+                              double gamma, int rank, int world, int64_t t_lo, int64_t t_hi,
+                              uint32_t out_flags, uint32_t* tallies_d, void* ccc_d, uint64_t* checksum_d,
+                              void* stream) {
+    g_launches = 0;
+    ccc::FsGeom g;
+    CCC_CHECK(fs_geom(n_v, 0, 0, n_v, n_v, 0, 1, &g));
+    if (n_v < 2) return CCC_OK;
+    return fs_finish_impl(slots_d, s_d, s_d, g, n_f, gamma, rank, world, t_lo, t_hi, out_flags, tallies_d,
+                          ccc_d, checksum_d, stream);
+}
+
+ccc_status ccc_2way_fs_block_export(const int8_t* N_a, const int32_t* s_a, int64_t n_a, int64_t a_lo,
+                                    int64_t a_hi, const int8_t* N_b, const int32_t* s_b, int64_t n_b, int diag,
+                                    int64_t n_f_slice, int32_t* const* slots_d, int rank, int world,
+                                    int64_t t_lo, int64_t t_hi, void* stream) {
+    g_launches = 0;
+    ccc::FsGeom g;
+    CCC_CHECK(fs_geom(n_a, 0, a_lo, a_hi, n_b, 0, diag, &g));
+    return fs_export_impl(N_a, s_a, n_a, N_b, s_b, g, n_f_slice, slots_d, rank, world, t_lo, t_hi, stream);
+}
+
+ccc_status ccc_2way_fs_block_finish(const int32_t* slots_d, const int32_t* s_a, int64_t n_a, int64_t a_row0,
+                                    int64_t a_lo, int64_t a_hi, const int32_t* s_b, int64_t n_b, int64_t b_row0,
+                                    int diag, int64_t n_f, double gamma, int rank, int world, int64_t t_lo,
+                                    int64_t t_hi, uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
+                                    uint64_t* checksum_d, void* stream) {
+    g_launches = 0;
+    ccc::FsGeom g;
+    CCC_CHECK(fs_geom(n_a, a_row0, a_lo, a_hi, n_b, b_row0, diag, &g));
+    if (diag && s_a != s_b) return fail(CCC_ERR_INVALID_ARGUMENT, "diag block needs s_a == s_b");
+    return fs_finish_impl(slots_d, s_a, s_b, g, n_f, gamma, rank, world, t_lo, t_hi, out_flags, tallies_d,
+                          ccc_d, checksum_d, stream);
 }
 
 ccc_status ccc_ipc_malloc(size_t bytes, void** dptr) {

@@ -160,6 +160,14 @@ struct Tally2Args {
     int32_t xp_rank, xp_world;   // this field slice; number of slices (= owners)
 };
 
+// f3 field split: the 2-way block whose tiles are exported / finished (the geometry of
+// ccc_2way_block: rows [a_lo, a_lo + nA) of block A against the nB rows of block B; diag:
+// A and B are one block and only i < j; a_row0 / b_row0 global index of local row 0).
+struct FsGeom {
+    int64_t a_lo, nA, nB, a_row0, b_row0;
+    int32_t diag, pad_;
+};
+
 // One vector block as seen by the 3-way kernel.
 struct Blk3 {
     const int8_t* N;       // [rows][k_pad]

@@ -12,6 +12,10 @@
 // with the full allele sums s_i = sum_f s_i^f:
 //     T11 = G, T10 = 2 s_i - G, T01 = 2 s_j - G, T00 = 4 n_f - 2 s_i - 2 s_j + G,
 //     CCC(a,b) = T(a,b) / (4 n_f) w_i(a) w_j(b),  w(a) = 1 - gamma S(a) / (2 n_f)   (Eq.1).
+// The same holds for one block of the block-circulant decomposition (FsGeom: rows
+// [a_lo, a_lo + nA) of block A against block B, the geometry of ccc_2way_block), which is
+// how the field split composes with the vector-block ring into the paper's 2-D
+// n_pv x n_pf grid: the tiles of that block's schedule are exported / owned.
 // Slot layout per owner and wave [t_lo, t_hi): tile t (t mod world == owner) has slot
 // q = (t - t_lo) / world; the partial of slice f sits at int32 offset
 // ((q * world + f) << 16) + row * 256 + col (row < tile rows, col < 256).
@@ -50,7 +54,8 @@ __device__ __forceinline__ void fs_fold(unsigned long long& lo, unsigned long lo
 // and needs the bytes in flight).
 template <int W, bool CK>
 __global__ void __launch_bounds__(128, CCC_FS_MINB) fs_finish_kernel(const int32_t* __restrict__ slots,
-                                                        const int32_t* __restrict__ s, int64_t n_v,
+                                                        const int32_t* __restrict__ s_a,
+                                                        const int32_t* __restrict__ s_b, FsGeom g,
                                                         int64_t n_f, double gamma, int32_t owner,
                                                         int32_t world_rt, int64_t t_lo, int64_t t_end,
                                                         int32_t tile_m, uint32_t flags,
@@ -60,7 +65,9 @@ __global__ void __launch_bounds__(128, CCC_FS_MINB) fs_finish_kernel(const int32
     __shared__ uint32_t row_s[256];
     const int32_t world = W > 0 ? W : world_rt;
     TriSched sch;
-    sch.init(0, n_v, n_v, 1, tile_m, 2048, 2048);   // the schedule of ccc_2way_block(diag)
+    sch.init(g.a_lo, g.nA, g.nB, g.diag, tile_m, 2048, 2048);   // the schedule of ccc_2way_block
+    const int64_t a_end = g.a_lo + g.nA, nB = g.nB;
+    const int64_t rec_base = g.diag ? (g.a_lo * (2 * nB - g.a_lo - 1)) / 2 : 0;
     const int64_t first = t_lo + ((owner - t_lo % world) % world + world) % world;
     const int64_t owned = first < t_end ? (t_end - first + world - 1) / world : 0;
     const bool want_t = flags & 1u, want_c64 = flags & 2u, want_c32 = flags & 4u;
@@ -76,24 +83,25 @@ __global__ void __launch_bounds__(128, CCC_FS_MINB) fs_finish_kernel(const int32
         const int32_t* tile = slots + ((q * world) << 16);
         __syncthreads();   // the previous tile's row terms are no longer read
         for (int r = threadIdx.x; r < tile_m; r += blockDim.x) {
-            const int64_t i = (int64_t)bm * tile_m + r;
-            const uint32_t si = i < n_v ? (uint32_t)__ldg(s + i) : 0u;
+            const int64_t i = g.a_lo + (int64_t)bm * tile_m + r;
+            const uint32_t si = i < a_end ? (uint32_t)__ldg(s_a + i) : 0u;
             row_s[r] = si;
             row_w0[r] = (1.0 - gamma * ((two_nf - (double)si) / two_nf)) * inv4nf;
             row_w1[r] = (1.0 - gamma * ((double)si / two_nf)) * inv4nf;
         }
         __syncthreads();
         const int64_t j0 = (int64_t)bn * kBN + col;
-        const bool ok0 = j0 < n_v, ok1 = j0 + 1 < n_v;
-        const uint32_t sj0 = ok0 ? (uint32_t)__ldg(s + j0) : 0u;
-        const uint32_t sj1 = ok1 ? (uint32_t)__ldg(s + j0 + 1) : 0u;
+        const bool ok0 = j0 < nB, ok1 = j0 + 1 < nB;
+        const uint32_t sj0 = ok0 ? (uint32_t)__ldg(s_b + j0) : 0u;
+        const uint32_t sj1 = ok1 ? (uint32_t)__ldg(s_b + j0 + 1) : 0u;
         const double wj00 = 1.0 - gamma * ((two_nf - (double)sj0) / two_nf);
         const double wj01 = 1.0 - gamma * ((double)sj0 / two_nf);
         const double wj10 = 1.0 - gamma * ((two_nf - (double)sj1) / two_nf);
         const double wj11 = 1.0 - gamma * ((double)sj1 / two_nf);
-        const int64_t i0 = (int64_t)bm * tile_m;
-        // rows of this tile holding a record of column j0 + 1: i < j0 + 1 and i < n_v - 1
-        int64_t r_end = (j0 + 1 < n_v ? j0 + 1 : n_v - 1) - i0;
+        const int64_t i0 = g.a_lo + (int64_t)bm * tile_m;
+        // rows of this tile holding a record of column j0 or j0 + 1: i < a_end, and with
+        // diag also i < j0 + 1 (A and B are one block, only i < j)
+        int64_t r_end = (g.diag && j0 + 1 < a_end ? j0 + 1 : a_end) - i0;
         if (!ok0) r_end = 0;
         r_end = r_end < 0 ? 0 : (r_end > tile_m ? tile_m : r_end);
         constexpr int kR = W == 1 ? 8 : 4;   // rows in flight per thread
@@ -136,11 +144,15 @@ __global__ void __launch_bounds__(128, CCC_FS_MINB) fs_finish_kernel(const int32
                 const int64_t i = i0 + r;
                 const uint32_t si = row_s[r];
                 const double wi0 = row_w0[r], wi1 = row_w1[r];
-                const bool okA = j0 > i, okB = ok1;   // column j0 + 1 > i holds for every r < r_end
+                // diag: column j0 + 1 > i holds for every r < r_end
+                const bool okA = !g.diag || j0 > i, okB = ok1;
                 const uint32_t GA = (uint32_t)Gr[u].x, GB = (uint32_t)Gr[u].y;
                 const uint32_t a3 = GA, a2 = 2u * si - GA, a1 = 2u * sj0 - GA, a0 = four_nf - 2u * si - 2u * sj0 + GA;
                 const uint32_t b3 = GB, b2 = 2u * si - GB, b1 = 2u * sj1 - GB, b0 = four_nf - 2u * si - 2u * sj1 + GB;
-                const int64_t rec = i * (2 * n_v - i - 1) / 2 + (j0 - i - 1);   // record of column j0
+                // record of column j0 (ccc_2way_block's layout)
+                const int64_t rec = g.diag ? i * (2 * nB - i - 1) / 2 + (j0 - i - 1) - rec_base
+                                           : (i - g.a_lo) * nB + j0;
+                const uint64_t gi = (uint64_t)(g.a_row0 + i), gj = (uint64_t)(g.b_row0 + j0);
                 if (want_t) {
                     if (okA && okB && !(rec & 1))
                         stg_256_u32(tallies + 4 * rec, a0, a1, a2, a3, b0, b1, b2, b3);
@@ -172,10 +184,10 @@ __global__ void __launch_bounds__(128, CCC_FS_MINB) fs_finish_kernel(const int32
                 }
                 if constexpr (CK) {
                     if (okA)
-                        fs_fold(ck_lo, ck_hi, (2ull << 60) | ((uint64_t)i << 40) | ((uint64_t)j0 << 20),
+                        fs_fold(ck_lo, ck_hi, (2ull << 60) | (gi << 40) | (gj << 20),
                                 (uint64_t)a0 | ((uint64_t)a1 << 32), (uint64_t)a2 | ((uint64_t)a3 << 32));
                     if (okB)
-                        fs_fold(ck_lo, ck_hi, (2ull << 60) | ((uint64_t)i << 40) | ((uint64_t)(j0 + 1) << 20),
+                        fs_fold(ck_lo, ck_hi, (2ull << 60) | (gi << 40) | ((gj + 1) << 20),
                                 (uint64_t)b0 | ((uint64_t)b1 << 32), (uint64_t)b2 | ((uint64_t)b3 << 32));
                 }
             }
@@ -196,17 +208,24 @@ __global__ void __launch_bounds__(128, CCC_FS_MINB) fs_finish_kernel(const int32
     }
 }
 
-int64_t fs_total_tiles(int64_t n_v) {
+int64_t fs_block_tiles(const FsGeom& g) {
     TriSched sch;
-    sch.init(0, n_v, n_v, 1, tally2_tile_rows(), 2048, 2048);
+    sch.init(g.a_lo, g.nA, g.nB, g.diag, tally2_tile_rows(), 2048, 2048);
     return sch.total();
 }
 
-cudaError_t launch_fs_finish(const int32_t* slots, const int32_t* s, int64_t n_v, int64_t n_f, double gamma,
-                             int owner, int world, int64_t t_lo, int64_t t_hi, uint32_t flags,
-                             uint32_t* tallies, void* ccc, unsigned long long* checksum, int num_sms,
-                             cudaStream_t stream) {
-    const int64_t all = fs_total_tiles(n_v);
+int64_t fs_total_tiles(int64_t n_v) {
+    FsGeom g{};
+    g.nA = g.nB = n_v;
+    g.diag = 1;
+    return fs_block_tiles(g);
+}
+
+cudaError_t launch_fs_finish(const int32_t* slots, const int32_t* s_a, const int32_t* s_b, const FsGeom& g,
+                             int64_t n_f, double gamma, int owner, int world, int64_t t_lo, int64_t t_hi,
+                             uint32_t flags, uint32_t* tallies, void* ccc, unsigned long long* checksum,
+                             int num_sms, cudaStream_t stream) {
+    const int64_t all = fs_block_tiles(g);
     const int64_t t_end = (t_hi > 0 && t_hi < all) ? t_hi : all;
     if (t_end <= t_lo) return cudaSuccess;
     const int64_t owned = (t_end - t_lo + world - 1) / world;
@@ -217,7 +236,7 @@ cudaError_t launch_fs_finish(const int32_t* slots, const int32_t* s, int64_t n_v
             per_sm = 4;
         const int64_t cap = (int64_t)per_sm * num_sms;
         const int64_t grid = owned < cap ? owned : cap;
-        kern<<<(unsigned)grid, 128, 0, stream>>>(slots, s, n_v, n_f, gamma, owner, world, t_lo, t_end,
+        kern<<<(unsigned)grid, 128, 0, stream>>>(slots, s_a, s_b, g, n_f, gamma, owner, world, t_lo, t_end,
                                                  tally2_tile_rows(), flags, tallies, ccc, checksum);
     };
 #define CCC_FS_CASE(w)                                                   \

@@ -663,8 +663,12 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
 #else
             const bool any_row = __any_sync(0xffffffffu, my_any);
 #endif
-            // column groups of 8 that hold any valid n (warp-uniform)
+            // column groups of 8 that hold any valid n (warp-uniform): up to the last valid
+            // column, and from the first group with an n above the warp's lowest row bound
+            // (on the diagonal tiles of a triangle the groups left of it are all masked)
             const int c_end = !any_row ? 0 : (nval + 7) / 8;
+            const int32_t lo_w = __reduce_min_sync(0xffffffffu, lo_r[0] < lo_r[1] ? lo_r[0] : lo_r[1]);
+            const int c_beg = lo_w < 0 ? 0 : (lo_w + 1) / 8;
             // G_mn for column group c: g[r][h] = G(m_r, col0 + 8c + cpair + h), clamped
             auto load_gmn = [&](int c, uint32_t (&g)[2][2]) {
 #pragma unroll
@@ -680,15 +684,15 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 }
             };
             uint32_t gnext[2][2] = {{0u, 0u}, {0u, 0u}};
-            if (c_end > 0) load_gmn(0, gnext);
+            if (c_beg < c_end) load_gmn(c_beg, gnext);
             named_bar_sync(1, 32 * kEpiWarps3);   // column table of this unit is complete
             mbar_wait_sleep(&tfull[acc], acc_phase);
             tc_fence_after();
             if (tr && lane == 0) tr[4] = globaltimer();
             const uint32_t taddr = tmem_base + ((quad * 32u + half * 16u) << 16) + acc * kBN;
             uint32_t vnext[4];
-            if (c_end > 0) tmem_ld_16x256(taddr, vnext);
-            for (int c = 0; c < c_end; ++c) {
+            if (c_beg < c_end) tmem_ld_16x256(taddr + c_beg * 8, vnext);
+            for (int c = c_beg; c < c_end; ++c) {
                 tmem_ld_wait_keep(vnext);
                 const uint32_t va[4] = {vnext[0], vnext[1], vnext[2], vnext[3]};
                 const uint32_t gcur[2][2] = {{gnext[0][0], gnext[0][1]}, {gnext[1][0], gnext[1][1]}};

@@ -95,6 +95,58 @@ def unit2_pairs(u: Unit2, bounds):
             yield (a0 + il, b0 + jl)
 
 
+# ------------------------------------------------------- 2-way process grid (n_pv x n_pr x n_pf)
+@dataclass(frozen=True)
+class Grid:
+    """The paper's process grid for the 2-way method: n_pv vector
+    blocks (block-circulant ring), n_pr parts of every block row's result (the "n_pr axis
+    ... parallelize the computation of the blocks of this block row"), n_pf field slices
+    (a reduction of partial tallies follows the GEMM).  rank = (v n_pr + r) n_pf + f."""
+    n_pv: int
+    n_pr: int = 1
+    n_pf: int = 1
+
+    @property
+    def world(self) -> int:
+        return self.n_pv * self.n_pr * self.n_pf
+
+    def coords(self, rank: int):
+        if not 0 <= rank < self.world:
+            raise ValueError("rank outside the grid")
+        return rank // (self.n_pr * self.n_pf), (rank // self.n_pf) % self.n_pr, rank % self.n_pf
+
+    def rank(self, v: int, r: int, f: int) -> int:
+        return (v * self.n_pr + r) * self.n_pf + f
+
+    def ring_ranks(self, r: int, f: int):
+        """Global ranks of the vector-block ring that rank (., r, f) belongs to, by v."""
+        return [self.rank(v, r, f) for v in range(self.n_pv)]
+
+    def field_ranks(self, v: int, r: int):
+        """Global ranks sharing block row v's part r over the n_pf field slices, by f."""
+        return [self.rank(v, r, f) for f in range(self.n_pf)]
+
+
+def split_rows(u: Unit2, bounds, parts: int):
+    """The n_pr split of a unit: `parts` contiguous row ranges of [u.a_lo, u.a_hi) with
+    record counts as equal as whole rows allow (some may be empty)."""
+    n_b = bounds[u.b][1] - bounds[u.b][0]
+    rows = list(range(u.a_lo, u.a_hi))
+    cum = [0]
+    for i in rows:
+        cum.append(cum[-1] + ((n_b - 1 - i) if u.diag else n_b))
+    tot = cum[-1]
+    cuts = [u.a_lo]
+    k = 0
+    for p in range(1, parts):
+        target = p * tot / parts
+        while k < len(rows) and cum[k] < target:
+            k += 1
+        cuts.append(max(cuts[-1], u.a_lo + k))
+    cuts.append(u.a_hi)
+    return [(cuts[p], cuts[p + 1]) for p in range(parts)]
+
+
 # --------------------------------------------------------------------------- 3-way
 @dataclass(frozen=True)
 class Unit3:

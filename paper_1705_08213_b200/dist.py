@@ -156,19 +156,23 @@ class _StagedRecv:
         self.dst.copy_(self.host)
 
 
-def ring_shift(cur: torch.Tensor, nxt: torch.Tensor, r: int, P: int, group=None):
+def ring_shift(cur: torch.Tensor, nxt: torch.Tensor, r: int, P: int, group=None, ranks=None):
     """Post send(cur -> r-1) and recv(nxt <- r+1); returns the requests to wait on.
+    r, P: position and size of the ring; ranks[k] = global rank of ring position k (a
+    sub-ring of a process grid), default k itself.
 
     NCCL moves the device buffers directly (NVLink).  gloo cannot move CUDA tensors point to
     point, so under a gloo group the packed block is staged through host memory -- the
     transport that lets several ranks share one GPU in the tests; the kernels are the same."""
+    to = ranks[(r - 1) % P] if ranks is not None else (r - 1) % P
+    frm = ranks[(r + 1) % P] if ranks is not None else (r + 1) % P
     if cur.is_cuda and dist.get_backend(group) == "gloo":
         host = torch.empty(nxt.shape, dtype=nxt.dtype)
-        ops = [dist.P2POp(dist.isend, cur.contiguous().cpu(), (r - 1) % P, group),
-               dist.P2POp(dist.irecv, host, (r + 1) % P, group)]
+        ops = [dist.P2POp(dist.isend, cur.contiguous().cpu(), to, group),
+               dist.P2POp(dist.irecv, host, frm, group)]
         return [_StagedRecv(dist.batch_isend_irecv(ops), host, nxt)]
-    ops = [dist.P2POp(dist.isend, cur.contiguous(), (r - 1) % P, group),
-           dist.P2POp(dist.irecv, nxt, (r + 1) % P, group)]
+    ops = [dist.P2POp(dist.isend, cur.contiguous(), to, group),
+           dist.P2POp(dist.irecv, nxt, frm, group)]
     return dist.batch_isend_irecv(ops)
 
 
