@@ -6,8 +6,10 @@ python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 One step = one pass of the whole hot path over one synthetic batch resident in HBM:
   2-way (default, BASELINE configs[1] = C2: 20,000 vectors x 50,000 individuals):
-      ccc_pack -> ccc_expand -> ccc_2way_block (fused tally GEMM + CCC epilogue,
-      every unique pair's uint32 tallies + fp64 CCC written to HBM)
+      ccc_expand_codes (a1+a2 fused: unpacked codes -> int8 operand, s, w in one HBM
+      pass) -> ccc_2way_block (fused tally GEMM + CCC epilogue, every unique pair's uint32
+      tallies + fp64 CCC written to HBM); ccc_pack / ccc_expand (the ring's packed path) are
+      timed on their own after the timed region ("hbm_passes")
   3-way (--workload c4: 4,096 x 16,384, 16 stages, FULL output, buffer reused)
   sparse 2-way (--workload c2s: C2's shape, ~15% missing entries):
       ccc_pack -> ccc_expand_sparse -> ccc_2way_sparse_block
@@ -347,6 +349,39 @@ def _ev(kev, k, i, which):
         kev[k][i][which].record(torch.cuda.current_stream())
 
 
+def hbm_passes(codes, packed, N, s, w, n_v, n_f, reps=5):
+    """Rows a1 / a2 on their own (after the timed region, CUDA events, best of `reps`):
+    ccc_pack (1 + 0.25 B / element), ccc_expand of the packed form (0.25 + 1 B / element +
+    20 B / vector) and the fused ccc_expand_codes the single-GPU step runs (1 + 1 B /
+    element + 20 B / vector), each against the measured HBM copy bandwidth."""
+    import torch
+
+    from paper_1705_08213_b200 import ccc
+    pk, _ = peaks()
+    el = n_v * n_f
+    kp = ccc.ccc_k_pad(n_f)
+    out = {}
+    for name, fn, nbytes in (
+            ("pack", lambda: ccc.ccc_pack(codes, packed), el + n_v * ccc.ccc_packed_stride(n_f)),
+            ("expand", lambda: ccc.ccc_expand(packed, n_f, ccc.GAMMA, N, s, w),
+             n_v * ccc.ccc_packed_stride(n_f) + n_v * kp + 20 * n_v),
+            ("expand_codes", lambda: ccc.ccc_expand_codes(codes, ccc.GAMMA, N, s, w), el + n_v * kp + 20 * n_v)):
+        ts = []
+        for _ in range(reps + 1):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        ms = min(ts[1:])
+        gbs = nbytes / (ms / 1e3) / 1e9
+        out[name] = {"ms": ms, "GB_per_s": gbs, "frac_of_hbm": gbs / pk["hbm_gbs"], "bytes": nbytes}
+    out["note"] = ("algorithmic bytes (read + write) per launch / best launch time; the timed step "
+                   "runs expand_codes (a1+a2 fused), pack and expand are the ring's path")
+    return out
+
+
 def run_2way_single(args, wl):  # noqa: C901
     import torch
 
@@ -378,6 +413,16 @@ def run_2way_single(args, wl):  # noqa: C901
             launches[0] += ccc.ccc_last_launch_count()
 
     def step(k):
+        if not (sparse or popcount):
+            # one GPU fed unpacked codes: a1+a2 fused into one HBM pass (ccc_expand_codes);
+            # the 2-bit packed form only matters where it crosses NVLink (the ring)
+            ccc.ccc_expand_codes(codes, ccc.GAMMA, N, s, w)
+            count(k)
+            _ev(kev, k, 0, 0)
+            ccc.ccc_2way_block(N, s, w, 0, 0, n_v, N, s, w, 0, True, n_f, flags, T, C)
+            count(k)
+            _ev(kev, k, 0, 1)
+            return
         ccc.ccc_pack(codes, packed)
         count(k)
         if popcount:
@@ -404,6 +449,8 @@ def run_2way_single(args, wl):  # noqa: C901
     res.update(kernel_ms=sum(k_ms) / args.steps, kernel_ms_best=min(k_ms),
                comparisons=comparisons(2, n_v, n_f), launches=launches[0],
                kernel="popc_tally2_kernel" if popcount else "tally2_kernel", out_bytes=m * 48)
+    if not (sparse or popcount):
+        res["hbm_passes"] = hbm_passes(codes, packed, N, s, w, n_v, n_f)
     if args.cpu:
         cb, idx, To, Co = cpu_baseline(2, n_v, n_f, kind=kind, with_records=True)
         res["cpu_baseline"] = cb
@@ -744,7 +791,7 @@ def line_for(args, wl, r, pk, pk_kind):
         "data": "synthetic", "config": config_of(wl),
         "roofline": roofline(args, wl, r, ms_step, pk, pk_kind),
         "gpu_launches": r["launches"], "clocks": r["clocks"]})
-    for k in ("parity", "e2e", "cpu_baseline"):
+    for k in ("parity", "e2e", "cpu_baseline", "hbm_passes"):
         if k in r:
             out[k] = r[k]
     return out

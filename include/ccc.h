@@ -147,6 +147,15 @@ typedef struct {
 ccc_status ccc_expand(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
                       int8_t* N_d, int32_t* s_d, double* w_d, void* stream);
 
+/* KB-expand straight from unpacked codes (§8(a) a1+a2 fused for a single GPU; Eq.1,
+ * P:270-278): codes_d uint8 [n_v][n_f] (row-major, code = 2 r1 + r2, only the low 2 bits
+ * of each byte are read) -> the same N_d / s_d / w_d as ccc_pack followed by ccc_expand,
+ * in one HBM pass.  The 2-bit packed form exists for storage and for the
+ * multi-GPU ring, where it is what crosses NVLink; one GPU fed unpacked codes skips it.
+ * N_d 128-B aligned; errors as ccc_expand. */
+ccc_status ccc_expand_codes(const uint8_t* codes_d, int64_t n_v, int64_t n_f, double gamma,
+                            int8_t* N_d, int32_t* s_d, double* w_d, void* stream);
+
 /* Whole 2-way problem on one GPU (§8(a) a2-a4): expand packed_d into the workspace,
  * then the persistent tcgen05 kind::i8 tally GEMM G = N N^T over the upper
  * triangle with the fused epilogue

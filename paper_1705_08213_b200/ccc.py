@@ -102,6 +102,7 @@ _SIGS = {
     "ccc_workspace_bytes": (_sz, [_int, _i64, _i64]),
     "ccc_pack": (_int, [_vp, _i64, _i64, _vp, _vp]),
     "ccc_expand": (_int, [_vp, _i64, _i64, _dbl, _vp, _vp, _vp, _vp]),
+    "ccc_expand_codes": (_int, [_vp, _i64, _i64, _dbl, _vp, _vp, _vp, _vp]),
     "ccc_2way": (_int, [_vp, _i64, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _sz, _vp, _vp]),
     "ccc_2way_popcount": (_int, [_vp, _i64, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "ccc_2way_fs_tiles": (_i64, [_i64]),
@@ -344,6 +345,24 @@ def ccc_expand(packed: torch.Tensor, n_f: int, gamma: float = GAMMA, N=None, s=N
     _dev(s, torch.int32, "s", (n_v,))
     _dev(w, torch.float64, "w", (n_v, 2))
     _check(lib().ccc_expand(_p(packed), n_v, n_f, gamma, _p(N), _p(s), _p(w), _stream(stream)))
+    return N, s, w
+
+
+def ccc_expand_codes(codes: torch.Tensor, gamma: float = GAMMA, N=None, s=None, w=None, stream=None):
+    """Unpacked codes [n_v][n_f] -> (N, s, w) in one pass (= ccc_expand(ccc_pack(codes)))."""
+    _dev(codes, torch.uint8, "codes", (None, None))
+    n_v, n_f = codes.shape
+    dev = codes.device
+    if N is None:
+        N = torch.empty((n_v, ccc_k_pad(n_f)), dtype=torch.int8, device=dev)
+    if s is None:
+        s = torch.empty(n_v, dtype=torch.int32, device=dev)
+    if w is None:
+        w = torch.empty((n_v, 2), dtype=torch.float64, device=dev)
+    _dev(N, torch.int8, "N", (n_v, ccc_k_pad(n_f)))
+    _dev(s, torch.int32, "s", (n_v,))
+    _dev(w, torch.float64, "w", (n_v, 2))
+    _check(lib().ccc_expand_codes(_p(codes), n_v, n_f, gamma, _p(N), _p(s), _p(w), _stream(stream)))
     return N, s, w
 
 

@@ -351,6 +351,21 @@ ccc_status ccc_expand(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double 
     return CCC_OK;
 }
 
+ccc_status ccc_expand_codes(const uint8_t* codes_d, int64_t n_v, int64_t n_f, double gamma,
+                            int8_t* N_d, int32_t* s_d, double* w_d, void* stream) {
+    g_launches = 0;
+    CCC_CHECK(check_sizes(n_v, n_f));
+    if (n_v == 0) return CCC_OK;
+    if (!codes_d || !N_d || !s_d || !w_d || !aligned(N_d, 128) || !aligned(s_d, 4) || !aligned(w_d, 8))
+        return fail(CCC_ERR_INVALID_ARGUMENT, "codes_d, N_d (128-B), s_d, w_d must be non-NULL and aligned");
+    int sms;
+    CCC_CHECK(check_device(&sms));
+    CCC_CUDA(ccc::launch_expand_codes(codes_d, n_v, n_f, gamma, N_d, s_d, w_d, sms, (cudaStream_t)stream),
+             "expand_codes launch");
+    g_launches = 1;
+    return CCC_OK;
+}
+
 ccc_status ccc_2way_block(const int8_t* N_a, const int32_t* s_a, const double* w_a, int64_t n_a,
                           int64_t a_row0, int64_t a_lo, int64_t a_hi, const int8_t* N_b,
                           const int32_t* s_b, const double* w_b, int64_t n_b, int64_t b_row0,
@@ -1114,7 +1129,6 @@ ccc_status ccc_2way_host(const uint8_t* codes_h, int64_t n_v, int64_t n_f, doubl
     CCC_CHECK(check_device(&sms));
     uint8_t* base = static_cast<uint8_t*>(dev_ws_d);
     uint8_t* codes = base + L.codes;
-    uint8_t* packed = base + L.packed;
     const WsLayout W = ws_layout(2, n_v, n_f);
     int8_t* N = reinterpret_cast<int8_t*>(base + L.ws + W.N);
     int32_t* s = reinterpret_cast<int32_t*>(base + L.ws + W.s);
@@ -1125,9 +1139,9 @@ ccc_status ccc_2way_host(const uint8_t* codes_h, int64_t n_v, int64_t n_f, doubl
     const bool want_c = out_flags & (CCC_OUT_CCC_F64 | CCC_OUT_CCC_F32);
 
     CCC_CUDA(cudaMemcpyAsync(codes, codes_h, (size_t)n_v * n_f, cudaMemcpyHostToDevice, st), "H2D codes");
-    CCC_CUDA(ccc::launch_pack(codes, n_v, n_f, packed, sms, st), "pack launch");
-    CCC_CUDA(ccc::launch_expand(packed, n_v, n_f, gamma, N, s, w, sms, st), "expand launch");
-    int64_t launches = 2;
+    // unpacked codes straight to the operand (no 2-bit intermediate on one GPU)
+    CCC_CUDA(ccc::launch_expand_codes(codes, n_v, n_f, gamma, N, s, w, sms, st), "expand_codes launch");
+    int64_t launches = 1;
     if (out_flags & CCC_OUT_CHECKSUM) CCC_CUDA(cudaMemsetAsync(ck, 0, 16, st), "memset");
 
     cudaStream_t cs = nullptr;

@@ -12,6 +12,8 @@ cudaError_t launch_pack(const uint8_t* codes, int64_t n_v, int64_t n_f, uint8_t*
                         int num_sms, cudaStream_t stream);
 cudaError_t launch_expand(const uint8_t* packed, int64_t n_v, int64_t n_f, double gamma,
                           int8_t* N, int32_t* s, double* w, int num_sms, cudaStream_t stream);
+cudaError_t launch_expand_codes(const uint8_t* codes, int64_t n_v, int64_t n_f, double gamma, int8_t* N,
+                                int32_t* s, double* w, int num_sms, cudaStream_t stream);
 cudaError_t launch_expand_sparse(const uint8_t* packed, int64_t n_v, int64_t n_f, double gamma,
                                  int8_t* X, int32_t* s, int32_t* c, double* w, int num_sms,
                                  cudaStream_t stream);

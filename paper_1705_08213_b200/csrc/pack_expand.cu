@@ -134,6 +134,77 @@ __global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict_
     }
 }
 
+// Single-GPU fused form of pack + expand: unpacked codes (one byte each, 0..3) straight to
+// the int8 operand N, s and w -- the same outputs as expand_kernel on ccc_pack's output,
+// in one HBM pass (1 B read + 1 B written per element instead of 1 + 0.25 + 0.25 + 1).
+// The 2-bit packed form is what crosses NVLink in the multi-GPU ring; a single GPU whose
+// input arrives unpacked never needs it.  Warp per vector row, warp passes of 128 output
+// words (16 counts each): lane l handles words base + 32 u + l, four 16-B code loads in
+// flight, four coalesced 16-B streaming stores; n = r1 + r2 per byte, s = popcount of the
+// 2-bit codes (the same as popcount of the packed word).
+__device__ __forceinline__ uint32_t count4(uint32_t c) {
+    c &= 0x03030303u;                                   // 4 codes, one per byte
+    return (c & 0x01010101u) + ((c >> 1) & 0x01010101u);
+}
+
+__device__ __forceinline__ uint4 codes16_tail(const uint8_t* row, int64_t n_f, int64_t g) {
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    for (int u = 0; u < 16; ++u) {
+        const int64_t q = g * 16 + u;
+        if (q < n_f) w[u >> 2] |= (uint32_t)row[q] << (8 * (u & 3));
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+__global__ void __launch_bounds__(256) expand_codes_kernel(const uint8_t* __restrict__ codes, int64_t n_v,
+                                                           int64_t n_f, int64_t k_pad, double gamma,
+                                                           int8_t* __restrict__ N, int32_t* __restrict__ s_out,
+                                                           double* __restrict__ w_out) {
+    const uintptr_t base_addr = reinterpret_cast<uintptr_t>(codes);
+    const bool vec16 = (n_f % 16) == 0 && (base_addr % 16) == 0;
+    const bool vec4 = !vec16 && (n_f % 4) == 0 && (base_addr % 4) == 0;
+    const int64_t full = (vec16 || vec4) ? n_f / 16 : 0;   // output words of 16 in-range codes
+    const int64_t groups = k_pad / 16;
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); i < n_v; i += (int64_t)gridDim.x * 8) {
+        const uint8_t* row = codes + i * n_f;
+        const uint4* crow = reinterpret_cast<const uint4*>(row);
+        const uint32_t* crow4 = reinterpret_cast<const uint32_t*>(row);
+        uint4* nrow = reinterpret_cast<uint4*>(N + i * k_pad);
+        auto load16 = [&](int64_t g) -> uint4 {
+            if (vec16) return __ldcs(crow + g);
+            return make_uint4(__ldcs(crow4 + 4 * g), __ldcs(crow4 + 4 * g + 1), __ldcs(crow4 + 4 * g + 2),
+                              __ldcs(crow4 + 4 * g + 3));
+        };
+        auto emit = [&](int64_t g, uint4 c, int32_t& sum) {
+            const uint4 n = make_uint4(count4(c.x), count4(c.y), count4(c.z), count4(c.w));
+            sum += __popc(c.x & 0x03030303u) + __popc(c.y & 0x03030303u) + __popc(c.z & 0x03030303u) +
+                   __popc(c.w & 0x03030303u);
+            __stcs(nrow + g, n);
+        };
+        int32_t sum = 0;
+        int64_t base = 0;
+        for (; base + 128 <= full; base += 128) {
+            uint4 c[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) c[u] = load16(base + 32 * u + lane);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) emit(base + 32 * u + lane, c[u], sum);
+        }
+        for (int64_t g = base + lane; g < groups; g += 32)
+            emit(g, g < full ? load16(g) : codes16_tail(row, n_f, g), sum);
+        for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+        if (lane == 0) {
+            s_out[i] = sum;
+            const double two_nf = 2.0 * (double)n_f;
+            const double f1 = (double)sum / two_nf;                       // Eq.1, a = 1
+            const double f0 = (double)(2 * n_f - (int64_t)sum) / two_nf;  // Eq.1, a = 0
+            w_out[2 * i + 0] = 1.0 - gamma * f0;
+            w_out[2 * i + 1] = 1.0 - gamma * f1;
+        }
+    }
+}
+
 // Sparse (missing-data) mode, §7 item 1, reading A-17: the code
 // (1,0) marks a missing entry.  One warp per vector i writes two operand rows of the
 // group-interleaved matrix X (groups of 16 vectors: 16 rows n, then 16 rows v):
@@ -314,6 +385,16 @@ cudaError_t launch_expand(const uint8_t* packed, int64_t n_v, int64_t n_f, doubl
     if (blocks < 1) blocks = 1;
     expand_kernel<<<(int)blocks, 256, 0, stream>>>(reinterpret_cast<const uint32_t*>(packed),
                                                    n_v, n_f, wpr, k_pad, gamma, N, s, w);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_expand_codes(const uint8_t* codes, int64_t n_v, int64_t n_f, double gamma, int8_t* N,
+                                int32_t* s, double* w, int num_sms, cudaStream_t stream) {
+    const int64_t k_pad = (n_f + 127) / 128 * 128;
+    const int64_t rows_blocks = (n_v + 7) / 8;   // a warp per row, 8 per CTA
+    int64_t blocks = rows_blocks < (int64_t)num_sms * 8 ? rows_blocks : (int64_t)num_sms * 8;
+    if (blocks < 1) blocks = 1;
+    expand_codes_kernel<<<(int)blocks, 256, 0, stream>>>(codes, n_v, n_f, k_pad, gamma, N, s, w);
     return cudaGetLastError();
 }
 

@@ -63,6 +63,27 @@ def test_pack_expand(n_v, n_f):
     np.testing.assert_array_equal(s.cpu().numpy(), S[:, 1])
     f = oracle.frequencies(codes)
     np.testing.assert_allclose(w.cpu().numpy(), 1.0 - oracle.GAMMA * f, rtol=1e-15, atol=0)
+    # the single-GPU fused pass (unpacked codes -> N, s, w) is bit-identical to pack + expand
+    N2, s2, w2 = ccc.ccc_expand_codes(codes.cuda())
+    assert bool((N2 == N).all()) and bool((s2 == s).all()) and bool((w2 == w).all())
+
+
+@pytest.mark.parametrize("n_v,n_f,offset", [(9, 1, 1), (33, 65, 3), (40, 1000, 0), (17, 1024, 4), (8, 4097, 2)])
+def test_expand_codes_alignment_and_high_bits(n_v, n_f, offset):
+    """ccc_expand_codes on rows that are not 16-B aligned (odd n_f, a base offset) and on
+    bytes with garbage above the 2 code bits: N, s, w as the oracle's Eq.1 of the codes."""
+    codes = _codes("random", n_v, n_f, seed=n_f + offset)
+    junk = torch.randint(0, 64, (n_v, n_f), dtype=torch.uint8) << 2
+    buf = torch.empty(n_v * n_f + offset, dtype=torch.uint8, device="cuda")
+    view = buf[offset:].view(n_v, n_f)
+    view.copy_((codes | junk).cuda())
+    N, s, w = ccc.ccc_expand_codes(view)
+    n1 = ((codes.numpy() >> 1) & 1) + (codes.numpy() & 1)
+    Nn = N.cpu().numpy()
+    np.testing.assert_array_equal(Nn[:, :n_f], n1)
+    assert np.all(Nn[:, n_f:] == 0)
+    np.testing.assert_array_equal(s.cpu().numpy(), oracle.allele_sums(codes)[:, 1])
+    np.testing.assert_allclose(w.cpu().numpy(), 1.0 - oracle.GAMMA * oracle.frequencies(codes), rtol=1e-15, atol=0)
 
 
 # ------------------------------------------------------------------- 2-way, full
