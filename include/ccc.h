@@ -417,15 +417,17 @@ ccc_status ccc_2way_sparse(const uint8_t* packed_d, int64_t n_v, int64_t n_f, do
  * vector's present entries, CCC = f_ijk (1-g f_i(a))(1-g f_j(b))(1-g f_k(c)), 0 if
  * c_ijk = 0.  With n = allele-1 count (0 where missing) and v = [present],
  * rho(1) = n and rho(0) = 2v - n, so every cell is a signed sum of the 8 trilinear forms
- * sum_q x_i x_j x_k (x in {n, v}); each form is one pass of the Hadamard pivot GEMM
- * (tally3) over the N_s / V operands -- 8 int8 MACs per comparison.  Passes 0..6 store
- * their form (uint32 per record) in the caller's scratch; pass 7 (v v v = c_ijk) reads
- * them in its epilogue and writes the records.
- * prepare: packed_d -> ws_d (>= ccc_sparse3_workspace_bytes): N_s, V [n_v][K_pad] int8,
- *          s_i, c_i int32, w_i(a) double (sparse weights, gamma given here).
+ * sum_q x_i x_j x_k (x in {n, v}).  All 8 come out of ONE tcgen05 GEMM per (pivot, 64 j's,
+ * 128 k's): B = the group-interleaved X rows (n and v) of the k's, A = the X rows of the
+ * j's weighted by the pivot's n_i and by its v_i, stacked -- 8 int8 MACs per comparison,
+ * no form leaves the chip (kernel tally3s.cu).
+ * prepare: packed_d -> ws_d (>= ccc_sparse3_workspace_bytes): X [ccc_sparse_rows(n_v)]
+ *          [K_pad] int8 (ccc_expand_sparse's layout), s_i, c_i int32, w_i(a) double
+ *          (sparse weights, gamma given here).
  * stage:   records of stage `stage` of n_stages (ccc_stage_range), outputs as
  *          ccc_3way_stage (a-major cells, lexicographic triples minus the stage's first
- *          record); scratch_d >= ccc_3way_sparse_scratch_bytes(n_v, n_stages, stage). */
+ *          record).  ccc_3way_sparse_scratch_bytes returns 0: scratch_d / scratch_bytes
+ *          are unused (kept for ABI stability; NULL is fine). */
 size_t     ccc_sparse3_workspace_bytes(int64_t n_v, int64_t n_f);
 size_t     ccc_3way_sparse_scratch_bytes(int64_t n_v, int64_t n_stages, int64_t stage);
 ccc_status ccc_3way_sparse_prepare(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,

@@ -764,7 +764,7 @@ def three_way(codes: torch.Tensor, gamma: float = GAMMA, out_flags: int = OUT_TA
 
 # ------------------------------------------------------------- f1: sparse 3-way
 def ccc_3way_sparse_prepare(packed: torch.Tensor, n_f: int, gamma: float = GAMMA, ws=None, stream=None):
-    """Expand for the sparse 3-way mode: the workspace (N_s, V, s, c, w)."""
+    """Expand for the sparse 3-way mode: the workspace (X interleaved, s, c, w)."""
     n_v = _packed(packed, n_f)
     if ws is None:
         ws = torch.empty(max(256, lib().ccc_sparse3_workspace_bytes(n_v, n_f)), dtype=torch.uint8,
@@ -777,7 +777,7 @@ def ccc_3way_sparse_prepare(packed: torch.Tensor, n_f: int, gamma: float = GAMMA
 def ccc_3way_sparse_stage(n_v: int, n_f: int, n_stages: int, stage: int, ws: torch.Tensor,
                           out_flags: int = OUT_TALLY | OUT_CCC_F64, tallies=None, ccc=None, checksum=None,
                           scratch=None, gamma: float = GAMMA, stream=None):
-    """One stage of the sparse 3-way records (8 pivot-GEMM passes)."""
+    """One stage of the sparse 3-way records (one pivot GEMM with all 8 forms)."""
     rc = ccc_stage_range(n_v, n_stages, stage)[3]
     T, C, ck = _outputs(rc, 8, out_flags, ws.device, tallies, ccc, checksum)
     nb = lib().ccc_3way_sparse_scratch_bytes(n_v, n_stages, stage)

@@ -704,17 +704,15 @@ ccc_status ccc_3way_stage(int64_t n_v, int64_t n_f, double gamma, int64_t n_stag
 
 // ---------------------------------------------------------------- f1: sparse 3-way
 namespace {
+// workspace: the group-interleaved X of the sparse mode (ccc_expand_sparse's layout), s, c, w
 struct Sp3Layout {
-    size_t Ns = 0, V = 0, s = 0, c = 0, w = 0, total = 0;
+    size_t X = 0, s = 0, c = 0, w = 0, total = 0;
 };
 Sp3Layout sp3_layout(int64_t n_v, int64_t n_f) {
     Sp3Layout L;
     size_t off = 0;
-    const size_t mat = al256((size_t)n_v * (size_t)kpad_of(n_f));
-    L.Ns = off;
-    off += mat;
-    L.V = off;
-    off += mat;
+    L.X = off;
+    off += al256((size_t)(2 * ((n_v + 15) / 16 * 16)) * (size_t)kpad_of(n_f));
     L.s = off;
     off += al256((size_t)n_v * 4);
     L.c = off;
@@ -732,9 +730,10 @@ size_t ccc_sparse3_workspace_bytes(int64_t n_v, int64_t n_f) {
 }
 
 size_t ccc_3way_sparse_scratch_bytes(int64_t n_v, int64_t n_stages, int64_t stage) {
-    int64_t rng[4];
-    if (n_v < 3 || ccc_stage_range(n_v, n_stages, stage, rng) != CCC_OK) return 0;
-    return (size_t)7 * (size_t)rng[3] * sizeof(uint32_t);
+    (void)n_v;
+    (void)n_stages;
+    (void)stage;
+    return 0;   // single pass: no stored forms
 }
 
 ccc_status ccc_3way_sparse_prepare(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
@@ -750,11 +749,10 @@ ccc_status ccc_3way_sparse_prepare(const uint8_t* packed_d, int64_t n_v, int64_t
     int sms;
     CCC_CHECK(check_device(&sms));
     uint8_t* ws = static_cast<uint8_t*>(ws_d);
-    CCC_CUDA(ccc::launch_expand_sparse3(packed_d, n_v, n_f, gamma, reinterpret_cast<int8_t*>(ws + L.Ns),
-                                        reinterpret_cast<int8_t*>(ws + L.V), reinterpret_cast<int32_t*>(ws + L.s),
-                                        reinterpret_cast<int32_t*>(ws + L.c), reinterpret_cast<double*>(ws + L.w),
-                                        sms, (cudaStream_t)stream),
-             "expand_sparse3 launch");
+    CCC_CUDA(ccc::launch_expand_sparse(packed_d, n_v, n_f, gamma, reinterpret_cast<int8_t*>(ws + L.X),
+                                       reinterpret_cast<int32_t*>(ws + L.s), reinterpret_cast<int32_t*>(ws + L.c),
+                                       reinterpret_cast<double*>(ws + L.w), sms, (cudaStream_t)stream),
+             "expand_sparse launch");
     g_launches = 1;
     return CCC_OK;
 }
@@ -764,6 +762,8 @@ ccc_status ccc_3way_sparse_stage(int64_t n_v, int64_t n_f, double gamma, int64_t
                                  void* ws_d, size_t ws_bytes, void* scratch_d, size_t scratch_bytes,
                                  void* stream) {
     (void)gamma;   // the weights were formed by ccc_3way_sparse_prepare
+    (void)scratch_d;
+    (void)scratch_bytes;   // kept for ABI stability; the single-pass kernel stores no forms
     g_launches = 0;
     CCC_CHECK(check_sizes(n_v, n_f));
     if (out_flags & ~15u) return fail(CCC_ERR_INVALID_ARGUMENT, "unknown out_flags bits");
@@ -774,55 +774,22 @@ ccc_status ccc_3way_sparse_stage(int64_t n_v, int64_t n_f, double gamma, int64_t
     const Sp3Layout L = sp3_layout(n_v, n_f);
     if (!ws_d || !aligned(ws_d, 256)) return fail(CCC_ERR_INVALID_ARGUMENT, "ws_d must be 256-B aligned");
     if (ws_bytes < L.total) return fail(CCC_ERR_WORKSPACE, "workspace too small (see ccc_sparse3_workspace_bytes)");
-    if (!scratch_d || !aligned(scratch_d, 16) || scratch_bytes < (size_t)7 * (size_t)rng[3] * 4)
-        return fail(CCC_ERR_WORKSPACE, "scratch too small (see ccc_3way_sparse_scratch_bytes)");
     int sms;
     CCC_CHECK(check_device(&sms));
     uint8_t* ws = static_cast<uint8_t*>(ws_d);
     const int64_t k_pad = kpad_of(n_f);
-    const int8_t* mats[2] = {reinterpret_cast<const int8_t*>(ws + L.Ns), reinterpret_cast<const int8_t*>(ws + L.V)};
-    const int32_t* s = reinterpret_cast<const int32_t*>(ws + L.s);
-    const double* w = reinterpret_cast<const double*>(ws + L.w);
-    CUtensorMap tm[2];
-    CCC_CHECK(make_tmap(&tm[0], mats[0], n_v, k_pad, 128));
-    CCC_CHECK(make_tmap(&tm[1], mats[1], n_v, k_pad, 128));
-    // passes f = 4 x_p + 2 x_m + x_n (x = 0: n, 1: v): forms 0..6 stored, form 7 (v v v =
-    // c_pmn) computed last and combined with the stored ones into the records
-    for (int f = 0; f < 8; ++f) {
-        const int xp = (f >> 2) & 1, xm = (f >> 1) & 1, xn = f & 1;
-        ccc::Tally3Args a{};
-        a.bp = ccc::Blk3{mats[xp], s, w, n_v, 0};
-        a.bm = ccc::Blk3{mats[xm], s, w, n_v, 0};
-        a.bn = ccc::Blk3{mats[xn], s, w, n_v, 0};
-        a.p_lo = rng[0];
-        a.p_hi = rng[1];
-        a.m_lo = 0;
-        a.m_hi = n_v;
-        a.n_lo = 0;
-        a.n_hi = n_v;
-        a.same_pm = a.same_mn = 1;
-        a.order = 0;
-        a.layout = 0;
-        a.G = nullptr;
-        a.ldG = n_v;
-        a.rec_base = rng[2];
-        a.k_pad = k_pad;
-        a.n_f = (int32_t)n_f;
-        a.k_blocks = (int32_t)(k_pad / ccc::kBK);
-        a.out_flags = (int32_t)out_flags;
-        a.exact23 = 0;
-        a.inv_d = 0.0;
-        a.tallies = tallies_d;
-        a.ccc = ccc_d;
-        a.checksum = reinterpret_cast<unsigned long long*>(checksum_d);
-        a.forms = static_cast<uint32_t*>(scratch_d);
-        a.form_stride = rng[3];
-        a.form_self = f;
-        a.mode = f < 7 ? 1 : 2;
-        int64_t units = 0;
-        CCC_CUDA(ccc::launch_tally3(tm[xm], tm[xn], a, sms, (cudaStream_t)stream, &units), "tally3 sparse launch");
-        if (units) ++g_launches;
-    }
+    const int8_t* X = reinterpret_cast<const int8_t*>(ws + L.X);
+    const int64_t rows = 2 * ((n_v + 15) / 16 * 16);
+    CUtensorMap tmS, tmB;
+    CCC_CHECK(make_tmap(&tmS, X, rows, k_pad, 64));    // 64 X rows = 32 m's x {n, v}
+    CCC_CHECK(make_tmap(&tmB, X, rows, k_pad, 128));   // 128 X rows = 64 n's x {n, v}
+    int64_t units = 0;
+    CCC_CUDA(ccc::launch_tally3_sparse(tmS, tmB, X, reinterpret_cast<const double*>(ws + L.w), n_v, rng[0], rng[1],
+                                       rng[2], k_pad, out_flags, tallies_d, ccc_d,
+                                       reinterpret_cast<unsigned long long*>(checksum_d), sms,
+                                       (cudaStream_t)stream, &units),
+             "tally3 sparse launch");
+    if (units) g_launches = 1;
     return CCC_OK;
 }
 

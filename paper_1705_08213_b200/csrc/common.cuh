@@ -200,8 +200,7 @@ struct Tally3Args {
     Compact cmp;               // used when compact != 0
     int32_t compact, pad4_;
     unsigned long long* trace; // optional per-unit %globaltimer trace (diagnostics)
-    // sparse 3-way (f1): mode 1 stores this pass's form at forms[form_self * form_stride + rec];
-    // mode 2 reads forms 0..6 there and writes the records
+    // paper route (f4 ii): mode 1 stores this pass's form at forms[form_self * form_stride + rec]
     uint32_t* forms;
     int64_t form_stride;
     int32_t form_self, mode;

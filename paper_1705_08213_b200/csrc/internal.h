@@ -17,9 +17,6 @@ cudaError_t launch_expand_codes(const uint8_t* codes, int64_t n_v, int64_t n_f, 
 cudaError_t launch_expand_sparse(const uint8_t* packed, int64_t n_v, int64_t n_f, double gamma,
                                  int8_t* X, int32_t* s, int32_t* c, double* w, int num_sms,
                                  cudaStream_t stream);
-cudaError_t launch_expand_sparse3(const uint8_t* packed, int64_t n_v, int64_t n_f, double gamma, int8_t* Ns,
-                                  int8_t* V, int32_t* s, int32_t* c, double* w, int num_sms,
-                                  cudaStream_t stream);
 cudaError_t launch_expand_masks(const uint8_t* packed, int64_t n_v, int64_t n_f, int8_t* M, int32_t* cnt,
                                 int num_sms, cudaStream_t stream);
 int tally2_b_box_rows();  // B rows per CTA per TMA box (256 single CTA, 128 CTA pair)
@@ -35,6 +32,11 @@ cudaError_t launch_tally2(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
 cudaError_t launch_tally3(const CUtensorMap& tmA, const CUtensorMap& tmB, const Tally3Args& a,
                           int num_sms, cudaStream_t stream, int64_t* n_units_out);
 
+cudaError_t launch_tally3_sparse(const CUtensorMap& tmSrc, const CUtensorMap& tmB, const int8_t* X,
+                                 const double* w, int64_t n_v, int64_t p_lo, int64_t p_hi, int64_t rec_base,
+                                 int64_t k_pad, uint32_t out_flags, uint32_t* tallies, void* ccc,
+                                 unsigned long long* checksum, int num_sms, cudaStream_t stream,
+                                 int64_t* n_units_out);
 cudaError_t launch_popc_2way(const uint8_t* packed, int64_t n_v, int64_t n_f, double gamma, uint32_t flags,
                              uint32_t* tallies, void* ccc, unsigned long long* checksum, int32_t* s,
                              double* w, int num_sms, cudaStream_t stream);

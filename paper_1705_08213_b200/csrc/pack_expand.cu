@@ -215,10 +215,8 @@ __global__ void __launch_bounds__(256) expand_codes_kernel(const uint8_t* __rest
 __global__ void __launch_bounds__(256) expand_sparse_kernel(
     const uint32_t* __restrict__ packed, int64_t n_v, int64_t n_v16, int64_t n_f,
     int64_t words_per_row, int64_t k_pad, double gamma, int8_t* __restrict__ X,
-    int32_t* __restrict__ s_out, int32_t* __restrict__ c_out, double* __restrict__ w_out,
-    int8_t* __restrict__ V) {
-    // V != NULL: the separate layout of the 3-way sparse mode -- n in row i of X, the
-    // presence bits in row i of V (n_v16 = n_v, no group interleaving)
+    int32_t* __restrict__ s_out, int32_t* __restrict__ c_out, double* __restrict__ w_out) {
+    // X is the operand of both sparse modes (2-way tally2, 3-way tally3s)
     // a warp per vector (8 per CTA), warp passes of 128 packed words as in expand_kernel
     const int64_t groups = k_pad / 16;
     const int lane = threadIdx.x & 31;
@@ -226,8 +224,8 @@ __global__ void __launch_bounds__(256) expand_sparse_kernel(
         const bool real = i < n_v;
         const uint32_t* prow = packed + i * words_per_row;
         const int64_t xr = 32 * (i / 16) + (i % 16);
-        uint4* nrow = reinterpret_cast<uint4*>(V ? X + i * k_pad : X + xr * k_pad);
-        uint4* vrow = reinterpret_cast<uint4*>(V ? V + i * k_pad : X + (xr + 16) * k_pad);
+        uint4* nrow = reinterpret_cast<uint4*>(X + xr * k_pad);
+        uint4* vrow = reinterpret_cast<uint4*>(X + (xr + 16) * k_pad);
         int32_t sum = 0, cnt = 0;
         for (int64_t base = 0; base < groups; base += 128) {
             uint32_t pw[4];
@@ -290,22 +288,10 @@ cudaError_t launch_expand_sparse(const uint8_t* packed, int64_t n_v, int64_t n_f
     int64_t blocks = rows_blocks < (int64_t)num_sms * 8 ? rows_blocks : (int64_t)num_sms * 8;
     if (blocks < 1) blocks = 1;
     expand_sparse_kernel<<<(int)blocks, 256, 0, stream>>>(
-        reinterpret_cast<const uint32_t*>(packed), n_v, n_v16, n_f, wpr, k_pad, gamma, X, s, c, w, nullptr);
+        reinterpret_cast<const uint32_t*>(packed), n_v, n_v16, n_f, wpr, k_pad, gamma, X, s, c, w);
     return cudaGetLastError();
 }
 
-cudaError_t launch_expand_sparse3(const uint8_t* packed, int64_t n_v, int64_t n_f, double gamma, int8_t* Ns,
-                                  int8_t* V, int32_t* s, int32_t* c, double* w, int num_sms,
-                                  cudaStream_t stream) {
-    const int64_t wpr = (n_f + 63) / 64 * 4;
-    const int64_t k_pad = (n_f + 127) / 128 * 128;
-    const int64_t rows_blocks = (n_v + 7) / 8;   // a warp per row, 8 per CTA
-    int64_t blocks = rows_blocks < (int64_t)num_sms * 8 ? rows_blocks : (int64_t)num_sms * 8;
-    if (blocks < 1) blocks = 1;
-    expand_sparse_kernel<<<(int)blocks, 256, 0, stream>>>(
-        reinterpret_cast<const uint32_t*>(packed), n_v, n_v, n_f, wpr, k_pad, gamma, Ns, s, c, w, V);
-    return cudaGetLastError();
-}
 
 // f4(ii), the paper's 3-way route (Table 1, P:457-516 with reading A-3): one int8 mask row
 // per class xi of the pivot's genotype -- xi = 1: (0,0), xi = 2: heterozygote, xi = 3:

@@ -17,6 +17,18 @@ __device__ __forceinline__ uint32_t lane_id() {
     return l;
 }
 
+// One lane of the (converged) warp, chosen by elect.sync.  The single-thread issuers
+// (TMA, tcgen05.mma, commit) run their loops with the whole warp so every address and
+// descriptor is warp-uniform (uniform registers, no per-instruction R2UR / ELECT loops)
+// and only the issuing instruction is predicated on the elected lane.
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 // ---------------------------------------------------------------- mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));

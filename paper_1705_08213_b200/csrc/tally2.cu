@@ -138,8 +138,9 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     sch.init(args.a_lo, args.nA, args.nB, args.diag, C::kTileM, args.sup_rows, args.sup_cols);
 
     if (warp == 0) {
-        if (lane == 0) {
+        {
             // ------------------------------------------------------------ TMA producer
+            // whole warp walks the loop (uniform coordinates); one elected lane issues
             uint32_t stage = 0, phase = 0;
             const uint64_t pol = policy_evict_last();
             for (int64_t t = unit0;; t += units) {
@@ -147,7 +148,7 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 if ((args.t_hi > 0 && t >= args.t_hi) || !sch.get(t, bm, bn)) break;
                 const int32_t arow = (int32_t)(args.a_lo + (int64_t)bm * C::kTileM + rank * 128);
                 const int32_t brow = (int32_t)sch.b_lo + bn * kBN + (int32_t)rank * C::kBRows;
-                if (args.trace && rank == 0) args.trace[8 * t + 6] = globaltimer();
+                if (args.trace && rank == 0 && lane == 0) args.trace[8 * t + 6] = globaltimer();
                 // odd waves walk K backwards: they start on the k-blocks the previous wave
                 // touched last, which are still in L2 (the MMA accumulates in any order)
                 const bool rev = args.k_alternate && (((t - unit0) / units) & 1);
@@ -156,33 +157,39 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sa = smA + stage * C::kABytes;
                     uint8_t* sb = smB + stage * C::kBBytes;
-                    if constexpr (kPair == 2) {
-                        const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
-                        if (rank == 0)
-                            mbar_arrive_expect_tx(&full[stage], 2 * (C::kABytes + C::kBBytes));
-                        else
-                            mbar_arrive_cluster(fb);
-                        tma_load_2d_pair(sa, &tmA, fb, kb * kBK, arow, pol);
-                        tma_load_2d_pair(sb, &tmB, fb, kb * kBK, brow, pol);
-                    } else {
-                        mbar_arrive_expect_tx(&full[stage], C::kABytes + C::kBBytes);
-                        tma_load_2d(sa, &tmA, &full[stage], kb * kBK, arow, pol);
-                        tma_load_2d(sb, &tmB, &full[stage], kb * kBK, brow, pol);
+                    if (elect_one()) {
+                        if constexpr (kPair == 2) {
+                            const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+                            if (rank == 0)
+                                mbar_arrive_expect_tx(&full[stage], 2 * (C::kABytes + C::kBBytes));
+                            else
+                                mbar_arrive_cluster(fb);
+                            tma_load_2d_pair(sa, &tmA, fb, kb * kBK, arow, pol);
+                            tma_load_2d_pair(sb, &tmB, fb, kb * kBK, brow, pol);
+                        } else {
+                            mbar_arrive_expect_tx(&full[stage], C::kABytes + C::kBBytes);
+                            tma_load_2d(sa, &tmA, &full[stage], kb * kBK, arow, pol);
+                            tma_load_2d(sb, &tmB, &full[stage], kb * kBK, brow, pol);
+                        }
                     }
+                    __syncwarp();
                     if (++stage == C::kStages) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && rank == 0) {
+        if (rank == 0) {
             // ------------------------------------------------------------ MMA issuer
+            // The whole warp walks the loop (descriptors stay warp-uniform, in uniform
+            // registers); one elected lane issues each tcgen05.mma / commit.
             constexpr uint32_t idesc = idesc_i8(C::kTileM, kBN);
             uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-            const uint32_t a0 = smem_u32(smA), b0 = smem_u32(smB);
+            const uint64_t a_desc0 = smem_desc_sw128(smem_u32(smA));
+            const uint64_t b_desc0 = smem_desc_sw128(smem_u32(smB));
             for (int64_t t = unit0;; t += units) {
                 int32_t bm, bn;
                 if ((args.t_hi > 0 && t >= args.t_hi) || !sch.get(t, bm, bn)) break;
-                unsigned long long* tr = args.trace ? args.trace + 8 * t : nullptr;
+                unsigned long long* tr = (args.trace && lane == 0) ? args.trace + 8 * t : nullptr;
                 if (tr) tr[0] = globaltimer();
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
@@ -191,20 +198,29 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint32_t sa = a0 + stage * C::kABytes, sb = b0 + stage * C::kBBytes;
+                    // descriptor start address is in 16-B units in the low bits: advancing
+                    // the operand by x bytes adds x >> 4 (no carry out of the 14-bit field
+                    // inside the CTA's shared window)
+                    const uint64_t ad = a_desc0 + ((stage * C::kABytes) >> 4);
+                    const uint64_t bd = b_desc0 + ((stage * C::kBBytes) >> 4);
+                    if (elect_one()) {
 #pragma unroll
-                    for (int k = 0; k < kBK / kUMMA_K; ++k) {
-                        const uint64_t ad = smem_desc_sw128(sa + k * kUMMA_K);
-                        const uint64_t bd = smem_desc_sw128(sb + k * kUMMA_K);
-                        if constexpr (kPair == 2) mma_i8_pair(d, ad, bd, idesc, (kb | k) != 0);
-                        else mma_i8(d, ad, bd, idesc, (kb | k) != 0);
+                        for (int k = 0; k < kBK / kUMMA_K; ++k) {
+                            if constexpr (kPair == 2)
+                                mma_i8_pair(d, ad + (k * kUMMA_K >> 4), bd + (k * kUMMA_K >> 4), idesc, (kb | k) != 0);
+                            else mma_i8(d, ad + (k * kUMMA_K >> 4), bd + (k * kUMMA_K >> 4), idesc, (kb | k) != 0);
+                        }
+                        if constexpr (kPair == 2) mma_commit_pair(&empty[stage], 3);
+                        else mma_commit(&empty[stage]);
                     }
-                    if constexpr (kPair == 2) mma_commit_pair(&empty[stage], 3);
-                    else mma_commit(&empty[stage]);
+                    __syncwarp();
                     if (++stage == C::kStages) { stage = 0; phase ^= 1; }
                 }
-                if constexpr (kPair == 2) mma_commit_pair(&tfull[acc], 3);
-                else mma_commit(&tfull[acc]);
+                if (elect_one()) {
+                    if constexpr (kPair == 2) mma_commit_pair(&tfull[acc], 3);
+                    else mma_commit(&tfull[acc]);
+                }
+                __syncwarp();
                 if (tr) tr[2] = globaltimer();
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }

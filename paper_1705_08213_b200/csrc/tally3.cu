@@ -22,8 +22,8 @@
 // 2..9 epilogue (2 per TMEM lane quadrant), 10..13 transform (A <- A o n_p in shared
 // memory, in place, then fence.proxy.async so the tensor core sees it).
 // Template modes beyond the dense CCC epilogue (kMode): 1 = store this pass's raw form
-// G3 (sparse 3-way form passes, paper-route masked passes), 2 = sparse final pass,
-// 3 = paper-route final pass; kFull / kF32 = flag-free FULL epilogues (gamma = 2/3).
+// G3 (the paper-route masked passes), 3 = paper-route final pass; kFull / kF32 = flag-free
+// FULL epilogues (gamma = 2/3).  The sparse 3-way mode has its own kernel (tally3s.cu).
 #include "sm100.cuh"
 #include "common.cuh"
 #include "internal.h"
@@ -197,75 +197,6 @@ __device__ __forceinline__ void emit3(const Tally3Args& a, uint64_t key, const u
     }
 }
 
-// Sparse (missing-data) 3-way record, reading A-17 for triples (oracle_sparse_triples):
-// with n = allele-1 count (0 where missing) and v = [present], rho(1) = n, rho(0) = 2v - n,
-// so T(a,b,c) = sum_q rho_p(a) rho_m(b) rho_n(c) expands into the 8 trilinear forms
-// F[4 x_p + 2 x_m + x_n] = sum_q x_p x_m x_n (x = 0: n, 1: v); c_pmn = F[7] = #fields
-// where all three are present; CCC = T / (8 c_pmn) w_p(a) w_m(b) w_n(c) (0 if c_pmn = 0).
-// F[7] is this (final) pass's accumulator, F[0..6] were stored by the form passes.
-template <class O>
-__device__ __forceinline__ void sparse3_record(const Tally3Args& a, bool ok, uint32_t g3, int64_t rec,
-                                               const double (&wpm)[4], double wn0, double wn1, int64_t gp,
-                                               int64_t gm, int64_t gn, bool want_t, bool want_c64,
-                                               bool want_c32, bool want_ck, unsigned long long& ck_lo,
-                                               unsigned long long& ck_hi) {
-    uint32_t F[8];
-    const int64_t rc = ok ? rec : 0;
-#pragma unroll
-    for (int f = 0; f < 7; ++f) F[f] = ok ? __ldg(a.forms + (int64_t)f * a.form_stride + rc) : 0u;
-    F[7] = g3;
-    uint32_t t[8];
-#pragma unroll
-    for (int cell = 0; cell < 8; ++cell) {
-        const int al[3] = {(cell >> 2) & 1, (cell >> 1) & 1, cell & 1};
-        uint32_t acc = 0;
-#pragma unroll
-        for (int f = 0; f < 8; ++f) {
-            const int x[3] = {(f >> 2) & 1, (f >> 1) & 1, f & 1};
-            int coef = 1;
-#pragma unroll
-            for (int r = 0; r < 3; ++r) {
-                // allele 1 uses n only (+1); allele 0 = 2v - n: v -> +2, n -> -1
-                if (al[r] == 1) coef *= (x[r] == 0) ? 1 : 0;
-                else coef *= (x[r] == 1) ? 2 : -1;
-            }
-            if (coef) acc += (uint32_t)coef * F[f];
-        }
-        t[cell] = acc;
-    }
-    const uint32_t cpmn = F[7];
-    double cr[8];
-    const double inv = cpmn ? 1.0 / (8.0 * (double)cpmn) : 0.0;
-#pragma unroll
-    for (int ab = 0; ab < 4; ++ab) {
-        cr[2 * ab + 0] = (double)t[2 * ab + 0] * inv * wpm[ab] * wn0;
-        cr[2 * ab + 1] = (double)t[2 * ab + 1] * inv * wpm[ab] * wn1;
-    }
-    uint32_t tc[8];
-    double cc[8];
-    perm_cells<O::R0, O::R1, O::R2>(t, tc);
-    perm_cells<O::R0, O::R1, O::R2>(cr, cc);
-    if (want_t)
-        stg_256_u32_if(ok, a.tallies + 8 * rec, tc[0], tc[1], tc[2], tc[3], tc[4], tc[5], tc[6], tc[7]);
-    if (want_c64) {
-        double* q = reinterpret_cast<double*>(a.ccc) + 8 * rec;
-        stg_256_f64_if(ok, q, cc[0], cc[1], cc[2], cc[3]);
-        stg_256_f64_if(ok, q + 4, cc[4], cc[5], cc[6], cc[7]);
-    } else if (want_c32) {
-        float* q = reinterpret_cast<float*>(a.ccc) + 8 * rec;
-        stg_256_u32_if(ok, q, __float_as_uint((float)cc[0]), __float_as_uint((float)cc[1]),
-                       __float_as_uint((float)cc[2]), __float_as_uint((float)cc[3]),
-                       __float_as_uint((float)cc[4]), __float_as_uint((float)cc[5]),
-                       __float_as_uint((float)cc[6]), __float_as_uint((float)cc[7]));
-    }
-    if (want_ck && ok) {
-        const int64_t g[3] = {gp, gm, gn};
-        ck_fold3(ck_lo, ck_hi,
-                 (3ull << 60) | ((uint64_t)g[O::R0] << 40) | ((uint64_t)g[O::R1] << 20) | (uint64_t)g[O::R2],
-                 tc);
-    }
-}
-
 // f4(ii): the paper's 3-way route on the tensor pipe (§3.2, Table 1 P:457-516,
 // masked tallies P:518-525, reconstruction P:527-560 under readings A-1..A-3), pivot on
 // the first index: with the class masks of the pivot's genotype (xi = 1: (0,0),
@@ -334,8 +265,7 @@ __device__ __forceinline__ void paper3_record(const Tally3Args& a, bool ok, uint
     }
 }
 
-// kMode: 0 dense CCC; 1 sparse form pass (store the raw trilinear form G3 of this pass);
-// 2 sparse final pass (read the 7 stored forms, build the sparse tallies + CCC);
+// kMode: 0 dense CCC; 1 form pass (store the raw masked form G3 of this pass);
 // 3 paper-route final pass (f4 ii: read 2 stored masked forms + masked marginals)
 template <int kOrder, bool kExact, bool kCompact, bool kFull, int kMode = 0, bool kF32 = false>
 __global__ void __launch_bounds__(kThreads3, 1)
@@ -386,8 +316,9 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     sch.init(args);
 
     if (warp == 0) {
-        if (lane == 0) {
+        {
             // ---------------------------------------------------------- TMA producer
+            // whole warp walks the loop (uniform coordinates); one elected lane issues
             uint32_t stage = 0, phase = 0;
             const uint64_t pol = policy_evict_last();
             for (int64_t u = unit0;; u += units) {
@@ -400,37 +331,45 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
                     mbar_wait_sleep(&empty[stage], phase ^ 1);
 #ifdef CCC_D3_NOTMA
-                    mbar_arrive(&aload[stage]);
-                    if (rank == 0) mbar_arrive(&ready[stage]);
-                    else mbar_arrive_cluster(ready_leader + stage * 8u);
+                    if (elect_one()) {
+                        mbar_arrive(&aload[stage]);
+                        if (rank == 0) mbar_arrive(&ready[stage]);
+                        else mbar_arrive_cluster(ready_leader + stage * 8u);
+                    }
+                    __syncwarp();
                     if (++stage == kStages3) { stage = 0; phase ^= 1; }
                     continue;
 #endif
-                    // own A half + pivot chunk -> local barrier (the transform warps wait)
-                    mbar_arrive_expect_tx(&aload[stage], kABytes3 + kPivBytes);
-                    tma_load_2d(smA + stage * kABytes3, &tmA, &aload[stage], kb * kBK, mrow, pol);
-                    bulk_load(smP + stage * kPivBytes, prow + (int64_t)kb * kBK, kPivBytes,
-                              &aload[stage]);
-                    // B half -> the leader's ready barrier
-                    const uint32_t rb = ready_leader + stage * 8u;
-                    if (rank == 0) mbar_arrive_expect_tx(&ready[stage], 2 * kBBytes3);
-                    else mbar_arrive_cluster(rb);
-                    tma_load_2d_pair(smB + stage * kBBytes3, &tmB, rb, kb * kBK, ncol, pol);
+                    if (elect_one()) {
+                        // own A half + pivot chunk -> local barrier (the transform warps wait)
+                        mbar_arrive_expect_tx(&aload[stage], kABytes3 + kPivBytes);
+                        tma_load_2d(smA + stage * kABytes3, &tmA, &aload[stage], kb * kBK, mrow, pol);
+                        bulk_load(smP + stage * kPivBytes, prow + (int64_t)kb * kBK, kPivBytes,
+                                  &aload[stage]);
+                        // B half -> the leader's ready barrier
+                        const uint32_t rb = ready_leader + stage * 8u;
+                        if (rank == 0) mbar_arrive_expect_tx(&ready[stage], 2 * kBBytes3);
+                        else mbar_arrive_cluster(rb);
+                        tma_load_2d_pair(smB + stage * kBBytes3, &tmB, rb, kb * kBK, ncol, pol);
+                    }
+                    __syncwarp();
                     if (++stage == kStages3) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && rank == 0) {
+        if (rank == 0) {
             // ---------------------------------------------------------- MMA issuer
+            // whole warp walks the loop (uniform descriptors); one elected lane issues
             constexpr uint32_t idesc = idesc_i8(kTileM3, kBN);
             uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-            const uint32_t a0 = smem_u32(smA), b0 = smem_u32(smB);
+            const uint64_t a_desc0 = smem_desc_sw128(smem_u32(smA));
+            const uint64_t b_desc0 = smem_desc_sw128(smem_u32(smB));
             for (int64_t u = unit0;; u += units) {
                 int32_t J, K;
                 int64_t p;
                 if (!sch.get(u, J, K, p)) break;
-                unsigned long long* tr = args.trace ? args.trace + 8 * u : nullptr;
+                unsigned long long* tr = (args.trace && lane == 0) ? args.trace + 8 * u : nullptr;
                 if (tr) tr[0] = globaltimer();
                 mbar_wait_sleep(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
@@ -439,17 +378,22 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
                     mbar_wait_sleep(&ready[stage], phase);
                     tc_fence_after();
-                    const uint32_t sa = a0 + stage * kABytes3, sb = b0 + stage * kBBytes3;
+                    // +x bytes of operand = +(x >> 4) in the descriptor's start-address field
+                    const uint64_t ad = a_desc0 + ((stage * kABytes3) >> 4);
+                    const uint64_t bd = b_desc0 + ((stage * kBBytes3) >> 4);
+                    if (elect_one()) {
 #ifndef CCC_D3_NOMMA
 #pragma unroll
-                    for (int k = 0; k < kBK / kUMMA_K; ++k)
-                        mma_i8_pair(d, smem_desc_sw128(sa + k * kUMMA_K),
-                                    smem_desc_sw128(sb + k * kUMMA_K), idesc, (kb | k) != 0);
+                        for (int k = 0; k < kBK / kUMMA_K; ++k)
+                            mma_i8_pair(d, ad + (k * kUMMA_K >> 4), bd + (k * kUMMA_K >> 4), idesc, (kb | k) != 0);
 #endif
-                    mma_commit_pair(&empty[stage], 3);
+                        mma_commit_pair(&empty[stage], 3);
+                    }
+                    __syncwarp();
                     if (++stage == kStages3) { stage = 0; phase ^= 1; }
                 }
-                mma_commit_pair(&tfull[acc], 3);
+                if (elect_one()) mma_commit_pair(&tfull[acc], 3);
+                __syncwarp();
                 if (tr) tr[2] = globaltimer();
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
@@ -584,7 +528,7 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             }
             // general gamma: w_p(a) / (8 n_f); gamma = 2/3: integer U_p(a) = 3 n_f - S_p(a)
             // (sparse final pass: no 1/(8 n_f) here, the divisor 8 c_pmn is per record)
-            const double wscale = kMode == 2 ? 1.0 : inv8nf;
+            const double wscale = inv8nf;
             const double wp0 = kExact ? 0.0 : __ldg(args.bp.w + 2 * p) * wscale;
             const double wp1 = kExact ? 0.0 : __ldg(args.bp.w + 2 * p + 1) * wscale;
             const uint64_t up0 = nf + s_p, up1 = 3u * nf - s_p;
@@ -677,7 +621,7 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     nl = nl < gn_max ? nl : gn_max;
 #pragma unroll
                     for (int r = 0; r < 2; ++r) {
-                        if constexpr (kMode != 0) g[r][h] = 0u;   // sparse passes: no G
+                        if constexpr (kMode != 0) g[r][h] = 0u;   // paper-route passes: no G
                         else if constexpr (kRowG) g[r][h] = (uint32_t)__ldg(grow[r] + nl);
                         else g[r][h] = (uint32_t)__ldg(args.G + (gcol0 + nl) * args.ldG + gm_r[r]);
                     }
@@ -722,11 +666,6 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                             paper3_record<O>(args, ok, g3, rec_r[r] + nl, wpm[r], cn.w0, cn.w1, mxm3[r], cp3, gp,
                                              gm_r[r], gcol0 + nl, want_t, want_c64, want_c32, want_ck, ck_lo,
                                              ck_hi);
-                            continue;
-                        }
-                        if constexpr (kMode == 2) {
-                            sparse3_record<O>(args, ok, g3, rec_r[r] + nl, wpm[r], cn.w0, cn.w1, gp, gm_r[r],
-                                              gcol0 + nl, want_t, want_c64, want_c32, want_ck, ck_lo, ck_hi);
                             continue;
                         }
                         const uint32_t gmn2 = 2u * gcur[r][h];
@@ -898,9 +837,8 @@ cudaError_t launch_tally3(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
             default: return go(tally3_kernel<5, E, Cp, Fu>);
         }
     };
-    if (a.mode == 1) return go(tally3_kernel<0, false, false, false, 1>);   // sparse passes:
-    if (a.mode == 2) return go(tally3_kernel<0, false, false, false, 2>);   // order 0 only
-    if (a.mode == 3) return go(tally3_kernel<0, false, false, false, 3>);
+    if (a.mode == 1) return go(tally3_kernel<0, false, false, false, 1>);   // paper-route passes:
+    if (a.mode == 3) return go(tally3_kernel<0, false, false, false, 3>);   // order 0 only
     using T = std::true_type;
     using F = std::false_type;
     // FULL with gamma = 2/3 (tallies + fp64 CCC, no checksum) gets a flag-free epilogue

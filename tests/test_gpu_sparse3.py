@@ -125,3 +125,35 @@ def test_sparse_hand_values_through_the_kernels():
         torch.cuda.synchronize()
         assert list(_t(T)[0]) == T_want
         _ccc_close(C.cpu().numpy()[0], np.array(C_want))
+
+
+def test_sparse3_bench_shape_sampled():
+    """configs[3]'s shape in sparse mode (4,096 x 16,384, 16 stages, bench.py's c4s
+    workload): first and last stage, sampled triples including the single-pass kernel's
+    tile edges (m at multiples of 64 +- 1, n at multiples of 128 +- 1) against the brute
+    force; sum T = 8 c_ijk on every record of both stages."""
+    n_v, n_f, n_st = 4096, 16384, 16
+    codes = synthgen.sparse_codes(n_v, n_f, seed=4, device="cuda")
+    ws = ccc.ccc_3way_sparse_prepare(ccc.ccc_pack(codes), n_f)
+    codes_h = codes.cpu()
+    rng = np.random.default_rng(9)
+    for st in (0, n_st - 1):
+        T, C, _ = ccc.ccc_3way_sparse_stage(n_v, n_f, n_st, st, ws, TAL | F64)
+        torch.cuda.synchronize()
+        i0, i1, r0, rc = ccc.ccc_stage_range(n_v, n_st, st)
+        tl = set()
+        edges = [e + d for e in range(64, n_v, 64) for d in (-1, 0, 1)]
+        while len(tl) < 1500:
+            i = int(rng.integers(i0, min(i1, n_v - 2)))
+            j = int(rng.choice(edges)) if rng.random() < 0.4 else int(rng.integers(i + 1, n_v - 1))
+            if not i < j < n_v - 1:
+                continue
+            k = int(rng.choice(edges)) if rng.random() < 0.4 else int(rng.integers(j + 1, n_v))
+            if j < k < n_v:
+                tl.add((i, j, k))
+        tl = sorted(tl)
+        rows = torch.tensor([ccc.ccc_triple_index(n_v, *t) - r0 for t in tl], device="cuda")
+        To, Co, _ = oracle.sparse_triples(codes_h, np.array(tl))
+        np.testing.assert_array_equal(_t(T[rows]), To)
+        _ccc_close(C[rows].cpu().numpy(), Co)
+        assert bool((T.to(torch.int64).sum(1) % 8 == 0).all())
