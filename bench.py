@@ -2,7 +2,7 @@
 
 python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                 [--workload c2|c2hwe|c4|c1|c2s|c4s|c4f32|c4ck|c2pop|c2fs|c4paper|c3|c5]
-                [--no-e2e] [--no-cpu] [--no-3way]
+                [--no-e2e] [--no-cpu] [--no-3way] [--grid n_pv,n_pr,n_pf]
 
 One step = one pass of the whole hot path over one synthetic batch resident in HBM:
   2-way (default, BASELINE configs[1] = C2: 20,000 vectors x 50,000 individuals):
@@ -818,7 +818,14 @@ def main():
     ap.add_argument("--no-cpu", dest="cpu", action="store_false")
     ap.add_argument("--no-3way", dest="three_way", action="store_false",
                     help="default c2 line: skip the three_way (C4) sub-object")
+    ap.add_argument("--grid", default=None,
+                    help="n_pv,n_pr,n_pf: run the 2-way workload on the paper's process grid "
+                         "(vector blocks x result parts x field slices, product = N; SURVEY 8(f) f3)")
     args = ap.parse_args()
+    if args.grid is not None:
+        args.grid = tuple(int(x) for x in args.grid.split(","))
+        if len(args.grid) != 3:
+            raise SystemExit("--grid takes n_pv,n_pr,n_pf")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     wl = dict(WORKLOADS[args.workload])
@@ -849,7 +856,7 @@ def main():
         print(json.dumps(out))
         return
 
-    if world > 1 or args.gpus > 1 or wl.get("strong"):
+    if world > 1 or args.gpus > 1 or wl.get("strong") or args.grid is not None:
         if wl.get("sparse"):
             raise SystemExit("the sparse workloads are single-GPU measurements")
         from paper_1705_08213_b200 import dist

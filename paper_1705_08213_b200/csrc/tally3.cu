@@ -702,8 +702,13 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                                     // P's bits under exponent 0x433, so CCC = P w_n =
                                     // fma(2^52 + P, w_n, -2^52 w_n): one rounding, one FP64 op
                                     // (FP64 shares its issue pipe with the tensor core)
+#ifdef CCC_D3_NOFP64   // diagnostics: the same stores without the FP64 multiply (values wrong)
+                                    cr[2 * ab + 0] = magic52(t[2 * ab + 0] * upm[r][ab]);
+                                    cr[2 * ab + 1] = magic52(t[2 * ab + 1] * upm[r][ab]);
+#else
                                     cr[2 * ab + 0] = __fma_rn(magic52(t[2 * ab + 0] * upm[r][ab]), wn0, cn.m0);
                                     cr[2 * ab + 1] = __fma_rn(magic52(t[2 * ab + 1] * upm[r][ab]), wn1, cn.m1);
+#endif
                                 } else {
                                     // exact: T U_p U_m rounded once (same as the 64-bit integer
                                     // product converted), times U_n / (216 n_f^4)

@@ -490,6 +490,10 @@ def bench_main(args, wl, metric, unit):  # noqa: C901
     strong = wl.get("strong", False)
     way = wl["way"]
     n_f = wl["n_f"]
+    gshape = getattr(args, "grid", None)
+    if gshape is not None:
+        if way != 2 or decomp.Grid(*gshape).world != P:
+            raise SystemExit("--grid n_pv,n_pr,n_pf is a 2-way decomposition of all ranks (product = N)")
     if way == 2:
         n_v = wl["n_v"] if strong else weak_scaled_nv(wl["n_v"], P)
     else:
@@ -502,7 +506,31 @@ def bench_main(args, wl, metric, unit):  # noqa: C901
     packed = be.packed_empty(hi - lo)
     k_pad, stride = ccc.ccc_k_pad(n_f), ccc.ccc_packed_stride(n_f)
     rec_bytes = 48 if way == 2 else 96
-    if way == 2:
+    if way == 2 and gshape is not None:
+        # the paper's process grid: vector blocks x result parts x field slices
+        from .fieldsplit import field_slices
+        from .grid import CudaGridBackend, Grid2Way
+        G = decomp.Grid(*gshape)
+        v, _, f = G.coords(rank)
+        bounds = decomp.block_bounds(n_v, G.n_pv, align=256)
+        lo, hi = bounds[v]
+        f0, f1 = field_slices(n_f, G.n_pf)[f]
+        be = CudaGridBackend(f1 - f0, n_f, ccc.GAMMA, full)
+        codes = synthgen.random_codes(hi - lo, n_f, seed=1, device="cuda", row0=lo)[:, f0:f1].contiguous()
+        packed = be.packed_empty(hi - lo)
+        k_pad, stride = ccc.ccc_k_pad(f1 - f0), ccc.ccc_packed_stride(f1 - f0)
+        parts = [decomp.split_rows(u, bounds, G.n_pr)[G.coords(rank)[1]]
+                 for u in decomp.plan_2way(G.n_pv, v, bounds)]
+        my_rec = sum(decomp.unit2_records(decomp.Unit2(u.a, u.b, a, b, u.diag, u.step), bounds)
+                     for u, (a, b) in zip(decomp.plan_2way(G.n_pv, v, bounds), parts))
+        max_rows = max(b - a for a, b in bounds)
+        fixed = 2 * max_rows * k_pad + 2 * max_rows * stride + (2 << 30)   # + slot buffers
+        budget = record_budget(rec_bytes, fixed)
+        max_rec = None if my_rec <= budget else budget
+        ring = Grid2Way(be, G, rank, bounds, max_records=max_rec)
+        phases = sum(len(b) for b in ring.bands)
+        my_rec = my_rec // G.n_pf     # records this rank writes (its owned tiles)
+    elif way == 2:
         units = decomp.plan_2way(P, rank, bounds)
         my_rec = sum(decomp.unit2_records(u, bounds) for u in units)
         max_rows = max(b - a for a, b in bounds)
@@ -522,7 +550,7 @@ def bench_main(args, wl, metric, unit):  # noqa: C901
     def step(timed):
         be.pack(codes, packed)
         ring.ck.zero_()
-        if way == 2:
+        if way == 2 and gshape is None:
             ring.run(packed, timed=timed)
         else:
             ring.run(packed)
@@ -530,7 +558,7 @@ def bench_main(args, wl, metric, unit):  # noqa: C901
             launches[0] += 1 + ring.launches
 
     ms, per, clk = _timed(W, step, args)
-    kms = sum(a.elapsed_time(b) for a, b in be.kernel_events) if way == 2 else None
+    kms = sum(a.elapsed_time(b) for a, b in be.kernel_events) if (way == 2 and gshape is None) else None
     if kms is not None:
         kms = W.max(kms)
     # verification: + the checksum, summed over ranks
@@ -542,7 +570,7 @@ def bench_main(args, wl, metric, unit):  # noqa: C901
     comps = n_f * (n_v * (n_v - 1) // 2 if way == 2 else n_v * (n_v - 1) * (n_v - 2) // 6)
     ms_step = ms / args.steps
     e2e = None
-    if args.e2e and way == 2 and ring.out is not None:
+    if args.e2e and way == 2 and gshape is None and ring.out is not None:
         # the same step through the public API with host buffers: H2D of this rank's genotype
         # codes from pinned memory, D2H of every record it computes, max over ranks
         import time
@@ -573,6 +601,8 @@ def bench_main(args, wl, metric, unit):  # noqa: C901
         del outs_h, codes_h
     # the single-GPU CHECKSUM-mode reference run of the whole problem (rank 0, untimed)
     ring_phases = phases
+    if gshape is not None:
+        ring.close()
     del ring
     torch.cuda.empty_cache()
     ref = None
@@ -603,6 +633,11 @@ def bench_main(args, wl, metric, unit):  # noqa: C901
         pipe = 148 * INT8_OPS_PER_CLK_SM * mhz * 1e6 / 1e12
         from bench import config_of
         cfg = config_of(wl, P)
+        if gshape is not None:
+            cfg["parallelism"] = "process grid n_pv x n_pr x n_pf = %d x %d x %d" % tuple(gshape)
+            cfg["ring"] = ("packed 2-bit blocks round each (r, f) sub-ring, NCCL send/recv; field groups: "
+                           "partial tiles stored from the GEMM epilogue into the owners' CUDA IPC slots, "
+                           "stream-ordered barrier, owner finish (P:583-606)")
         out = {"metric": metric, "value": comps / (ms_step / 1e3), "unit": unit, "n_gpus": P,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
                "ms_per_step_median": per_s[len(per_s) // 2], "ms_per_step_best": per_s[0],
@@ -613,7 +648,9 @@ def bench_main(args, wl, metric, unit):  # noqa: C901
                "phases_per_rank": ring_phases if max_rec is not None else 1}
         step_tops = 2.0 * comps / P / (ms_step / 1e3) / 1e12
         if way == 2:
-            ach = 2.0 * n_f * my_rec * args.steps / (kms / 1e3) / 1e12
+            # grid: the export GEMMs + finishes of a rank are the whole step (no per-kernel
+            # events), so the achieved rate is taken over the step
+            ach = 2.0 * n_f * my_rec * args.steps / ((kms if kms else ms) / 1e3) / 1e12
             peak = 2.0 * pk["bf16_tflops"]
             out["roofline"] = {
                 "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
