@@ -158,6 +158,15 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     uint8_t* sa = smA + stage * C::kABytes;
                     uint8_t* sb = smB + stage * C::kBBytes;
                     if (elect_one()) {
+#ifdef CCC_D2_NOTMA   // diagnostics: no operand loads (stale tiles; timing only)
+                        if constexpr (kPair == 2) {
+                            if (rank == 0) mbar_arrive(&full[stage]);
+                            else mbar_arrive_cluster(mapa_shared(smem_u32(&full[stage]), 0));
+                        } else {
+                            mbar_arrive(&full[stage]);
+                        }
+                        if (true) {} else
+#endif
                         if constexpr (kPair == 2) {
                             const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
                             if (rank == 0)
