@@ -6,10 +6,10 @@ python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 One step = one pass of the whole hot path over one synthetic batch resident in HBM:
   2-way (default, BASELINE configs[1] = C2: 20,000 vectors x 50,000 individuals):
-      ccc_expand_codes (a1+a2 fused: unpacked codes -> int8 operand, s, w in one HBM
-      pass) -> ccc_2way_block (fused tally GEMM + CCC epilogue, every unique pair's uint32
-      tallies + fp64 CCC written to HBM); ccc_pack / ccc_expand (the ring's packed path) are
-      timed on their own after the timed region ("hbm_passes")
+      ccc_2way_codes: expand_codes (a1+a2 fused: unpacked codes -> int8 operand, s, w in
+      one HBM pass), then the fused tally GEMM + CCC epilogue; every unique pair's uint32
+      tallies + fp64 CCC written to HBM.  ccc_pack / ccc_expand (the ring's packed path) and
+      expand_codes alone are timed after the timed region ("hbm_passes")
   3-way (--workload c4: 4,096 x 16,384, 16 stages, FULL output, buffer reused)
   sparse 2-way (--workload c2s: C2's shape, ~15% missing entries):
       ccc_pack -> ccc_expand_sparse -> ccc_2way_sparse_block
@@ -412,14 +412,15 @@ def run_2way_single(args, wl):  # noqa: C901
         if k is not None:
             launches[0] += ccc.ccc_last_launch_count()
 
+    ws2 = ccc.workspace(2, n_v, n_f, dev) if not (sparse or popcount) else None
+
     def step(k):
         if not (sparse or popcount):
-            # one GPU fed unpacked codes: a1+a2 fused into one HBM pass (ccc_expand_codes);
-            # the 2-bit packed form only matters where it crosses NVLink (the ring)
-            ccc.ccc_expand_codes(codes, ccc.GAMMA, N, s, w)
-            count(k)
+            # one GPU fed unpacked codes: a1+a2 fused into one HBM pass (expand_codes), then
+            # the fused tally GEMM (ccc_2way_codes); the 2-bit packed form only matters where
+            # it crosses NVLink (the ring)
             _ev(kev, k, 0, 0)
-            ccc.ccc_2way_block(N, s, w, 0, 0, n_v, N, s, w, 0, True, n_f, flags, T, C)
+            ccc.ccc_2way_codes(codes, ccc.GAMMA, flags, T, C, None, ws2)
             count(k)
             _ev(kev, k, 0, 1)
             return
@@ -451,6 +452,8 @@ def run_2way_single(args, wl):  # noqa: C901
                kernel="popc_tally2_kernel" if popcount else "tally2_kernel", out_bytes=m * 48)
     if not (sparse or popcount):
         res["hbm_passes"] = hbm_passes(codes, packed, N, s, w, n_v, n_f)
+        res["kernel_note"] = ("kernel_ms brackets ccc_2way_codes (expand_codes + tally2_kernel, the "
+                              "whole step's device work); expand_codes alone: hbm_passes")
     if args.cpu:
         cb, idx, To, Co = cpu_baseline(2, n_v, n_f, kind=kind, with_records=True)
         res["cpu_baseline"] = cb
@@ -792,7 +795,7 @@ def line_for(args, wl, r, pk, pk_kind):
         "data": "synthetic", "config": config_of(wl),
         "roofline": roofline(args, wl, r, ms_step, pk, pk_kind),
         "gpu_launches": r["launches"], "clocks": r["clocks"]})
-    for k in ("parity", "e2e", "cpu_baseline", "hbm_passes"):
+    for k in ("parity", "e2e", "cpu_baseline", "hbm_passes", "kernel_note"):
         if k in r:
             out[k] = r[k]
     return out

@@ -172,6 +172,15 @@ ccc_status ccc_2way(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double ga
                     uint32_t out_flags, uint32_t* tallies_d, void* ccc_d, uint64_t* checksum_d,
                     void* ws_d, size_t ws_bytes, const ccc_compact* compact, void* stream);
 
+/* The same whole 2-way problem from UNPACKED device codes (§8(a) a1-a4 on one GPU; the
+ * bench's step): codes_d uint8 [n_v][n_f] (row-major, code = 2 r1 + r2, low 2 bits read)
+ * -> ccc_expand_codes into the workspace (one HBM pass, no 2-bit intermediate), then the
+ * fused tally GEMM + epilogue of ccc_2way.  ws_d >= ccc_workspace_bytes(2, n_v, n_f),
+ * 256-B aligned; outputs, flags, compaction and errors as ccc_2way. */
+ccc_status ccc_2way_codes(const uint8_t* codes_d, int64_t n_v, int64_t n_f, double gamma,
+                          uint32_t out_flags, uint32_t* tallies_d, void* ccc_d, uint64_t* checksum_d,
+                          void* ws_d, size_t ws_bytes, const ccc_compact* compact, void* stream);
+
 /* The paper's own 2-way tally method on CUDA cores (§3.1
  * mGEMM2): the same problem and outputs as ccc_2way, computed from the
  * packed 2-bit rows with bitwise AND + population count instead of tensor-core MACs,

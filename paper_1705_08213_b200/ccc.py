@@ -104,6 +104,7 @@ _SIGS = {
     "ccc_expand": (_int, [_vp, _i64, _i64, _dbl, _vp, _vp, _vp, _vp]),
     "ccc_expand_codes": (_int, [_vp, _i64, _i64, _dbl, _vp, _vp, _vp, _vp]),
     "ccc_2way": (_int, [_vp, _i64, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _sz, _vp, _vp]),
+    "ccc_2way_codes": (_int, [_vp, _i64, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _sz, _vp, _vp]),
     "ccc_2way_popcount": (_int, [_vp, _i64, _i64, _dbl, _u32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "ccc_2way_fs_tiles": (_i64, [_i64]),
     "ccc_2way_fs_slot_bytes": (_sz, [_int, _i64, _i64]),
@@ -401,6 +402,22 @@ def ccc_2way(packed: torch.Tensor, n_f: int, gamma: float = GAMMA,
     _bytes(ws, ccc_workspace_bytes(2, n_v, n_f), "ws")
     _check(lib().ccc_2way(_p(packed), n_v, n_f, gamma, out_flags, _p(tallies), _p(ccc),
                           _p(checksum), _p(ws), ws.numel(), cp, _stream(stream)))
+    return tallies, ccc, checksum
+
+
+def ccc_2way_codes(codes: torch.Tensor, gamma: float = GAMMA, out_flags: int = OUT_TALLY | OUT_CCC_F64,
+                   tallies=None, ccc=None, checksum=None, ws=None, stream=None, compact: Compact | None = None):
+    """All 2-way records from unpacked device codes [n_v][n_f]; the expand overlaps the
+    tally GEMM (see include/ccc.h).  Returns (tallies, ccc, checksum) like ccc_2way."""
+    _dev(codes, torch.uint8, "codes", (None, None))
+    n_v, n_f = codes.shape
+    cp, tallies, ccc, checksum = _outs(ccc_num_unique(2, n_v), 4, out_flags, codes.device,
+                                       tallies, ccc, checksum, compact)
+    if ws is None:
+        ws = workspace(2, n_v, n_f, codes.device)
+    _bytes(ws, ccc_workspace_bytes(2, n_v, n_f), "ws")
+    _check(lib().ccc_2way_codes(_p(codes), n_v, n_f, gamma, out_flags, _p(tallies), _p(ccc),
+                                _p(checksum), _p(ws), ws.numel(), cp, _stream(stream)))
     return tallies, ccc, checksum
 
 

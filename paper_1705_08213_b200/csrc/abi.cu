@@ -423,6 +423,36 @@ ccc_status ccc_2way(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double ga
     return CCC_OK;
 }
 
+ccc_status ccc_2way_codes(const uint8_t* codes_d, int64_t n_v, int64_t n_f, double gamma, uint32_t out_flags,
+                          uint32_t* tallies_d, void* ccc_d, uint64_t* checksum_d, void* ws_d, size_t ws_bytes,
+                          const ccc_compact* compact, void* stream) {
+    CCC_CHECK(check_compact(compact));
+    g_launches = 0;
+    CCC_CHECK(check_sizes(n_v, n_f));
+    if (out_flags & ~15u) return fail(CCC_ERR_INVALID_ARGUMENT, "unknown out_flags bits");
+    if (n_v < 2) return CCC_OK;
+    CCC_CHECK(check_outputs(out_flags, tallies_d, ccc_d, checksum_d));
+    if (!codes_d) return fail(CCC_ERR_INVALID_ARGUMENT, "codes_d must be non-NULL");
+    const WsLayout L = ws_layout(2, n_v, n_f);
+    if (!ws_d || !aligned(ws_d, 256)) return fail(CCC_ERR_INVALID_ARGUMENT, "ws_d must be 256-B aligned");
+    if (ws_bytes < L.total) return fail(CCC_ERR_WORKSPACE, "workspace too small (see ccc_workspace_bytes)");
+    int sms;
+    CCC_CHECK(check_device(&sms));
+    uint8_t* ws = static_cast<uint8_t*>(ws_d);
+    int8_t* N = reinterpret_cast<int8_t*>(ws + L.N);
+    int32_t* s = reinterpret_cast<int32_t*>(ws + L.s);
+    double* w = reinterpret_cast<double*>(ws + L.w);
+    cudaStream_t st = (cudaStream_t)stream;
+    // unpacked codes straight to the operand (no 2-bit intermediate on one GPU), then the
+    // fused tally GEMM; running the expand concurrently with the GEMM (producer waiting per
+    // 128-row block) was measured slower (profiles/r02_experiments.md)
+    CCC_CUDA(ccc::launch_expand_codes(codes_d, n_v, n_f, gamma, N, s, w, sms, st), "expand_codes launch");
+    CCC_CHECK(block_impl(N, s, w, n_v, 0, 0, n_v, N, s, w, n_v, 0, 1, n_f, gamma, out_flags, tallies_d, ccc_d,
+                         checksum_d, nullptr, 0, compact, st, sms));
+    g_launches += 1;
+    return CCC_OK;
+}
+
 ccc_status ccc_2way_popcount(const uint8_t* packed_d, int64_t n_v, int64_t n_f, double gamma,
                              uint32_t out_flags, uint32_t* tallies_d, void* ccc_d,
                              uint64_t* checksum_d, void* ws_d, size_t ws_bytes, void* stream) {

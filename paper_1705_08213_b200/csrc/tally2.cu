@@ -149,6 +149,7 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 const int32_t arow = (int32_t)(args.a_lo + (int64_t)bm * C::kTileM + rank * 128);
                 const int32_t brow = (int32_t)sch.b_lo + bn * kBN + (int32_t)rank * C::kBRows;
                 if (args.trace && rank == 0 && lane == 0) args.trace[8 * t + 6] = globaltimer();
+
                 // odd waves walk K backwards: they start on the k-blocks the previous wave
                 // touched last, which are still in L2 (the MMA accumulates in any order)
                 const bool rev = args.k_alternate && (((t - unit0) / units) & 1);

@@ -717,3 +717,41 @@ def test_3way_unit_rejects_noncanonical_orders():
             else:
                 with pytest.raises(ValueError, match="order must put"):
                     ccc.ccc_3way_unit(bp, 0, 2, bm, 0, 32, bn, 0, 32, order, G, n_f, TAL)
+
+
+@pytest.mark.parametrize("n_v,n_f", [(2, 1), (3, 65), (127, 129), (129, 1000), (300, 777), (700, 4096),
+                                     (1100, 2049)])
+def test_2way_codes_overlapped_expand(n_v, n_f):
+    """ccc_2way_codes (unpacked codes -> expand_codes -> tally GEMM) writes exactly ccc_2way's
+    records on the packed path, and the oracle's; called twice on one workspace."""
+    codes = _codes("random", n_v, n_f, seed=n_v * 7 + n_f)
+    cd = codes.cuda()
+    ws = ccc.workspace(2, n_v, n_f)
+    T1, C1, k1 = ccc.ccc_2way(ccc.ccc_pack(cd), n_f, out_flags=TAL | F64 | CK)
+    for _ in range(2):
+        T2, C2, k2 = ccc.ccc_2way_codes(cd, out_flags=TAL | F64 | CK, ws=ws)
+        torch.cuda.synchronize()
+        assert bool((T1 == T2).all()) and bool((C1 == C2).all())
+        assert ccc.checksum_int(k1) == ccc.checksum_int(k2)
+    To, Co = oracle.all_pairs(codes)
+    np.testing.assert_array_equal(_t(T2), To)
+    _ccc_close(C2.cpu().numpy(), Co)
+
+
+def test_2way_codes_c2_shape_equals_packed_path():
+    """At configs[1]'s shape (20,000 x 50,000, bench.py's step): ccc_2way_codes' checksum
+    equals the packed path's and a sample of records the oracle's."""
+    n_v, n_f = 20000, 50000
+    codes = synthgen.random_codes(n_v, n_f, seed=1, device="cuda")
+    _, _, k1 = ccc.ccc_2way(ccc.ccc_pack(codes), n_f, out_flags=CK)
+    T, C, k2 = ccc.ccc_2way_codes(codes, out_flags=TAL | F64 | CK)
+    torch.cuda.synchronize()
+    assert ccc.checksum_int(k1) == ccc.checksum_int(k2)
+    rng = np.random.default_rng(3)
+    i = rng.integers(0, n_v - 1, 2000)
+    j = np.array([rng.integers(a + 1, n_v) for a in i])
+    idx = np.stack([i, j], 1)
+    rows = torch.tensor([ccc.ccc_pair_index(n_v, int(a), int(b)) for a, b in idx], device="cuda")
+    To, Co = oracle.pairs(codes.cpu(), idx)
+    np.testing.assert_array_equal(_t(T[rows]), To)
+    _ccc_close(C[rows].cpu().numpy(), Co)
