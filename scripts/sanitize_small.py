@@ -42,5 +42,15 @@ c16 = synthgen.random_codes(130, 4096 + 256, seed=6)              # vector pack 
 T16, _, _ = ccc.two_way(c16.cuda(), out_flags=ccc.OUT_TALLY)
 To16, _ = oracle.all_pairs(c16)
 assert np.array_equal(T16.cpu().numpy().astype(np.int64) & 0xFFFFFFFF, To16)
+# round 2: expand_codes / ccc_2way_codes, the grid's block export/finish, the 3-way sparse
+# single pass (tally3s) at a shape spanning several of its 64 x 128 tiles
+Tc, _, _ = ccc.ccc_2way_codes(codes.cuda(), out_flags=F)
+assert bool((Tc == Td).all())
+from paper_1705_08213_b200 import grid as gridmod
+res, _ = gridmod.run_grid_simulated(codes.cuda(), decomp.Grid(2, 1, 2), F, wave_tiles=1)
+sc3 = synthgen.sparse_codes(200, 300, seed=7)
+T3b, _, _ = ccc.three_way_sparse(sc3.cuda(), out_flags=F, n_stages=3)
+To3b, _, _ = oracle.sparse_all_triples(sc3)
+assert np.array_equal(T3b.cpu().numpy().astype(np.int64) & 0xFFFFFFFF, To3b)
 torch.cuda.synchronize()
 print("sanitize run ok")

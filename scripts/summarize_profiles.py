@@ -17,7 +17,8 @@ PROF = os.path.join(ROOT, "profiles")
 
 def short(name):
     for k in ("popc_tally2_kernel", "popc_stats_kernel", "fs_finish_kernel", "tally2_kernel",
-              "tally3_kernel", "pack_kernel", "expand_masks_kernel", "expand_sparse_kernel", "expand_kernel"):
+              "tally3s_kernel", "tally3_kernel", "pack_kernel", "expand_masks_kernel", "expand_sparse_kernel",
+              "expand_codes_kernel", "expand_kernel"):
         if k in name:
             return k
     return name.split("(")[0][:60]
@@ -41,8 +42,9 @@ def launches(path):
         k = short(r["Kernel Name"])
         agg[k][0] += 1
         agg[k][1] += ns
-    ours = {"tally2_kernel", "tally3_kernel", "pack_kernel", "expand_kernel", "popc_tally2_kernel",
-            "popc_stats_kernel", "fs_finish_kernel", "expand_masks_kernel", "expand_sparse_kernel"}
+    ours = {"tally2_kernel", "tally3_kernel", "tally3s_kernel", "pack_kernel", "expand_kernel",
+            "expand_codes_kernel", "popc_tally2_kernel", "popc_stats_kernel", "fs_finish_kernel",
+            "expand_masks_kernel", "expand_sparse_kernel"}
     tot = sum(v[1] for k, v in agg.items() if k in ours)   # the step = our kernels only
     res = {k: {"launches": c, "total_ms": t / 1e6, "mean_ms": t / 1e6 / c, "share_of_step": t / tot}
            for k, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]) if k in ours}

@@ -171,8 +171,10 @@ def test_validation_of_later_rows():
                                        null) == ccc.ERR_WORKSPACE
     wsb = lib.ccc_sparse3_workspace_bytes(10, 10)
     assert lib.ccc_3way_sparse_stage(10, 10, 2 / 3, 1, 0, ccc.OUT_TALLY, ctypes.c_void_p(256), null, null,
-                                     ctypes.c_void_p(256), wsb, ctypes.c_void_p(256), 4, null) == ccc.ERR_WORKSPACE
-    assert lib.ccc_3way_sparse_scratch_bytes(10, 1, 0) == 7 * 120 * 4
+                                     ctypes.c_void_p(256), wsb - 1, null, 0, null) == ccc.ERR_WORKSPACE
+    assert lib.ccc_3way_sparse_scratch_bytes(10, 1, 0) == 0      # single pass: no stored forms
+    assert lib.ccc_3way_sparse_stage(10, 10, 2 / 3, 1, 0, ccc.OUT_TALLY, null, null, null,
+                                     ctypes.c_void_p(256), wsb, null, 0, null) == ccc.ERR_INVALID_ARGUMENT
     assert lib.ccc_3way_paper_scratch_bytes(10, 1, 0) == 2 * 120 * 4
     assert lib.ccc_3way_paper_workspace_bytes(10, 10) > 3 * 10 * 10 * 4
     assert lib.ccc_3way_paper_prepare(null, 2, 10, 2 / 3, null, 0, null) == ccc.OK   # n_v < 3: nothing
