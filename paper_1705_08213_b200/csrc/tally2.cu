@@ -532,8 +532,13 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     if (want_c) {
                         if (want_c64) {
                             double* p = reinterpret_cast<double*>(args.ccc) + 4 * recA;
+#ifdef CCC_D2_CCC_NOALLOC   // experiment: the fp64 CCC half of the records bypasses L1 allocation
+                            stg_256_f64_if(stA, p, ca00, ca01, ca10, ca11);
+                            stg_256_f64_if(stB, p + 4, cb00, cb01, cb10, cb11);
+#else
                             if (stA) stg_256_f64(p, ca00, ca01, ca10, ca11);
                             if (stB) stg_256_f64(p + 4, cb00, cb01, cb10, cb11);
+#endif
                         } else {
                             float* p = reinterpret_cast<float*>(args.ccc) + 4 * recA;
                             if (stA && stB && !(recA & 1)) {

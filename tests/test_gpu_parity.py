@@ -755,3 +755,22 @@ def test_2way_codes_c2_shape_equals_packed_path():
     To, Co = oracle.pairs(codes.cpu(), idx)
     np.testing.assert_array_equal(_t(T[rows]), To)
     _ccc_close(C[rows].cpu().numpy(), Co)
+
+
+def test_2way_codes_compacted_equals_dense_filter():
+    """ccc_2way_codes with threshold compaction (f2) keeps exactly the records
+    of the dense output whose largest CCC cell exceeds theta, with their tallies and CCC."""
+    n_v, n_f = 900, 3001
+    codes = synthgen.random_codes(n_v, n_f, seed=41, device="cuda")
+    T, C, _ = ccc.ccc_2way_codes(codes, out_flags=TAL | F64)
+    mx = C.max(dim=1).values
+    theta = float(torch.kthvalue(mx, mx.numel() - 300).values)
+    cp = ccc.Compact(theta, 1000, 4)
+    ccc.ccc_2way_codes(codes, out_flags=TAL | F64, compact=cp)
+    n, keys, Tk, Ck = cp.result()
+    want = torch.nonzero(mx > theta).flatten()
+    assert n == want.numel() == 300
+    idx = ccc.decode_keys(keys, 2).cpu().numpy()
+    rows = torch.tensor([ccc.ccc_pair_index(n_v, int(i), int(j)) for i, j in idx], device="cuda")
+    assert sorted(rows.tolist()) == want.tolist()
+    assert bool((T[rows] == Tk).all()) and bool((C[rows] == Ck).all())
