@@ -165,6 +165,37 @@ ccc_status check_outputs(uint32_t flags, const uint32_t* tallies, const void* cc
     return CCC_OK;
 }
 
+// B operand of the 3-way pivot GEMM as the 4-D view (K, a: 2 [stride 4 rows], b: 4 [1 row],
+// g [8 rows]) of a row-major [rows][k_pad] matrix: a 128-row box lands in shared memory as
+// row 8g + 2b + a <- n = 8g + 4a + b (tally3_kernel's args.permb).  Needs the memory of
+// ceil8(rows) rows to be readable: `readable_rows` says how many the buffer holds; with
+// fewer the plain 2-D map is made and *permb = 0 (rows past `rows` are masked columns).
+ccc_status make_tmap_b3(CUtensorMap* tm, const void* base, int64_t rows, int64_t readable_rows, int64_t k_pad,
+                        int32_t* permb) {
+    const int64_t r8 = (rows + 7) / 8 * 8;
+    if (readable_rows < r8) {
+        *permb = 0;
+        return make_tmap(tm, base, rows, k_pad, 128);
+    }
+    EncodeTiledFn enc;
+    CCC_CHECK(get_encode(&enc));
+    cuuint64_t dims[4] = {(cuuint64_t)k_pad, 2, 4, (cuuint64_t)(r8 / 8)};
+    cuuint64_t strides[3] = {(cuuint64_t)(4 * k_pad), (cuuint64_t)k_pad, (cuuint64_t)(8 * k_pad)};
+    cuuint32_t box[4] = {(cuuint32_t)ccc::kBK, 2, 4, 16};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(base), dims, strides,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        char buf[96];
+        snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled (4-D) failed (CUresult %d)", (int)r);
+        return fail(CCC_ERR_CUDA, buf);
+    }
+    *permb = 1;
+    return CCC_OK;
+}
+
+
 struct WsLayout {
     size_t N = 0, s = 0, w = 0, G = 0, total = 0;
 };
@@ -172,8 +203,8 @@ struct WsLayout {
 WsLayout ws_layout(int way, int64_t n_v, int64_t n_f) {
     WsLayout L;
     size_t off = 0;
-    L.N = off;
-    off += al256((size_t)n_v * (size_t)kpad_of(n_f));
+    L.N = off;   // rows padded to a multiple of 8: the 3-way B operand's 4-D view reads them
+    off += al256((size_t)((n_v + 7) / 8 * 8) * (size_t)kpad_of(n_f));
     L.s = off;
     off += al256((size_t)n_v * 4);
     L.w = off;
@@ -725,7 +756,7 @@ ccc_status ccc_3way_stage(int64_t n_v, int64_t n_f, double gamma, int64_t n_stag
     a.checksum = reinterpret_cast<unsigned long long*>(checksum_d);
     CUtensorMap tmA, tmB;
     CCC_CHECK(make_tmap(&tmA, b.N, n_v, k_pad, 128));
-    CCC_CHECK(make_tmap(&tmB, b.N, n_v, k_pad, 128));   // per-CTA halves of the pair tile
+    CCC_CHECK(make_tmap_b3(&tmB, b.N, n_v, (n_v + 7) / 8 * 8, k_pad, &a.permb));   // workspace: padded
     int64_t units = 0;
     CCC_CUDA(ccc::launch_tally3(tmA, tmB, a, sms, (cudaStream_t)stream, &units), "tally3 launch");
     if (units) g_launches = 1;
@@ -832,8 +863,8 @@ PapLayout pap_layout(int64_t n_v, int64_t n_f) {
     PapLayout L;
     size_t off = 0;
     const size_t mat = al256((size_t)n_v * (size_t)kpad_of(n_f));
-    L.N = off;
-    off += mat;
+    L.N = off;   // rows padded to a multiple of 8 (the B operand's 4-D view)
+    off += al256((size_t)((n_v + 7) / 8 * 8) * (size_t)kpad_of(n_f));
     L.s = off;
     off += al256((size_t)n_v * 4);
     L.w = off;
@@ -918,8 +949,10 @@ ccc_status ccc_3way_paper_stage(int64_t n_v, int64_t n_f, double gamma, int64_t 
     const double* w = reinterpret_cast<const double*>(ws + L.w);
     const int8_t* M = reinterpret_cast<const int8_t*>(ws + L.M);
     const int32_t* mx = reinterpret_cast<const int32_t*>(ws + L.mx);
-    CUtensorMap tm;
+    CUtensorMap tm, tmB;
+    int32_t permb = 0;
     CCC_CHECK(make_tmap(&tm, N, n_v, k_pad, 128));
+    CCC_CHECK(make_tmap_b3(&tmB, N, n_v, (n_v + 7) / 8 * 8, k_pad, &permb));
     for (int x = 0; x < 3; ++x) {   // the three masked pivot GEMMs (the paper's 3 mGEMM3)
         ccc::Tally3Args a{};
         a.bp = ccc::Blk3{M + x * mat, s, w, n_v, 0};   // pivot rows: the class-xi mask
@@ -944,7 +977,8 @@ ccc_status ccc_3way_paper_stage(int64_t n_v, int64_t n_f, double gamma, int64_t 
         for (int y = 0; y < 3; ++y) a.mx[y] = mx + (size_t)y * n_v * n_v;
         a.mcnt = reinterpret_cast<const int32_t*>(ws + L.cnt);
         int64_t units = 0;
-        CCC_CUDA(ccc::launch_tally3(tm, tm, a, sms, (cudaStream_t)stream, &units), "tally3 paper-route launch");
+        a.permb = permb;
+        CCC_CUDA(ccc::launch_tally3(tm, tmB, a, sms, (cudaStream_t)stream, &units), "tally3 paper-route launch");
         if (units) ++g_launches;
     }
     return CCC_OK;
@@ -1047,7 +1081,9 @@ ccc_status ccc_3way_unit(const ccc_block* bp, int64_t p_lo, int64_t p_hi, const 
     a.checksum = reinterpret_cast<unsigned long long*>(checksum_d);
     CUtensorMap tmA, tmB;
     CCC_CHECK(make_tmap(&tmA, bm->N, bm->rows, k_pad, 128));
-    CCC_CHECK(make_tmap(&tmB, bn->N, bn->rows, k_pad, 128));   // per-CTA halves of the pair tile
+    // a caller's block: the permuted view only when its rows are a multiple of 8 and every
+    // column tile starts on a multiple of 8 (tiles start at n_lo + 256 K)
+    CCC_CHECK(make_tmap_b3(&tmB, bn->N, bn->rows, n_lo % 8 == 0 ? bn->rows : 0, k_pad, &a.permb));
     int64_t units = 0;
     CCC_CUDA(ccc::launch_tally3(tmA, tmB, a, sms, (cudaStream_t)stream, &units), "tally3 launch");
     if (units) g_launches = 1;

@@ -193,7 +193,9 @@ struct Tally3Args {
     int64_t ldG;
     int64_t rec_base;          // subtracted from every record index (stages)
     int64_t k_pad;
-    int32_t n_f, k_blocks, out_flags, pad_;
+    int32_t n_f, k_blocks, out_flags;
+    int32_t permb;             // B rows arrive permuted within 8 (tmB is the 4-D view of
+                               // make_tmap_b3): TMEM chunk columns (2j, 2j+1) hold n = j, j + 4
     uint32_t* tallies;         // [records][8]
     void* ccc;                 // [records][8] double or float
     unsigned long long* checksum;

@@ -320,6 +320,18 @@ __device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const void* tma
         : "memory");
 }
 
+// 4-D form (a permuted row view, see make_tmap_permb): coordinates (c0, c1, c2, c3).
+__device__ __forceinline__ void tma_load_4d_pair(void* smem_dst, const void* tmap, uint32_t bar_cluster,
+                                                 int32_t c0, int32_t c1, int32_t c2, int32_t c3,
+                                                 uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".L2::cache_hint [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+        "l"(policy)
+        : "memory");
+}
+
 // 1-D bulk copy whose completion is counted on a (possibly peer) cluster barrier.
 __device__ __forceinline__ void bulk_load_cluster(void* smem_dst, const void* gsrc, uint32_t bytes,
                                                   uint32_t bar_cluster) {

@@ -350,7 +350,10 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         const uint32_t rb = ready_leader + stage * 8u;
                         if (rank == 0) mbar_arrive_expect_tx(&ready[stage], 2 * kBBytes3);
                         else mbar_arrive_cluster(rb);
-                        tma_load_2d_pair(smB + stage * kBBytes3, &tmB, rb, kb * kBK, ncol, pol);
+                        if (args.permb)   // the 4-D row view: rows land permuted within 8
+                            tma_load_4d_pair(smB + stage * kBBytes3, &tmB, rb, kb * kBK, 0, 0, ncol / 8, pol);
+                        else
+                            tma_load_2d_pair(smB + stage * kBBytes3, &tmB, rb, kb * kBK, ncol, pol);
                     }
                     __syncwarp();
                     if (++stage == kStages3) { stage = 0; phase ^= 1; }
@@ -483,7 +486,13 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         const double inv8nf = 1.0 / (8.0 * (double)args.n_f);
         const uint32_t nf = (uint32_t)args.n_f;
         const int64_t nbp = args.bp.rows, nN = args.n_hi - args.n_lo, nM = args.m_hi - args.m_lo;
-        const uint32_t cpair = 2u * (lane & 3u);
+        // With args.permb the B rows arrive permuted within 8 (smem row 2b + a <- n = 4a + b),
+        // so the tcgen05.ld.16x256b columns (2j, 2j + 1) of a chunk hold n = j and n = j + 4:
+        // the 4 lanes of a row then store 4 consecutive records per instruction (half the L2
+        // sectors touched per 256-bit store; ~5% per FULL stage, profiles/r02_experiments.md).
+        // Without it (a caller's block whose row count is not a multiple of 8) n = 2j, 2j + 1.
+        const uint32_t cpair = args.permb ? (lane & 3u) : 2u * (lane & 3u);
+        const int32_t kHStep = args.permb ? 4 : 1;
         constexpr bool kRowG = O::pos(1) < O::pos(2);   // G_mn = G[gm][gn]: a row of G per m
         ColT3* coltab = reinterpret_cast<ColT3*>(smem + kColOff3);
         unsigned long long ck_lo = 0, ck_hi = 0;
@@ -617,7 +626,7 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             auto load_gmn = [&](int c, uint32_t (&g)[2][2]) {
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    int32_t nl = c * 8 + (int32_t)cpair + h;
+                    int32_t nl = c * 8 + (int32_t)cpair + kHStep * h;
                     nl = nl < gn_max ? nl : gn_max;
 #pragma unroll
                     for (int r = 0; r < 2; ++r) {
@@ -645,14 +654,14 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     load_gmn(c + 1, gnext);
                 }
                 const int32_t nA = c * 8 + (int32_t)cpair;    // local column of h = 0
-                const ColT3 cA = ct[nA], cB = ct[nA + 1];
+                const ColT3 cA = ct[nA], cB = ct[nA + kHStep];
 #pragma unroll
                 for (int r = 0; r < 2; ++r) {
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         // every record is computed; invalid ones (tile edges, j <= i) are
                         // only not stored, so the loop body has no branches
-                        const int32_t nl = nA + h;
+                        const int32_t nl = nA + kHStep * h;
                         const bool ok = nl > lo_r[r] && nl < nval;
                         const ColT3& cn = h ? cB : cA;
                         const uint32_t g3 = va[r * 2 + h];
