@@ -90,6 +90,15 @@ class CudaBackend:
         self.ccc.ccc_2way_block(N, s, w, 0, 0, ring.n_v, N, s, w, 0, True, self.n_f, 0,
                                 g=ring.G, ldg=ring.n_v)
 
+    def g_pair(self, ring, a, b):
+        """Pairwise G between blocks a < b (all of a's vectors precede b's) into the global G."""
+        N, s, w = ring.full
+        (alo, ahi), (blo, bhi) = ring.bounds[a], ring.bounds[b]
+        n_v = ring.n_v
+        Gv = ring.G.view(-1)[alo * n_v + blo:]
+        self.ccc.ccc_2way_block(N[alo:ahi], s[alo:ahi], w[alo:ahi], alo, 0, ahi - alo, N[blo:bhi], s[blo:bhi],
+                                w[blo:bhi], blo, False, self.n_f, 0, g=Gv, ldg=n_v)
+
     def _blk(self, ring, b):
         N, s, w = ring.full
         lo, hi = ring.bounds[b]
@@ -294,10 +303,10 @@ class Ring3Way:
     """Per-rank tetrahedral 3-way computation.  Every rank
     needs every block: a ring all-gather *with retention* of the packed blocks (P-1
     steps, NCCL send/recv) fills a full expanded N in place (blocks are contiguous
-    rows), overlapped with the rank's {A,A,A} unit, which needs only its own block and
-    the own-block part of G.  Then the pairwise G over all vectors (KB-2W, ~1/n_f of the
-    3-way work) and the remaining units.  Each unit is cut into pivot sub-ranges so
-    that no output buffer exceeds `max_records` (the paper's stages)."""
+    rows).  Each unit runs as soon as its blocks are resident, while the next block is in
+    flight: first the pairwise G among its blocks (KB-2W block GEMMs, ~1/n_f of the 3-way
+    work, each block pair once), then the unit cut into pivot sub-ranges so that no output
+    buffer exceeds `max_records` (the paper's stages)."""
 
     def __init__(self, backend, bounds, rank: int, world: int, max_records: int, group=None):
         self.be = backend
@@ -334,12 +343,18 @@ class Ring3Way:
     def run(self, packed_own, sink=None):
         """One pass; sink(unit, p_lo, p_hi, outputs) receives each piece's records (on the
         device, in a buffer the next piece overwrites: copy on the current stream to keep
-        them; the default drops them after the checksum fold)."""
+        them; the default drops them after the checksum fold).
+
+        Every unit runs as soon as its three blocks have arrived -- while the next block is
+        in flight round the ring -- after the pairwise G among those blocks (the epilogue's
+        G_pm, G_pn, G_mn) has been computed block pair by block pair."""
         be, r, P = self.be, self.rank, self.P
         lo, hi = self.bounds[r]
         be.expand_into(packed_own, self.full, lo, hi)
-        be.g_block(self, r, r)
-        self.launches = 2
+        self.launches = 1
+        self.arrived = {r}
+        self.g_done = set()
+        done = [False] * len(self.units)
         cur = packed_own
         reqs = []
         for d in range(P):
@@ -348,32 +363,47 @@ class Ring3Way:
                 nb = (r + d + 1) % P
                 nxt = self.recv[d % 2][: self.bounds[nb][1] - self.bounds[nb][0]]
                 reqs = ring_shift(cur, nxt, r, P, self.group)
-            if d == 0:   # own-block unit overlaps the gather
-                self.launches += self._run_units(lambda u: u.pb == u.mb == u.nb, sink)
+            self._run_ready(done, sink)          # overlaps the block in flight
             for q in reqs:
                 q.wait()
             reqs = []
             if nxt is not None:
                 nb = (r + d + 1) % P
                 be.expand_into(nxt, self.full, *self.bounds[nb])
+                self.arrived.add(nb)
                 self.launches += 1
                 cur = nxt
-        be.g_full(self)
-        self.launches += 1
-        self.launches += self._run_units(lambda u: not (u.pb == u.mb == u.nb), sink)
+        self._run_ready(done, sink)
+        assert all(done)
         return self.ck
 
-    def _run_units(self, pick, sink):
-        n = 0
-        for u in self.units:
-            if not pick(u):
+    def _g(self, a, b):
+        """The pairwise G of blocks a, b (once per pass)."""
+        a, b = min(a, b), max(a, b)
+        if (a, b) in self.g_done:
+            return
+        if a == b:
+            self.be.g_block(self, a, a)
+        else:
+            self.be.g_pair(self, a, b)
+        self.g_done.add((a, b))
+        self.launches += 1
+
+    def _run_ready(self, done, sink):
+        for k, u in enumerate(self.units):
+            blocks = {u.pb, u.mb, u.nb}
+            if done[k] or not blocks <= self.arrived:
                 continue
+            for a in blocks:
+                for b in blocks:
+                    if a <= b:
+                        self._g(a, b)
             for plo, phi in self._pieces(u):
                 out = self.be.unit(self, u, plo, phi, self.ck)
-                n += 1
+                self.launches += 1
                 if sink is not None:
                     sink(u, plo, phi, out)
-        return n
+            done[k] = True
 
 
 def checksum_total(ck_local: torch.Tensor, group=None) -> int:

@@ -212,7 +212,11 @@ class Oracle3Backend(OracleBackend):
         full[0][lo:hi] = packed
 
     def g_block(self, ring, a, b):
-        pass
+        ring.g_log = getattr(ring, "g_log", set()) | {(a, b)}
+
+    def g_pair(self, ring, a, b):
+        assert a < b and {a, b} <= ring.arrived        # both blocks resident
+        ring.g_log = getattr(ring, "g_log", set()) | {(a, b)}
 
     def g_full(self, ring):
         pass
@@ -222,6 +226,10 @@ class Oracle3Backend(OracleBackend):
                                                u.n_lo, u.n_hi, u.order), ring.bounds)
 
     def unit(self, ring, u, p_lo, p_hi, ck):
+        # a unit runs only once its blocks are resident and their pairwise G is computed
+        blocks = {u.pb, u.mb, u.nb}
+        assert blocks <= ring.arrived
+        assert all((a, b) in ring.g_log for a in blocks for b in blocks if a <= b)
         sub = decomp.Unit3(u.pb, p_lo, p_hi, u.mb, u.m_lo, u.m_hi, u.nb, u.n_lo, u.n_hi, u.order)
         tr = np.array(list(decomp.unit3_triples(sub, ring.bounds)), dtype=np.int64).reshape(-1, 3)
         codes = ring.full[0].numpy()
@@ -252,7 +260,7 @@ def _worker3(rank, world, port, n_v, n_f, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])
 def test_ring_3way_gloo(world):
     n_v, n_f = 17, 29
     ctx = mp.get_context("spawn")
