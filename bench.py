@@ -751,7 +751,62 @@ def run_3way_single(args, wl):  # noqa: C901
         else:
             res["parity"] = {"records": 0, "mismatches": None,
                              "note": "CHECKSUM mode stores no record (covered by tests/)"}
+    if getattr(args, "e2e", False) and not (sparse or paper) and wl.get("flags") is None:
+        # theta from the last stage's records still in C (largest CCC cell per record)
+        mx = C[: ccc.ccc_stage_range(n_v, n_st, n_st - 1)[3]].max(dim=1).values
+        del T, C
+        torch.cuda.empty_cache()
+        res["e2e_compacted"] = run_3way_e2e_compacted(args, wl, codes, mx)
     return res
+
+
+def run_3way_e2e_compacted(args, wl, codes_dev, mx_last, keep_last=100):
+    """3-way in the paper's production output mode end to end: per step the
+    packed input goes H2D, ccc_3way_prepare + every stage with threshold compaction, the
+    kept records come back D2H.  theta keeps `keep_last` records of the last stage (about
+    1e-7 of all triples of this input), taken from the FULL run's last-stage CCC."""
+    import torch
+
+    from paper_1705_08213_b200 import ccc
+    n_v, n_f, n_st = wl["n_v"], wl["n_f"], wl["n_st"]
+    flags = ccc.OUT_TALLY | ccc.OUT_CCC_F64
+    theta = float(torch.kthvalue(mx_last, mx_last.numel() - keep_last).values)
+    cap = 1 << 16
+    cp = ccc.Compact(theta, cap, 8, flags)
+    packed_d = ccc.ccc_pack(codes_dev)
+    packed_h = packed_d.cpu().pin_memory()
+    ws = ccc.workspace(3, n_v, n_f)
+    cnt_h = torch.empty(1, dtype=torch.int64, pin_memory=True)
+    keys_h = torch.empty(cap, dtype=torch.int64, pin_memory=True)
+    T_h = torch.empty((cap, 8), dtype=torch.int32, pin_memory=True)
+    C_h = torch.empty((cap, 8), dtype=torch.float64, pin_memory=True)
+
+    def step():
+        packed_d.copy_(packed_h, non_blocking=True)
+        cp.reset()
+        ccc.ccc_3way_prepare(packed_d, n_f, ccc.GAMMA, ws)
+        for st in range(n_st):
+            ccc.ccc_3way_stage(n_v, n_f, n_st, st, ws, flags, compact=cp)
+        cnt_h.copy_(cp.count, non_blocking=True)
+        keys_h.copy_(cp.keys, non_blocking=True)
+        T_h.copy_(cp.tallies, non_blocking=True)
+        C_h.copy_(cp.ccc, non_blocking=True)
+        torch.cuda.synchronize()
+        return int(cnt_h[0])
+
+    kept = step()
+    steps = max(1, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        kept = step()
+    dt = (time.perf_counter() - t0) / steps
+    tot = comparisons(3, n_v, n_f) // n_f
+    return {"value": comparisons(3, n_v, n_f) / dt, "unit": UNIT, "h2d_bytes_per_step": packed_h.numel(),
+            "d2h_bytes_per_step": 8 + cap * (8 + 32 + 64), "steps": steps, "ms_per_step": dt * 1e3,
+            "theta": theta, "kept_records": kept, "kept_fraction": kept / tot,
+            "api": "ccc_3way_prepare + ccc_3way_stage x 16 with ccc_compact: pinned packed input in, the "
+                   "kept records + their count out (the whole capacity buffer is copied back)",
+            "note": "the paper's production output mode (P:1089-1095); the FULL line above stores every record"}
 
 
 # ------------------------------------------------------------------------ reporting
