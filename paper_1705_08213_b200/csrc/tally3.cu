@@ -870,7 +870,9 @@ cudaError_t launch_tally3(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
         }
     }
     if (a.exact23) {
-        if (a.compact) return pick(T{}, T{}, F{});
+        // compaction (the paper's production mode) with tallies + fp64 CCC: the one-DFMA
+        // cell formula of the FULL epilogue for the threshold test as well
+        if (a.compact) return (a.exact52 && a.out_flags == 3) ? pick(T{}, T{}, T{}) : pick(T{}, T{}, F{});
         return full ? pick(T{}, F{}, T{}) : pick(T{}, F{}, F{});
     }
     return a.compact ? pick(F{}, T{}, F{}) : pick(F{}, F{}, F{});
