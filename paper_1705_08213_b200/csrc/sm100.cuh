@@ -443,6 +443,14 @@ __device__ __forceinline__ void stg_256_f64_if(bool ok, void* p, double a, doubl
         "d"(a), "d"(b), "d"(c), "d"(d), "r"((uint32_t)ok)
         : "memory");
 }
+// predicated, plain caching (the 2-way FULL epilogue: branch-free, L1 allocation as usual)
+__device__ __forceinline__ void stg_256_f64_p(bool ok, void* p, double a, double b, double c, double d) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+        "@q st.global.v4.f64 [%0], {%1,%2,%3,%4};\n\t}" ::"l"(p),
+        "d"(a), "d"(b), "d"(c), "d"(d), "r"((uint32_t)ok)
+        : "memory");
+}
 __device__ __forceinline__ void stg_256_f64(void* p, double a, double b, double c, double d) {
     asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
                  : "memory");

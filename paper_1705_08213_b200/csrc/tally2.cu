@@ -89,7 +89,9 @@ __device__ __forceinline__ void emit2(const Tally2Args& a, uint64_t key, uint32_
                     __float_as_uint((float)c01), __float_as_uint((float)c10), __float_as_uint((float)c11));
 }
 
-template <int kPair, bool kCompact, bool kSparse>
+// kFull: the FULL headline output (tallies + fp64 CCC, gamma = 2/3 with 12 n_f^2 < 2^52, no
+// raw G, no export, no checksum) as a flag-free epilogue: straight-line record code.
+template <int kPair, bool kCompact, bool kSparse, bool kFull = false>
 __global__ void __launch_bounds__(kThreads2, 1)
 tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const Tally2Args args) {
@@ -338,14 +340,15 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         const int c_end = c_begin + kBN / 8 / (kEpiWarps2 / 4);
         const int64_t nB = args.nB, a_end = args.a_lo + args.nA;
         const uint32_t fl = (uint32_t)args.out_flags;
-        const bool want_t = fl & 1u, want_c64 = fl & 2u, want_c32 = fl & 4u, want_ck = fl & 8u;
+        const bool want_t = kFull || (fl & 1u), want_c64 = kFull || (fl & 2u);
+        const bool want_c32 = !kFull && (fl & 4u), want_ck = !kFull && (fl & 8u);
         const bool want_c = want_c64 | want_c32;
         const uint32_t nf = (uint32_t)args.n_f;
         const uint32_t four_nf = 4u * nf;
         const double inv4nf = 1.0 / (4.0 * (double)args.n_f);
-        const bool exact23 = args.exact23 != 0;
+        const bool exact23 = kFull || args.exact23 != 0;
         // gamma = 2/3 and 12 n_f^2 < 2^52: the single-DFMA cell form below
-        const bool exact52 = exact23 && (uint64_t)12 * nf * nf < (1ull << 52);
+        const bool exact52 = kFull || (exact23 && (uint64_t)12 * nf * nf < (1ull << 52));
         const uint32_t tempty_leader = kPair == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
         const int32_t cpair = 2 * (int32_t)(lane & 3);   // my 2 columns within a chunk
         unsigned long long ck_lo = 0, ck_hi = 0;
@@ -433,7 +436,7 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     const uint32_t gB = (r >> 1) ? vb[(r & 1) * 2 + 1] : va[(r & 1) * 2 + 1];
                     const bool okA = jA >= jlo_r[r] && jA < jhi_r[r];
                     const bool okB = jB >= jlo_r[r] && jB < jhi_r[r];
-                    if (args.xp_ptrs && (okA | okB)) {
+                    if (!kFull && args.xp_ptrs && (okA | okB)) {
                         // f3 field split: this field slice's partial G of the tile goes
                         // straight to the owner's slot (a peer-mapped pointer over NVLink
                         // on a multi-GPU run), overlapped with the MMAs of later tiles
@@ -536,8 +539,13 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                             stg_256_f64_if(stA, p, ca00, ca01, ca10, ca11);
                             stg_256_f64_if(stB, p + 4, cb00, cb01, cb10, cb11);
 #else
-                            if (stA) stg_256_f64(p, ca00, ca01, ca10, ca11);
-                            if (stB) stg_256_f64(p + 4, cb00, cb01, cb10, cb11);
+                            if constexpr (kFull) {   // branch-free
+                                stg_256_f64_p(stA, p, ca00, ca01, ca10, ca11);
+                                stg_256_f64_p(stB, p + 4, cb00, cb01, cb10, cb11);
+                            } else {
+                                if (stA) stg_256_f64(p, ca00, ca01, ca10, ca11);
+                                if (stB) stg_256_f64(p + 4, cb00, cb01, cb10, cb11);
+                            }
 #endif
                         } else {
                             float* p = reinterpret_cast<float*>(args.ccc) + 4 * recA;
@@ -557,7 +565,7 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         }
                     }
                     }
-                    if (args.g_out) {
+                    if (!kFull && args.g_out) {
                         const int64_t row = (int64_t)(gi[r] - (uint64_t)args.a_row0);
                         if (okA) args.g_out[row * args.ldg + jA] = (int32_t)gA;
                         if (okB) args.g_out[row * args.ldg + jB] = (int32_t)gB;
@@ -647,7 +655,10 @@ cudaError_t launch_tally2(const CUtensorMap& tmA, const CUtensorMap& tmB, const 
         kern<<<grid, kThreads2, Cfg2<1>::kSmem, stream>>>(tmA, tmB, a2);
         return cudaGetLastError();
     }
+    const bool full = !a.sparse && !a.compact && a.out_flags == 3 && a.exact23 && !a.g_out && !a.xp_ptrs &&
+                      (uint64_t)12 * (uint64_t)a.n_f * (uint64_t)a.n_f < (1ull << 52);
     auto kern = a.sparse ? (a.compact ? tally2_kernel<2, true, true> : tally2_kernel<2, false, true>)
+                : full   ? tally2_kernel<2, false, false, true>
                          : (a.compact ? tally2_kernel<2, true, false> : tally2_kernel<2, false, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg2<2>::kSmem);
