@@ -112,7 +112,9 @@ def test_2way_C1_full():
 def test_2way_ragged_shapes(n_v, n_f):
     if n_v * n_v * n_f > 2e8:
         pytest.skip("covered by smaller combos")
-    _check_2way_full(_codes("random", n_v, n_f, seed=n_v * 1000 + n_f))
+    codes = _codes("random", n_v, n_f, seed=n_v * 1000 + n_f)
+    _check_2way_full(codes)                        # generic epilogue (+ checksum)
+    _check_2way_full(codes, flags=TAL | F64)       # the flag-free FULL specialisation
 
 
 @pytest.mark.parametrize("kind", ["hwe", "planted"])
