@@ -82,18 +82,39 @@ def _s_full_check(codes_dev, s, w, n_f):
 
 
 def test_C2_planted_every_record():
-    """configs[1] 20,000 x 50,000, planted input: all 199,990,000 records (9.6 GB)."""
+    """configs[1] 20,000 x 50,000, planted input, through bench.py's step (ccc_2way_codes:
+    expand_codes + the flag-free FULL tally kernel): all 199,990,000 records (9.6 GB)."""
     n_v, n_f = 20000, 50000
     codes, L, H, _ = synthgen.planted_codes(n_v, n_f, seed=3, device="cuda")
-    packed = ccc.ccc_pack(codes)
-    N, s, w = ccc.ccc_expand(packed, n_f)
+    N, s, w = ccc.ccc_expand_codes(codes)
     _s_full_check(codes, s, w, n_f)
     np.testing.assert_array_equal(s.cpu().numpy(), oracle.planted_sums(L, H, n_f)[:, 1])
-    del codes, packed
+    del N, s, w
     m = ccc.ccc_num_unique(2, n_v)
     T = torch.empty((m, 4), dtype=torch.int32, device="cuda")
     C = torch.empty((m, 4), dtype=torch.float64, device="cuda")
-    ccc.ccc_2way_block(N, s, w, 0, 0, n_v, N, s, w, 0, True, n_f, TAL | F64, T, C)
+    ccc.ccc_2way_codes(codes, ccc.GAMMA, TAL | F64, T, C)
+    del codes
+    r = check_records(2, L, H, n_f, 0, T, C)
+    assert r["records"] == m
+    assert (r["bad_tallies"], r["bad_ccc"]) == (0, 0), r
+    assert r["max_rel"] <= 1e-12
+
+
+def test_C2_planted_every_record_packed_path():
+    """The same on the packed path (pack + expand + ccc_2way_block: the ring's kernels)."""
+    n_v, n_f = 20000, 50000
+    codes, L, H, _ = synthgen.planted_codes(n_v, n_f, seed=3, device="cuda")
+    packed = ccc.ccc_pack(codes)
+    del codes
+    N, s, w = ccc.ccc_expand(packed, n_f)
+    np.testing.assert_array_equal(s.cpu().numpy(), oracle.planted_sums(L, H, n_f)[:, 1])
+    del packed
+    m = ccc.ccc_num_unique(2, n_v)
+    T = torch.empty((m, 4), dtype=torch.int32, device="cuda")
+    C = torch.empty((m, 4), dtype=torch.float64, device="cuda")
+    ccc.ccc_2way_block(N, s, w, 0, 0, n_v, N, s, w, 0, True, n_f, TAL | F64 | ccc.OUT_CHECKSUM, T, C,
+                       torch.zeros(2, dtype=torch.int64, device="cuda"))
     r = check_records(2, L, H, n_f, 0, T, C)
     assert r["records"] == m
     assert (r["bad_tallies"], r["bad_ccc"]) == (0, 0), r
@@ -107,6 +128,8 @@ def test_C2_timing_input_allele_sums_full():
     codes = synthgen.random_codes(n_v, n_f, seed=1, device="cuda")
     N, s, w = ccc.ccc_expand(ccc.ccc_pack(codes), n_f)
     _s_full_check(codes, s, w, n_f)
+    N2, s2, w2 = ccc.ccc_expand_codes(codes)       # the bench step's fused pass: bit-identical
+    assert bool((N2 == N).all()) and bool((s2 == s).all()) and bool((w2 == w).all())
 
 
 def test_C4_planted_every_record_all_stages():
