@@ -173,3 +173,16 @@ def test_grid_processes_one_gpu(shape, max_rec):
     codes = synthgen.random_codes(n_v, n_f, seed=23)
     To, _ = oracle.all_pairs(codes)
     assert total == oracle.checksum(2, oracle.pair_list(n_v), To)
+
+
+@pytest.mark.parametrize("shape", [(2, 1, 2), (2, 2, 2), (4, 1, 2)])
+def test_grid_simulated_C2_size_checksum(shape):
+    """configs[1] (20,000 x 50,000) on simulated grids: every rank's export/finish work on one
+    GPU; the ranks' checksums (every record's tallies and global indices) sum to the
+    checksum of the single-GPU path."""
+    n_v, n_f = 20000, 50000
+    codes = synthgen.random_codes(n_v, n_f, seed=1, device="cuda")
+    _, _, k1 = ccc.ccc_2way_codes(codes, out_flags=CK)
+    _, k2 = gridmod.run_grid_simulated(codes, decomp.Grid(*shape), CK, align=256)
+    torch.cuda.synchronize()
+    assert ccc.checksum_int(k1) == ccc.checksum_int(k2)
