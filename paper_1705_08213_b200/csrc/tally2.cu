@@ -216,6 +216,9 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     const uint64_t ad = a_desc0 + ((stage * C::kABytes) >> 4);
                     const uint64_t bd = b_desc0 + ((stage * C::kBBytes) >> 4);
                     if (elect_one()) {
+#ifdef CCC_D2_NOMMA   // diagnostics: no MMAs (the accumulator holds stale values; timing only)
+                        if (false)
+#endif
 #pragma unroll
                         for (int k = 0; k < kBK / kUMMA_K; ++k) {
                             if constexpr (kPair == 2)
