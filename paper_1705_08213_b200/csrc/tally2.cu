@@ -543,8 +543,17 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                             stg_256_f64_if(stB, p + 4, cb00, cb01, cb10, cb11);
 #else
                             if constexpr (kFull) {   // branch-free
+#if defined(CCC_D2_NOCCCST)   // diagnostics: CCC computed, never stored (kept alive by a test)
+                                const bool never = recA < -1;
+                                stg_256_f64_p(never && stA, p, ca00, ca01, ca10, ca11);
+                                stg_256_f64_p(never && stB, p + 4, cb00, cb01, cb10, cb11);
+#elif defined(CCC_D2_CCCCONST)   // diagnostics: CCC bytes stored, no FP64 / 64-bit math
+                                stg_256_f64_p(stA, p, magic52(a00), magic52(a01), magic52(a10), magic52(a11));
+                                stg_256_f64_p(stB, p + 4, magic52(b00), magic52(b01), magic52(b10), magic52(b11));
+#else
                                 stg_256_f64_p(stA, p, ca00, ca01, ca10, ca11);
                                 stg_256_f64_p(stB, p + 4, cb00, cb01, cb10, cb11);
+#endif
                             } else {
                                 if (stA) stg_256_f64(p, ca00, ca01, ca10, ca11);
                                 if (stB) stg_256_f64(p + 4, cb00, cb01, cb10, cb11);

@@ -326,7 +326,11 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 int64_t p;
                 if (!sch.get(u, J, K, p)) break;
                 const int8_t* prow = args.bp.N + p * args.k_pad;
+#ifdef CCC_D3_SAMEA   // diagnostics: both CTAs of the pair load the same A rows (timing only)
+                const int32_t mrow = (int32_t)sch.row0(J);
+#else
                 const int32_t mrow = (int32_t)(sch.row0(J) + rank * 128);
+#endif
                 const int32_t ncol = (int32_t)(sch.col0(K) + rank * 128);
                 for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
                     mbar_wait_sleep(&empty[stage], phase ^ 1);
@@ -348,8 +352,14 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                                   &aload[stage]);
                         // B half -> the leader's ready barrier
                         const uint32_t rb = ready_leader + stage * 8u;
+#ifdef CCC_D3_NOB   // diagnostics: no B loads (stale B tiles; timing only)
+                        if (rank == 0) mbar_arrive(&ready[stage]);
+                        else mbar_arrive_cluster(rb);
+                        if (true) {} else
+#else
                         if (rank == 0) mbar_arrive_expect_tx(&ready[stage], 2 * kBBytes3);
                         else mbar_arrive_cluster(rb);
+#endif
                         if (args.permb)   // the 4-D row view: rows land permuted within 8
                             tma_load_4d_pair(smB + stage * kBBytes3, &tmB, rb, kb * kBK, 0, 0, ncol / 8, pol);
                         else
