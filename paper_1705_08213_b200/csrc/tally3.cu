@@ -611,6 +611,9 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 else
                     rec_r[r] = ((p - args.p_lo) * nM + (mc - args.m_lo)) * nN - args.n_lo;
                 rec_r[r] += col0;   // record of local column 0
+#ifdef CCC_D3_COMPACTADDR   // diagnostics: each unit writes one contiguous 64K-record block
+                rec_r[r] = ((u % 1024) * 256 + rank * 128 + quad * 32 + half * 16 + r * 8 + (lane >> 2)) * 256;
+#endif
                 // n > m is needed only when m and n share a block
                 const int64_t lo = args.same_mn ? m - col0 : -1;
                 lo_r[r] = !ok ? kBN : lo < -1 ? -1 : lo > kBN ? kBN : (int32_t)lo;
