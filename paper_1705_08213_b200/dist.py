@@ -447,12 +447,21 @@ class _World:
 
     def __init__(self):
         self.P = int(os.environ.get("WORLD_SIZE", "1"))
+        # CCC_DIST_BACKEND=gloo is the functional test of this N > 1 path on a one-GPU box:
+        # the ranks share the visible GPU(s) and the ring moves packed blocks through host
+        # memory (ring_shift); a timing taken that way is not a multi-GPU number.
+        self.backend = os.environ.get("CCC_DIST_BACKEND", "nccl")
         if self.P > 1:
-            dist.init_process_group("nccl")
+            dist.init_process_group(self.backend)
             self.rank, self.P = dist.get_rank(), dist.get_world_size()
         else:
             self.rank = 0
         self.local = int(os.environ.get("LOCAL_RANK", self.rank))
+        if self.backend == "gloo":
+            global _SHARE
+            n_dev = torch.cuda.device_count()
+            self.local %= n_dev
+            _SHARE = -(-self.P // n_dev)
         torch.cuda.set_device(self.local)
 
     def barrier(self):
@@ -472,9 +481,15 @@ class _World:
             dist.destroy_process_group()
 
 
+_SHARE = 1   # ranks per GPU: > 1 only under the gloo test hook (_World)
+
+
 def record_budget(bytes_per_record: int, reserve_bytes: int) -> int:
-    """Records that fit in the free HBM after `reserve_bytes` more are set aside."""
-    free, _ = torch.cuda.mem_get_info()
+    """Records that fit in the free HBM after `reserve_bytes` more are set aside (ranks that
+    share a GPU under the test hook each get an equal part of its total memory)."""
+    free, total = torch.cuda.mem_get_info()
+    if _SHARE > 1:
+        free = total // _SHARE
     return max(1, int((free - reserve_bytes - (6 << 30)) // bytes_per_record))
 
 
@@ -700,6 +715,10 @@ def bench_main(args, wl, metric, unit):  # noqa: C901
                 "tensor": {"int8_pipe_at_clock": {"sm_mhz": mhz, "TOPS": pipe, "step_frac": step_tops / pipe},
                            "nominal_int8": {"TOPS": NOMINAL_INT8_TOPS,
                                             "step_frac": step_tops / NOMINAL_INT8_TOPS}}}
+        if W.backend != "nccl":
+            out["transport"] = ("%s test hook (CCC_DIST_BACKEND): %d ranks share %d GPU(s), blocks staged "
+                                "through host memory; a functional run of the N > 1 path, not a "
+                                "multi-GPU timing" % (W.backend, P, torch.cuda.device_count()))
         out["e2e"] = e2e
         if e2e is None:
             out["e2e_note"] = ("not measured on this workload: one step's records (%.0f GB) are "
