@@ -347,7 +347,12 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     if (elect_one()) {
                         // own A half + pivot chunk -> local barrier (the transform warps wait)
                         mbar_arrive_expect_tx(&aload[stage], kABytes3 + kPivBytes);
+#ifdef CCC_D3_MCA   // diagnostics: the leader's A rows multicast to both CTAs (timing only)
+                        if (rank == 0)
+                            tma_load_2d_mc(smA + stage * kABytes3, &tmA, &aload[stage], kb * kBK, mrow, 3, pol);
+#else
                         tma_load_2d(smA + stage * kABytes3, &tmA, &aload[stage], kb * kBK, mrow, pol);
+#endif
                         bulk_load(smP + stage * kPivBytes, prow + (int64_t)kb * kBK, kPivBytes,
                                   &aload[stage]);
                         // B half -> the leader's ready barrier
