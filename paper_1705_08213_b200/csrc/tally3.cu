@@ -619,6 +619,15 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
 #ifdef CCC_D3_COMPACTADDR   // diagnostics: each unit writes one contiguous 64K-record block
                 rec_r[r] = ((u % 1024) * 256 + rank * 128 + quad * 32 + half * 16 + r * 8 + (lane >> 2)) * 256;
 #endif
+#ifdef CCC_D3_SPREADADDR    // diagnostics: the same blocks 4M records (128 / 256 MB) apart
+                rec_r[r] = (u % 160) * 4194304 + (int64_t)(rank * 128 + quad * 32 + half * 16 + r * 8 + (lane >> 2)) * 256;
+#endif
+#ifdef CCC_D3_ODDADDR       // diagnostics: as STRIDEADDR with rows 4,093 records apart (unaligned)
+                rec_r[r] = (u % 160) * 4194304 + (int64_t)(rank * 128 + quad * 32 + half * 16 + r * 8 + (lane >> 2)) * 4093;
+#endif
+#ifdef CCC_D3_STRIDEADDR    // diagnostics: contiguous unit blocks, rows 4,096 records apart
+                rec_r[r] = (u % 160) * 4194304 + (int64_t)(rank * 128 + quad * 32 + half * 16 + r * 8 + (lane >> 2)) * 4096;
+#endif
                 // n > m is needed only when m and n share a block
                 const int64_t lo = args.same_mn ? m - col0 : -1;
                 lo_r[r] = !ok ? kBN : lo < -1 ? -1 : lo > kBN ? kBN : (int32_t)lo;
@@ -637,17 +646,41 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             // column groups of 8 that hold any valid n (warp-uniform): up to the last valid
             // column, and from the first group with an n above the warp's lowest row bound
             // (on the diagonal tiles of a triangle the groups left of it are all masked)
-            const int c_end = !any_row ? 0 : (nval + 7) / 8;
+            // Aligned record groups (permb): the 4 lanes of a row hold n = j and j + 4 of a
+            // chunk (j = lane % 4), so one store instruction per row writes 4 consecutive
+            // records.  A row's records start at an arbitrary index (the lexicographic layout),
+            // so each lane takes the record of column n - d_r instead, d_r = (row's record
+            // index of column 0) mod 4: every row-instruction then covers whole 128-B lines
+            // (4 x 32 B tallies, 2 x 128 B of CCC) instead of straddling two or three.  The
+            // accumulator values move with one shuffle per (row, h) among the row's 4 lanes;
+            // n - d_r < 0 takes the previous chunk's h = 1 value, and one extra chunk writes
+            // the last d_r columns.  G_mn and the column terms are read at n - d_r directly.
+            int32_t dl[2] = {0, 0};
+            uint32_t srcl[2] = {lane, lane};
+            bool geq[2] = {true, true};
+            if (args.permb) {
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    dl[r] = (int32_t)(((rec_r[r] % 4) + 4) % 4);
+                    srcl[r] = (lane & ~3u) | ((cpair - (uint32_t)dl[r]) & 3u);
+                    geq[r] = (int32_t)cpair >= dl[r];
+                }
+            }
+            constexpr int kChunks = kBN / 8;
+            const int c_end = !any_row ? 0
+                              : args.permb ? ((nval + 10) / 8 < kChunks + 1 ? (nval + 10) / 8 : kChunks + 1)
+                                           : (nval + 7) / 8;
             const int32_t lo_w = __reduce_min_sync(0xffffffffu, lo_r[0] < lo_r[1] ? lo_r[0] : lo_r[1]);
             const int c_beg = lo_w < 0 ? 0 : (lo_w + 1) / 8;
-            // G_mn for column group c: g[r][h] = G(m_r, col0 + 8c + cpair + h), clamped
+            // G_mn for column group c: g[r][h] = G(m_r, col0 + 8c + cpair + kHStep h - d_r),
+            // clamped to the block
             auto load_gmn = [&](int c, uint32_t (&g)[2][2]) {
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    int32_t nl = c * 8 + (int32_t)cpair + kHStep * h;
-                    nl = nl < gn_max ? nl : gn_max;
 #pragma unroll
                     for (int r = 0; r < 2; ++r) {
+                        int32_t nl = c * 8 + (int32_t)cpair + kHStep * h - dl[r];
+                        nl = nl < 0 ? 0 : nl < gn_max ? nl : gn_max;
                         if constexpr (kMode != 0) g[r][h] = 0u;   // paper-route passes: no G
                         else if constexpr (kRowG) g[r][h] = (uint32_t)__ldg(grow[r] + nl);
                         else g[r][h] = (uint32_t)__ldg(args.G + (gcol0 + nl) * args.ldG + gm_r[r]);
@@ -661,28 +694,47 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             tc_fence_after();
             if (tr && lane == 0) tr[4] = globaltimer();
             const uint32_t taddr = tmem_base + ((quad * 32u + half * 16u) << 16) + acc * kBN;
-            uint32_t vnext[4];
-            if (c_beg < c_end) tmem_ld_16x256(taddr + c_beg * 8, vnext);
+            uint32_t vnext[4] = {0u, 0u, 0u, 0u};
+            if (c_beg < c_end && c_beg < kChunks) tmem_ld_16x256(taddr + c_beg * 8, vnext);
+            uint32_t prev1[2] = {0u, 0u};   // the previous chunk's h = 1 value from lane srcl[r]
             for (int c = c_beg; c < c_end; ++c) {
-                tmem_ld_wait_keep(vnext);
-                const uint32_t va[4] = {vnext[0], vnext[1], vnext[2], vnext[3]};
+                uint32_t va[4] = {0u, 0u, 0u, 0u};
+                if (c < kChunks) {                       // warp-uniform
+                    tmem_ld_wait_keep(vnext);
+                    va[0] = vnext[0];
+                    va[1] = vnext[1];
+                    va[2] = vnext[2];
+                    va[3] = vnext[3];
+                }
                 const uint32_t gcur[2][2] = {{gnext[0][0], gnext[0][1]}, {gnext[1][0], gnext[1][1]}};
                 if (c + 1 < c_end) {
-                    tmem_ld_16x256(taddr + (c + 1) * 8, vnext);
+                    if (c + 1 < kChunks) tmem_ld_16x256(taddr + (c + 1) * 8, vnext);
                     load_gmn(c + 1, gnext);
                 }
-                const int32_t nA = c * 8 + (int32_t)cpair;    // local column of h = 0
-                const ColT3 cA = ct[nA], cB = ct[nA + kHStep];
+                uint32_t g3v[2][2];
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    if (args.permb) {
+                        const uint32_t s0 = __shfl_sync(0xffffffffu, va[r * 2], srcl[r]);
+                        const uint32_t s1 = __shfl_sync(0xffffffffu, va[r * 2 + 1], srcl[r]);
+                        g3v[r][0] = geq[r] ? s0 : prev1[r];
+                        g3v[r][1] = geq[r] ? s1 : s0;
+                        prev1[r] = s1;
+                    } else {
+                        g3v[r][0] = va[r * 2];
+                        g3v[r][1] = va[r * 2 + 1];
+                    }
+                }
 #pragma unroll
                 for (int r = 0; r < 2; ++r) {
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         // every record is computed; invalid ones (tile edges, j <= i) are
                         // only not stored, so the loop body has no branches
-                        const int32_t nl = nA + kHStep * h;
+                        const int32_t nl = c * 8 + (int32_t)cpair + kHStep * h - dl[r];
                         const bool ok = nl > lo_r[r] && nl < nval;
-                        const ColT3& cn = h ? cB : cA;
-                        const uint32_t g3 = va[r * 2 + h];
+                        const ColT3& cn = ct[nl < 0 ? 0 : nl < kBN ? nl : kBN - 1];
+                        const uint32_t g3 = g3v[r][h];
                         if constexpr (kMode == 1) {
                             // sparse form pass: the raw trilinear form of this pass
                             const int64_t rec = rec_r[r] + nl;
