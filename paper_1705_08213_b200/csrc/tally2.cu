@@ -383,6 +383,12 @@ tally2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 wi1[r] = (row_ok && !exact23) ? __ldg(args.w_a + 2 * i + 1) * inv4nf : 0.0;
                 rec_r[r] = args.diag ? (i * (2 * nB - i - 1)) / 2 - i - 1 - args.rec_row_base
                                      : (i - args.a_lo) * nB;
+#ifdef CCC_D2_ALIGNADDR   // diagnostics: every row's records start at a multiple of 8 (timing only)
+                rec_r[r] = (rec_r[r] + 8) & ~(int64_t)7;
+#endif
+#ifdef CCC_D2_ALIGN2ADDR  // diagnostics: every row's records start at a multiple of 2 (timing only)
+                rec_r[r] = (rec_r[r] + 2) & ~(int64_t)1;
+#endif
                 jlo_r[r] = args.diag ? (int32_t)(i + 1) : 0;
                 jhi_r[r] = row_ok ? (int32_t)nB : 0;
                 gi[r] = (uint64_t)(args.a_row0 + i);
