@@ -733,7 +733,11 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         // only not stored, so the loop body has no branches
                         const int32_t nl = c * 8 + (int32_t)cpair + kHStep * h - dl[r];
                         const bool ok = nl > lo_r[r] && nl < nval;
+#if defined(CCC_D3_CTNOSHIFT)   // diagnostics: rows share the unshifted column terms (values wrong)
+                        const ColT3& cn = ct[c * 8 + (int32_t)cpair + kHStep * h < kBN ? c * 8 + (int32_t)cpair + kHStep * h : kBN - 1];
+#else
                         const ColT3& cn = ct[nl < 0 ? 0 : nl < kBN ? nl : kBN - 1];
+#endif
                         const uint32_t g3 = g3v[r][h];
                         if constexpr (kMode == 1) {
                             // sparse form pass: the raw trilinear form of this pass
