@@ -15,6 +15,9 @@ To, _ = oracle.all_pairs(codes)
 assert np.array_equal(T.cpu().numpy().astype(np.int64) & 0xFFFFFFFF, To)
 codes = synthgen.random_codes(150, 200, seed=4)
 T, C, ck = ccc.three_way(codes.cuda(), out_flags=F, n_stages=2, stage=1)
+# the flag-free FULL epilogue (aligned record groups, extra chunk) over two column tiles
+T, C, _ = ccc.three_way(synthgen.random_codes(300, 130, seed=6).cuda(),
+                        out_flags=ccc.OUT_TALLY | ccc.OUT_CCC_F64, n_stages=3, stage=2)
 n_v, n_f = 150, 200
 N, s, w = ccc.ccc_expand(ccc.ccc_pack(codes.cuda()), n_f)
 G = torch.zeros((n_v, n_v), dtype=torch.int32, device="cuda")
