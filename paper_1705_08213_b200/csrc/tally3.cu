@@ -811,9 +811,15 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                                                     (uint64_t)g[O::R2], tc, cc);
                                 }
                             } else if (want_c64) {
+#ifdef CCC_D3_CCCLINE   // diagnostics: each CCC instruction writes one whole line per row (wrong places)
+                                double* q = reinterpret_cast<double*>(args.ccc) + 8 * rec - 4 * (int64_t)cpair;
+                                stg_256_f64_if(st_ok, q, cc[0], cc[1], cc[2], cc[3]);
+                                stg_256_f64_if(st_ok, q + 16, cc[4], cc[5], cc[6], cc[7]);
+#else
                                 double* q = reinterpret_cast<double*>(args.ccc) + 8 * rec;
                                 stg_256_f64_if(st_ok, q, cc[0], cc[1], cc[2], cc[3]);
                                 stg_256_f64_if(st_ok, q + 4, cc[4], cc[5], cc[6], cc[7]);
+#endif
                             } else if constexpr (kF32) {
                                 // fp32 only: T < 2^23 is exact as (2^23 + T) - 2^23, U_p U_m and
                                 // U_n / (216 n_f^4) rounded once each: error < 4 x 2^-24 << 1e-6
