@@ -741,6 +741,7 @@ ccc_status ccc_3way_stage(int64_t n_v, int64_t n_f, double gamma, int64_t n_stag
     a.same_pm = a.same_mn = 1;
     a.order = 0;
     a.layout = 0;
+    a.ppair = 1;
     a.G = reinterpret_cast<const int32_t*>(ws + L.G);
     a.ldG = n_v;
     a.rec_base = rng[2];
@@ -961,6 +962,7 @@ ccc_status ccc_3way_paper_stage(int64_t n_v, int64_t n_f, double gamma, int64_t 
         a.p_hi = rng[1];
         a.m_hi = a.n_hi = n_v;
         a.same_pm = a.same_mn = 1;
+        a.ppair = 1;
         a.ldG = n_v;
         a.rec_base = rng[2];
         a.k_pad = k_pad;
@@ -1063,6 +1065,7 @@ ccc_status ccc_3way_unit(const ccc_block* bp, int64_t p_lo, int64_t p_hi, const 
     a.same_mn = smn;
     a.order = order;
     a.layout = (spm && smn) ? 0 : spm ? 1 : 2;
+    a.ppair = a.layout == 0;
     const int64_t nb = bp->rows;
     if (a.layout == 0) a.rec_base = c3(nb) - c3(nb - p_lo);
     else if (a.layout == 1) a.rec_base = (p_lo * (2 * nb - p_lo - 1) / 2) * (n_hi - n_lo);

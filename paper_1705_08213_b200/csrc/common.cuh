@@ -200,7 +200,9 @@ struct Tally3Args {
     void* ccc;                 // [records][8] double or float
     unsigned long long* checksum;
     Compact cmp;               // used when compact != 0
-    int32_t compact, pad4_;
+    int32_t compact;
+    int32_t ppair;             // single-block triangle: pivot pairs (PivotSched) -- the two CTAs
+                               // of a pair share 128 rows m and take consecutive pivots
     unsigned long long* trace; // optional per-unit %globaltimer trace (diagnostics)
     // paper route (f4 ii): mode 1 stores this pass's form at forms[form_self * form_stride + rec]
     uint32_t* forms;

@@ -66,9 +66,17 @@ struct PivotSched {
     TriSched tiles;
     int64_t p_lo, p_hi, m_lo, m_hi, n_lo, n_hi, tt, base, cnt;
     int32_t same_pm, same_mn, J, K;
+    // Pivot pairs (pp, single-block triangle): a unit is (128-row tile J, column tile K,
+    // pivots p, p + 1) -- both CTAs of the pair multiply the same 128 rows m, the leader
+    // weighted by pivot p and the follower by p + 1 (its own transform of its own A copy),
+    // against the pair's shared 256 columns.  Row tiles of 128 instead of 256 cut the
+    // masked records of the pivot triangles (C4: 1.195x -> 1.146x computed/valid records,
+    // 1.54x -> 1.39x in the last stage).  plim = first pivot past this tile's range.
+    int32_t pp, tile_m;
+    int64_t plim;
 
     __host__ __device__ int64_t pivots(int32_t Jt, int32_t Kt) const {
-        int64_t m_max = tiles.a_lo + (int64_t)Jt * kTileM3 + kTileM3 - 1;
+        int64_t m_max = tiles.a_lo + (int64_t)Jt * tile_m + tile_m - 1;
         if (m_max > m_hi - 1) m_max = m_hi - 1;
         int64_t n_max = tiles.b_lo + (int64_t)Kt * kBN + kBN - 1;
         if (n_max > n_hi - 1) n_max = n_hi - 1;
@@ -86,8 +94,11 @@ struct PivotSched {
         n_hi = a.n_hi;
         same_pm = a.same_pm;
         same_mn = a.same_mn;
+        pp = (a.ppair && same_pm && same_mn) ? 1 : 0;
+        tile_m = pp ? 128 : kTileM3;
+        plim = 0;
         if (same_mn) {
-            tiles.init(0, m_hi, n_hi, 1, kTileM3);  // m, n over the same [0, rows) range
+            tiles.init(0, m_hi, n_hi, 1, tile_m);   // m, n over the same [0, rows) range
         } else {
             tiles.init(m_lo, m_hi - m_lo, n_hi - n_lo, 0, kTileM3);
             tiles.b_lo = n_lo;
@@ -96,8 +107,12 @@ struct PivotSched {
         base = 0;
         cnt = 0;
         J = K = 0;
-        if (tiles.get(0, J, K)) cnt = pivots(J, K);
+        if (tiles.get(0, J, K)) cnt = units_of(J, K);
         else tt = -1;
+    }
+    __host__ __device__ int64_t units_of(int32_t Jt, int32_t Kt) const {
+        const int64_t n = pivots(Jt, Kt);
+        return pp ? (n + 1) / 2 : n;
     }
     __host__ __device__ bool get(int64_t u, int32_t& Jo, int32_t& Ko, int64_t& po) {
         if (tt < 0) return false;
@@ -105,14 +120,15 @@ struct PivotSched {
             base += cnt;
             ++tt;
             if (!tiles.get(tt, J, K)) { tt = -1; return false; }
-            cnt = pivots(J, K);
+            cnt = units_of(J, K);
         }
         Jo = J;
         Ko = K;
-        po = p_lo + (u - base);
+        po = p_lo + (pp ? 2 : 1) * (u - base);
+        plim = p_lo + pivots(J, K);
         return true;
     }
-    __host__ __device__ int64_t row0(int32_t Jt) const { return tiles.a_lo + (int64_t)Jt * kTileM3; }
+    __host__ __device__ int64_t row0(int32_t Jt) const { return tiles.a_lo + (int64_t)Jt * tile_m; }
     __host__ __device__ int64_t col0(int32_t Kt) const { return tiles.b_lo + (int64_t)Kt * kBN; }
 };
 
@@ -325,11 +341,13 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 int32_t J, K;
                 int64_t p;
                 if (!sch.get(u, J, K, p)) break;
-                const int8_t* prow = args.bp.N + p * args.k_pad;
+                // pivot pairs: the follower weights the same rows by pivot p + 1 (if it exists)
+                const int64_t pc = (sch.pp && p + (int64_t)rank < sch.plim) ? p + rank : p;
+                const int8_t* prow = args.bp.N + pc * args.k_pad;
 #ifdef CCC_D3_SAMEA   // diagnostics: both CTAs of the pair load the same A rows (timing only)
                 const int32_t mrow = (int32_t)sch.row0(J);
 #else
-                const int32_t mrow = (int32_t)(sch.row0(J) + rank * 128);
+                const int32_t mrow = (int32_t)(sch.row0(J) + (sch.pp ? 0u : rank * 128u));
 #endif
                 const int32_t ncol = (int32_t)(sch.col0(K) + rank * 128);
                 for (int32_t kb = 0; kb < args.k_blocks; ++kb) {
@@ -516,6 +534,11 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             int32_t J, K;
             int64_t p;
             if (!sch.get(u, J, K, p)) break;
+            bool p_ok = true;   // pivot pairs: the follower's pivot is p + 1, if in range
+            if (sch.pp) {
+                p_ok = p + (int64_t)rank < sch.plim;
+                if (p_ok) p += rank;
+            }
             unsigned long long* tr = (args.trace && warp == 2 && rank == 0) ? args.trace + 8 * u : nullptr;
             if (tr && lane == 0) tr[3] = globaltimer();
             const int64_t gp = args.bp.row0 + p;
@@ -572,8 +595,8 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             }
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
-                const int64_t m = sch.row0(J) + rank * 128 + quad * 32 + half * 16 + r * 8 + (lane >> 2);
-                const bool ok = m >= args.m_lo && m < args.m_hi && (!args.same_pm || m > p);
+                const int64_t m = sch.row0(J) + (sch.pp ? 0u : rank * 128u) + quad * 32 + half * 16 + r * 8 + (lane >> 2);
+                const bool ok = p_ok && m >= args.m_lo && m < args.m_hi && (!args.same_pm || m > p);
                 const int64_t mc = m < args.m_hi ? m : args.m_hi - 1;
                 gm_r[r] = args.bm.row0 + mc;
                 s_m[r] = (uint32_t)__ldg(args.bm.s + mc);
@@ -884,7 +907,7 @@ int64_t tally3_units(const Tally3Args& a) {
     t.cnt = (t.SP > 0 && t.SQ > 0) ? t.super_count(0, 0) : 0;
     int64_t units = 0;
     int32_t J, K;
-    for (int64_t tt = 0; t.get(tt, J, K); ++tt) units += sch.pivots(J, K);
+    for (int64_t tt = 0; t.get(tt, J, K); ++tt) units += sch.units_of(J, K);
     return units;
 }
 
