@@ -1,7 +1,7 @@
 #!/bin/bash
 # Secondary 3-way bench lines after the aligned record groups: c4f32, c4paper, c5.
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
-O=gpurun_out/r02x
+O=gpurun_out/r02x2
 mkdir -p $O
 for wl in c4f32 c4paper; do
   timeout 900 python bench.py --workload $wl --steps 3 --warmup 3 --no-e2e > $O/bench_$wl.json 2> $O/bench_$wl.err
