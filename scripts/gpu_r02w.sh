@@ -1,7 +1,7 @@
 #!/bin/bash
 # ncu --set full of one C4 stage (0 and 15, FULL) with the aligned 3-way epilogue.
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
-O=gpurun_out/r02w
+O=gpurun_out/r02w2
 mkdir -p $O
 for st in 15 0; do
   STAGE=$st FLAGS=3 timeout 900 ncu --set full --import-source on --clock-control none -k regex:tally3 -c 1 \
