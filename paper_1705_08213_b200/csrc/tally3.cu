@@ -15,9 +15,11 @@
 // needs one int8 MAC per unique 3-way comparison.
 //
 // A work unit is (row tile J of 256 m's on a CTA pair -- 128 per CTA --, column tile K of
-// 256 n's, pivot p); units are ordered tile-outer / pivot-inner so the 74 concurrent CTA
-// pairs share the same N_M, N_N panels and G_mn tile in L2 and differ only in their
-// 128-byte pivot rows.
+// 256 n's, pivot p); on the single-block triangle (C4 stages, {A,A,A} units) it is
+// (row tile of 128 m's, column tile K, pivots p and p + 1): both CTAs hold the same rows,
+// each weighted by its own pivot ("pivot pairs", PivotSched).  Units are ordered
+// tile-outer / pivot-inner so the 74 concurrent CTA pairs share the same N_M, N_N panels
+// and G_mn tile in L2 and differ only in their 128-byte pivot rows.
 // Warp roles: 0 TMA producer (A, B tiles + pivot chunk), 1 TMEM alloc + MMA issuer,
 // 2..9 epilogue (2 per TMEM lane quadrant), 10..13 transform (A <- A o n_p in shared
 // memory, in place, then fence.proxy.async so the tensor core sees it).
