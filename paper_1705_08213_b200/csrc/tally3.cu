@@ -52,11 +52,15 @@ constexpr int kPivBytes = kBK;       // 128 B of the pivot row per stage
 constexpr int kPivOff3 = kStages3 * (kABytes3 + kBBytes3);
 // per-unit column terms (s_n, G_pn, n-side weights), one table per TMEM accumulator
 struct ColT3 {
-    uint32_t gpn2, cn, en, sn;   // 2 G_pn, 4 s_n - 2 G_pn, 2 G_pn - 4 s_n, s_n (mod 2^32)
     double w0, w1;               // n-side weights (exact: U_n(c) / (216 n_f^4))
-    double m0, m1;               // -2^52 w0, -2^52 w1 (kFull cell formula)
+    uint32_t gpn2, sn;           // 2 G_pn, s_n (mod 2^32); 4 s_n - 2 G_pn etc. formed in registers
     float f0, f1;                // w0, w1 in fp32 (kF32 cell formula)
-};
+};                               // 32 B: the FULL epilogue reads one 16-B and one 8-B chunk
+// -2^52 w for a positive normal double w: sign set, exponent + 52 (exact; the kFull cell
+// formula's addend, formed by one integer add instead of stored in the column table)
+__device__ __forceinline__ double neg_two52_times(double w) {
+    return __longlong_as_double(__double_as_longlong(w) + (long long)0x8340000000000000ull);
+}
 constexpr int kColOff3 = kPivOff3 + kStages3 * kPivBytes;
 constexpr int kBarOff3 = kColOff3 + 2 * kBN * (int)sizeof(ColT3);
 constexpr int kSmem3 = kBarOff3 + 512 + 1024;
@@ -559,14 +563,10 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 const uint32_t gpn = kMode ? 0u : gord<kOrder, 0, 2>(args.G, args.ldG, gp, args.bn.row0 + nc);
                 ColT3 v;
                 v.gpn2 = 2u * gpn;
-                v.cn = 4u * sn - 2u * gpn;
-                v.en = 2u * gpn - 4u * sn;
                 v.sn = sn;
                 if constexpr (kExact) {   // U_n(c) / (216 n_f^4)
                     v.w0 = (double)(nf + sn) * args.inv_d;
                     v.w1 = (double)(3u * nf - sn) * args.inv_d;
-                    v.m0 = -4503599627370496.0 * v.w0;
-                    v.m1 = -4503599627370496.0 * v.w1;
                     v.f0 = (float)v.w0;
                     v.f1 = (float)v.w1;
                 } else {
@@ -784,8 +784,8 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         t[3] = gmn2 - g3;
                         t[4] = A_r[r] - cn.gpn2 + g3;
                         t[2] = B_r[r] - gmn2 + g3;
-                        t[1] = cn.cn - gmn2 + g3;
-                        t[0] = D_r[r] + cn.en + gmn2 - g3;
+                        t[1] = 4u * cn.sn - cn.gpn2 - gmn2 + g3;
+                        t[0] = D_r[r] + cn.gpn2 - 4u * cn.sn + gmn2 - g3;
                         uint32_t tc[8];
                         perm_cells<O::R0, O::R1, O::R2>(t, tc);
                         const int64_t rec = rec_r[r] + nl;
@@ -814,8 +814,8 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                                     cr[2 * ab + 0] = magic52(t[2 * ab + 0] * upm[r][ab]);
                                     cr[2 * ab + 1] = magic52(t[2 * ab + 1] * upm[r][ab]);
 #else
-                                    cr[2 * ab + 0] = __fma_rn(magic52(t[2 * ab + 0] * upm[r][ab]), wn0, cn.m0);
-                                    cr[2 * ab + 1] = __fma_rn(magic52(t[2 * ab + 1] * upm[r][ab]), wn1, cn.m1);
+                                    cr[2 * ab + 0] = __fma_rn(magic52(t[2 * ab + 0] * upm[r][ab]), wn0, neg_two52_times(wn0));
+                                    cr[2 * ab + 1] = __fma_rn(magic52(t[2 * ab + 1] * upm[r][ab]), wn1, neg_two52_times(wn1));
 #endif
                                 } else {
                                     // exact: T U_p U_m rounded once (same as the 64-bit integer
