@@ -375,7 +375,16 @@ tally3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         if (rank == 0)
                             tma_load_2d_mc(smA + stage * kABytes3, &tmA, &aload[stage], kb * kBK, mrow, 3, pol);
 #else
-                        tma_load_2d(smA + stage * kABytes3, &tmA, &aload[stage], kb * kBK, mrow, pol);
+                        if (sch.pp) {
+                            // pivot pairs: both CTAs need the same A rows -- the leader's one
+                            // load lands in both (same offset; each CTA's aload barrier counts
+                            // it).  The follower's stage is free: the pair's MMA commit that
+                            // released the leader's stage read both CTAs' stages.
+                            if (rank == 0)
+                                tma_load_2d_mc(smA + stage * kABytes3, &tmA, &aload[stage], kb * kBK, mrow, 3, pol);
+                        } else {
+                            tma_load_2d(smA + stage * kABytes3, &tmA, &aload[stage], kb * kBK, mrow, pol);
+                        }
 #endif
                         bulk_load(smP + stage * kPivBytes, prow + (int64_t)kb * kBK, kPivBytes,
                                   &aload[stage]);
