@@ -264,6 +264,16 @@ def test_3way_full(n_v, n_f):
     _check_3way_full(_codes("random", n_v, n_f, seed=n_v + n_f))
 
 
+@pytest.mark.parametrize("n_v,n_f,n_stages", [(385, 77, 1), (385, 77, 5), (513, 130, 3), (300, 64, 7)])
+def test_3way_pivot_pairs_full_epilogue(n_v, n_f, n_stages):
+    """The flag-free FULL epilogue (tallies + fp64 CCC, gamma = 2/3) on the pivot-pair units:
+    several 128-row tiles and 256-column tiles, stages that cut the pivot range mid-pair
+    (odd pivot counts per tile leave the follower CTA without a pivot), aligned record
+    groups with every row offset mod 4 -- against the oracle record by record."""
+    _check_3way_full(_codes("random", n_v, n_f, seed=n_v * 7 + n_stages), n_stages=n_stages, flags=TAL | F64)
+    _check_3way_full(_codes("hwe", n_v, n_f, seed=n_v + n_stages), n_stages=n_stages, flags=TAL | F64 | CK)
+
+
 def test_3way_stages_and_variants():
     codes = _codes("hwe", 150, 333)
     _check_3way_full(codes, n_stages=7)
